@@ -138,7 +138,8 @@ static int row_logp(const rows_in* in, int64_t b, int64_t t, double* logp, doubl
   double m = -INFINITY;
   for (int64_t v = 0; v < V; ++v) {
     double x = load_x(in->logits, in->dtype, base + v);
-    if (!isfinite(x)) *st |= ORC_FLAG_NONFINITE_LOGIT;
+    /* reading R14: NaN and +inf are errors; -inf is a legal "impossible token" logit */
+    if (isnan(x) || x == INFINITY) *st |= ORC_FLAG_NONFINITE_LOGIT;
     double y = x * in->invT;
     if (y > m) m = y;
   }
@@ -152,6 +153,8 @@ static int row_logp(const rows_in* in, int64_t b, int64_t t, double* logp, doubl
   }
   double ytok = load_x(in->logits, in->dtype, base + tok) * in->invT;
   *logp = (ytok - m) - log(s);
+  /* ... but an all -inf row, or a -inf sampled logit, has no finite log-prob (R14) */
+  if (!isfinite(m) || !isfinite(*logp)) *st |= ORC_FLAG_NONFINITE_LOGIT;
   return 0;
 }
 

@@ -397,3 +397,21 @@ def test_dl_rows_subset_matches_full(orc):
     rows = np.array([3, 17, 0, 39], np.int64)
     sub = orc.online_dpo_loss_fwd_bwd(x, ref, tok, mask, 0.1, dl_rows=rows)
     assert np.array_equal(sub["dlogits"], full["dlogits"].reshape(-1, 7)[rows])
+
+
+def test_neg_inf_reading_r14(orc):
+    """Reading R14 (DESIGN.md): -inf marks an impossible token (probability 0) and is legal;
+    NaN, +inf, an all -inf row, or a -inf sampled logit are flagged."""
+    x = np.array([[[0.0, -np.inf, 1.0], [-np.inf, -np.inf, -np.inf]]])
+    tok = np.array([[0, 1]], np.int32)
+    m1 = np.array([[1, 0]], np.uint8)
+    o = orc.seq_logprobs(x, tok, m1)
+    assert o["status"] == 0
+    assert abs(o["tok_logp"][0, 0] - (0.0 - math.log(1.0 + math.e))) < 1e-15
+    assert orc.seq_logprobs(x, tok, np.array([[0, 1]], np.uint8))["status"] & orc.FLAG_NONFINITE_LOGIT
+    x2 = np.array([[[0.0, -np.inf, 1.0]]])
+    assert orc.seq_logprobs(x2, np.array([[1]], np.int32), np.ones((1, 1), np.uint8))["status"] \
+        & orc.FLAG_NONFINITE_LOGIT
+    x3 = np.array([[[0.0, np.inf, 1.0]]])
+    assert orc.seq_logprobs(x3, np.array([[0]], np.int32), np.ones((1, 1), np.uint8))["status"] \
+        & orc.FLAG_NONFINITE_LOGIT
