@@ -1,0 +1,397 @@
+#!/usr/bin/env python
+"""bench.py -- Online-DPO learner hot path on B200: pairs/s and achieved HBM GB/s.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config pythia] [--impl ours|reference]
+
+One STEP = one pass of the whole hot path over one batch of synthetic input
+(SURVEY.md §8(a) rows S1-S6): pair_select over the rewards, the Online-DPO loss
+forward + dlogits backward over the policy logits [B,T,V], and (N > 1) the SUM
+all-reduce of the 128-byte statistics buffer over NCCL.  The reference log-probs
+(one forward pass over a second "reference model" logits tensor) are computed once at
+setup, as stored log pi_init values; that pass is timed separately ("ref_pass").
+
+Multi-GPU: torchrun, one process per GPU; every rank processes its own contiguous
+block of pairs of the same shape (weak scaling, global P = N * P_rank, static
+P_global), data keyed by global pair index.  Timing: CUDA events on the launching
+stream per step with an L2 flush (untimed 256 MiB write) between steps, summed,
+max over ranks.  Rank 0 prints ONE JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Online DPO fwd+bwd pairs/s and achieved HBM GB/s (% of B200 peak) at 1/2/4/8 GPUs"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="pythia", choices=["tiny", "pythia", "rho", "llama"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--schedule", default="auto", choices=["auto", "fused", "two_pass"])
+    ap.add_argument("--lag", type=int, default=0)
+    ap.add_argument("--ctas-per-sm", type=int, default=0)
+    ap.add_argument("--mask", default="dense", choices=["dense", "prefix"])
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    return ap.parse_args()
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, b.copy_ read+write)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """NVML SM-clock / throttle-reason sampler running during the timed region."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.stop_ev = [], 0, threading.Event()
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max_mhz = None
+
+    def _run(self):
+        while not self.stop_ev.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.reasons |= int(self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h))
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self.stop_ev.set()
+        if self.ok:
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        names = [n for bit, n in self.REASONS.items() if self.reasons & bit and bit != 0x1]
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": names, "samples": len(self.samples)}
+
+
+def workload(name):
+    from synth.configs import CONFIGS
+    return CONFIGS[name]
+
+
+# ----------------------------------------------------------------------------- oracle timing
+def oracle_sample(w, seed, npairs, mask_kind, n_threads, p0=0):
+    """Time the CPU oracle (as it stands) on npairs pairs of the same workload."""
+    import oracle
+    import synth
+    seqs = np.arange(2 * npairs) + 2 * p0
+    rows = (seqs[:, None] * w.T + np.arange(w.T)[None, :]).reshape(-1)
+    tok = synth.tokens_rows(seed, rows, w.V).reshape(-1, w.T)
+    mask = synth.mask_for(seed, seqs, w.T, mask_kind, w.lbar)
+    x = synth.logits_rows(seed, rows, w.V, tokens=tok.reshape(-1), peak=14.0).astype(np.float32)
+    x = x.reshape(len(seqs), w.T, w.V)
+    if w.dtype == "bf16":
+        x = oracle.to_bf16_bits(x)
+    rewards = synth.rewards_for(seed, npairs, 2, p0=p0, kind=w.reward_kind)
+    eos = synth.has_eos_for(seed, npairs, 2, p0=p0) if w.eos_penalty is not None else None
+    ref = np.full(len(seqs), -0.08 * w.T, np.float32)
+    t0 = time.perf_counter()
+    sel = oracle.pair_select(rewards, eos, w.eos_penalty if w.eos_penalty is not None else 0.0)
+    o = oracle.online_dpo_loss_fwd_bwd(x, ref, tok, mask, w.beta, pair_rows=sel["pair_rows"],
+                                       want_dlogits=True, n_threads=n_threads)
+    dt = time.perf_counter() - t0
+    return dt, o
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the CPU oracle is this tier's reference arm (rank 0 only)."""
+    if rank != 0:
+        return
+    w = workload(args.config)
+    cores = os.cpu_count() or 1
+    npairs = max(1, min(w.P, cores // 2 if w.T * w.V < 1e7 else 1))
+    threads = min(cores, 2 * npairs)
+    for _ in range(max(0, min(args.warmup, 1))):
+        oracle_sample(w, args.seed, npairs, args.mask, threads)
+    times = []
+    for _ in range(args.steps):
+        dt, _ = oracle_sample(w, args.seed, npairs, args.mask, threads)
+        times.append(dt)
+    tot = float(np.sum(times))
+    value = npairs * len(times) / tot
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "pairs/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * tot / len(times), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.config, "pairs_per_step": npairs, "T": w.T, "V": w.V,
+                   "logits_dtype": w.dtype, "mask": args.mask},
+        "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": threads, "kind": "oracle",
+                         "sample": f"{npairs} pairs of {args.config} per step (pair_select + "
+                                   f"loss + full dlogits, fp64, {threads} threads)"},
+        "e2e": {"value": value, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- ours
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    import paper_2410_18252_b200 as odpo
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    w = workload(args.config)
+    P, T, V = w.P, w.T, w.V
+    B = 2 * P
+    p0 = rank * P                       # global pair offset of this rank
+    Pg = P * world
+    tdt = torch.bfloat16 if w.dtype == "bf16" else torch.float32
+    s_in = 2 if w.dtype == "bf16" else 4
+    seqs = np.arange(B) + 2 * p0
+    rows = (seqs[:, None] * T + np.arange(T)[None, :]).reshape(-1)
+
+    # ---------------- inputs (untimed): rewards, tokens, mask on device; logits via device twin
+    rewards = torch.from_numpy(synth.rewards_for(args.seed, P, 2, p0=p0, kind=w.reward_kind)).to(dev)
+    eos = (torch.from_numpy(synth.has_eos_for(args.seed, P, 2, p0=p0)).to(dev)
+           if w.eos_penalty is not None else None)
+    pen = w.eos_penalty if w.eos_penalty is not None else 0.0
+    tokens = torch.from_numpy(synth.tokens_rows(args.seed, rows, V).reshape(B, T)).to(dev)
+    mask_np = synth.mask_for(args.seed, seqs, T, args.mask, w.lbar)
+    mask = torch.from_numpy(mask_np).to(dev)
+    rho = float(mask_np.mean())
+    logits = torch.empty((B, T, V), dtype=tdt, device=dev)
+    dlogits = torch.empty_like(logits)
+
+    # reference model log-probs: one forward pass over independent "reference" logits
+    synth.fill_logits_device(logits, args.seed, row0=int(rows[0]), tokens=tokens, peak=14.0, ref=True)
+    torch.cuda.synchronize()
+    ref_logp = odpo.seq_logprobs(logits, tokens, mask)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ref_ms = []
+    for _ in range(3):
+        e0.record()
+        ref_logp = odpo.seq_logprobs(logits, tokens, mask)
+        e1.record()
+        torch.cuda.synchronize()
+        ref_ms.append(e0.elapsed_time(e1))
+    synth.fill_logits_device(logits, args.seed, row0=int(rows[0]), tokens=tokens, peak=14.0)
+    torch.cuda.synchronize()
+
+    stats = torch.zeros(16, dtype=torch.float64, device=dev)
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    launches = [0]
+
+    def step(timed_loss=None):
+        sel = odpo.pair_select(rewards, eos, pen, status=status, sel_stats=stats[10:13])
+        if timed_loss is not None:
+            timed_loss[0].record()
+        out = odpo.online_dpo_loss_fwd_bwd(logits, ref_logp, tokens, mask, w.beta,
+                                           pair_rows=sel.pair_rows, p_global=Pg, dlogits=dlogits,
+                                           schedule=args.schedule, lag_pairs=args.lag,
+                                           ctas_per_sm=args.ctas_per_sm, stats=stats, status=status)
+        if timed_loss is not None:
+            timed_loss[1].record()
+        odpo.allreduce_stats(stats)
+        launches[0] = 1 + out.launches
+        return out
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+
+    K = args.steps
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    lev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    clk = ClockSampler(local_rank)
+    with clk:
+        for k in range(K):
+            flush.zero_()                      # untimed L2 flush between steps
+            torch.cuda.synchronize()
+            ev[k][0].record()
+            step(lev[k])
+            ev[k][1].record()
+        torch.cuda.synchronize()
+    step_ms = np.array([a.elapsed_time(b) for a, b in ev])
+    loss_ms = np.array([a.elapsed_time(b) for a, b in lev])
+    tot = torch.tensor([step_ms.sum()], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.barrier()
+        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+    tot_ms = float(tot.item())
+    value = world * P * K / (tot_ms / 1e3)
+    st = int(status.item())
+
+    # algorithmic bytes per loss launch: read the live rows once, write every dlogit once
+    alg_bytes = rho * B * T * V * s_in + B * T * V * s_in
+    achieved = alg_bytes / (loss_ms.mean() / 1e3) / 1e9
+    peak, peak_src = peaks()
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", f"ncu_traffic_{args.config}.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    # ---------------- e2e through host buffers (pinned H2D inputs, D2H stats + z each step)
+    e2e = None
+    if not args.no_e2e:
+        h_logits = torch.empty(logits.shape, dtype=tdt, pin_memory=True)
+        h_logits.copy_(logits)
+        h_rew = rewards.cpu().pin_memory()
+        h_eos = eos.cpu().pin_memory() if eos is not None else None
+        h_tok = tokens.cpu().pin_memory()
+        h_mask = mask.cpu().pin_memory()
+        h_ref = ref_logp.cpu().pin_memory()
+        h_stats = torch.empty(16, dtype=torch.float64, pin_memory=True)
+        h_z = torch.empty(P, dtype=torch.float32, pin_memory=True)
+        d_rew, d_tok, d_mask, d_ref = (torch.empty_like(rewards), torch.empty_like(tokens),
+                                       torch.empty_like(mask), torch.empty_like(ref_logp))
+        d_eos = torch.empty_like(eos) if eos is not None else None
+        h2d = (h_logits.numel() * s_in + h_rew.numel() * 4 + (h_eos.numel() if h_eos is not None else 0)
+               + h_tok.numel() * 4 + h_mask.numel() + h_ref.numel() * 4)
+        d2h = 16 * 8 + P * 4
+
+        def e2e_step():
+            logits.copy_(h_logits, non_blocking=True)
+            d_rew.copy_(h_rew, non_blocking=True)
+            if d_eos is not None:
+                d_eos.copy_(h_eos, non_blocking=True)
+            d_tok.copy_(h_tok, non_blocking=True)
+            d_mask.copy_(h_mask, non_blocking=True)
+            d_ref.copy_(h_ref, non_blocking=True)
+            sel = odpo.pair_select(d_rew, d_eos, pen, status=status, sel_stats=stats[10:13])
+            out = odpo.online_dpo_loss_fwd_bwd(logits, d_ref, d_tok, d_mask, w.beta,
+                                               pair_rows=sel.pair_rows, p_global=Pg,
+                                               dlogits=dlogits, schedule=args.schedule,
+                                               lag_pairs=args.lag, stats=stats, status=status)
+            odpo.allreduce_stats(stats)
+            h_stats.copy_(stats, non_blocking=True)
+            h_z.copy_(out.z, non_blocking=True)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(args.e2e_steps):
+            e2e_step()
+        b.record()
+        torch.cuda.synchronize()
+        et = torch.tensor([a.elapsed_time(b)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        e2e = {"value": world * P * args.e2e_steps / (float(et.item()) / 1e3), "unit": "pairs/s",
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "steps": args.e2e_steps,
+               "note": "pinned host->device copy of logits, rewards, eos, tokens, mask, ref_logp; "
+                       "device->host of the stats buffer and per-pair z; dlogits stay resident "
+                       "for the LM-head backward"}
+        del h_logits
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cores = os.cpu_count() or 1
+        npairs = max(1, min(P, max(2, cores // 4))) if w.T * w.V < 1e7 else 1
+        threads = min(cores, 2 * npairs)
+        dt, _ = oracle_sample(w, args.seed, npairs, args.mask, threads)
+        cpu = {"value": npairs / dt, "unit": "pairs/s", "cores": threads, "kind": "oracle",
+               "sample": f"{npairs} pairs of the {args.config} workload (pair_select + fp64 loss + "
+                         f"full dlogits), {dt:.1f} s on {threads} host threads"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": world, "steps": K,
+            "warmup": args.warmup, "ms_per_step": tot_ms / K, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": w.dtype, "data": "synthetic",
+            "config": {"workload": args.config, "pairs_per_rank": P, "global_pairs": P * world,
+                       "K": 2, "T": T, "V": V, "beta": w.beta, "mask": args.mask,
+                       "ref_logp": "seq_logprobs over independent reference logits (setup)",
+                       "schedule": args.schedule, "parallelism": f"dp{world}",
+                       "l2": "inputs (%.2f GB) > L2; plus 256 MiB L2 flush between timed steps"
+                             % (B * T * V * s_in / 1e9)},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                         "kernel": "odpo_online_dpo_loss_fwd_bwd (prep + fused fwd/bwd)",
+                         "alg_bytes_per_launch": alg_bytes,
+                         "loss_ms_mean": float(loss_ms.mean())},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(launches[0] * K),
+            "clocks": clk.summary(),
+            "tokens_vocab_per_s": world * B * T * V * K / (tot_ms / 1e3),
+            "eff_gbs_step": world * alg_bytes * K / (tot_ms / 1e3) / 1e9,
+            "step_ms_p10_p50_p90": [float(np.percentile(step_ms, q)) for q in (10, 50, 90)],
+            "ref_pass_ms": float(np.median(ref_ms)),
+            "ref_pass_gbs": rho * B * T * V * s_in / (np.median(ref_ms) / 1e3) / 1e9,
+            "status": st,
+            "loss": float(stats[1].item()),
+        }
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

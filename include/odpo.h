@@ -1,0 +1,211 @@
+/*
+ * odpo.h -- C ABI of libodpo.so, the B200 (sm_100a) Online-DPO learner hot path.
+ *
+ * The method (arXiv 2410.18252, "Asynchronous RLHF"): Online DPO samples two
+ * completions per prompt, ranks them with the reward model into chosen y+ and
+ * rejected y- (Sec 2.1; App A.1), and maximises
+ *
+ *     E log sigma( beta log pi(y+|x)/pi_init(y+|x) - beta log pi(y-|x)/pi_init(y-|x) )
+ *                                                             (Sec 2.1)
+ *
+ * Three calls follow the paper's statement of the problem:
+ *   odpo_pair_select              rewards -> (chosen, rejected) pairs
+ *   odpo_seq_logprobs             logits, tokens, mask -> log pi(y|x)
+ *   odpo_online_dpo_loss_fwd_bwd  policy logits, ref log-probs, beta ->
+ *                                 -log sigma loss, statistics, dlogits
+ *
+ * General conventions (all calls):
+ *  - Every tensor argument is a DEVICE pointer unless noted; the caller allocates and
+ *    owns every buffer (outputs included).  The library never allocates, frees or
+ *    synchronises, and keeps no per-call global state.
+ *  - Calls are asynchronous and stream-ordered on `stream` (a cudaStream_t passed as
+ *    void*; NULL = the legacy default stream).  Calls are re-entrant across streams and
+ *    devices; the current device must own the pointers.
+ *  - ARGUMENT errors are synchronous return codes (odpo_status).  DATA-dependent
+ *    errors are OR-ed into a caller-owned device uint32 `status` word (ODPO_FLAG_*),
+ *    read by the caller at its own sync point; outputs of flagged sequences/pairs are
+ *    unspecified (except EMPTY_SEQ, where the sequence log-prob is 0).
+ *  - Logits are [B, T, V] with element strides (stride_b, stride_t) and contiguous V;
+ *    logits[b, t, :] is the (pre-shifted) distribution that produced tokens[b, t]
+ *    (reading R1).  The logits base pointer and both strides in bytes must
+ *    be multiples of 16 (128-bit vector path; no scalar fallback) -> ODPO_ERR_ALIGNMENT.
+ *    V need not be a multiple of the vector width.
+ *  - tokens are int32 [B, T]; mask is uint8 [B, T] (1 = response token that counts).
+ *    Rows with mask = 0 are never read, so their logits may hold anything.
+ */
+#ifndef ODPO_H
+#define ODPO_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  ODPO_OK = 0,
+  ODPO_ERR_INVALID_ARG = 1, /* null required pointer, bad size, beta/invT <= 0 or non-finite, ... */
+  ODPO_ERR_ALIGNMENT = 2,   /* logits/dlogits base or stride (bytes) not a multiple of 16 */
+  ODPO_ERR_WORKSPACE = 3,   /* workspace NULL or smaller than odpo_workspace_bytes() */
+  ODPO_ERR_UNSUPPORTED = 4, /* shape beyond the 32-bit work-ticket range, unknown schedule */
+  ODPO_ERR_CUDA = 5         /* a launch failed (cudaGetLastError after launch) */
+} odpo_status;
+
+typedef enum { ODPO_F32 = 0, ODPO_BF16 = 1 } odpo_dtype;
+
+/* Data-dependent status bits, OR-ed into *status on the device. */
+enum {
+  ODPO_FLAG_TOKEN_RANGE = 1,       /* a token outside [0, V) where mask = 1 */
+  ODPO_FLAG_NONFINITE_LOGIT = 2,   /* NaN or +inf in a read row, an all -inf row, or a -inf sampled logit */
+  ODPO_FLAG_EMPTY_SEQ = 4,         /* a sequence with no mask = 1 token (its log-prob := 0) */
+  ODPO_FLAG_NONFINITE_REWARD = 8,  /* a shaped reward is NaN or +-inf */
+  ODPO_FLAG_DUP_ROW = 16,          /* chosen == rejected, or a sequence referenced by two pairs */
+  ODPO_FLAG_DEGENERATE_PAIR = 32,  /* informational: max reward == min reward in a group */
+  ODPO_FLAG_PAIR_RANGE = 64        /* a pair_rows entry outside [0, B): that pair is skipped */
+};
+
+/* Loss statistics: LOCAL partial sums over this call's pairs, fp64.  Turning them into
+   global means is the caller's SUM all-reduce (one 128-byte message, see below). */
+enum {
+  ODPO_ST_NPAIRS = 0,      /* number of pairs                                         */
+  ODPO_ST_LOSS = 1,        /* sum_p softplus(-z_p) / P_global   (the loss, already a mean) */
+  ODPO_ST_NCORRECT = 2,    /* sum_p [z_p > 0]                   (accuracy numerator)  */
+  ODPO_ST_Z = 3,           /* sum_p z_p                         (implicit-reward margin) */
+  ODPO_ST_RCHOSEN = 4,     /* sum_p beta (S_c - ref_c)          (chosen implicit reward) */
+  ODPO_ST_RREJ = 5,        /* sum_p beta (S_r - ref_r)          (rejected implicit reward) */
+  ODPO_ST_SCHOSEN = 6,     /* sum_p S_c                                                */
+  ODPO_ST_SREJ = 7,        /* sum_p S_r                                                */
+  ODPO_ST_NTOK_CHOSEN = 8, /* sum_p #mask tokens of the chosen sequence                */
+  ODPO_ST_NTOK_REJ = 9,    /* sum_p #mask tokens of the rejected sequence              */
+  ODPO_NSTATS = 10
+};
+/* Selection statistics (odpo_pair_select), fp64 local partial sums. */
+enum {
+  ODPO_SEL_MARGIN_SUM = 0, /* sum_p (max - min) shaped reward      */
+  ODPO_SEL_NDEGEN = 1,     /* groups with max == min                                 */
+  ODPO_SEL_NTRUNC = 2,     /* completions without EOS (penalised)                     */
+  ODPO_SEL_NSTATS = 3
+};
+/* Recommended layout: ONE fp64[16] buffer, loss stats at [0,10), selection stats at
+   [10,13), [13,16) zero; a single SUM all-reduce of these 128 bytes gives every global
+   statistic. */
+#define ODPO_STATS_BUFFER_DOUBLES 16
+
+/* Work schedules of odpo_online_dpo_loss_fwd_bwd_ex. */
+enum {
+  ODPO_SCHED_AUTO = 0,     /* = FUSED                                                   */
+  ODPO_SCHED_FUSED = 1,    /* one persistent kernel: forward rows of pair s interleaved with
+                              backward rows of pair s - lag, per-pair completion counters;
+                              backward re-reads hit L2 when lag pairs fit in L2           */
+  ODPO_SCHED_TWO_PASS = 2  /* forward kernel, pair-reduce kernel, backward kernel (2R+1W) */
+};
+
+typedef struct {
+  int32_t schedule;     /* ODPO_SCHED_*                                            */
+  int32_t lag_pairs;    /* FUSED: backward of pair s is issued after forward of s+lag (0 = auto) */
+  int32_t ctas_per_sm;  /* FUSED: persistent CTAs per SM (0 = auto)               */
+  int32_t launches;     /* OUT: number of kernels this call launched               */
+} odpo_launch_opts;
+
+/*
+ * odpo_pair_select -- reward-ranked pair selection (Sec 2.1 "rank them as
+ * better (y+) and worse (y-) with the reward model"; App A.1 "the completion
+ * with the higher score as the chosen"; Sec 4.2 best/worst of K and the
+ * reward margin; PAPER.md:434-435, 518-519 EOS penalty).
+ *
+ *   rewards      [P][K] f32 device, raw reward-model scores.
+ *   has_eos      [P][K] u8 device or NULL (NULL = every completion has EOS).
+ *   eos_penalty  shaped score of a completion WITHOUT EOS: it REPLACES the reward (R7).
+ *   P >= 0, K >= 2.
+ *   chosen[P], rejected[P]  i32 device out: the FIRST index of the max and the LAST index
+ *                of the min of the shaped scores (R5), so chosen != rejected always.
+ *   pair_rows    [P][2] i32 device out or NULL: (p*K + chosen, p*K + rejected).
+ *   reward_margin[P] f32 device out or NULL: max - min (one fp32 subtraction).
+ *   sel_stats    [ODPO_SEL_NSTATS] f64 device out or NULL: local sums (overwritten).
+ *   status       u32 device or NULL: NONFINITE_REWARD, DEGENERATE_PAIR.
+ * One launch.  Bit-exact with the oracle.
+ */
+odpo_status odpo_pair_select(const float* rewards, const uint8_t* has_eos, float eos_penalty,
+                             int64_t P, int32_t K, int32_t* chosen, int32_t* rejected,
+                             int32_t* pair_rows, float* reward_margin, double* sel_stats,
+                             uint32_t* status, void* stream);
+
+/*
+ * odpo_seq_logprobs -- log pi(y|x) = sum_t mask[b,t] * log_softmax(invT * logits[b,t,:])[tokens[b,t]]
+ * (reading R1: token-wise, pre-shifted, not length-normalised).
+ *
+ *   logits       [B,T,V] device, dtype dt, strides (stride_b, stride_t) in ELEMENTS, stride_t >= V.
+ *   inv_temperature  > 0, finite (R2; 1.0 by default).
+ *   seq_logp[B]  f32 device out.
+ *   tok_logp[B][T], row_lse[B][T]  f32 device out or NULL (0 where mask = 0).
+ *   workspace    device scratch of >= odpo_workspace_bytes(B, T, B/2 + 1) bytes.
+ * Single read of the logits: one online log-sum-exp pass per row, then a fixed-order
+ * sequence sum.  Bit-identical seq_logp to the fused loss call on the same inputs.
+ */
+odpo_status odpo_seq_logprobs(const void* logits, odpo_dtype dt, int64_t B, int64_t T, int64_t V,
+                              int64_t stride_b, int64_t stride_t, const int32_t* tokens,
+                              const uint8_t* mask, float inv_temperature, float* seq_logp,
+                              float* tok_logp, float* row_lse, uint32_t* status, void* workspace,
+                              size_t workspace_bytes, void* stream);
+
+/*
+ * odpo_online_dpo_loss_fwd_bwd -- Online DPO loss, statistics and dlogits.
+ *
+ *   policy_logits  [B,T,V] device (as above).
+ *   ref_logp[B]    f32 device: log pi_init(y|x) of the same completions (R13).
+ *   pair_rows      [P][2] i32 device (chosen row, rejected row) or NULL => rows (2p, 2p+1)
+ *                  (then B must equal 2P).  Sequences not referenced by a pair get zero
+ *                  gradient.
+ *   P_global >= P  pairs in the whole optimiser step across ranks/micro-batches (R3): the
+ *                  loss is the MEAN over P_global pairs, so no collective is needed before
+ *                  the backward.
+ *   beta > 0, inv_temperature > 0 (finite).
+ *   dlogits        [B,T,V] device out, same dtype as the logits, strides (dstride_b,
+ *                  dstride_t); may EQUAL policy_logits (in place) only with identical
+ *                  strides.  dlogits[b,t,:] = coef_b * mask[b,t] * (softmax - onehot(tok)),
+ *                  coef_c = +beta sigma(-z) invT / P_global, coef_r = -coef_c.
+ *   seq_logp[B]    f32 device out (S_b).
+ *   pair_logit[P]  f32 device out or NULL: z_p = beta((S_c - ref_c) - (S_r - ref_r)).
+ *   stats          [ODPO_NSTATS] f64 device out: local partial sums (overwritten).
+ *   status         u32 device or NULL.
+ *   workspace      >= odpo_workspace_bytes(B, T, P) bytes of device scratch.
+ * Deterministic: every reduction has a fixed order; no float atomics.
+ */
+odpo_status odpo_online_dpo_loss_fwd_bwd(const void* policy_logits, odpo_dtype dt, int64_t B,
+                                         int64_t T, int64_t V, int64_t stride_b, int64_t stride_t,
+                                         const float* ref_logp, const int32_t* tokens,
+                                         const uint8_t* mask, const int32_t* pair_rows, int64_t P,
+                                         int64_t P_global, float beta, float inv_temperature,
+                                         void* dlogits, int64_t dstride_b, int64_t dstride_t,
+                                         float* seq_logp, float* pair_logit, double* stats,
+                                         uint32_t* status, void* workspace, size_t workspace_bytes,
+                                         void* stream);
+
+/* Same as odpo_online_dpo_loss_fwd_bwd with an explicit schedule (opts may be NULL = AUTO);
+   opts->launches returns the number of kernels launched. */
+odpo_status odpo_online_dpo_loss_fwd_bwd_ex(const void* policy_logits, odpo_dtype dt, int64_t B,
+                                            int64_t T, int64_t V, int64_t stride_b,
+                                            int64_t stride_t, const float* ref_logp,
+                                            const int32_t* tokens, const uint8_t* mask,
+                                            const int32_t* pair_rows, int64_t P, int64_t P_global,
+                                            float beta, float inv_temperature, void* dlogits,
+                                            int64_t dstride_b, int64_t dstride_t, float* seq_logp,
+                                            float* pair_logit, double* stats, uint32_t* status,
+                                            void* workspace, size_t workspace_bytes,
+                                            odpo_launch_opts* opts, void* stream);
+
+/* Host-only: device scratch bytes needed by the calls above for B sequences of T tokens
+   and P pairs (about 13 bytes per row + 80 bytes per pair + small). */
+size_t odpo_workspace_bytes(int64_t B, int64_t T, int64_t P);
+
+/* Host-only: static description of a status code. */
+const char* odpo_status_string(odpo_status s);
+
+/* Host-only: library version string. */
+const char* odpo_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ODPO_H */

@@ -1,0 +1,278 @@
+"""paper_2410_18252_b200 -- B200-native Online-DPO learner hot path (arXiv 2410.18252).
+
+Thin Python binding over the C-ABI library ``libodpo.so`` (declared in
+``include/odpo.h``).  This module only marshals arguments: every step of the path
+runs in the library's sm_100a kernels.  PyTorch supplies device memory, the
+current CUDA stream and ``torch.distributed`` process groups.  There is no CPU
+fallback: importing this package without the built library, or calling it with
+CPU tensors, raises.
+
+Calls (Sec 2.1):
+  pair_select(rewards, has_eos, eos_penalty)
+  seq_logprobs(logits, tokens, mask, inv_temperature)
+  online_dpo_loss_fwd_bwd(policy_logits, ref_logp, tokens, mask, beta, ...)
+  allreduce_stats(stats_buffer)   -- the batch-sharded NCCL stats reduction
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import torch
+
+__all__ = ["pair_select", "seq_logprobs", "online_dpo_loss_fwd_bwd", "allreduce_stats",
+           "workspace_bytes", "LossOutput", "SelectOutput", "OdpoError", "lib_path",
+           "STAT_NAMES", "SEL_NAMES", "FLAGS"]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libodpo.so")
+
+STAT_NAMES = ["npairs", "loss", "ncorrect", "z_sum", "rchosen_sum", "rrej_sum",
+              "schosen_sum", "srej_sum", "ntok_chosen", "ntok_rej"]
+SEL_NAMES = ["margin_sum", "ndegen", "ntrunc"]
+NSTATS, NSEL, STATS_BUF = 10, 3, 16
+FLAGS = {"TOKEN_RANGE": 1, "NONFINITE_LOGIT": 2, "EMPTY_SEQ": 4, "NONFINITE_REWARD": 8,
+         "DUP_ROW": 16, "DEGENERATE_PAIR": 32, "PAIR_RANGE": 64}
+SCHEDULES = {"auto": 0, "fused": 1, "two_pass": 2}
+_DT = {torch.float32: 0, torch.bfloat16: 1}
+
+
+class OdpoError(RuntimeError):
+    pass
+
+
+class _Opts(C.Structure):
+    _fields_ = [("schedule", C.c_int32), ("lag_pairs", C.c_int32), ("ctas_per_sm", C.c_int32),
+                ("launches", C.c_int32)]
+
+
+_lib = None
+
+
+def lib_path() -> str:
+    return LIB_PATH
+
+
+def _L():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise OdpoError(f"libodpo.so not built ({LIB_PATH}); run __graft_entry__.build()")
+        L = C.CDLL(LIB_PATH)
+        P, i64, i32, f32, sz = C.c_void_p, C.c_int64, C.c_int32, C.c_float, C.c_size_t
+        L.odpo_pair_select.argtypes = [P, P, f32, i64, i32, P, P, P, P, P, P, P]
+        L.odpo_seq_logprobs.argtypes = [P, C.c_int, i64, i64, i64, i64, i64, P, P, f32, P, P, P, P,
+                                        P, sz, P]
+        L.odpo_online_dpo_loss_fwd_bwd.argtypes = [P, C.c_int, i64, i64, i64, i64, i64, P, P, P, P,
+                                                   i64, i64, f32, f32, P, i64, i64, P, P, P, P, P,
+                                                   sz, P]
+        L.odpo_online_dpo_loss_fwd_bwd_ex.argtypes = (L.odpo_online_dpo_loss_fwd_bwd.argtypes[:-1]
+                                                      + [C.POINTER(_Opts), P])
+        for f in (L.odpo_pair_select, L.odpo_seq_logprobs, L.odpo_online_dpo_loss_fwd_bwd,
+                  L.odpo_online_dpo_loss_fwd_bwd_ex):
+            f.restype = C.c_int
+        L.odpo_workspace_bytes.argtypes = [i64, i64, i64]
+        L.odpo_workspace_bytes.restype = sz
+        L.odpo_status_string.argtypes = [C.c_int]
+        L.odpo_status_string.restype = C.c_char_p
+        L.odpo_version.restype = C.c_char_p
+        _lib = L
+    return _lib
+
+
+def _check(rc: int, what: str):
+    if rc != 0:
+        raise OdpoError(f"{what}: {_L().odpo_status_string(rc).decode()} (code {rc})")
+
+
+def _p(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _dev(t, name, dtype=None):
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise OdpoError(f"{name} must be a CUDA tensor (no CPU fallback)")
+    if dtype is not None and t.dtype != dtype:
+        raise OdpoError(f"{name} must be {dtype}, got {t.dtype}")
+    return t
+
+
+def _stream():
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def workspace_bytes(B: int, T: int, P: int) -> int:
+    return int(_L().odpo_workspace_bytes(B, T, P))
+
+
+_ws_cache: dict = {}
+
+
+def _workspace(device, nbytes: int):
+    key = (device.index if device.index is not None else torch.cuda.current_device())
+    buf = _ws_cache.get(key)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
+        _ws_cache[key] = buf
+    return buf
+
+
+@dataclass
+class SelectOutput:
+    chosen: torch.Tensor
+    rejected: torch.Tensor
+    pair_rows: torch.Tensor
+    reward_margin: torch.Tensor
+    sel_stats: torch.Tensor
+    status: torch.Tensor
+
+
+def pair_select(rewards: torch.Tensor, has_eos: torch.Tensor | None = None, eos_penalty: float = -1.0,
+                status: torch.Tensor | None = None, sel_stats: torch.Tensor | None = None) -> SelectOutput:
+    """Reward-ranked pair selection (EOS penalty PAPER.md:434-435)."""
+    _dev(rewards, "rewards", torch.float32)
+    rewards = rewards.contiguous()
+    P, K = rewards.shape
+    dev = rewards.device
+    if has_eos is not None:
+        has_eos = _dev(has_eos, "has_eos", torch.uint8).contiguous()
+    chosen = torch.empty(P, dtype=torch.int32, device=dev)
+    rejected = torch.empty(P, dtype=torch.int32, device=dev)
+    pair_rows = torch.empty((P, 2), dtype=torch.int32, device=dev)
+    margin = torch.empty(P, dtype=torch.float32, device=dev)
+    if sel_stats is None:
+        sel_stats = torch.zeros(NSEL, dtype=torch.float64, device=dev)
+    if status is None:
+        status = torch.zeros(1, dtype=torch.int32, device=dev)
+    _check(_L().odpo_pair_select(_p(rewards), _p(has_eos), float(eos_penalty), P, K, _p(chosen),
+                                 _p(rejected), _p(pair_rows), _p(margin), _p(sel_stats), _p(status),
+                                 _stream()), "odpo_pair_select")
+    return SelectOutput(chosen, rejected, pair_rows, margin, sel_stats, status)
+
+
+def _logits_meta(x: torch.Tensor, name="logits"):
+    _dev(x, name)
+    if x.dtype not in _DT:
+        raise OdpoError(f"{name} dtype must be float32 or bfloat16")
+    if x.dim() != 3 or x.stride(2) != 1:
+        raise OdpoError(f"{name} must be [B, T, V] with a contiguous last dimension")
+    return _DT[x.dtype], x.shape[0], x.shape[1], x.shape[2], x.stride(0), x.stride(1)
+
+
+def seq_logprobs(logits: torch.Tensor, tokens: torch.Tensor, mask: torch.Tensor,
+                 inv_temperature: float = 1.0, per_token: bool = False,
+                 status: torch.Tensor | None = None):
+    """log pi(y|x) per sequence.  Returns seq_logp[B] (and tok_logp, row_lse
+    [B, T] when per_token=True)."""
+    dt, B, T, V, sb, st = _logits_meta(logits)
+    tokens = _dev(tokens, "tokens", torch.int32).contiguous()
+    mask = _dev(mask, "mask", torch.uint8).contiguous()
+    dev = logits.device
+    seq = torch.empty(B, dtype=torch.float32, device=dev)
+    tok = lse = None
+    if per_token:
+        tok = torch.empty((B, T), dtype=torch.float32, device=dev)
+        lse = torch.empty((B, T), dtype=torch.float32, device=dev)
+    if status is None:
+        status = torch.zeros(1, dtype=torch.int32, device=dev)
+    nb = workspace_bytes(B, T, B // 2 + 1)
+    ws = _workspace(dev, nb)
+    _check(_L().odpo_seq_logprobs(_p(logits), dt, B, T, V, sb, st, _p(tokens), _p(mask),
+                                  float(inv_temperature), _p(seq), _p(tok), _p(lse), _p(status),
+                                  _p(ws), ws.numel(), _stream()), "odpo_seq_logprobs")
+    if per_token:
+        return seq, tok, lse, status
+    return seq
+
+
+@dataclass
+class LossOutput:
+    stats: torch.Tensor       # fp64 [16]: loss stats [0,10), selection stats [10,13)
+    dlogits: torch.Tensor
+    seq_logp: torch.Tensor
+    z: torch.Tensor
+    status: torch.Tensor
+    launches: int
+
+    def named(self) -> dict:
+        s = self.stats.tolist()
+        return {k: s[i] for i, k in enumerate(STAT_NAMES)}
+
+
+def online_dpo_loss_fwd_bwd(policy_logits: torch.Tensor, ref_logp: torch.Tensor,
+                            tokens: torch.Tensor, mask: torch.Tensor, beta: float,
+                            pair_rows: torch.Tensor | None = None, p_global: int | None = None,
+                            inv_temperature: float = 1.0, inplace: bool = False,
+                            dlogits: torch.Tensor | None = None, schedule: str = "auto",
+                            lag_pairs: int = 0, ctas_per_sm: int = 0,
+                            stats: torch.Tensor | None = None,
+                            status: torch.Tensor | None = None) -> LossOutput:
+    """Online DPO loss, statistics and dlogits in one call.
+
+    stats: optional fp64 buffer of >= 10 doubles (the recommended 16-double buffer whose
+    [10,13) holds pair_select's sel_stats); loss stats are written to stats[0:10]."""
+    dt, B, T, V, sb, st = _logits_meta(policy_logits, "policy_logits")
+    ref_logp = _dev(ref_logp, "ref_logp", torch.float32).contiguous()
+    tokens = _dev(tokens, "tokens", torch.int32).contiguous()
+    mask = _dev(mask, "mask", torch.uint8).contiguous()
+    dev = policy_logits.device
+    if pair_rows is not None:
+        pair_rows = _dev(pair_rows, "pair_rows", torch.int32).contiguous()
+        P = pair_rows.shape[0]
+    else:
+        P = B // 2
+    Pg = P if p_global is None else int(p_global)
+    if inplace:
+        dl = policy_logits
+    elif dlogits is not None:
+        dl = _dev(dlogits, "dlogits", policy_logits.dtype)
+    else:
+        dl = torch.empty_like(policy_logits)
+    if dl.dim() != 3 or dl.stride(2) != 1:
+        raise OdpoError("dlogits must be [B, T, V] with a contiguous last dimension")
+    seq = torch.empty(B, dtype=torch.float32, device=dev)
+    z = torch.empty(max(P, 1), dtype=torch.float32, device=dev)
+    if stats is None:
+        stats = torch.zeros(STATS_BUF, dtype=torch.float64, device=dev)
+    if status is None:
+        status = torch.zeros(1, dtype=torch.int32, device=dev)
+    nb = workspace_bytes(B, T, max(P, 1))
+    ws = _workspace(dev, nb)
+    opts = _Opts(SCHEDULES[schedule], int(lag_pairs), int(ctas_per_sm), 0)
+    _check(_L().odpo_online_dpo_loss_fwd_bwd_ex(
+        _p(policy_logits), dt, B, T, V, sb, st, _p(ref_logp), _p(tokens), _p(mask), _p(pair_rows),
+        P, Pg, float(beta), float(inv_temperature), _p(dl), dl.stride(0), dl.stride(1), _p(seq),
+        _p(z), _p(stats), _p(status), _p(ws), ws.numel(), C.byref(opts), _stream()),
+        "odpo_online_dpo_loss_fwd_bwd")
+    return LossOutput(stats, dl, seq, z[:P], status, int(opts.launches))
+
+
+def allreduce_stats(stats: torch.Tensor, group=None) -> torch.Tensor:
+    """SUM all-reduce of the fp64 statistics buffer across data-parallel ranks (NCCL over
+    NVLink/NVSwitch on GPU process groups; gloo for CPU tests).  One 128-byte message:
+    the loss is already divided by the static P_global, so the summed buffer holds the
+    global loss, accuracy numerator and margins."""
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(stats, op=dist.ReduceOp.SUM, group=group)
+    return stats
+
+
+def summarize(stats: torch.Tensor) -> dict:
+    """Global means from a (reduced) 16-double stats buffer."""
+    s = stats.double().cpu().tolist()
+    n = max(s[0], 1.0)
+    return {
+        "loss": s[1],
+        "accuracy": s[2] / n,
+        "implicit_margin": s[3] / n,
+        "chosen_reward": s[4] / n,
+        "rejected_reward": s[5] / n,
+        "chosen_logp": s[6] / n,
+        "rejected_logp": s[7] / n,
+        "reward_margin": s[10] / n,
+        "npairs": s[0],
+        "ndegenerate": s[11],
+        "ntruncated": s[12],
+    }

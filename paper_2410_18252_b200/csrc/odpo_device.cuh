@@ -1,0 +1,392 @@
+// odpo_device.cuh -- device building blocks of the Online-DPO hot path (sm_100a).
+//
+// Row forward  (K2): single-read online log-sum-exp over V in "log1p form"
+//                    (track r = sum_{v != argmax} exp(invT (x_v - m)), so 1 + r is never
+//                    formed by adding tiny terms to 1), plus the sampled-token gather.
+//                    PAPER.md:83 (log pi(y|x)); numerics: DESIGN.md section 5.
+// Row backward (K4): dlogits = coef * (softmax - onehot), onehot entry via expm1(logp).
+// Sequence sum (K3a): fixed-order masked sum over t (double accumulation).
+//
+// No library kernels; 128-bit vector loads/stores with explicit L2 cache policies.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace odpo {
+
+constexpr int kRowThreads = 512;   // threads per row-CTA (all row kernels; fixes the reduction tree)
+constexpr int kU = 8;              // 16-byte vectors in flight per thread per batch
+constexpr int kWarps = kRowThreads / 32;
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr unsigned kFull = 0xffffffffu;
+
+// ------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float fmax_nan(float a, float b) {
+  float d;
+  asm("max.NaN.f32 %0, %1, %2;" : "=f"(d) : "f"(a), "f"(b));
+  return d;
+}
+__device__ __forceinline__ uint32_t bmax2_nan(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("max.NaN.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+__device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf_hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
+
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+// Load kinds for the logits stream.
+enum { LD_STREAM = 0, LD_HINT = 1 };
+
+template <int LK>
+__device__ __forceinline__ uint4 ld16(const uint4* p, uint64_t pol) {
+  uint4 v;
+  if (LK == LD_HINT) {
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p), "l"(pol));
+  } else {
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p));
+  }
+  return v;
+}
+
+__device__ __forceinline__ void st16_stream(uint4* p, uint4 v) {
+  asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
+}
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// ------------------------------------------------------------------ dtype traits
+// DT 0 = f32 (4 per 16 B), DT 1 = bf16 (8 per 16 B)
+template <int DT>
+struct Traits;
+
+template <>
+struct Traits<0> {
+  static constexpr int N = 4;
+  static constexpr uint32_t kNegInfWord = 0xFF800000u;
+  __device__ static __forceinline__ float vmax(const uint4& v) {
+    return fmax_nan(fmax_nan(__uint_as_float(v.x), __uint_as_float(v.y)),
+                    fmax_nan(__uint_as_float(v.z), __uint_as_float(v.w)));
+  }
+  __device__ static __forceinline__ void unpack(const uint4& v, float* f) {
+    f[0] = __uint_as_float(v.x);
+    f[1] = __uint_as_float(v.y);
+    f[2] = __uint_as_float(v.z);
+    f[3] = __uint_as_float(v.w);
+  }
+  __device__ static __forceinline__ uint4 pack(const float* g) {
+    return make_uint4(__float_as_uint(g[0]), __float_as_uint(g[1]), __float_as_uint(g[2]),
+                      __float_as_uint(g[3]));
+  }
+  __device__ static __forceinline__ float load1(const void* row, int64_t v) {
+    return __ldg(reinterpret_cast<const float*>(row) + v);
+  }
+  __device__ static __forceinline__ void store1(void* row, int64_t v, float g) {
+    reinterpret_cast<float*>(row)[v] = g;
+  }
+};
+
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+  uint32_t d;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(hi), "f"(lo));
+  return d;
+}
+
+template <>
+struct Traits<1> {
+  static constexpr int N = 8;
+  static constexpr uint32_t kNegInfWord = 0xFF80FF80u;
+  // packed max over the 16-byte vector, NaN-propagating; returns a bf16x2 word
+  __device__ static __forceinline__ uint32_t vmax2(const uint4& v) {
+    return bmax2_nan(bmax2_nan(v.x, v.y), bmax2_nan(v.z, v.w));
+  }
+  __device__ static __forceinline__ float vmax(const uint4& v) {
+    uint32_t w = vmax2(v);
+    return fmax_nan(bf_lo(w), bf_hi(w));
+  }
+  __device__ static __forceinline__ void unpack(const uint4& v, float* f) {
+    f[0] = bf_lo(v.x); f[1] = bf_hi(v.x);
+    f[2] = bf_lo(v.y); f[3] = bf_hi(v.y);
+    f[4] = bf_lo(v.z); f[5] = bf_hi(v.z);
+    f[6] = bf_lo(v.w); f[7] = bf_hi(v.w);
+  }
+  __device__ static __forceinline__ uint4 pack(const float* g) {
+    return make_uint4(pack_bf16x2(g[0], g[1]), pack_bf16x2(g[2], g[3]), pack_bf16x2(g[4], g[5]),
+                      pack_bf16x2(g[6], g[7]));
+  }
+  __device__ static __forceinline__ float load1(const void* row, int64_t v) {
+    uint16_t b = __ldg(reinterpret_cast<const unsigned short*>(row) + v);
+    return __uint_as_float(static_cast<uint32_t>(b) << 16);
+  }
+  __device__ static __forceinline__ void store1(void* row, int64_t v, float g) {
+    uint32_t w = pack_bf16x2(g, 0.f);
+    reinterpret_cast<unsigned short*>(row)[v] = static_cast<unsigned short>(w & 0xFFFFu);
+  }
+};
+
+// batch max over U vectors (NaN-propagating)
+template <int DT>
+__device__ __forceinline__ float batch_max(const uint4* v) {
+  if constexpr (DT == 1) {
+    uint32_t w = Traits<1>::vmax2(v[0]);
+#pragma unroll
+    for (int u = 1; u < kU; ++u) w = bmax2_nan(w, Traits<1>::vmax2(v[u]));
+    return fmax_nan(bf_lo(w), bf_hi(w));
+  } else {
+    float m = Traits<0>::vmax(v[0]);
+#pragma unroll
+    for (int u = 1; u < kU; ++u) m = fmax_nan(m, Traits<0>::vmax(v[u]));
+    return m;
+  }
+}
+
+// ------------------------------------------------------------------ (m, r) state
+// 1 + r = sum_v exp(invT (x_v - m)) where m = max_v x_v (raw units); exp2 with k2 = invT*log2e.
+struct MR {
+  float m, r;
+};
+
+__device__ __forceinline__ MR mr_merge(MR a, MR b, float k2) {
+  MR big = a, sm = b;
+  if (b.m > a.m) { big = b; sm = a; }
+  if (sm.m == -INFINITY) return big;
+  big.r = big.r + (1.f + sm.r) * ex2((sm.m - big.m) * k2);
+  return big;
+}
+
+// Per-thread online pass over this thread's vectors of one row.
+// Vectors i = tid, tid + NT, ... (coalesced across the CTA), kU of them per batch.
+template <int DT, int LK>
+__device__ __forceinline__ MR row_fwd_thread(const uint4* __restrict__ vrow, int nvec, float k2,
+                                             uint64_t pol) {
+  constexpr int N = Traits<DT>::N;
+  const uint32_t NI = Traits<DT>::kNegInfWord;
+  float m = -INFINITY, r = 0.f;
+  for (int base = threadIdx.x; base < nvec; base += kRowThreads * kU) {
+    uint4 v[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int i = base + u * kRowThreads;
+      v[u] = (i < nvec) ? ld16<LK>(vrow + i, pol) : make_uint4(NI, NI, NI, NI);
+    }
+    const float mc = batch_max<DT>(v);
+    if (!(mc <= m)) {
+      // new running max (or NaN): demote the old max into r, then add this batch
+      // excluding exactly ONE element equal to the new max (it is the "1" of 1 + r).
+      const float sc = (m == -INFINITY) ? 0.f : ex2((m - mc) * k2);
+      r = (1.f + r) * sc;
+      m = mc;
+      const float mk = m * k2;
+      float s = 0.f;
+      int neq = 0;
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        float f[N];
+        Traits<DT>::unpack(v[u], f);
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+          if (f[j] == m) ++neq;
+          else s += ex2(fmaf(f[j], k2, -mk));
+        }
+      }
+      r += s + (float)(neq - 1);
+    } else {
+      const float mk = m * k2;
+      float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        float f[N];
+        Traits<DT>::unpack(v[u], f);
+#pragma unroll
+        for (int j = 0; j < N; j += 2) {
+          s0 += ex2(fmaf(f[j], k2, -mk));
+          s1 += ex2(fmaf(f[j + 1], k2, -mk));
+        }
+      }
+      r += s0 + s1;
+    }
+  }
+  return MR{m, r};
+}
+
+// scalar tail element (V not a multiple of the vector width): same update rules
+__device__ __forceinline__ MR mr_push1(MR s, float y, float k2) {
+  if (!(y <= s.m)) {
+    const float sc = (s.m == -INFINITY) ? 0.f : ex2((s.m - y) * k2);
+    s.r = (1.f + s.r) * sc;
+    s.m = y;
+  } else {
+    s.r += ex2(fmaf(y, k2, -(s.m * k2)));
+  }
+  return s;
+}
+
+// Fixed-order CTA merge; result valid in thread 0.  smem: 2*kWarps floats.
+__device__ __forceinline__ MR block_merge(MR v, float k2, float* sm) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    MR o;
+    o.m = __shfl_down_sync(kFull, v.m, off);
+    o.r = __shfl_down_sync(kFull, v.r, off);
+    v = mr_merge(v, o, k2);
+  }
+  if (lane == 0) {
+    sm[warp] = v.m;
+    sm[kWarps + warp] = v.r;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    v.m = lane < kWarps ? sm[lane] : -INFINITY;
+    v.r = lane < kWarps ? sm[kWarps + lane] : 0.f;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      MR o;
+      o.m = __shfl_down_sync(kFull, v.m, off);
+      o.r = __shfl_down_sync(kFull, v.r, off);
+      v = mr_merge(v, o, k2);
+    }
+  }
+  return v;
+}
+
+struct RowOut {
+  float m, l1p, logp, lse;
+  uint32_t flags;
+};
+
+// Whole-CTA row forward; result valid in thread 0 (others get garbage).
+// row: element pointer of logits[b, t, 0]; V elements; tok: sampled token.
+template <int DT, int LK>
+__device__ __forceinline__ RowOut row_forward(const void* row, int V, int tok, float invT,
+                                              uint64_t pol, float* sm) {
+  constexpr int N = Traits<DT>::N;
+  const float k2 = invT * kLog2e;
+  const int nvec = V / N;
+  MR s = row_fwd_thread<DT, LK>(reinterpret_cast<const uint4*>(row), nvec, k2, pol);
+  const int tail = V - nvec * N;
+  if ((int)threadIdx.x < tail) s = mr_push1(s, Traits<DT>::load1(row, (int64_t)nvec * N + threadIdx.x), k2);
+  s = block_merge(s, k2, sm);
+  RowOut o;
+  o.flags = 0;
+  o.m = s.m;
+  o.l1p = log1pf(s.r);
+  o.lse = __fadd_rn(__fmul_rn(s.m, invT), o.l1p);
+  if (threadIdx.x == 0) {
+    if (tok < 0 || tok >= V) {
+      o.flags |= ODPO_FLAG_TOKEN_RANGE;
+      o.logp = 0.f;
+    } else {
+      const float xt = Traits<DT>::load1(row, tok);
+      o.logp = __fsub_rn(__fmul_rn(__fsub_rn(xt, s.m), invT), o.l1p);
+      if (!isfinite(o.logp)) o.flags |= ODPO_FLAG_NONFINITE_LOGIT;
+    }
+    if (!isfinite(s.m) || !isfinite(s.r)) o.flags |= ODPO_FLAG_NONFINITE_LOGIT;
+  }
+  return o;
+}
+
+// Whole-CTA row backward: drow[v] = coef * (exp(invT (x_v - m) - l1p) - [v == tok]).
+// tok entry written as coef * expm1(logp) (no p - 1 cancellation).
+template <int DT, int LK>
+__device__ __forceinline__ void row_backward(const void* row, void* drow, int V, int tok,
+                                             float invT, float m, float l1p, float logp,
+                                             float coef, uint64_t pol) {
+  constexpr int N = Traits<DT>::N;
+  const float k2 = invT * kLog2e;
+  const float c = fmaf(l1p, kLog2e, m * k2);
+  const int nvec = V / N;
+  const uint4* vrow = reinterpret_cast<const uint4*>(row);
+  uint4* vout = reinterpret_cast<uint4*>(drow);
+  for (int base = threadIdx.x; base < nvec; base += kRowThreads * kU) {
+    uint4 v[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int i = base + u * kRowThreads;
+      if (i < nvec) v[u] = ld16<LK>(vrow + i, pol);
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int i = base + u * kRowThreads;
+      if (i < nvec) {
+        float f[N];
+        Traits<DT>::unpack(v[u], f);
+#pragma unroll
+        for (int j = 0; j < N; ++j) f[j] = coef * ex2(fmaf(f[j], k2, -c));
+        st16_stream(vout + i, Traits<DT>::pack(f));
+      }
+    }
+  }
+  const int tail = V - nvec * N;
+  if ((int)threadIdx.x < tail) {
+    const int64_t v = (int64_t)nvec * N + threadIdx.x;
+    const float x = Traits<DT>::load1(row, v);
+    Traits<DT>::store1(drow, v, (v == tok) ? coef * expm1f(logp) : coef * ex2(fmaf(x, k2, -c)));
+  }
+  // onehot entry: written by the thread that stored tok's vector (program order)
+  if (tok >= 0 && tok < nvec * N && (tok / N) % kRowThreads == (int)threadIdx.x)
+    Traits<DT>::store1(drow, tok, coef * expm1f(logp));
+}
+
+template <int DT>
+__device__ __forceinline__ void row_zero(void* drow, int V) {
+  constexpr int N = Traits<DT>::N;
+  const int nvec = V / N;
+  uint4* vout = reinterpret_cast<uint4*>(drow);
+  for (int i = threadIdx.x; i < nvec; i += kRowThreads) st16_stream(vout + i, make_uint4(0, 0, 0, 0));
+  const int tail = V - nvec * N;
+  if ((int)threadIdx.x < tail) Traits<DT>::store1(drow, (int64_t)nvec * N + threadIdx.x, 0.f);
+}
+
+// Fixed-order masked sum of one sequence's per-token log-probs, by ONE warp.
+// lane l sums t = l, l+32, ... in order (double), then a shfl_down tree.  Valid in lane 0.
+__device__ __forceinline__ void seq_sum_warp(const float* row_logp, const uint8_t* mask, int64_t T,
+                                             double& S, int& n) {
+  const int lane = threadIdx.x & 31;
+  double s = 0.0;
+  int c = 0;
+  for (int64_t t = lane; t < T; t += 32) {
+    if (__ldcg(mask + t)) {
+      s += (double)__ldcg(row_logp + t);
+      ++c;
+    }
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    s += __shfl_down_sync(kFull, s, off);
+    c += __shfl_down_sync(kFull, c, off);
+  }
+  S = s;
+  n = c;
+}
+
+}  // namespace odpo

@@ -129,3 +129,57 @@ def permutation(seed: int, n: int, stream: int = S_PERM) -> np.ndarray:
     """A seeded permutation of range(n) (sort by hash)."""
     h = hash_u64(seed, stream, np.arange(n))
     return np.argsort(h, kind="stable").astype(np.int32)
+
+
+# ----------------------------------------------------------------------------- device twin
+import ctypes as _C
+import os as _os
+import subprocess as _sp
+
+_HERE = _os.path.dirname(_os.path.abspath(__file__))
+SYNTH_LIB = _os.path.join(_HERE, "libsynth.so")
+_slib = None
+
+
+def build_device(force: bool = False) -> str:
+    src = _os.path.join(_HERE, "synth.cu")
+    if force or not _os.path.exists(SYNTH_LIB) or _os.path.getmtime(SYNTH_LIB) < _os.path.getmtime(src):
+        _sp.check_call(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17",
+                        "-Xcompiler", "-fPIC", "-shared", "-o", SYNTH_LIB, src])
+    return SYNTH_LIB
+
+
+def _dev_lib():
+    global _slib
+    if _slib is None:
+        if not _os.path.exists(SYNTH_LIB):
+            build_device()
+        L = _C.CDLL(SYNTH_LIB)
+        L.synth_fill_logits.argtypes = [_C.c_void_p, _C.c_int, _C.c_int64, _C.c_int64, _C.c_int64,
+                                        _C.c_int64, _C.c_int64, _C.c_uint64, _C.c_int, _C.c_int64,
+                                        _C.c_void_p, _C.c_float, _C.c_int, _C.c_void_p]
+        L.synth_fill_logits.restype = _C.c_int
+        L.synth_stream_key.argtypes = [_C.c_uint64, _C.c_int]
+        L.synth_stream_key.restype = _C.c_uint64
+        _slib = L
+    return _slib
+
+
+def fill_logits_device(x, seed: int, row0: int = 0, tokens=None, peak: float | None = 14.0,
+                       ref: bool = False) -> None:
+    """Fill a CUDA tensor x[B, T, V] (f32 or bf16, last dim contiguous) with the same values
+    logits_rows() produces for global rows row0 + b*T + t.  tokens: CUDA int32 [B, T] or None."""
+    import torch
+    assert x.is_cuda and x.dim() == 3 and x.stride(2) == 1
+    dt = {torch.float32: 0, torch.bfloat16: 1}[x.dtype]
+    B, T, V = x.shape
+    tk = None
+    if tokens is not None and peak is not None:
+        assert tokens.is_cuda and tokens.dtype == torch.int32 and tokens.is_contiguous()
+        tk = tokens.data_ptr()
+    rc = _dev_lib().synth_fill_logits(
+        x.data_ptr(), dt, B, T, V, x.stride(0), x.stride(1), seed,
+        S_LOGITS_REF if ref else S_LOGITS, row0, tk, float(peak if peak is not None else 0.0),
+        1 if tk is not None else 0, torch.cuda.current_stream().cuda_stream)
+    if rc:
+        raise RuntimeError(f"synth_fill_logits failed ({rc})")

@@ -1,0 +1,112 @@
+"""Shared builders for the GPU parity tests: seeded synthetic inputs drawn once from
+``synth`` and handed to BOTH the CUDA path (device tensors) and the CPU oracle (host
+arrays).  Tolerances follow SURVEY.md §8(c) / DESIGN.md section 7."""
+from __future__ import annotations
+
+import os
+
+import numpy as np
+import torch
+
+import oracle
+import synth
+
+NCPU = os.cpu_count() or 1
+
+TOL_SEQ = {"f32": 1e-5, "bf16": 2e-3}            # north_star: 1e-5 fp32, 2e-3 bf16 (relative)
+DL_RTOL = {"f32": 1e-5, "bf16": 2.0 ** -8}
+DL_ATOL = {"f32": 1e-7, "bf16": 2.0 ** -20}      # times |coef_b|
+TORCH_DT = {"f32": torch.float32, "bf16": torch.bfloat16}
+
+
+def alloc_rows(B, T, V, dtype, device="cuda"):
+    """[B, T, V] view whose row stride is padded to a multiple of 16 bytes (the C ABI's
+    128-bit alignment contract; V itself may be ragged)."""
+    es = 4 if dtype == "f32" else 2
+    vp = -(-V * es // 16) * 16 // es
+    return torch.empty((B, T, vp), dtype=TORCH_DT[dtype], device=device)[:, :, :V]
+
+
+class Batch:
+    """One synthetic Online-DPO batch: P pairs, rows (2p, 2p+1) unless perm is given."""
+
+    def __init__(self, P, T, V, dtype="bf16", seed=0, mask_kind="dense", lbar=None, peak=14.0,
+                 p0=0, extra_seqs=0, permute=False, device="cuda", host=True, invT=1.0):
+        self.P, self.T, self.V, self.dtype, self.seed = P, T, V, dtype, seed
+        self.B = 2 * P + extra_seqs
+        self.invT = invT
+        B = self.B
+        seqs = np.arange(B) + 2 * p0
+        rows = (seqs[:, None] * T + np.arange(T)[None, :]).reshape(-1)
+        self.rows_global = rows
+        self.tokens = synth.tokens_rows(seed, rows, V).reshape(B, T)
+        self.mask = synth.mask_for(seed, seqs, T, mask_kind, lbar)
+        self.peak = peak
+        if permute or extra_seqs:
+            perm = synth.permutation(seed, B)
+            self.pair_rows = perm[: 2 * P].reshape(P, 2).astype(np.int32)
+        else:
+            self.pair_rows = None
+        dev = torch.device(device)
+        self.d_tokens = torch.from_numpy(self.tokens).to(dev)
+        self.d_mask = torch.from_numpy(self.mask).to(dev)
+        self.d_pair_rows = None if self.pair_rows is None else torch.from_numpy(self.pair_rows).to(dev)
+        self.d_logits = alloc_rows(B, T, V, dtype, dev)
+        synth.fill_logits_device(self.d_logits, seed, row0=int(rows[0]), tokens=self.d_tokens,
+                                 peak=peak)
+        self.h_logits = None
+        if host:
+            self.h_logits = self.host_rows(np.arange(B))
+
+    def new_out(self):
+        """An output buffer with the same (16-byte aligned, padded) row layout."""
+        return alloc_rows(self.B, self.T, self.V, self.dtype, self.d_logits.device)
+
+    def host_rows(self, seqs):
+        """Host logits [len(seqs), T, V] in the oracle's input encoding (f32 or bf16 bits).
+        Rows with mask 0 are never read by either side and are left at zero."""
+        seqs = np.asarray(seqs)
+        rows = (seqs[:, None] * self.T + np.arange(self.T)[None, :]).reshape(-1)
+        live = self.mask.reshape(-1)[rows] == 1
+        x = np.zeros((rows.size, self.V))
+        x[live] = synth.logits_rows(self.seed, self.rows_global[rows[live]], self.V,
+                                    tokens=self.tokens.reshape(-1)[rows[live]], peak=self.peak)
+        x = x.reshape(len(seqs), self.T, self.V)
+        if self.dtype == "f32":
+            return x.astype(np.float32)
+        return oracle.to_bf16_bits(x.astype(np.float32))
+
+
+def check_seq(gpu, orc, dtype, what="seq_logp"):
+    gpu = np.asarray(gpu, dtype=np.float64)
+    tol = TOL_SEQ[dtype]
+    err = np.abs(gpu - orc)
+    bound = tol * np.maximum(np.abs(orc), 1.0)
+    assert np.all(err <= bound), f"{what}: max rel err {np.max(err / np.maximum(np.abs(orc), 1.0)):.3e}"
+    return float(np.max(err / np.maximum(np.abs(orc), 1.0))) if err.size else 0.0
+
+
+def check_dlogits(g_gpu, g_orc, coef_abs, dtype):
+    """|g_gpu - g_orc| <= rtol |g_orc| + atol |coef_b| per element (coef_abs broadcast per row)."""
+    g_gpu = np.asarray(g_gpu, dtype=np.float64)
+    err = np.abs(g_gpu - g_orc)
+    bound = DL_RTOL[dtype] * np.abs(g_orc) + DL_ATOL[dtype] * coef_abs
+    bad = err > bound
+    assert not np.any(bad), (
+        f"dlogits: {np.count_nonzero(bad)} elements out of tolerance; "
+        f"worst excess {np.max(err - bound):.3e}")
+
+
+def to_f64(t: torch.Tensor) -> np.ndarray:
+    return t.detach().float().cpu().double().numpy()
+
+
+def coef_from_oracle(o, P, Pg, beta, invT, pair_rows, B):
+    """|coef_b| per sequence from the oracle's z (for the dlogits absolute tolerance)."""
+    coef = np.zeros(B)
+    beta = float(np.float32(beta))
+    for p in range(P):
+        c, r = (2 * p, 2 * p + 1) if pair_rows is None else pair_rows[p]
+        sig = 1.0 / (1.0 + np.exp(o["z"][p]))
+        coef[c] = coef[r] = beta * sig * float(np.float32(invT)) / Pg
+    return coef

@@ -1,0 +1,117 @@
+"""C-ABI boundary checks that need no GPU: libodpo.so loads, exports every symbol that
+include/odpo.h declares, and rejects bad arguments synchronously (before any launch)."""
+import ctypes as C
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "odpo.h")
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2410_18252_b200 import build
+    build.build()
+    import paper_2410_18252_b200 as odpo
+    return odpo._L()
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(odpo_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_header_declares_the_three_paper_calls():
+    fns = declared_functions()
+    for f in ("odpo_pair_select", "odpo_seq_logprobs", "odpo_online_dpo_loss_fwd_bwd",
+              "odpo_workspace_bytes", "odpo_status_string"):
+        assert f in fns
+
+
+def test_library_exports_every_declared_symbol(lib):
+    so = os.path.join(ROOT, "paper_2410_18252_b200", "libodpo.so")
+    out = subprocess.run(["nm", "-D", "--defined-only", so], capture_output=True, text=True).stdout
+    exported = set(re.findall(r"\bT (odpo_\w+)", out))
+    for f in declared_functions():
+        assert f in exported, f
+        assert hasattr(lib, f)
+
+
+def test_header_compiles_as_c():
+    r = subprocess.run(["gcc", "-std=c99", "-Wall", "-Werror", "-fsyntax-only", "-x", "c", HEADER],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+
+
+def test_status_strings_and_version(lib):
+    for code in range(6):
+        assert lib.odpo_status_string(code)
+    assert b"sm_100a" in lib.odpo_version()
+
+
+def test_workspace_bytes(lib):
+    n = lib.odpo_workspace_bytes(512, 53, 256)
+    rows = 512 * 53
+    assert 12 * rows <= n <= 12 * rows + 512 * 12 + 256 * 100 + 16 * 256
+    assert lib.odpo_workspace_bytes(0, 5, 1) == 0
+
+
+FAKE = C.c_void_p(0x7000_0000_0000)  # never dereferenced: validation returns first
+FAKE_MIS = C.c_void_p(0x7000_0000_0008)
+
+
+def _loss(lib, **kw):
+    a = dict(logits=FAKE, dt=1, B=4, T=3, V=64, sb=192, st=64, ref=FAKE, tok=FAKE, mask=FAKE,
+             pr=None, P=2, Pg=2, beta=0.1, invT=1.0, dl=FAKE, dsb=192, dst=64, seq=FAKE, z=None,
+             stats=FAKE, status=None, ws=FAKE, wsb=1 << 20)
+    a.update(kw)
+    return lib.odpo_online_dpo_loss_fwd_bwd(a["logits"], a["dt"], a["B"], a["T"], a["V"], a["sb"],
+                                            a["st"], a["ref"], a["tok"], a["mask"], a["pr"], a["P"],
+                                            a["Pg"], a["beta"], a["invT"], a["dl"], a["dsb"],
+                                            a["dst"], a["seq"], a["z"], a["stats"], a["status"],
+                                            a["ws"], a["wsb"], None)
+
+
+def test_argument_errors_are_synchronous(lib):
+    assert _loss(lib, beta=0.0) == 1
+    assert _loss(lib, beta=float("nan")) == 1
+    assert _loss(lib, invT=-1.0) == 1
+    assert _loss(lib, Pg=1) == 1
+    assert _loss(lib, P=3) == 1            # pair_rows NULL requires B == 2P
+    assert _loss(lib, st=63, sb=189) == 1  # stride_t < V
+    assert _loss(lib, logits=None) == 1
+    assert _loss(lib, dl=None) == 1
+    assert _loss(lib, dt=7) == 1
+    assert _loss(lib, logits=FAKE_MIS) == 2
+    assert _loss(lib, st=68, sb=204) == 2  # 136-byte bf16 row stride: not 16-byte aligned
+    assert _loss(lib, dl=FAKE_MIS) == 2
+    assert _loss(lib, wsb=16) == 3
+    assert _loss(lib, ws=None) == 3
+    assert _loss(lib, dl=FAKE, dsb=96, dst=32) == 1   # dlogits rows overlap
+    # in place requires identical strides
+    assert _loss(lib, dl=FAKE, logits=FAKE, dsb=256, dst=64) == 1
+    assert lib.odpo_pair_select(FAKE, None, -1.0, 4, 1, FAKE, FAKE, None, None, None, None, None) == 1
+    assert lib.odpo_pair_select(None, None, -1.0, 4, 2, FAKE, FAKE, None, None, None, None, None) == 1
+    assert lib.odpo_seq_logprobs(FAKE, 1, 4, 3, 64, 192, 64, FAKE, FAKE, 0.0, FAKE, None, None,
+                                 None, FAKE, 1 << 20, None) == 1
+    assert lib.odpo_seq_logprobs(FAKE, 1, 4, 3, 64, 192, 64, FAKE, FAKE, 1.0, FAKE, None, None,
+                                 None, FAKE, 8, None) == 3
+
+
+def test_product_has_no_oracle_or_cpu_fallback():
+    """The product package never imports the oracle and refuses CPU tensors."""
+    pkg = os.path.join(ROOT, "paper_2410_18252_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h")):
+                text = open(os.path.join(dirpath, f)).read()
+                assert "import oracle" not in text and "liboracle" not in text, f
+                assert "orc_" not in text, f
+    import torch
+    import paper_2410_18252_b200 as odpo
+    with pytest.raises(odpo.OdpoError):
+        odpo.pair_select(torch.zeros(3, 2))
