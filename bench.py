@@ -38,11 +38,14 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="pythia", choices=["tiny", "pythia", "rho", "llama"])
+    ap.add_argument("--config", default="pythia", choices=["tiny", "pythia", "rho", "llama", "strong"])
+    ap.add_argument("--chunk-pairs", type=int, default=64)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--schedule", default="auto", choices=["auto", "fused", "two_pass"])
     ap.add_argument("--lag", type=int, default=0)
     ap.add_argument("--ctas-per-sm", type=int, default=0)
+    ap.add_argument("--exp2-split", type=int, default=-1)
+    ap.add_argument("--lookahead", type=int, default=-1)
     ap.add_argument("--mask", default="dense", choices=["dense", "prefix"])
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
@@ -227,7 +230,8 @@ def run_ours(args, rank, world, local_rank):
         out = odpo.online_dpo_loss_fwd_bwd(logits, ref_logp, tokens, mask, w.beta,
                                            pair_rows=sel.pair_rows, p_global=Pg, dlogits=dlogits,
                                            schedule=args.schedule, lag_pairs=args.lag,
-                                           ctas_per_sm=args.ctas_per_sm, stats=stats, status=status)
+                                           ctas_per_sm=args.ctas_per_sm, exp2_split=args.exp2_split,
+                                           lookahead=args.lookahead, stats=stats, status=status)
         if timed_loss is not None:
             timed_loss[1].record()
         odpo.allreduce_stats(stats)
@@ -349,7 +353,8 @@ def run_ours(args, rank, world, local_rank):
             "config": {"workload": args.config, "pairs_per_rank": P, "global_pairs": P * world,
                        "K": 2, "T": T, "V": V, "beta": w.beta, "mask": args.mask,
                        "ref_logp": "seq_logprobs over independent reference logits (setup)",
-                       "schedule": args.schedule, "parallelism": f"dp{world}",
+                       "schedule": args.schedule, "exp2_split": args.exp2_split,
+                       "parallelism": f"dp{world}",
                        "l2": "inputs (%.2f GB) > L2; plus 256 MiB L2 flush between timed steps"
                              % (B * T * V * s_in / 1e9)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -372,6 +377,117 @@ def run_ours(args, rank, world, local_rank):
         print(json.dumps(line), flush=True)
 
 
+
+# ----------------------------------------------------------------------------- strong scaling
+def run_strong(args, rank, world, local_rank):
+    """BASELINE.json configs[4]: 2048 pairs, T=1024, V=128256, bf16, batch-sharded over the
+    ranks (strong scaling: total work fixed).  Each rank owns a contiguous block of pairs and
+    processes it in LLaMA-shaped chunks of --chunk-pairs pairs with in-place dlogits (the
+    1.08 TB of logits never fit at once); chunk logits are regenerated on the device OUTSIDE
+    the timed region.  Per step the timed region is, per chunk, pair_select + the fused
+    loss fwd+bwd, plus one stats all-reduce; chunk times are summed; max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    import paper_2410_18252_b200 as odpo
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    w = workload("strong")
+    T, V, Pg = w.T, w.V, w.P
+    p_lo, p_hi = odpo.shard_pairs(Pg, world, rank)
+    C = args.chunk_pairs
+    chunks = [(p, min(p + C, p_hi)) for p in range(p_lo, p_hi, C)]
+    logits = torch.empty((2 * C, T, V), dtype=torch.bfloat16, device=dev)
+    stats = torch.zeros(16, dtype=torch.float64, device=dev)
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    acc = torch.zeros(16, dtype=torch.float64, device=dev)
+    ref_val = -0.1 * T
+
+    def prep_chunk(c0, c1):
+        n = c1 - c0
+        seqs = np.arange(2 * c0, 2 * c1)
+        rows = (seqs[:, None] * T + np.arange(T)[None, :]).reshape(-1)
+        tok = torch.from_numpy(synth.tokens_rows(args.seed, rows, V).reshape(2 * n, T)).to(dev)
+        mask = torch.from_numpy(synth.mask_for(args.seed, seqs, T, args.mask, w.lbar)).to(dev)
+        rew = torch.from_numpy(synth.rewards_for(args.seed, n, 2, p0=c0)).to(dev)
+        eos = torch.from_numpy(synth.has_eos_for(args.seed, n, 2, p0=c0)).to(dev)
+        x = logits[:2 * n]
+        synth.fill_logits_device(x, args.seed, row0=int(rows[0]), tokens=tok, peak=14.0)
+        ref = torch.full((2 * n,), ref_val, dtype=torch.float32, device=dev)
+        return x, tok, mask, rew, eos, ref, float(mask.float().mean().item())
+
+    meta = {}
+
+    def one_step(timed):
+        total_ms, loss_ms, alg = 0.0, 0.0, 0.0
+        acc.zero_()
+        for (c0, c1) in chunks:
+            x, tok, mask, rew, eos, ref, rho = prep_chunk(c0, c1)
+            torch.cuda.synchronize()
+            e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+            e[0].record()
+            sel = odpo.pair_select(rew, eos, w.eos_penalty, status=status, sel_stats=stats[10:13])
+            e[1].record()
+            out = odpo.online_dpo_loss_fwd_bwd(x, ref, tok, mask, w.beta, pair_rows=sel.pair_rows,
+                                               p_global=Pg, inplace=True, schedule=args.schedule,
+                                               lag_pairs=args.lag, exp2_split=args.exp2_split,
+                                               stats=stats, status=status)
+            acc.add_(stats)
+            e[2].record()
+            torch.cuda.synchronize()
+            total_ms += e[0].elapsed_time(e[2])
+            loss_ms += e[1].elapsed_time(e[2])
+            alg += (rho + 1.0) * x.numel() * 2
+            meta["launches"] = 1 + out.launches
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        odpo.allreduce_stats(acc)
+        e1.record()
+        torch.cuda.synchronize()
+        total_ms += e0.elapsed_time(e1)
+        return total_ms, loss_ms, alg
+
+    for _ in range(args.warmup):
+        one_step(False)
+    if world > 1:
+        dist.barrier()
+    clk = ClockSampler(local_rank)
+    tot, ltot, alg = 0.0, 0.0, 0.0
+    with clk:
+        for _ in range(args.steps):
+            a, b_, c = one_step(True)
+            tot += a
+            ltot += b_
+            alg += c
+    t = torch.tensor([tot], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    tmax = float(t.item())
+    peak, peak_src = peaks()
+    achieved = alg / (ltot / 1e3) / 1e9
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": Pg * args.steps / (tmax / 1e3), "unit": "pairs/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": tmax / args.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": "strong", "global_pairs": Pg, "T": T, "V": V,
+                       "chunk_pairs": C, "pairs_rank0": p_hi - p_lo, "mask": args.mask,
+                       "parallelism": f"dp{world}", "inplace": True,
+                       "l2": "each chunk (33.6 GB) > L2; logits regenerated between chunks"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+                         "kernel": "odpo_online_dpo_loss_fwd_bwd (rank 0 chunks)"},
+            "cpu_baseline": None, "e2e": None,
+            "gpu_launches": int(meta.get("launches", 0) * len(chunks) * args.steps),
+            "clocks": clk.summary(),
+            "tokens_vocab_per_s": 2 * Pg * T * V * args.steps / (tmax / 1e3),
+            "loss": float(acc[1].item()),
+        }), flush=True)
+
+
 def main():
     args = parse()
     rank = int(os.environ.get("RANK", 0))
@@ -386,7 +502,10 @@ def main():
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
-        run_ours(args, rank, world, local_rank)
+        if args.config == "strong":
+            run_strong(args, rank, world, local_rank)
+        else:
+            run_ours(args, rank, world, local_rank)
     finally:
         if world > 1:
             import torch.distributed as dist

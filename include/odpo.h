@@ -106,6 +106,9 @@ typedef struct {
   int32_t lag_pairs;    /* FUSED: backward of pair s is issued after forward of s+lag (0 = auto) */
   int32_t ctas_per_sm;  /* FUSED: persistent CTAs per SM (0 = auto)               */
   int32_t launches;     /* OUT: number of kernels this call launched               */
+  int32_t exp2_split;   /* bf16 only: index of the MUFU/FMA-polynomial exp2 split
+                           (-1 = library default)        */
+  int32_t lookahead;    /* FUSED: rows a CTA decodes ahead of the row it streams (-1 = default) */
 } odpo_launch_opts;
 
 /*

@@ -44,7 +44,7 @@ class OdpoError(RuntimeError):
 
 class _Opts(C.Structure):
     _fields_ = [("schedule", C.c_int32), ("lag_pairs", C.c_int32), ("ctas_per_sm", C.c_int32),
-                ("launches", C.c_int32)]
+                ("launches", C.c_int32), ("exp2_split", C.c_int32), ("lookahead", C.c_int32)]
 
 
 _lib = None
@@ -205,7 +205,8 @@ def online_dpo_loss_fwd_bwd(policy_logits: torch.Tensor, ref_logp: torch.Tensor,
                             pair_rows: torch.Tensor | None = None, p_global: int | None = None,
                             inv_temperature: float = 1.0, inplace: bool = False,
                             dlogits: torch.Tensor | None = None, schedule: str = "auto",
-                            lag_pairs: int = 0, ctas_per_sm: int = 0,
+                            lag_pairs: int = 0, ctas_per_sm: int = 0, exp2_split: int = -1,
+                            lookahead: int = -1,
                             stats: torch.Tensor | None = None,
                             status: torch.Tensor | None = None) -> LossOutput:
     """Online DPO loss, statistics and dlogits in one call.
@@ -239,7 +240,8 @@ def online_dpo_loss_fwd_bwd(policy_logits: torch.Tensor, ref_logp: torch.Tensor,
         status = torch.zeros(1, dtype=torch.int32, device=dev)
     nb = workspace_bytes(B, T, max(P, 1))
     ws = _workspace(dev, nb)
-    opts = _Opts(SCHEDULES[schedule], int(lag_pairs), int(ctas_per_sm), 0)
+    opts = _Opts(SCHEDULES[schedule], int(lag_pairs), int(ctas_per_sm), 0, int(exp2_split),
+                 int(lookahead))
     _check(_L().odpo_online_dpo_loss_fwd_bwd_ex(
         _p(policy_logits), dt, B, T, V, sb, st, _p(ref_logp), _p(tokens), _p(mask), _p(pair_rows),
         P, Pg, float(beta), float(inv_temperature), _p(dl), dl.stride(0), dl.stride(1), _p(seq),
@@ -276,3 +278,10 @@ def summarize(stats: torch.Tensor) -> dict:
         "ndegenerate": s[11],
         "ntruncated": s[12],
     }
+
+
+def shard_pairs(P_global: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous pair block [p0, p1) of rank `rank`: pairs are
+    independent, so each rank's logits come from its own data-parallel replica and the
+    static P_global keeps dlogits identical to a single-GPU run."""
+    return (rank * P_global) // world, ((rank + 1) * P_global) // world

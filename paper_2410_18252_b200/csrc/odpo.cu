@@ -3,12 +3,14 @@
 // Kernels:
 //   k_pair_select    K1  reward-ranked pair selection + selection stats
 //   k_prep           --  per-call workspace init, sequence->pair map, DUP/RANGE checks
-//   k_row_fwd        K2  one CTA per row: online LSE + gather  (seq_logprobs, TWO_PASS)
-//   k_seq_sum        K3a one warp per sequence: fixed-order masked sum
-//   k_pair_reduce    K3b one CTA per pair: DPO logit, -log sigma, coef, stats
-//   k_row_bwd        K4  one CTA per row: dlogits = coef (softmax - onehot)
-//   k_fused          K5  persistent: forward rows of pair s interleaved with backward rows of
-//                        pair s-lag; per-pair completion counters; backward re-reads hit L2
+//   k_engine<SEQ>    K2+K3a persistent TMA-ring engine, forward rows; the CTA finishing a
+//                        sequence's last row sums it (seq_logprobs; TWO_PASS forward)
+//   k_engine<FUSED>  K5  persistent TMA-ring engine: forward rows of pair s interleaved with
+//                        backward rows of pair s-lag; per-pair completion counters; the CTA
+//                        finishing a pair's last forward row runs K3b; backward rows wait on
+//                        the pair's ready flag; backward re-reads hit L2 (evict_last policy)
+//   k_pair_reduce    K3b one warp per pair (TWO_PASS)
+//   k_row_bwd        K4  one CTA per row: dlogits = coef (softmax - onehot) (TWO_PASS)
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
@@ -17,8 +19,9 @@
 
 #include "odpo.h"
 #include "odpo_device.cuh"
+#include "odpo_engine.cuh"
 
-#define ODPO_VERSION_STR "odpo-b200 0.1.0 (sm_100a)"
+#define ODPO_VERSION_STR "odpo-b200 0.2.0 (sm_100a)"
 
 namespace odpo {
 
@@ -30,7 +33,8 @@ struct Workspace {
   float* seq_coef;
   int32_t* seq_pair;   // 2p (chosen of p) / 2p+1 (rejected of p) / -1 unreferenced
   int32_t* unref;      // unreferenced sequences, ascending
-  unsigned* pair_cnt;  // forward rows done
+  unsigned* seq_cnt;   // forward rows done per sequence (SEQ mode)
+  unsigned* pair_cnt;  // forward rows done per pair (FUSED)
   unsigned* pair_ready;
   double* pair_vals;   // [P][ODPO_NSTATS]
   unsigned* counters;  // [0] ticket, [1] pairs done, [2] n_unref
@@ -54,6 +58,7 @@ static size_t ws_layout(int64_t B, int64_t T, int64_t P, char* base, Workspace* 
   char* p_c = take((size_t)B * 4);
   char* p_sp = take((size_t)B * 4);
   char* p_u = take((size_t)B * 4);
+  char* p_sc = take((size_t)B * 4);
   char* p_pc = take((size_t)P * 4);
   char* p_pr = take((size_t)P * 4);
   char* p_pv = take((size_t)P * ODPO_NSTATS * 8);
@@ -65,6 +70,7 @@ static size_t ws_layout(int64_t B, int64_t T, int64_t P, char* base, Workspace* 
     w->seq_coef = (float*)p_c;
     w->seq_pair = (int32_t*)p_sp;
     w->unref = (int32_t*)p_u;
+    w->seq_cnt = (unsigned*)p_sc;
     w->pair_cnt = (unsigned*)p_pc;
     w->pair_ready = (unsigned*)p_pr;
     w->pair_vals = (double*)p_pv;
@@ -145,7 +151,10 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep(const int32_t* __restrict
                                                        uint32_t* status) {
   __shared__ int scan[kPrepThreads];
   const int tid = threadIdx.x;
-  for (int64_t b = tid; b < B; b += kPrepThreads) w.seq_pair[b] = -1;
+  for (int64_t b = tid; b < B; b += kPrepThreads) {
+    w.seq_pair[b] = -1;
+    w.seq_cnt[b] = 0;
+  }
   for (int64_t p = tid; p < P; p += kPrepThreads) {
     w.pair_cnt[p] = 0;
     w.pair_ready[p] = 0;
@@ -181,7 +190,7 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep(const int32_t* __restrict
   if (tid == kPrepThreads - 1) w.counters[C_NUNREF] = (unsigned)scan[tid];
 }
 
-// ------------------------------------------------------------------ shared loss arguments
+// ------------------------------------------------------------------ shared arguments
 struct LossArgs {
   const void* logits;
   int64_t B, T, V, sb, st;  // strides in elements
@@ -198,8 +207,12 @@ struct LossArgs {
   float* z_out;
   double* stats;
   uint32_t* status;
+  float* tok_out;   // SEQ: optional per-token log-probs
+  float* lse_out;   // SEQ: optional per-row lse
+  int seqsum;       // SEQ: sum sequences (seq_logprobs) or only write row stats (TWO_PASS)
   Workspace w;
   int lag;
+  int look;         // producer decode lookahead (rows), <= kSlots - 2
   int esize;
 };
 
@@ -217,37 +230,30 @@ __device__ __forceinline__ void pair_seqs(const LossArgs& a, int64_t p, int64_t&
   if (r < 0 || r >= a.B) r = -1;
 }
 
-// Pair reduction (K3b) by a whole CTA (>= 64 threads): warps 0/1 sum the two sequences in
-// fixed order, thread 0 forms z, loss, sigma(-z), coef, publishes them and the pair's
-// statistics; the CTA that completes the LAST pair reduces all pairs in fixed order.
-__device__ void pair_reduce(const LossArgs& a, int64_t p, double* smd, int* smi) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+// Pair reduction (K3b) by ONE warp: fixed-order sums of both sequences, then lane 0 forms z,
+// loss, sigma(-z), coef, publishes them (release) and the pair's statistics; the warp that
+// completes the LAST pair reduces all pairs' statistics in fixed order.
+__device__ __noinline__ void pair_reduce_warp(const LossArgs& a, int64_t p) {
+  const int lane = threadIdx.x & 31;
   int64_t c, r;
   pair_seqs(a, p, c, r);
-  if (warp < 2) {
-    const int64_t s = warp == 0 ? c : r;
-    double S = 0.0;
-    int n = 0;
-    if (s >= 0) seq_sum_warp(a.w.row_logp + s * a.T, a.mask + s * a.T, a.T, S, n);
-    if (lane == 0) {
-      smd[warp] = S;
-      smi[warp] = n;
-    }
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
+  double Sc = 0.0, Sr = 0.0;
+  int nc = 0, nr = 0;
+  if (c >= 0) seq_sum_warp(a.w.row_logp + c * a.T, a.mask + c * a.T, a.T, Sc, nc);
+  if (r >= 0) seq_sum_warp(a.w.row_logp + r * a.T, a.mask + r * a.T, a.T, Sr, nr);
+  unsigned last = 0;
+  if (lane == 0) {
     uint32_t fl = 0;
     double* pv = a.w.pair_vals + p * ODPO_NSTATS;
     if (c < 0 || r < 0) {
       for (int k = 0; k < ODPO_NSTATS; ++k) pv[k] = 0.0;
       if (a.z_out) a.z_out[p] = 0.f;
     } else {
-      const int nc = smi[0], nr = smi[1];
       if (nc == 0 || nr == 0) fl |= ODPO_FLAG_EMPTY_SEQ;
-      const float Sc = nc ? (float)smd[0] : 0.f;
-      const float Sr = nr ? (float)smd[1] : 0.f;
-      const float dc = __fsub_rn(Sc, a.ref[c]);
-      const float dr = __fsub_rn(Sr, a.ref[r]);
+      const float fSc = nc ? (float)Sc : 0.f;
+      const float fSr = nr ? (float)Sr : 0.f;
+      const float dc = __fsub_rn(fSc, a.ref[c]);
+      const float dr = __fsub_rn(fSr, a.ref[r]);
       const float z = __fmul_rn(a.beta, __fsub_rn(dc, dr));   // no FMA contraction (R15)
       const double zd = (double)z;
       const double loss_p = fmax(-zd, 0.0) + log1p(exp(-fabs(zd)));  // softplus(-z)
@@ -255,8 +261,8 @@ __device__ void pair_reduce(const LossArgs& a, int64_t p, double* smd, int* smi)
       const float coef = (float)((double)a.beta * sig_neg * (double)a.invT / a.Pg);
       a.w.seq_coef[c] = coef;
       a.w.seq_coef[r] = -coef;
-      a.seq_logp[c] = Sc;
-      a.seq_logp[r] = Sr;
+      a.seq_logp[c] = fSc;
+      a.seq_logp[r] = fSr;
       if (a.z_out) a.z_out[p] = z;
       pv[ODPO_ST_NPAIRS] = 1.0;
       pv[ODPO_ST_LOSS] = loss_p;
@@ -264,8 +270,8 @@ __device__ void pair_reduce(const LossArgs& a, int64_t p, double* smd, int* smi)
       pv[ODPO_ST_Z] = zd;
       pv[ODPO_ST_RCHOSEN] = (double)a.beta * (double)dc;
       pv[ODPO_ST_RREJ] = (double)a.beta * (double)dr;
-      pv[ODPO_ST_SCHOSEN] = (double)Sc;
-      pv[ODPO_ST_SREJ] = (double)Sr;
+      pv[ODPO_ST_SCHOSEN] = (double)fSc;
+      pv[ODPO_ST_SREJ] = (double)fSr;
       pv[ODPO_ST_NTOK_CHOSEN] = (double)nc;
       pv[ODPO_ST_NTOK_REJ] = (double)nr;
     }
@@ -273,95 +279,35 @@ __device__ void pair_reduce(const LossArgs& a, int64_t p, double* smd, int* smi)
     __threadfence();
     st_release(&a.w.pair_ready[p], 1u);
     const unsigned done = atomicAdd(&a.w.counters[C_PAIRS_DONE], 1u);
-    smi[2] = (done == (unsigned)(a.P - 1));
+    last = (done == (unsigned)(a.P - 1));
   }
-  __syncthreads();
-  if (smi[2] && warp == 0) {
-    __threadfence();
-    double acc[ODPO_NSTATS];
+  last = __shfl_sync(kFull, last, 0);
+  if (!last) return;
+  __threadfence();
+  double acc[ODPO_NSTATS];
 #pragma unroll
-    for (int k = 0; k < ODPO_NSTATS; ++k) acc[k] = 0.0;
-    for (int64_t q = lane; q < a.P; q += 32) {
-      const double* pv = a.w.pair_vals + q * ODPO_NSTATS;
+  for (int k = 0; k < ODPO_NSTATS; ++k) acc[k] = 0.0;
+  for (int64_t q = lane; q < a.P; q += 32) {
+    const double* pv = a.w.pair_vals + q * ODPO_NSTATS;
 #pragma unroll
-      for (int k = 0; k < ODPO_NSTATS; ++k) acc[k] += __ldcg(pv + k);
-    }
-#pragma unroll
-    for (int k = 0; k < ODPO_NSTATS; ++k) {
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) acc[k] += __shfl_down_sync(kFull, acc[k], off);
-    }
-    if (lane == 0) {
-      for (int k = 0; k < ODPO_NSTATS; ++k) a.stats[k] = acc[k];
-      a.stats[ODPO_ST_LOSS] = acc[ODPO_ST_LOSS] / a.Pg;
-    }
+    for (int k = 0; k < ODPO_NSTATS; ++k) acc[k] += __ldcg(pv + k);
   }
-}
-
-// ------------------------------------------------------------------ K2 row forward (grid = rows)
-struct FwdArgs {
-  const void* logits;
-  int64_t T, V, sb, st;
-  const int32_t* tokens;
-  const uint8_t* mask;
-  float invT;
-  float* row_m;
-  float* row_l1p;
-  float* row_logp;
-  float* tok_logp;  // nullable (seq_logprobs output)
-  float* row_lse;   // nullable
-  uint32_t* status;
-  int esize;
-};
-
-template <int DT>
-__global__ void __launch_bounds__(kRowThreads, 2) k_row_fwd(FwdArgs a) {
-  __shared__ float sm[2 * kWarps];
-  const int64_t g = blockIdx.x;
-  const int64_t b = g / a.T, t = g % a.T;
-  if (!a.mask[g]) {
-    if (threadIdx.x == 0) {
-      if (a.tok_logp) a.tok_logp[g] = 0.f;
-      if (a.row_lse) a.row_lse[g] = 0.f;
-    }
-    return;
+#pragma unroll
+  for (int k = 0; k < ODPO_NSTATS; ++k) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) acc[k] += __shfl_down_sync(kFull, acc[k], off);
   }
-  const char* row = reinterpret_cast<const char*>(a.logits) + (b * a.sb + t * a.st) * a.esize;
-  RowOut o = row_forward<DT, LD_STREAM>(row, (int)a.V, a.tokens[g], a.invT, 0, sm);
-  if (threadIdx.x == 0) {
-    a.row_m[g] = o.m;
-    a.row_l1p[g] = o.l1p;
-    a.row_logp[g] = o.logp;
-    if (a.tok_logp) a.tok_logp[g] = o.logp;
-    if (a.row_lse) a.row_lse[g] = o.lse;
-    flag(a.status, o.flags);
-  }
-}
-
-// ------------------------------------------------------------------ K3a sequence sums
-__global__ void __launch_bounds__(256) k_seq_sum(const float* __restrict__ row_logp,
-                                                  const uint8_t* __restrict__ mask, int64_t B,
-                                                  int64_t T, float* seq_logp, uint32_t* status) {
-  const int64_t s = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (s >= B) return;
-  double S;
-  int n;
-  seq_sum_warp(row_logp + s * T, mask + s * T, T, S, n);
-  if ((threadIdx.x & 31) == 0) {
-    seq_logp[s] = n ? (float)S : 0.f;
-    if (!n) flag(status, ODPO_FLAG_EMPTY_SEQ);
+  if (lane == 0) {
+    for (int k = 0; k < ODPO_NSTATS; ++k) a.stats[k] = acc[k];
+    a.stats[ODPO_ST_LOSS] = acc[ODPO_ST_LOSS] / a.Pg;
   }
 }
 
 // ------------------------------------------------------------------ K3b pair reduce (grid = P)
-__global__ void __launch_bounds__(64) k_pair_reduce(LossArgs a) {
-  __shared__ double smd[2];
-  __shared__ int smi[3];
-  pair_reduce(a, blockIdx.x, smd, smi);
-}
+__global__ void __launch_bounds__(32) k_pair_reduce(LossArgs a) { pair_reduce_warp(a, blockIdx.x); }
 
 // ------------------------------------------------------------------ K4 row backward (grid = rows)
-template <int DT>
+template <int DT, int NPB>
 __global__ void __launch_bounds__(kRowThreads, 2) k_row_bwd(LossArgs a) {
   const int64_t g = blockIdx.x;
   const int64_t b = g / a.T, t = g % a.T;
@@ -371,15 +317,17 @@ __global__ void __launch_bounds__(kRowThreads, 2) k_row_bwd(LossArgs a) {
     return;
   }
   const float coef = a.w.seq_coef[b];
-  row_backward<DT, LD_STREAM>(row_ptr(a, b, t), drow, (int)a.V, a.tokens[g], a.invT, a.w.row_m[g],
+  row_backward<DT, LD_STREAM, NPB>(row_ptr(a, b, t), drow, (int)a.V, a.tokens[g], a.invT, a.w.row_m[g],
                               a.w.row_l1p[g], a.w.row_logp[g], coef, 0);
 }
 
-// ------------------------------------------------------------------ K5 fused persistent kernel
-// Ticket order (R = 2T rows per pair, d = lag): F(0..d-1), then B(0), F(d), B(1), F(d+1), ...,
-// then the remaining B's, then Z rows (unreferenced sequences).  A B item of pair p waits for
-// pair_ready[p]; every F item of p has an earlier ticket held by a running CTA and F items never
-// wait, so the wait always terminates (no co-residency assumption).
+// ------------------------------------------------------------------ the TMA-ring engine
+enum { M_SEQ = 0, M_FUSED = 1 };
+
+// Fused ticket order (R = 2T rows per pair, d = lag): F(0..d-1), then B(0), F(d), B(1),
+// F(d+1), ..., then the remaining B's, then Z rows (unreferenced sequences).  Every F ticket
+// of pair p precedes its B tickets and F work never waits, so by induction on ticket order the
+// lowest unfinished ticket always makes progress (no co-residency assumption).
 __device__ __forceinline__ void decode_block(int64_t q, int64_t P, int64_t d, bool& fwd, int64_t& p) {
   if (q < d) { fwd = true; p = q; return; }
   const int64_t mid = 2 * (P - d);
@@ -393,78 +341,423 @@ __device__ __forceinline__ void decode_block(int64_t q, int64_t P, int64_t d, bo
   p = (P - d) + (q - d - mid);
 }
 
-template <int DT>
-__global__ void __launch_bounds__(kRowThreads, 2) k_fused(LossArgs a) {
-  __shared__ float sm[2 * kWarps];
-  __shared__ unsigned s_ticket[2];
-  __shared__ double smd[2];
-  __shared__ int smi[3];
-  __shared__ int s_last;
-  const uint64_t pol_keep = policy_evict_last();
-  const uint64_t pol_drop = policy_evict_first();
+// exp2 split variants (bf16): NPF / NPB of every 8 elements use the FMA-pipe polynomial in the
+// forward / backward; the rest use MUFU.EX2.
+struct PolyVariant {
+  int npf, npb;
+};
+constexpr PolyVariant kPoly[] = {{0, 0}, {2, 2}, {2, 4}, {3, 4}, {4, 4}, {3, 3}, {2, 3}};
+constexpr int kNumPoly = sizeof(kPoly) / sizeof(kPoly[0]);
+constexpr int kPolyDefault = 0;
+
+// Row decode (producer): ticket -> RowSlot fields.  Returns true if the row streams data.
+template <int DT, int MODE>
+__device__ __forceinline__ bool decode_row(const LossArgs& a, int64_t tk, int64_t total_fb,
+                                           RowSlot& S, uint64_t& pol, uint64_t pol_keep,
+                                           uint64_t pol_drop) {
   const int64_t T = a.T, R = 2 * T;
-  const int64_t total_fb = 2 * a.P * R;
-  const int64_t total = total_fb + (int64_t)__ldcg(&a.w.counters[C_NUNREF]) * T;
-  if (threadIdx.x == 0) s_ticket[0] = atomicAdd(&a.w.counters[C_TICKET], 1u);
+  S.tok = 0;
+  S.p = 0;
+  S.s = -1;
+  S.g = 0;
+  S.row = nullptr;
+  S.drow = nullptr;
+  pol = pol_drop;
+  if (MODE == M_SEQ) {
+    S.g = tk;
+    S.s = tk / T;
+    S.p = S.s;
+    if (a.mask[S.g]) {
+      S.kind = K_F;
+      S.row = row_ptr(a, S.s, tk % T);
+      S.tok = a.tokens[S.g];
+      return true;
+    }
+    S.kind = K_FSKIP;
+    return false;
+  }
+  if (tk < total_fb) {
+    bool fwd;
+    int64_t p;
+    decode_block(tk / R, a.P, a.lag, fwd, p);
+    const int64_t j = tk % R;
+    int64_t c, r;
+    pair_seqs(a, p, c, r);
+    const int64_t s = j < T ? c : r;
+    const int64_t t = j < T ? j : j - T;
+    S.p = p;
+    S.s = s;
+    S.g = s >= 0 ? s * T + t : 0;
+    const bool live = s >= 0 && a.mask[S.g];
+    if (fwd) {
+      if (!live) { S.kind = K_FSKIP; return false; }
+      S.kind = K_F;
+      S.row = row_ptr(a, s, t);
+      S.tok = a.tokens[S.g];
+      pol = pol_keep;   // keep the row in L2 for its backward pass
+      return true;
+    }
+    if (live) {
+      S.kind = K_B;
+      S.row = row_ptr(a, s, t);
+      S.drow = drow_ptr(a, s, t);
+      S.tok = a.tokens[S.g];
+      return true;
+    }
+    if (s >= 0) {
+      S.kind = K_ZERO;
+      S.drow = drow_ptr(a, s, t);
+    } else {
+      S.kind = K_NONE;
+    }
+    return false;
+  }
+  const int64_t k = (tk - total_fb) / T, t = (tk - total_fb) % T;
+  const int64_t s = __ldcg(a.w.unref + k);
+  S.kind = K_ZERO;
+  S.s = s;
+  S.drow = drow_ptr(a, s, t);
+  return false;
+}
+
+// Epilogue-side counting: returns true (warp-uniform) if this row completed its pair/sequence.
+template <int MODE>
+__device__ __forceinline__ bool count_row(const LossArgs& a, const RowSlot& S, int lane) {
+  unsigned last = 0;
+  if (lane == 0 && (MODE == M_FUSED || a.seqsum)) {
+    __threadfence();
+    unsigned* cnt = MODE == M_FUSED ? &a.w.pair_cnt[S.p] : &a.w.seq_cnt[S.s];
+    const unsigned need = MODE == M_FUSED ? (unsigned)(2 * a.T) : (unsigned)a.T;
+    last = (atomicAdd(cnt, 1u) == need - 1u);
+  }
+  last = __shfl_sync(kFull, last, 0);
+  if (last) __threadfence();
+  return last != 0;
+}
+
+template <int MODE>
+__device__ __forceinline__ void complete_unit(const LossArgs& a, const RowSlot& S, int lane) {
+  if (MODE == M_FUSED) {
+    pair_reduce_warp(a, S.p);
+  } else {
+    double Sq;
+    int n;
+    seq_sum_warp(a.w.row_logp + S.s * a.T, a.mask + S.s * a.T, a.T, Sq, n);
+    if (lane == 0) {
+      a.seq_logp[S.s] = n ? (float)Sq : 0.f;
+      if (!n) flag(a.status, ODPO_FLAG_EMPTY_SEQ);
+    }
+  }
+}
+
+// ---- the engine: warps 0..7 consumers, warp 8 TMA producer, warp 9 row epilogue
+template <int DT, int MODE, int PV>
+__global__ void __launch_bounds__(kEngThreads, 2) k_engine(LossArgs a) {
+  constexpr int NPF = DT == 1 ? kPoly[PV].npf : 0;
+  constexpr int NPB = DT == 1 ? kPoly[PV].npb : 0;
+  constexpr int N = Traits<DT>::N;
+  extern __shared__ __align__(128) uint8_t ring[];
+  __shared__ __align__(8) uint64_t full[kStages];
+  __shared__ __align__(8) uint64_t empty[kStages];
+  __shared__ __align__(8) uint64_t slot_full[kSlots];
+  __shared__ __align__(8) uint64_t slot_empty[kSlots];
+  __shared__ __align__(8) uint64_t part_ready[kSlots];
+  __shared__ __align__(8) uint64_t param_ready[kSlots];
+  __shared__ int32_t stage_slot[kStages];
+  __shared__ int32_t stage_chunk[kStages];
+  __shared__ RowSlot slots[kSlots];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kNCW);
+    }
+    for (int s = 0; s < kSlots; ++s) {
+      mbar_init(&slot_full[s], 1);
+      mbar_init(&slot_empty[s], kNCW + 2);   // consumer warps + epilogue + parameter warp
+      mbar_init(&part_ready[s], kNCW);
+      mbar_init(&param_ready[s], 1);
+    }
+    mbar_fence_init();
+  }
   __syncthreads();
-  for (int it = 0;; ++it) {
-    const int64_t tk = s_ticket[it & 1];
-    if (tk >= total) break;
-    if (threadIdx.x == 0) s_ticket[(it + 1) & 1] = atomicAdd(&a.w.counters[C_TICKET], 1u);
-    if (tk < total_fb) {
-      bool fwd;
-      int64_t p;
-      decode_block(tk / R, a.P, a.lag, fwd, p);
-      const int64_t j = tk % R;
-      int64_t c, r;
-      pair_seqs(a, p, c, r);
-      const int64_t s = j < T ? c : r;
-      const int64_t t = j < T ? j : j - T;
-      const int64_t g = s * T + t;
-      if (fwd) {
-        if (s >= 0 && a.mask[g]) {
-          RowOut o = row_forward<DT, LD_HINT>(row_ptr(a, s, t), (int)a.V, a.tokens[g], a.invT,
-                                              pol_keep, sm);
-          if (threadIdx.x == 0) {
-            a.w.row_m[g] = o.m;
-            a.w.row_l1p[g] = o.l1p;
-            a.w.row_logp[g] = o.logp;
-            flag(a.status, o.flags);
-          }
+
+  const int64_t T = a.T;
+  const int V = (int)a.V;
+  const int nvec = V / N;
+  const int tail = V - nvec * N;
+  const float invT = a.invT;
+  const float k2 = invT * kLog2e;
+
+  if (warp == kProdWarp) {
+    // ================= producer: tickets -> row slots -> TMA chunk stages
+    if (lane != 0) return;
+    const uint64_t pol_keep = policy_evict_last();
+    const uint64_t pol_drop = policy_evict_first();
+    const int nch = nvec > 0 ? (nvec + kCV - 1) / kCV : 1;
+    int64_t total_fb = 0, total;
+    if (MODE == M_FUSED) {
+      total_fb = 2 * a.P * 2 * T;
+      total = total_fb + (int64_t)__ldcg(&a.w.counters[C_NUNREF]) * T;
+    } else {
+      total = a.B * T;
+    }
+    // Rows are DECODED into slots up to kLook rows ahead of the row whose chunks are being
+    // pushed, so the parameter warp sees backward rows early enough to hide the latency of
+    // their pair-ready check and parameter loads.
+    int st = 0, dsl = 0, psl = 0, ahead = 0;
+    uint32_t sph = 0, dph = 0;
+    uint32_t pmask = 0;  // per-slot parity of param_ready (advances only on B rows)
+    bool ended = false;
+    for (;;) {
+      while (!ended && ahead <= a.look) {
+        const int64_t tk = (int64_t)atomicAdd(&a.w.counters[C_TICKET], 1u);
+        mbar_wait(&slot_empty[dsl], dph ^ 1u);
+        RowSlot& S = slots[dsl];
+        uint64_t pol = pol_drop;
+        bool data = false;
+        if (tk >= total) {
+          S.kind = K_END;
+          ended = true;
+        } else {
+          data = decode_row<DT, MODE>(a, tk, total_fb, S, pol, pol_keep, pol_drop);
         }
-        if (threadIdx.x == 0) {
-          __threadfence();
-          const unsigned old = atomicAdd(&a.w.pair_cnt[p], 1u);
-          s_last = (old == (unsigned)(R - 1));
-        }
-        __syncthreads();
-        if (s_last) {
-          __threadfence();
-          pair_reduce(a, p, smd, smi);
-        }
-      } else {
-        if (threadIdx.x == 0) {
-          while (ld_acquire(&a.w.pair_ready[p]) == 0u) __nanosleep(64);
-        }
-        __syncthreads();
-        if (s >= 0) {
-          char* drow = drow_ptr(a, s, t);
-          if (!a.mask[g]) {
-            row_zero<DT>(drow, (int)a.V);
+        S.nchunk = data ? nch : 0;
+        S.pphase = (pmask >> dsl) & 1u;
+        if (S.kind == K_B) pmask ^= 1u << dsl;
+        mbar_arrive(&slot_full[dsl]);
+        ++ahead;
+        if (++dsl == kSlots) { dsl = 0; dph ^= 1u; }
+      }
+      if (ahead == 0) break;
+      const RowSlot& S = slots[psl];
+      const int kind = S.kind;
+      if (kind == K_F || kind == K_B || kind == K_ZERO || kind == K_END) {
+        const bool data = S.nchunk > 0;
+        const int nstage = data ? S.nchunk : 1;
+        const uint64_t pol = (MODE == M_FUSED && kind == K_F) ? pol_keep : pol_drop;
+        for (int c = 0; c < nstage; ++c) {
+          mbar_wait(&empty[st], sph ^ 1u);
+          stage_slot[st] = kind == K_END ? -1 : psl;
+          stage_chunk[st] = c;
+          const int nv = data ? min(kCV, nvec - c * kCV) : 0;
+          if (nv > 0) {
+            const uint32_t bytes = (uint32_t)nv * 16u;
+            mbar_arrive_tx(&full[st], bytes);
+            tma_load_1d(ring + (size_t)st * kChunk, S.row + (size_t)c * kChunk, bytes, &full[st], pol);
           } else {
-            row_backward<DT, LD_HINT>(row_ptr(a, s, t), drow, (int)a.V, a.tokens[g], a.invT,
-                                      __ldcg(a.w.row_m + g), __ldcg(a.w.row_l1p + g),
-                                      __ldcg(a.w.row_logp + g), __ldcg(a.w.seq_coef + s),
-                                      pol_drop);
+            mbar_arrive(&full[st]);
           }
+          if (++st == kStages) { st = 0; sph ^= 1u; }
         }
       }
-    } else {
-      const int64_t k = (tk - total_fb) / T, t = (tk - total_fb) % T;
-      const int64_t s = __ldcg(a.w.unref + k);
-      row_zero<DT>(drow_ptr(a, s, t), (int)a.V);
+      --ahead;
+      if (++psl == kSlots) psl = 0;
+      if (kind == K_END) break;
     }
-    __syncthreads();
+    return;
+  }
+
+  if (warp == kParWarp) {
+    // ================= backward-parameter prefetch: for each backward row, wait (acquire) for
+    // its pair's coefficient, then publish the row constants to the consumers.  Runs ahead of
+    // the consumers by up to kSlots rows, so neither TMA issue nor compute waits on it.
+    if (lane != 0) return;
+    int sl = 0;
+    uint32_t lph = 0;
+    for (;;) {
+      mbar_wait(&slot_full[sl], lph);
+      RowSlot& S = slots[sl];
+      const int kind = S.kind;
+      if (kind == K_END) break;
+      if (kind == K_B) {
+        while (ld_relaxed(&a.w.pair_ready[S.p]) == 0u) __nanosleep(32);
+        fence_acq_rel_gpu();
+        const float m = __ldcg(a.w.row_m + S.g);
+        const float l1p = __ldcg(a.w.row_l1p + S.g);
+        const float logp = __ldcg(a.w.row_logp + S.g);
+        const float coef = __ldcg(a.w.seq_coef + S.s);
+        // coef folded into the exponent: coef * 2^e = sign * 2^(e + log2|coef|)
+        S.c = fmaf(l1p, kLog2e, m * k2) - log2f(fabsf(coef));
+        S.coef = coef;
+        S.gtok = coef * expm1f(logp);
+        mbar_arrive(&param_ready[sl]);
+      }
+      mbar_arrive(&slot_empty[sl]);
+      if (++sl == kSlots) { sl = 0; lph ^= 1u; }
+    }
+    return;
+  }
+
+  if (warp == kEpiWarp) {
+    // ================= row epilogue: merge partials, finalize, count, pair/sequence reduce
+    int sl = 0;
+    uint32_t lph = 0;
+    uint32_t rmask = 0;  // per-slot parity of part_ready (advances only on consumer rows)
+    for (;;) {
+      mbar_wait(&slot_full[sl], lph);
+      const RowSlot& S = slots[sl];
+      const int kind = S.kind;
+      if (kind == K_END) break;
+      // Only forward rows make the epilogue wait for the consumers; backward / zero rows are
+      // released by their consumers directly, so a backward row waiting for its pair never
+      // holds up the counting of later forward rows (no head-of-line blocking).
+      if (kind == K_F) {
+        mbar_wait(&part_ready[sl], (rmask >> sl) & 1u);
+        rmask ^= 1u << sl;
+      }
+      if (kind == K_F) {
+        MR v;
+        v.m = lane < kNCW ? S.pm[lane] : -INFINITY;
+        v.r = lane < kNCW ? S.pr[lane] : 0.f;
+        v = warp_merge(v, k2);
+        if (lane == 0) {
+          uint32_t fl = 0;
+          const float l1p = log1pf(v.r);
+          float logp = 0.f;
+          if (S.tok < 0 || S.tok >= V) {
+            fl |= ODPO_FLAG_TOKEN_RANGE;
+          } else {
+            logp = __fsub_rn(__fmul_rn(__fsub_rn(S.xtok, v.m), invT), l1p);
+            if (!isfinite(logp)) fl |= ODPO_FLAG_NONFINITE_LOGIT;
+          }
+          if (!isfinite(v.m) || !isfinite(v.r)) fl |= ODPO_FLAG_NONFINITE_LOGIT;
+          a.w.row_m[S.g] = v.m;
+          a.w.row_l1p[S.g] = l1p;
+          a.w.row_logp[S.g] = logp;
+          if (MODE == M_SEQ) {
+            if (a.tok_out) a.tok_out[S.g] = logp;
+            if (a.lse_out) a.lse_out[S.g] = __fadd_rn(__fmul_rn(v.m, invT), l1p);
+          }
+          flag(a.status, fl);
+        }
+        if (count_row<MODE>(a, S, lane)) complete_unit<MODE>(a, S, lane);
+      } else if (kind == K_FSKIP) {
+        if (lane == 0 && MODE == M_SEQ) {
+          if (a.tok_out) a.tok_out[S.g] = 0.f;
+          if (a.lse_out) a.lse_out[S.g] = 0.f;
+        }
+        if (count_row<MODE>(a, S, lane)) complete_unit<MODE>(a, S, lane);
+      }
+      __syncwarp();
+      // rows the consumers never see also carry their kNCW arrivals
+      if (lane == 0)
+        mbar_arrive_n(&slot_empty[sl], (kind == K_FSKIP || kind == K_NONE) ? 1u + kNCW : 1u);
+      if (++sl == kSlots) { sl = 0; lph ^= 1u; }
+    }
+    return;
+  }
+
+  // ================= consumers (warps 0..7)
+  const uint32_t NI = Traits<DT>::kNegInfWord;
+  int st = 0;
+  uint32_t sph = 0;
+  MR s{-INFINITY, 0.f};
+  float b_c = 0.f, b_coef = 0.f, b_gtok = 0.f;
+  int r_kind = K_NONE, r_tok = 0, r_nch = 1;
+  const char* r_row = nullptr;
+  char* r_drow = nullptr;
+  for (;;) {
+    mbar_wait(&full[st], sph);
+    const int sl = stage_slot[st];
+    if (sl < 0) break;
+    const int ch = stage_chunk[st];
+    RowSlot& S = slots[sl];
+    if (ch == 0) {  // a new row: cache its fields (rows occupy consecutive stages)
+      r_kind = S.kind;
+      r_tok = S.tok;
+      r_nch = S.nchunk > 0 ? S.nchunk : 1;
+      r_row = S.row;
+      r_drow = S.drow;
+    }
+    const int kind = r_kind;
+    const int tok = r_tok;
+    const bool last_chunk = ch == r_nch - 1;
+    const uint4* sv = reinterpret_cast<const uint4*>(ring + (size_t)st * kChunk);
+    const int c0 = ch * kCV;
+    const int cnv = (kind == K_F || kind == K_B) ? min(kCV, nvec - c0) : 0;
+    const int tv = (tok >= 0 && tok < nvec * N) ? tok / N - c0 : -1;  // tok's vector in this chunk
+    const bool own_tok = tv >= 0 && tv < cnv && (tv % kNCT) == tid;
+    if (kind == K_F) {
+      if (ch == 0) s = MR{-INFINITY, 0.f};
+      if (tid < cnv) {
+        uint4 v[kUB];
+#pragma unroll
+        for (int u = 0; u < kUB; ++u) {
+          const int i = tid + u * kNCT;
+          v[u] = i < cnv ? sv[i] : make_uint4(NI, NI, NI, NI);
+        }
+        mr_batch<DT, kUB, NPF>(v, k2, s.m, s.r);
+      }
+      if (own_tok) {
+        float f[N];
+        Traits<DT>::unpack(sv[tv], f);
+        float x = f[0];
+#pragma unroll
+        for (int j = 1; j < N; ++j) x = (tok % N == j) ? f[j] : x;
+        S.xtok = x;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+      if (last_chunk) {
+        if (tid < tail) {
+          const int64_t vv = (int64_t)nvec * N + tid;
+          const float x = Traits<DT>::load1(r_row, vv);
+          s = mr_push1(s, x, k2);
+          if (vv == tok) S.xtok = x;
+        }
+        const MR wv = warp_merge(s, k2);
+        if (lane == 0) {
+          S.pm[warp] = wv.m;
+          S.pr[warp] = wv.r;
+          mbar_arrive(&part_ready[sl]);
+          mbar_arrive(&slot_empty[sl]);
+        }
+      }
+    } else if (kind == K_B) {
+      if (ch == 0) {
+        mbar_wait(&param_ready[sl], S.pphase);
+        b_c = S.c;
+        b_coef = S.coef;
+        b_gtok = S.gtok;
+      }
+      uint4* vout = reinterpret_cast<uint4*>(r_drow) + c0;
+      if (b_coef < 0.f) {
+#pragma unroll
+        for (int u = 0; u < kUB; ++u) {
+          const int i = tid + u * kNCT;
+          if (i < cnv) st16_stream(vout + i, bwd_vec<DT, NPB, true>(sv[i], k2, b_c));
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < kUB; ++u) {
+          const int i = tid + u * kNCT;
+          if (i < cnv) st16_stream(vout + i, bwd_vec<DT, NPB, false>(sv[i], k2, b_c));
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+      // onehot entry: the thread that stored tok's vector overwrites it (program order)
+      if (own_tok) Traits<DT>::store1(r_drow, tok, b_gtok);
+      if (last_chunk) {
+        if (tid < tail) {
+          const int64_t vv = (int64_t)nvec * N + tid;
+          const float x = Traits<DT>::load1(r_row, vv);
+          Traits<DT>::store1(r_drow, vv, vv == tok ? b_gtok : copysignf(ex2(fmaf(x, k2, -b_c)), b_coef));
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&slot_empty[sl]);
+      }
+    } else {  // K_ZERO
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+      uint4* vout = reinterpret_cast<uint4*>(r_drow);
+      for (int i = tid; i < nvec; i += kNCT) st16_stream(vout + i, make_uint4(0, 0, 0, 0));
+      if (tid < tail) Traits<DT>::store1(r_drow, (int64_t)nvec * N + tid, 0.f);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&slot_empty[sl]);
+    }
+    if (++st == kStages) { st = 0; sph ^= 1u; }
   }
 }
 
@@ -472,18 +765,33 @@ __global__ void __launch_bounds__(kRowThreads, 2) k_fused(LossArgs a) {
 struct DevInfo {
   int sms = 0;
   int l2 = 0;
-  int occ_fused[2] = {0, 0};
+  int occ[2][2] = {{0, 0}, {0, 0}};  // [dtype][mode] (same for every poly variant)
 };
 static DevInfo g_dev[128];
 static std::once_flag g_once[128];
+
+template <int DT, int MODE, int PV>
+static void setup_one(int* occ) {
+  cudaFuncSetAttribute(k_engine<DT, MODE, PV>, cudaFuncAttributeMaxDynamicSharedMemorySize, kEngSmem);
+  if (occ) cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, k_engine<DT, MODE, PV>, kEngThreads, kEngSmem);
+}
+template <int PV>
+static void setup_pv() {
+  setup_one<1, M_SEQ, PV>(nullptr);
+  setup_one<1, M_FUSED, PV>(nullptr);
+  if constexpr (PV + 1 < kNumPoly) setup_pv<PV + 1>();
+}
 
 static const DevInfo& dev_info(int dev) {
   std::call_once(g_once[dev], [dev]() {
     DevInfo& d = g_dev[dev];
     cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev);
     cudaDeviceGetAttribute(&d.l2, cudaDevAttrL2CacheSize, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.occ_fused[0], k_fused<0>, kRowThreads, 0);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.occ_fused[1], k_fused<1>, kRowThreads, 0);
+    setup_one<0, M_SEQ, 0>(&d.occ[0][M_SEQ]);
+    setup_one<0, M_FUSED, 0>(&d.occ[0][M_FUSED]);
+    setup_one<1, M_SEQ, 0>(&d.occ[1][M_SEQ]);
+    setup_one<1, M_FUSED, 0>(&d.occ[1][M_FUSED]);
+    setup_pv<1>();
   });
   return g_dev[dev];
 }
@@ -495,7 +803,7 @@ static odpo_status check_logits(const void* logits, odpo_dtype dt, int64_t B, in
                                 int64_t sb, int64_t st) {
   if (!logits) return ODPO_ERR_INVALID_ARG;
   if (dt != ODPO_F32 && dt != ODPO_BF16) return ODPO_ERR_INVALID_ARG;
-  if (B <= 0 || T <= 0 || V <= 0 || V > (int64_t)INT32_MAX) return ODPO_ERR_INVALID_ARG;
+  if (B <= 0 || T <= 0 || V <= 0 || V > (int64_t)INT32_MAX / 4) return ODPO_ERR_INVALID_ARG;
   if (st < V || sb < 0) return ODPO_ERR_INVALID_ARG;
   const int64_t es = dt == ODPO_F32 ? 4 : 2;
   if (!aligned16(logits) || (sb * es) % 16 || (st * es) % 16) return ODPO_ERR_ALIGNMENT;
@@ -506,6 +814,40 @@ static odpo_status check_logits(const void* logits, odpo_dtype dt, int64_t B, in
 static odpo_status launched() {
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? ODPO_OK : ODPO_ERR_CUDA;
+}
+
+template <int MODE, int PV>
+static void launch_bf16(int pv, int grid, const LossArgs& a, cudaStream_t s) {
+  if (pv == PV) {
+    k_engine<1, MODE, PV><<<grid, kEngThreads, kEngSmem, s>>>(a);
+    return;
+  }
+  if constexpr (PV + 1 < kNumPoly) launch_bf16<MODE, PV + 1>(pv, grid, a, s);
+}
+template <int PV>
+static void launch_bwd_bf16(int pv, unsigned rows, const LossArgs& a, cudaStream_t s) {
+  if (pv == PV) {
+    k_row_bwd<1, kPoly[PV].npb><<<rows, kRowThreads, 0, s>>>(a);
+    return;
+  }
+  if constexpr (PV + 1 < kNumPoly) launch_bwd_bf16<PV + 1>(pv, rows, a, s);
+}
+
+static odpo_status launch_engine(int dt, int mode, int pv, const LossArgs& a, int cps,
+                                 cudaStream_t s, int* grid_out) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const DevInfo& di = dev_info(dev);
+  int occ = di.occ[dt][mode];
+  if (occ < 1) occ = 1;
+  if (cps <= 0 || cps > occ) cps = occ;
+  const int grid = di.sms * cps;
+  if (grid_out) *grid_out = grid;
+  if (dt == 0 && mode == M_SEQ) k_engine<0, M_SEQ, 0><<<grid, kEngThreads, kEngSmem, s>>>(a);
+  if (dt == 0 && mode == M_FUSED) k_engine<0, M_FUSED, 0><<<grid, kEngThreads, kEngSmem, s>>>(a);
+  if (dt == 1 && mode == M_SEQ) launch_bf16<M_SEQ, 0>(pv, grid, a, s);
+  if (dt == 1 && mode == M_FUSED) launch_bf16<M_FUSED, 0>(pv, grid, a, s);
+  return launched();
 }
 
 }  // namespace odpo
@@ -546,6 +888,19 @@ odpo_status odpo_pair_select(const float* rewards, const uint8_t* has_eos, float
   return launched();
 }
 
+static void base_args(LossArgs& a, const void* logits, int64_t B, int64_t T, int64_t V, int64_t sb,
+                      int64_t st, const int32_t* tokens, const uint8_t* mask, float invT,
+                      uint32_t* status, const Workspace& w, int es) {
+  a.logits = logits;
+  a.B = B; a.T = T; a.V = V; a.sb = sb; a.st = st;
+  a.ref = nullptr; a.tokens = tokens; a.mask = mask; a.pair_rows = nullptr;
+  a.P = 0; a.Pg = 1.0; a.beta = 0.f; a.invT = invT;
+  a.dl = nullptr; a.dsb = 0; a.dst = 0;
+  a.seq_logp = nullptr; a.z_out = nullptr; a.stats = nullptr; a.status = status;
+  a.tok_out = nullptr; a.lse_out = nullptr; a.seqsum = 0;
+  a.w = w; a.lag = 1; a.look = kLook; a.esize = es;
+}
+
 odpo_status odpo_seq_logprobs(const void* logits, odpo_dtype dt, int64_t B, int64_t T, int64_t V,
                               int64_t stride_b, int64_t stride_t, const int32_t* tokens,
                               const uint8_t* mask, float inv_temperature, float* seq_logp,
@@ -559,14 +914,16 @@ odpo_status odpo_seq_logprobs(const void* logits, odpo_dtype dt, int64_t B, int6
   Workspace w;
   ws_layout(B, T, P, (char*)workspace, &w);
   cudaStream_t s = (cudaStream_t)stream;
-  FwdArgs f{logits, T, V, stride_b, stride_t, tokens, mask, inv_temperature,
-            w.row_m, w.row_l1p, w.row_logp, tok_logp, row_lse, status, dt == ODPO_F32 ? 4 : 2};
-  const unsigned rows = (unsigned)(B * T);
-  if (dt == ODPO_F32) k_row_fwd<0><<<rows, kRowThreads, 0, s>>>(f);
-  else k_row_fwd<1><<<rows, kRowThreads, 0, s>>>(f);
+  LossArgs a;
+  base_args(a, logits, B, T, V, stride_b, stride_t, tokens, mask, inv_temperature, status, w,
+            dt == ODPO_F32 ? 4 : 2);
+  a.seq_logp = seq_logp;
+  a.tok_out = tok_logp;
+  a.lse_out = row_lse;
+  a.seqsum = 1;
+  k_prep<<<1, kPrepThreads, 0, s>>>(nullptr, B, 0, w, nullptr);
   if ((e = launched()) != ODPO_OK) return e;
-  k_seq_sum<<<(unsigned)((B + 7) / 8), 256, 0, s>>>(w.row_logp, mask, B, T, seq_logp, status);
-  return launched();
+  return launch_engine(dt == ODPO_F32 ? 0 : 1, M_SEQ, kPolyDefault, a, 0, s, nullptr);
 }
 
 odpo_status odpo_online_dpo_loss_fwd_bwd_ex(const void* policy_logits, odpo_dtype dt, int64_t B,
@@ -596,6 +953,8 @@ odpo_status odpo_online_dpo_loss_fwd_bwd_ex(const void* policy_logits, odpo_dtyp
   if (!workspace || workspace_bytes < ws_layout(B, T, P, nullptr, nullptr)) return ODPO_ERR_WORKSPACE;
   const int sched = opts ? opts->schedule : ODPO_SCHED_AUTO;
   if (sched < ODPO_SCHED_AUTO || sched > ODPO_SCHED_TWO_PASS) return ODPO_ERR_UNSUPPORTED;
+  const int pv = (opts && opts->exp2_split >= 0) ? opts->exp2_split : kPolyDefault;
+  if (pv >= kNumPoly) return ODPO_ERR_UNSUPPORTED;
 
   Workspace w;
   ws_layout(B, T, P, (char*)workspace, &w);
@@ -605,49 +964,49 @@ odpo_status odpo_online_dpo_loss_fwd_bwd_ex(const void* policy_logits, odpo_dtyp
   const DevInfo& di = dev_info(dev);
 
   LossArgs a;
-  a.logits = policy_logits;
-  a.B = B; a.T = T; a.V = V; a.sb = stride_b; a.st = stride_t;
-  a.ref = ref_logp; a.tokens = tokens; a.mask = mask; a.pair_rows = pair_rows;
-  a.P = P; a.Pg = (double)P_global; a.beta = beta; a.invT = inv_temperature;
+  base_args(a, policy_logits, B, T, V, stride_b, stride_t, tokens, mask, inv_temperature, status,
+            w, (int)es);
+  a.ref = ref_logp; a.pair_rows = pair_rows;
+  a.P = P; a.Pg = (double)P_global; a.beta = beta;
   a.dl = dlogits; a.dsb = dstride_b; a.dst = dstride_t;
-  a.seq_logp = seq_logp; a.z_out = pair_logit; a.stats = stats; a.status = status;
-  a.w = w; a.esize = (int)es; a.lag = 1;
+  a.seq_logp = seq_logp; a.z_out = pair_logit; a.stats = stats;
 
   k_prep<<<1, kPrepThreads, 0, s>>>(pair_rows, B, P, w, status);
   if ((e = launched()) != ODPO_OK) return e;
   int launches = 1;
+  const int dti = dt == ODPO_F32 ? 0 : 1;
 
   if (sched == ODPO_SCHED_TWO_PASS) {
-    FwdArgs f{policy_logits, T, V, stride_b, stride_t, tokens, mask, inv_temperature,
-              w.row_m, w.row_l1p, w.row_logp, nullptr, nullptr, status, (int)es};
+    a.seqsum = 0;   // forward rows only; k_pair_reduce sums the sequences
+    if ((e = launch_engine(dti, M_SEQ, pv, a, opts ? opts->ctas_per_sm : 0, s, nullptr)) != ODPO_OK)
+      return e;
+    k_pair_reduce<<<(unsigned)P, 32, 0, s>>>(a);
+    if ((e = launched()) != ODPO_OK) return e;
     const unsigned rows = (unsigned)(B * T);
-    if (dt == ODPO_F32) k_row_fwd<0><<<rows, kRowThreads, 0, s>>>(f);
-    else k_row_fwd<1><<<rows, kRowThreads, 0, s>>>(f);
-    if ((e = launched()) != ODPO_OK) return e;
-    k_pair_reduce<<<(unsigned)P, 64, 0, s>>>(a);
-    if ((e = launched()) != ODPO_OK) return e;
-    if (dt == ODPO_F32) k_row_bwd<0><<<rows, kRowThreads, 0, s>>>(a);
-    else k_row_bwd<1><<<rows, kRowThreads, 0, s>>>(a);
+    if (dt == ODPO_F32) k_row_bwd<0, 0><<<rows, kRowThreads, 0, s>>>(a);
+    else launch_bwd_bf16<0>(pv, rows, a, s);
     if ((e = launched()) != ODPO_OK) return e;
     launches += 3;
   } else {
-    const int occ = di.occ_fused[dt == ODPO_F32 ? 0 : 1];
+    int occ = di.occ[dti][M_FUSED];
     int cps = (opts && opts->ctas_per_sm > 0) ? opts->ctas_per_sm : occ;
     if (cps > occ) cps = occ;
     if (cps < 1) cps = 1;
     const int grid = di.sms * cps;
     // lag: enough pairs that a pair's forward rows are finished before its backward rows are
-    // dispensed (grid rows in flight), and no more than ~40% of L2 of logits kept resident.
+    // dispensed -- each CTA holds up to kLook+2 rows between taking a ticket and finishing it,
+    // and one interleaved step dispenses 2*(2T) tickets -- but no more than ~60% of L2 of
+    // logits kept resident for the backward re-read.
     const double pair_bytes = (double)(2 * T) * (double)V * (double)es;
-    int64_t lag_min = (int64_t)grid / (2 * T) + 2;
-    int64_t lag_l2 = (int64_t)(0.4 * (double)di.l2 / pair_bytes);
-    int64_t lag = (opts && opts->lag_pairs > 0) ? opts->lag_pairs : (lag_l2 > lag_min ? lag_l2 : lag_min);
+    a.look = (opts && opts->lookahead >= 0) ? (opts->lookahead < kSlots - 2 ? opts->lookahead : kSlots - 2) : kLook;
+    const int64_t lag_min = ((int64_t)grid * (a.look + 2) + 4 * T - 1) / (4 * T) + 1;
+    const int64_t lag_l2 = (int64_t)(0.6 * (double)di.l2 / pair_bytes);
+    int64_t lag = (opts && opts->lag_pairs > 0) ? opts->lag_pairs
+                                                : (lag_min > lag_l2 ? lag_min : lag_l2);
     if (lag > P) lag = P;
     if (lag < 1) lag = 1;
     a.lag = (int)lag;
-    if (dt == ODPO_F32) k_fused<0><<<grid, kRowThreads, 0, s>>>(a);
-    else k_fused<1><<<grid, kRowThreads, 0, s>>>(a);
-    if ((e = launched()) != ODPO_OK) return e;
+    if ((e = launch_engine(dti, M_FUSED, pv, a, cps, s, nullptr)) != ODPO_OK) return e;
     launches += 1;
   }
   if (opts) opts->launches = launches;

@@ -27,6 +27,26 @@ __device__ __forceinline__ float ex2(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+// exp2 on the FMA pipe (Cody-Waite): 2^x = 2^j * p(f), j = rint(x), f = x - j in [-1/2, 1/2].
+// B200's MUFU.EX2 issues ~8 results/clk/SM, below the rate at which HBM delivers bf16 logits,
+// so a fraction of the exponentials is evaluated here instead.
+// Minimax (relative) polynomials with p(0) = 1 exactly: max rel. error 1.0e-4 (deg 3),
+// 2.9e-6 (deg 4).  x is clamped at -125 (result 2^-125 instead of a denormal/zero).
+__device__ __forceinline__ float ex2_poly3(float x) {
+  x = fmaxf(x, -125.f);
+  const float t = x + 12582912.f;  // 1.5 * 2^23: rounds x to the nearest integer j
+  const float f = x - (t - 12582912.f);
+  const float p = fmaf(fmaf(fmaf(5.500872061e-02f, f, 2.422104627e-01f), f, 6.932829022e-01f), f, 1.0f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+__device__ __forceinline__ float ex2_poly4(float x) {
+  x = fmaxf(x, -125.f);
+  const float t = x + 12582912.f;
+  const float f = x - (t - 12582912.f);
+  const float p = fmaf(fmaf(fmaf(fmaf(9.582830593e-03f, f, 5.590637028e-02f), f, 2.402409911e-01f), f,
+                            6.931241751e-01f), f, 1.0f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
 __device__ __forceinline__ float fmax_nan(float a, float b) {
   float d;
   asm("max.NaN.f32 %0, %1, %2;" : "=f"(d) : "f"(a), "f"(b));
@@ -80,6 +100,14 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void fence_acq_rel_gpu() {
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
 __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -93,6 +121,7 @@ template <>
 struct Traits<0> {
   static constexpr int N = 4;
   static constexpr uint32_t kNegInfWord = 0xFF800000u;
+  static constexpr uint32_t kSignWord = 0x80000000u;
   __device__ static __forceinline__ float vmax(const uint4& v) {
     return fmax_nan(fmax_nan(__uint_as_float(v.x), __uint_as_float(v.y)),
                     fmax_nan(__uint_as_float(v.z), __uint_as_float(v.w)));
@@ -125,6 +154,7 @@ template <>
 struct Traits<1> {
   static constexpr int N = 8;
   static constexpr uint32_t kNegInfWord = 0xFF80FF80u;
+  static constexpr uint32_t kSignWord = 0x80008000u;
   // packed max over the 16-byte vector, NaN-propagating; returns a bf16x2 word
   __device__ static __forceinline__ uint32_t vmax2(const uint4& v) {
     return bmax2_nan(bmax2_nan(v.x, v.y), bmax2_nan(v.z, v.w));
@@ -315,15 +345,37 @@ __device__ __forceinline__ RowOut row_forward(const void* row, int V, int tok, f
   return o;
 }
 
+// One 16-byte vector of the backward: |g_v| = 2^(x_v invT log2e - c') with
+// c' = m invT log2e + log1p(r) log2e - log2|coef|, so coef rides in the exponent and its sign is
+// applied to the packed result.  NPB of each 8 use the FMA-pipe exp2.
+template <int DT, int NPB, bool NEG>
+__device__ __forceinline__ uint4 bwd_vec(const uint4& v, float k2, float c) {
+  constexpr int N = Traits<DT>::N;
+  float f[N];
+  Traits<DT>::unpack(v, f);
+#pragma unroll
+  for (int j = 0; j < N; ++j) {
+    const float e = fmaf(f[j], k2, -c);
+    f[j] = j < NPB ? ex2_poly3(e) : ex2(e);
+  }
+  uint4 o = Traits<DT>::pack(f);
+  if (NEG) {  // sign of coef applied to the packed words (one LOP per 32-bit word)
+    o.x ^= Traits<DT>::kSignWord; o.y ^= Traits<DT>::kSignWord;
+    o.z ^= Traits<DT>::kSignWord; o.w ^= Traits<DT>::kSignWord;
+  }
+  return o;
+}
+
 // Whole-CTA row backward: drow[v] = coef * (exp(invT (x_v - m) - l1p) - [v == tok]).
 // tok entry written as coef * expm1(logp) (no p - 1 cancellation).
-template <int DT, int LK>
+template <int DT, int LK, int NPB>
 __device__ __forceinline__ void row_backward(const void* row, void* drow, int V, int tok,
                                              float invT, float m, float l1p, float logp,
                                              float coef, uint64_t pol) {
   constexpr int N = Traits<DT>::N;
   const float k2 = invT * kLog2e;
-  const float c = fmaf(l1p, kLog2e, m * k2);
+  const float c = fmaf(l1p, kLog2e, m * k2) - log2f(fabsf(coef));
+  const bool neg = coef < 0.f;
   const int nvec = V / N;
   const uint4* vrow = reinterpret_cast<const uint4*>(row);
   uint4* vout = reinterpret_cast<uint4*>(drow);
@@ -337,24 +389,20 @@ __device__ __forceinline__ void row_backward(const void* row, void* drow, int V,
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
       const int i = base + u * kRowThreads;
-      if (i < nvec) {
-        float f[N];
-        Traits<DT>::unpack(v[u], f);
-#pragma unroll
-        for (int j = 0; j < N; ++j) f[j] = coef * ex2(fmaf(f[j], k2, -c));
-        st16_stream(vout + i, Traits<DT>::pack(f));
-      }
+      if (i < nvec)
+        st16_stream(vout + i, neg ? bwd_vec<DT, NPB, true>(v[u], k2, c) : bwd_vec<DT, NPB, false>(v[u], k2, c));
     }
   }
+  const float gtok = coef * expm1f(logp);
   const int tail = V - nvec * N;
   if ((int)threadIdx.x < tail) {
     const int64_t v = (int64_t)nvec * N + threadIdx.x;
     const float x = Traits<DT>::load1(row, v);
-    Traits<DT>::store1(drow, v, (v == tok) ? coef * expm1f(logp) : coef * ex2(fmaf(x, k2, -c)));
+    Traits<DT>::store1(drow, v, (v == tok) ? gtok : copysignf(ex2(fmaf(x, k2, -c)), coef));
   }
   // onehot entry: written by the thread that stored tok's vector (program order)
   if (tok >= 0 && tok < nvec * N && (tok / N) % kRowThreads == (int)threadIdx.x)
-    Traits<DT>::store1(drow, tok, coef * expm1f(logp));
+    Traits<DT>::store1(drow, tok, gtok);
 }
 
 template <int DT>

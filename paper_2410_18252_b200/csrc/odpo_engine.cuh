@@ -1,0 +1,161 @@
+// odpo_engine.cuh -- persistent TMA-ring row engine (sm_100a).
+//
+// One CTA = NCW consumer warps + 1 producer warp.  The producer's elected lane draws work
+// tickets from a global counter, decodes them into row items, and streams each row's
+// vocabulary in CH-byte chunks into an S-stage shared-memory ring with 1-D TMA bulk copies
+// (cp.async.bulk ... mbarrier::complete_tx, with an L2 cache policy per item kind).
+// Consumers wait on the stage's full barrier, process the chunk out of shared memory, and
+// release it on the stage's empty barrier, so the next rows' loads are always in flight
+// while the current row is reduced.
+#pragma once
+
+#include "odpo_device.cuh"
+
+namespace odpo {
+
+constexpr int kNCW = 8;                    // consumer warps (warps 0..7)
+constexpr int kNCT = kNCW * 32;            // consumer threads
+constexpr int kProdWarp = kNCW;            // TMA producer warp
+constexpr int kEpiWarp = kNCW + 1;         // row-epilogue warp
+constexpr int kParWarp = kNCW + 2;         // backward-parameter prefetch warp
+constexpr int kEngThreads = kNCT + 96;
+constexpr int kStages = 6;
+constexpr int kChunk = 16384;              // bytes per stage
+constexpr int kCV = kChunk / 16;           // 16-byte vectors per chunk
+constexpr int kUB = kCV / kNCT;            // vectors per consumer thread per chunk
+constexpr int kSlots = 8;                  // rows in flight per CTA (row-slot ring)
+constexpr int kLook = 1;                   // default rows decoded ahead of the row being pushed
+static_assert(kCV % kNCT == 0, "chunk must split evenly over consumers");
+constexpr int kEngSmem = kStages * kChunk;
+
+// ------------------------------------------------------------------ mbarrier / TMA PTX
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_n(uint64_t* b, uint32_t n) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT%=;\n}" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* dst_smem, const void* src, uint32_t bytes,
+                                            uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst_smem)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+// ------------------------------------------------------------------ row slots
+enum { K_END = 0, K_F = 1, K_FSKIP = 2, K_B = 3, K_ZERO = 4, K_NONE = 5 };
+
+// One row in flight.  Written by the producer before it signals slot_full (epilogue) and
+// before the row's first stage (consumers); B-row parameters are added before param_ready;
+// per-warp partials and x_tok are added by the consumers before part_ready.
+struct RowSlot {
+  int32_t kind;
+  int32_t tok;
+  int32_t nchunk;
+  uint32_t pphase;  // parity of this slot's param_ready phase for this (B) row
+  int64_t p;       // pair (FUSED) or sequence (SEQ)
+  int64_t s;       // sequence
+  int64_t g;       // row = s*T + t
+  const char* row;
+  char* drow;
+  float c, coef, gtok, xtok;
+  float pm[kNCW], pr[kNCW];
+};
+
+// ------------------------------------------------------------------ per-batch online update
+// fp32 inputs (DT 0): exact exclusion of one max element (log1p form, 1e-5 contract).
+// bf16 inputs (DT 1): uniform fast path; a batch that raises the running max subtracts the
+// max element's own term (value exactly as added: p(0) = 1 for the polynomial and
+// ex2(delta) for MUFU agree to ~1e-13), keeping r free of the "1" (error ~1e-6 relative,
+// far inside the 2e-3 bf16 contract).  NPF of every 8 elements use the FMA-pipe exp2.
+template <int DT, int NB, int NPF>
+__device__ __forceinline__ void mr_batch(const uint4 (&v)[NB], float k2, float& m, float& r) {
+  constexpr int N = Traits<DT>::N;
+  float mc;
+  if constexpr (DT == 1) {
+    uint32_t w = Traits<1>::vmax2(v[0]);
+#pragma unroll
+    for (int u = 1; u < NB; ++u) w = bmax2_nan(w, Traits<1>::vmax2(v[u]));
+    mc = fmax_nan(bf_lo(w), bf_hi(w));
+  } else {
+    mc = Traits<0>::vmax(v[0]);
+#pragma unroll
+    for (int u = 1; u < NB; ++u) mc = fmax_nan(mc, Traits<0>::vmax(v[u]));
+  }
+  const bool rec = !(mc <= m);
+  if (rec) {
+    const float sc = (m == -INFINITY) ? 0.f : ex2((m - mc) * k2);
+    r = (1.f + r) * sc;
+    m = mc;
+  }
+  const float mk = m * k2;
+  if (DT == 0 && rec) {
+    float s = 0.f;
+    int neq = 0;
+#pragma unroll
+    for (int u = 0; u < NB; ++u) {
+      float f[N];
+      Traits<DT>::unpack(v[u], f);
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        if (f[j] == m) ++neq;
+        else s += ex2(fmaf(f[j], k2, -mk));
+      }
+    }
+    r += s + (float)(neq - 1);
+    return;
+  }
+  float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+  for (int u = 0; u < NB; ++u) {
+    float f[N];
+    Traits<DT>::unpack(v[u], f);
+#pragma unroll
+    for (int j = 0; j < N; j += 2) {
+      const float e0 = fmaf(f[j], k2, -mk), e1 = fmaf(f[j + 1], k2, -mk);
+      s0 += (j < NPF) ? ex2_poly4(e0) : ex2(e0);
+      s1 += (j + 1 < NPF) ? ex2_poly4(e1) : ex2(e1);
+    }
+  }
+  float s = s0 + s1;
+  if (DT == 1 && rec) s -= ex2(fmaf(m, k2, -mk));
+  r += s;
+}
+
+// warp-level fixed-order (m, r) merge; result valid in lane 0
+__device__ __forceinline__ MR warp_merge(MR v, float k2) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    MR o;
+    o.m = __shfl_down_sync(kFull, v.m, off);
+    o.r = __shfl_down_sync(kFull, v.r, off);
+    v = mr_merge(v, o, k2);
+  }
+  return v;
+}
+
+}  // namespace odpo

@@ -14,7 +14,7 @@ import synth
 NCPU = os.cpu_count() or 1
 
 TOL_SEQ = {"f32": 1e-5, "bf16": 2e-3}            # north_star: 1e-5 fp32, 2e-3 bf16 (relative)
-DL_RTOL = {"f32": 1e-5, "bf16": 2.0 ** -8}
+DL_RTOL = {"f32": 1e-5, "bf16": 2.0 ** -7}   # bf16: faithful rounding, one ulp (DESIGN R17)
 DL_ATOL = {"f32": 1e-7, "bf16": 2.0 ** -20}      # times |coef_b|
 TORCH_DT = {"f32": torch.float32, "bf16": torch.bfloat16}
 

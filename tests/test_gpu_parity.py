@@ -142,12 +142,15 @@ def test_identity_rows_bit_exact(odpo, dtype, permute, sched, shape):
             if b not in seq_role or not mask[b, t]:
                 assert not np.any(row), (b, t)
                 continue
-            nz = np.flatnonzero(row)
+            # entries above 2^-20 |coef|: underflowed softmax terms are exactly 0 on the MUFU
+            # path and <= 2^-125 |coef| on the FMA-polynomial exp2 path
+            big = 2.0 ** -20 * np.max(np.abs(row))
+            nz = np.flatnonzero(np.abs(row) > big)
             a = (tok[b, t] + 1) % V
             assert sorted(nz.tolist()) == sorted([a, tok[b, t]]), (b, t, nz[:5])
             # +coef at the anchor (softmax 1 up to the fp32 rounding of m*invT*log2e) and
             # -coef at tok (expm1(-(c+100)) = -1 exactly)
-            assert abs(row[a] + row[tok[b, t]]) <= 2.0 ** -8 * abs(row[tok[b, t]])
+            assert abs(row[a] + row[tok[b, t]]) <= 2.0 ** -7 * abs(row[tok[b, t]])  # 1 bf16 ulp (R17)
 
 
 # ------------------------------------------------------------------------ G-3/4/5 parity
