@@ -95,15 +95,16 @@ enum {
 /* Work schedules of odpo_online_dpo_loss_fwd_bwd_ex. */
 enum {
   ODPO_SCHED_AUTO = 0,     /* = FUSED                                                   */
-  ODPO_SCHED_FUSED = 1,    /* one persistent kernel: forward rows of pair s interleaved with
-                              backward rows of pair s - lag, per-pair completion counters;
-                              backward re-reads hit L2 when lag pairs fit in L2           */
+  ODPO_SCHED_FUSED = 1,    /* one persistent kernel: forward and backward rows dispatched
+                              adaptively (a backward row is taken as soon as its pair's
+                              forward pass has completed), per-pair completion counters;
+                              the backward re-read of a pair is served from L2            */
   ODPO_SCHED_TWO_PASS = 2  /* forward kernel, pair-reduce kernel, backward kernel (2R+1W) */
 };
 
 typedef struct {
   int32_t schedule;     /* ODPO_SCHED_*                                            */
-  int32_t lag_pairs;    /* FUSED: backward of pair s is issued after forward of s+lag (0 = auto) */
+  int32_t lag_pairs;    /* reserved (the fused dispatch adapts its lag); ignored             */
   int32_t ctas_per_sm;  /* FUSED: persistent CTAs per SM (0 = auto)               */
   int32_t launches;     /* OUT: number of kernels this call launched               */
   int32_t exp2_split;   /* bf16 only: index of the MUFU/FMA-polynomial exp2 split

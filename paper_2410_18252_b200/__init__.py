@@ -26,7 +26,7 @@ __all__ = ["pair_select", "seq_logprobs", "online_dpo_loss_fwd_bwd", "allreduce_
            "STAT_NAMES", "SEL_NAMES", "FLAGS"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libodpo.so")
+LIB_PATH = os.environ.get("ODPO_LIB") or os.path.join(_HERE, "libodpo.so")  # override: tuning builds
 
 STAT_NAMES = ["npairs", "loss", "ncorrect", "z_sum", "rchosen_sum", "rrej_sum",
               "schosen_sum", "srej_sum", "ntok_chosen", "ntok_rej"]

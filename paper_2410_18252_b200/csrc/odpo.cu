@@ -40,7 +40,7 @@ struct Workspace {
   unsigned* counters;  // [0] ticket, [1] pairs done, [2] n_unref
 };
 
-enum { C_TICKET = 0, C_PAIRS_DONE = 1, C_NUNREF = 2, C_COUNT = 8 };
+enum { C_TICKET = 0, C_PAIRS_DONE = 1, C_NUNREF = 2, C_BTICKET = 3, C_COUNT = 8 };
 
 static inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
@@ -324,21 +324,78 @@ __global__ void __launch_bounds__(kRowThreads, 2) k_row_bwd(LossArgs a) {
 // ------------------------------------------------------------------ the TMA-ring engine
 enum { M_SEQ = 0, M_FUSED = 1 };
 
-// Fused ticket order (R = 2T rows per pair, d = lag): F(0..d-1), then B(0), F(d), B(1),
-// F(d+1), ..., then the remaining B's, then Z rows (unreferenced sequences).  Every F ticket
-// of pair p precedes its B tickets and F work never waits, so by induction on ticket order the
-// lowest unfinished ticket always makes progress (no co-residency assumption).
-__device__ __forceinline__ void decode_block(int64_t q, int64_t P, int64_t d, bool& fwd, int64_t& p) {
-  if (q < d) { fwd = true; p = q; return; }
-  const int64_t mid = 2 * (P - d);
-  if (q < d + mid) {
-    const int64_t u = q - d;
-    fwd = (u & 1);
-    p = fwd ? d + (u >> 1) : (u >> 1);
-    return;
+// Fused dispatch (adaptive).  Two counters: forward rows in pair order (C_TICKET) and backward
+// rows followed by zero rows of unreferenced sequences (C_BTICKET).  A producer claims the
+// next backward row whenever the peeked row's pair has completed its forward pass (ready
+// flag); otherwise it claims a forward row.  Concurrent claims can overshoot the peeked row
+// into a pair whose forward rows are not all dispensed yet; such a claim is HELD by its
+// producer, which keeps dispensing forward rows itself until that pair's forward rows are all
+// dispensed, and only then queues the backward row.  Hence a queued backward row waits only on
+// forward rows that are already dispensed, forward rows never wait, and the kernel cannot
+// deadlock (no co-residency assumption).  The backward pass trails the forward pass by the
+// completion latency only, which keeps each pair's logits L2-resident for the re-read.
+struct Dispatch {
+  bool f_exh;
+  int64_t ready_pair;  // a pair known ready (cache; readiness is monotone)
+  int64_t held;        // held backward claim, -1 if none
+  int64_t ft_seen;     // lower bound of the forward counter (it only grows)
+};
+
+__device__ __forceinline__ bool fused_next(const LossArgs& a, int64_t totalF, int64_t totalB,
+                                           Dispatch& D, bool& fwd, int64_t& idx) {
+  const int64_t R = 2 * a.T;
+  unsigned* cnt = a.w.counters;
+  auto take_f = [&](int64_t& f) -> bool {
+    if (D.f_exh) return false;
+    f = (int64_t)atomicAdd(&cnt[C_TICKET], 1u);
+    if (f + 1 > D.ft_seen) D.ft_seen = f + 1;
+    if (f < totalF) return true;
+    D.f_exh = true;
+    return false;
+  };
+  for (;;) {
+    if (D.held >= 0) {
+      const int64_t need = (D.held / R + 1) * R;  // forward rows dispensed once ft >= need
+      bool disp = D.f_exh || D.ft_seen >= need;
+      if (!disp) {
+        const int64_t ft = (int64_t)ld_relaxed(&cnt[C_TICKET]);
+        if (ft > D.ft_seen) D.ft_seen = ft;
+        disp = ft >= need;
+      }
+      int64_t f;
+      if (!disp && take_f(f)) { fwd = true; idx = f; return true; }
+      fwd = false;
+      idx = D.held;
+      D.held = -1;
+      return true;
+    }
+    const int64_t bt = (int64_t)ld_relaxed(&cnt[C_BTICKET]);
+    bool takeB = false;
+    if (bt < totalB) {
+      if (bt >= totalF || D.f_exh) {
+        takeB = true;
+      } else {
+        const int64_t p = bt / R;
+        if (p == D.ready_pair) {
+          takeB = true;
+        } else if (ld_relaxed(&a.w.pair_ready[p]) != 0u) {
+          D.ready_pair = p;
+          takeB = true;
+        }
+      }
+    }
+    if (takeB) {
+      const int64_t b = (int64_t)atomicAdd(&cnt[C_BTICKET], 1u);
+      if (b >= totalB) continue;
+      if (b >= totalF || D.f_exh) { fwd = false; idx = b; return true; }
+      D.held = b;  // resolved at the top of the loop (queued now if its pair is dispensed)
+      continue;
+    }
+    int64_t f;
+    if (take_f(f)) { fwd = true; idx = f; return true; }
+    if (bt >= totalB) return false;  // everything dispensed
+    __nanosleep(128);                 // forward exhausted; wait for the next pair to complete
   }
-  fwd = false;
-  p = (P - d) + (q - d - mid);
 }
 
 // exp2 split variants (bf16): NPF / NPB of every 8 elements use the FMA-pipe polynomial in the
@@ -352,7 +409,7 @@ constexpr int kPolyDefault = 0;
 
 // Row decode (producer): ticket -> RowSlot fields.  Returns true if the row streams data.
 template <int DT, int MODE>
-__device__ __forceinline__ bool decode_row(const LossArgs& a, int64_t tk, int64_t total_fb,
+__device__ __forceinline__ bool decode_row(const LossArgs& a, int64_t tk, bool fwd_in,
                                            RowSlot& S, uint64_t& pol, uint64_t pol_keep,
                                            uint64_t pol_drop) {
   const int64_t T = a.T, R = 2 * T;
@@ -376,10 +433,10 @@ __device__ __forceinline__ bool decode_row(const LossArgs& a, int64_t tk, int64_
     S.kind = K_FSKIP;
     return false;
   }
-  if (tk < total_fb) {
-    bool fwd;
-    int64_t p;
-    decode_block(tk / R, a.P, a.lag, fwd, p);
+  const int64_t totalF = a.P * R;
+  if (tk < totalF) {
+    const bool fwd = fwd_in;
+    const int64_t p = tk / R;
     const int64_t j = tk % R;
     int64_t c, r;
     pair_seqs(a, p, c, r);
@@ -412,7 +469,7 @@ __device__ __forceinline__ bool decode_row(const LossArgs& a, int64_t tk, int64_
     }
     return false;
   }
-  const int64_t k = (tk - total_fb) / T, t = (tk - total_fb) % T;
+  const int64_t k = (tk - totalF) / T, t = (tk - totalF) % T;
   const int64_t s = __ldcg(a.w.unref + k);
   S.kind = K_ZERO;
   S.s = s;
@@ -452,7 +509,7 @@ __device__ __forceinline__ void complete_unit(const LossArgs& a, const RowSlot& 
 
 // ---- the engine: warps 0..7 consumers, warp 8 TMA producer, warp 9 row epilogue
 template <int DT, int MODE, int PV>
-__global__ void __launch_bounds__(kEngThreads, 2) k_engine(LossArgs a) {
+__global__ void __launch_bounds__(kEngThreads, ODPO_CTAS_PER_SM) k_engine(LossArgs a) {
   constexpr int NPF = DT == 1 ? kPoly[PV].npf : 0;
   constexpr int NPB = DT == 1 ? kPoly[PV].npb : 0;
   constexpr int N = Traits<DT>::N;
@@ -481,6 +538,11 @@ __global__ void __launch_bounds__(kEngThreads, 2) k_engine(LossArgs a) {
     mbar_fence_init();
   }
   __syncthreads();
+  // 32-bit shared-window addresses, hoisted out of every loop
+  const uint32_t ring_s = smem_u32(ring);
+  const uint32_t full_s = smem_u32(full), empty_s = smem_u32(empty);
+  const uint32_t sfull_s = smem_u32(slot_full), sempty_s = smem_u32(slot_empty);
+  const uint32_t pready_s = smem_u32(part_ready), mready_s = smem_u32(param_ready);
 
   const int64_t T = a.T;
   const int V = (int)a.V;
@@ -495,13 +557,10 @@ __global__ void __launch_bounds__(kEngThreads, 2) k_engine(LossArgs a) {
     const uint64_t pol_keep = policy_evict_last();
     const uint64_t pol_drop = policy_evict_first();
     const int nch = nvec > 0 ? (nvec + kCV - 1) / kCV : 1;
-    int64_t total_fb = 0, total;
-    if (MODE == M_FUSED) {
-      total_fb = 2 * a.P * 2 * T;
-      total = total_fb + (int64_t)__ldcg(&a.w.counters[C_NUNREF]) * T;
-    } else {
-      total = a.B * T;
-    }
+    const int64_t totalF = a.P * 2 * T;
+    const int64_t totalB = totalF + (int64_t)__ldcg(&a.w.counters[C_NUNREF]) * T;
+    const int64_t total = a.B * T;  // SEQ
+    Dispatch D{false, -1, -1, 0};
     // Rows are DECODED into slots up to kLook rows ahead of the row whose chunks are being
     // pushed, so the parameter warp sees backward rows early enough to hide the latency of
     // their pair-ready check and parameter loads.
@@ -511,21 +570,28 @@ __global__ void __launch_bounds__(kEngThreads, 2) k_engine(LossArgs a) {
     bool ended = false;
     for (;;) {
       while (!ended && ahead <= a.look) {
-        const int64_t tk = (int64_t)atomicAdd(&a.w.counters[C_TICKET], 1u);
-        mbar_wait(&slot_empty[dsl], dph ^ 1u);
+        int64_t tk;
+        bool fwd = true, more;
+        if (MODE == M_FUSED) {
+          more = fused_next(a, totalF, totalB, D, fwd, tk);
+        } else {
+          tk = (int64_t)atomicAdd(&a.w.counters[C_TICKET], 1u);
+          more = tk < total;
+        }
+        mbar_wait(sempty_s + 8 * dsl, dph ^ 1u);
         RowSlot& S = slots[dsl];
         uint64_t pol = pol_drop;
         bool data = false;
-        if (tk >= total) {
+        if (!more) {
           S.kind = K_END;
           ended = true;
         } else {
-          data = decode_row<DT, MODE>(a, tk, total_fb, S, pol, pol_keep, pol_drop);
+          data = decode_row<DT, MODE>(a, tk, fwd, S, pol, pol_keep, pol_drop);
         }
         S.nchunk = data ? nch : 0;
         S.pphase = (pmask >> dsl) & 1u;
         if (S.kind == K_B) pmask ^= 1u << dsl;
-        mbar_arrive(&slot_full[dsl]);
+        mbar_arrive(sfull_s + 8 * dsl);
         ++ahead;
         if (++dsl == kSlots) { dsl = 0; dph ^= 1u; }
       }
@@ -537,16 +603,16 @@ __global__ void __launch_bounds__(kEngThreads, 2) k_engine(LossArgs a) {
         const int nstage = data ? S.nchunk : 1;
         const uint64_t pol = (MODE == M_FUSED && kind == K_F) ? pol_keep : pol_drop;
         for (int c = 0; c < nstage; ++c) {
-          mbar_wait(&empty[st], sph ^ 1u);
+          mbar_wait(empty_s + 8 * st, sph ^ 1u);
           stage_slot[st] = kind == K_END ? -1 : psl;
           stage_chunk[st] = c;
           const int nv = data ? min(kCV, nvec - c * kCV) : 0;
           if (nv > 0) {
             const uint32_t bytes = (uint32_t)nv * 16u;
-            mbar_arrive_tx(&full[st], bytes);
-            tma_load_1d(ring + (size_t)st * kChunk, S.row + (size_t)c * kChunk, bytes, &full[st], pol);
+            mbar_arrive_tx(full_s + 8 * st, bytes);
+            tma_load_1d(ring_s + st * kChunk, S.row + (size_t)c * kChunk, bytes, full_s + 8 * st, pol);
           } else {
-            mbar_arrive(&full[st]);
+            mbar_arrive(full_s + 8 * st);
           }
           if (++st == kStages) { st = 0; sph ^= 1u; }
         }
@@ -566,7 +632,7 @@ __global__ void __launch_bounds__(kEngThreads, 2) k_engine(LossArgs a) {
     int sl = 0;
     uint32_t lph = 0;
     for (;;) {
-      mbar_wait(&slot_full[sl], lph);
+      mbar_wait(sfull_s + 8 * sl, lph);
       RowSlot& S = slots[sl];
       const int kind = S.kind;
       if (kind == K_END) break;
@@ -581,9 +647,9 @@ __global__ void __launch_bounds__(kEngThreads, 2) k_engine(LossArgs a) {
         S.c = fmaf(l1p, kLog2e, m * k2) - log2f(fabsf(coef));
         S.coef = coef;
         S.gtok = coef * expm1f(logp);
-        mbar_arrive(&param_ready[sl]);
+        mbar_arrive(mready_s + 8 * sl);
       }
-      mbar_arrive(&slot_empty[sl]);
+      mbar_arrive(sempty_s + 8 * sl);
       if (++sl == kSlots) { sl = 0; lph ^= 1u; }
     }
     return;
@@ -595,7 +661,7 @@ __global__ void __launch_bounds__(kEngThreads, 2) k_engine(LossArgs a) {
     uint32_t lph = 0;
     uint32_t rmask = 0;  // per-slot parity of part_ready (advances only on consumer rows)
     for (;;) {
-      mbar_wait(&slot_full[sl], lph);
+      mbar_wait(sfull_s + 8 * sl, lph);
       const RowSlot& S = slots[sl];
       const int kind = S.kind;
       if (kind == K_END) break;
@@ -603,7 +669,7 @@ __global__ void __launch_bounds__(kEngThreads, 2) k_engine(LossArgs a) {
       // released by their consumers directly, so a backward row waiting for its pair never
       // holds up the counting of later forward rows (no head-of-line blocking).
       if (kind == K_F) {
-        mbar_wait(&part_ready[sl], (rmask >> sl) & 1u);
+        mbar_wait(pready_s + 8 * sl, (rmask >> sl) & 1u);
         rmask ^= 1u << sl;
       }
       if (kind == K_F) {
@@ -642,7 +708,7 @@ __global__ void __launch_bounds__(kEngThreads, 2) k_engine(LossArgs a) {
       __syncwarp();
       // rows the consumers never see also carry their kNCW arrivals
       if (lane == 0)
-        mbar_arrive_n(&slot_empty[sl], (kind == K_FSKIP || kind == K_NONE) ? 1u + kNCW : 1u);
+        mbar_arrive_n(sempty_s + 8 * sl, (kind == K_FSKIP || kind == K_NONE) ? 1u + kNCW : 1u);
       if (++sl == kSlots) { sl = 0; lph ^= 1u; }
     }
     return;
@@ -654,33 +720,40 @@ __global__ void __launch_bounds__(kEngThreads, 2) k_engine(LossArgs a) {
   uint32_t sph = 0;
   MR s{-INFINITY, 0.f};
   float b_c = 0.f, b_coef = 0.f, b_gtok = 0.f;
-  int r_kind = K_NONE, r_tok = 0, r_nch = 1;
+  int r_kind = K_NONE, r_tok = 0, r_nch = 1, r_tch = -1, r_tvl = -1;
   const char* r_row = nullptr;
   char* r_drow = nullptr;
   for (;;) {
-    mbar_wait(&full[st], sph);
+    mbar_wait(full_s + 8 * st, sph);
     const int sl = stage_slot[st];
     if (sl < 0) break;
     const int ch = stage_chunk[st];
     RowSlot& S = slots[sl];
-    if (ch == 0) {  // a new row: cache its fields (rows occupy consecutive stages)
+    if (ch == 0) {  // a new row: cache its fields (a row's chunks occupy consecutive stages)
       r_kind = S.kind;
       r_tok = S.tok;
       r_nch = S.nchunk > 0 ? S.nchunk : 1;
       r_row = S.row;
       r_drow = S.drow;
+      // the vector holding tok: its chunk and its chunk-local vector index (-1: none / tail)
+      const int tvec = (r_tok >= 0 && r_tok < nvec * N) ? r_tok / N : -1;
+      r_tch = tvec >= 0 ? tvec / kCV : -1;
+      r_tvl = tvec >= 0 ? tvec - r_tch * kCV : -1;
     }
     const int kind = r_kind;
-    const int tok = r_tok;
     const bool last_chunk = ch == r_nch - 1;
     const uint4* sv = reinterpret_cast<const uint4*>(ring + (size_t)st * kChunk);
     const int c0 = ch * kCV;
-    const int cnv = (kind == K_F || kind == K_B) ? min(kCV, nvec - c0) : 0;
-    const int tv = (tok >= 0 && tok < nvec * N) ? tok / N - c0 : -1;  // tok's vector in this chunk
-    const bool own_tok = tv >= 0 && tv < cnv && (tv % kNCT) == tid;
+    const int cnv = min(kCV, nvec - c0);
+    const bool own_tok = ch == r_tch && (r_tvl % kNCT) == tid;
     if (kind == K_F) {
       if (ch == 0) s = MR{-INFINITY, 0.f};
-      if (tid < cnv) {
+      if (cnv == kCV) {  // full chunk: no predication
+        uint4 v[kUB];
+#pragma unroll
+        for (int u = 0; u < kUB; ++u) v[u] = sv[tid + u * kNCT];
+        mr_batch<DT, kUB, NPF>(v, k2, s.m, s.r);
+      } else if (tid < cnv) {
         uint4 v[kUB];
 #pragma unroll
         for (int u = 0; u < kUB; ++u) {
@@ -691,71 +764,77 @@ __global__ void __launch_bounds__(kEngThreads, 2) k_engine(LossArgs a) {
       }
       if (own_tok) {
         float f[N];
-        Traits<DT>::unpack(sv[tv], f);
+        Traits<DT>::unpack(sv[r_tvl], f);
         float x = f[0];
 #pragma unroll
-        for (int j = 1; j < N; ++j) x = (tok % N == j) ? f[j] : x;
+        for (int j = 1; j < N; ++j) x = (r_tok % N == j) ? f[j] : x;
         S.xtok = x;
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[st]);
+      if (lane == 0) mbar_arrive(empty_s + 8 * st);
       if (last_chunk) {
         if (tid < tail) {
           const int64_t vv = (int64_t)nvec * N + tid;
           const float x = Traits<DT>::load1(r_row, vv);
           s = mr_push1(s, x, k2);
-          if (vv == tok) S.xtok = x;
+          if (vv == r_tok) S.xtok = x;
         }
         const MR wv = warp_merge(s, k2);
         if (lane == 0) {
           S.pm[warp] = wv.m;
           S.pr[warp] = wv.r;
-          mbar_arrive(&part_ready[sl]);
-          mbar_arrive(&slot_empty[sl]);
+          mbar_arrive(pready_s + 8 * sl);
+          mbar_arrive(sempty_s + 8 * sl);
         }
       }
     } else if (kind == K_B) {
       if (ch == 0) {
-        mbar_wait(&param_ready[sl], S.pphase);
+        mbar_wait(mready_s + 8 * sl, S.pphase);
         b_c = S.c;
         b_coef = S.coef;
         b_gtok = S.gtok;
       }
       uint4* vout = reinterpret_cast<uint4*>(r_drow) + c0;
-      if (b_coef < 0.f) {
+      if (cnv == kCV) {
+        if (b_coef < 0.f) {
 #pragma unroll
-        for (int u = 0; u < kUB; ++u) {
-          const int i = tid + u * kNCT;
-          if (i < cnv) st16_stream(vout + i, bwd_vec<DT, NPB, true>(sv[i], k2, b_c));
+          for (int u = 0; u < kUB; ++u)
+            st16_stream(vout + tid + u * kNCT, bwd_vec<DT, NPB, true>(sv[tid + u * kNCT], k2, b_c));
+        } else {
+#pragma unroll
+          for (int u = 0; u < kUB; ++u)
+            st16_stream(vout + tid + u * kNCT, bwd_vec<DT, NPB, false>(sv[tid + u * kNCT], k2, b_c));
         }
       } else {
 #pragma unroll
         for (int u = 0; u < kUB; ++u) {
           const int i = tid + u * kNCT;
-          if (i < cnv) st16_stream(vout + i, bwd_vec<DT, NPB, false>(sv[i], k2, b_c));
+          if (i < cnv)
+            st16_stream(vout + i, b_coef < 0.f ? bwd_vec<DT, NPB, true>(sv[i], k2, b_c)
+                                               : bwd_vec<DT, NPB, false>(sv[i], k2, b_c));
         }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[st]);
+      if (lane == 0) mbar_arrive(empty_s + 8 * st);
       // onehot entry: the thread that stored tok's vector overwrites it (program order)
-      if (own_tok) Traits<DT>::store1(r_drow, tok, b_gtok);
+      if (own_tok) Traits<DT>::store1(r_drow, r_tok, b_gtok);
       if (last_chunk) {
         if (tid < tail) {
           const int64_t vv = (int64_t)nvec * N + tid;
           const float x = Traits<DT>::load1(r_row, vv);
-          Traits<DT>::store1(r_drow, vv, vv == tok ? b_gtok : copysignf(ex2(fmaf(x, k2, -b_c)), b_coef));
+          Traits<DT>::store1(r_drow, vv, vv == r_tok ? b_gtok : copysignf(ex2(fmaf(x, k2, -b_c)), b_coef));
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(&slot_empty[sl]);
+        if (lane == 0) mbar_arrive(sempty_s + 8 * sl);
       }
     } else {  // K_ZERO
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[st]);
+      if (lane == 0) mbar_arrive(empty_s + 8 * st);
       uint4* vout = reinterpret_cast<uint4*>(r_drow);
       for (int i = tid; i < nvec; i += kNCT) st16_stream(vout + i, make_uint4(0, 0, 0, 0));
       if (tid < tail) Traits<DT>::store1(r_drow, (int64_t)nvec * N + tid, 0.f);
       __syncwarp();
-      if (lane == 0) mbar_arrive(&slot_empty[sl]);
+      if (lane == 0) mbar_arrive(sempty_s + 8 * sl);
     }
     if (++st == kStages) { st = 0; sph ^= 1u; }
   }
@@ -993,19 +1072,7 @@ odpo_status odpo_online_dpo_loss_fwd_bwd_ex(const void* policy_logits, odpo_dtyp
     if (cps > occ) cps = occ;
     if (cps < 1) cps = 1;
     const int grid = di.sms * cps;
-    // lag: enough pairs that a pair's forward rows are finished before its backward rows are
-    // dispensed -- each CTA holds up to kLook+2 rows between taking a ticket and finishing it,
-    // and one interleaved step dispenses 2*(2T) tickets -- but no more than ~60% of L2 of
-    // logits kept resident for the backward re-read.
-    const double pair_bytes = (double)(2 * T) * (double)V * (double)es;
     a.look = (opts && opts->lookahead >= 0) ? (opts->lookahead < kSlots - 2 ? opts->lookahead : kSlots - 2) : kLook;
-    const int64_t lag_min = ((int64_t)grid * (a.look + 2) + 4 * T - 1) / (4 * T) + 1;
-    const int64_t lag_l2 = (int64_t)(0.6 * (double)di.l2 / pair_bytes);
-    int64_t lag = (opts && opts->lag_pairs > 0) ? opts->lag_pairs
-                                                : (lag_min > lag_l2 ? lag_min : lag_l2);
-    if (lag > P) lag = P;
-    if (lag < 1) lag = 1;
-    a.lag = (int)lag;
     if ((e = launch_engine(dti, M_FUSED, pv, a, cps, s, nullptr)) != ODPO_OK) return e;
     launches += 1;
   }

@@ -47,6 +47,26 @@ __device__ __forceinline__ float ex2_poly4(float x) {
                             6.931241751e-01f), f, 1.0f);
   return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
 }
+// ---- packed fp32x2 arithmetic (Blackwell FFMA2 / FADD2: two lanes of fp32 per instruction)
+typedef unsigned long long f32x2;
+__device__ __forceinline__ f32x2 pk2(float a, float b) {
+  f32x2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void upk2(f32x2 v, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ f32x2 ffma2(f32x2 a, f32x2 b, f32x2 c) {
+  f32x2 r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ f32x2 fadd2(f32x2 a, f32x2 b) {
+  f32x2 r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
 __device__ __forceinline__ float fmax_nan(float a, float b) {
   float d;
   asm("max.NaN.f32 %0, %1, %2;" : "=f"(d) : "f"(a), "f"(b));
@@ -353,10 +373,13 @@ __device__ __forceinline__ uint4 bwd_vec(const uint4& v, float k2, float c) {
   constexpr int N = Traits<DT>::N;
   float f[N];
   Traits<DT>::unpack(v, f);
+  const f32x2 K2 = pk2(k2, k2), NC = pk2(-c, -c);
 #pragma unroll
-  for (int j = 0; j < N; ++j) {
-    const float e = fmaf(f[j], k2, -c);
-    f[j] = j < NPB ? ex2_poly3(e) : ex2(e);
+  for (int j = 0; j < N; j += 2) {
+    float e0, e1;   // two exp2 arguments per FFMA2
+    upk2(ffma2(pk2(f[j], f[j + 1]), K2, NC), e0, e1);
+    f[j] = j < NPB ? ex2_poly3(e0) : ex2(e0);
+    f[j + 1] = j + 1 < NPB ? ex2_poly3(e1) : ex2(e1);
   }
   uint4 o = Traits<DT>::pack(f);
   if (NEG) {  // sign of coef applied to the packed words (one LOP per 32-bit word)

@@ -13,14 +13,26 @@
 
 namespace odpo {
 
-constexpr int kNCW = 8;                    // consumer warps (warps 0..7)
+#ifndef ODPO_NCW
+#define ODPO_NCW 8
+#endif
+#ifndef ODPO_STAGES
+#define ODPO_STAGES 6
+#endif
+#ifndef ODPO_CHUNK
+#define ODPO_CHUNK 16384
+#endif
+#ifndef ODPO_CTAS_PER_SM
+#define ODPO_CTAS_PER_SM 2
+#endif
+constexpr int kNCW = ODPO_NCW;             // consumer warps (warps 0..kNCW-1)
 constexpr int kNCT = kNCW * 32;            // consumer threads
 constexpr int kProdWarp = kNCW;            // TMA producer warp
 constexpr int kEpiWarp = kNCW + 1;         // row-epilogue warp
 constexpr int kParWarp = kNCW + 2;         // backward-parameter prefetch warp
 constexpr int kEngThreads = kNCT + 96;
-constexpr int kStages = 6;
-constexpr int kChunk = 16384;              // bytes per stage
+constexpr int kStages = ODPO_STAGES;
+constexpr int kChunk = ODPO_CHUNK;         // bytes per stage
 constexpr int kCV = kChunk / 16;           // 16-byte vectors per chunk
 constexpr int kUB = kCV / kNCT;            // vectors per consumer thread per chunk
 constexpr int kSlots = 8;                  // rows in flight per CTA (row-slot ring)
@@ -38,32 +50,34 @@ __device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
 __device__ __forceinline__ void mbar_fence_init() {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
-__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+// All barrier operations below take 32-bit shared-window addresses (hoisted out of loops).
+__device__ __forceinline__ void mbar_arrive(uint32_t b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(b) : "memory");
 }
-__device__ __forceinline__ void mbar_arrive_n(uint64_t* b, uint32_t n) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(n) : "memory");
+__device__ __forceinline__ void mbar_arrive_n(uint32_t b, uint32_t n) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(n) : "memory");
 }
-__device__ __forceinline__ void mbar_arrive_tx(uint64_t* b, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
-               "r"(bytes)
+__device__ __forceinline__ void mbar_arrive_tx(uint32_t b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes)
                : "memory");
 }
-__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+// Blocking wait on the phase with the given parity.  The suspend-time hint lets the hardware
+// park the warp until the phase completes instead of spinning through issue slots.
+__device__ __forceinline__ void mbar_wait(uint32_t b, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n"
       "WAIT%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAIT%=;\n}" ::"r"(smem_u32(b)),
-      "r"(parity)
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+      "@!p bra WAIT%=;\n}" ::"r"(b),
+      "r"(parity), "r"(1000000u)
       : "memory");
 }
-__device__ __forceinline__ void tma_load_1d(void* dst_smem, const void* src, uint32_t bytes,
-                                            uint64_t* bar, uint64_t pol) {
+__device__ __forceinline__ void tma_load_1d(uint32_t dst_smem, const void* src, uint32_t bytes,
+                                            uint32_t bar, uint64_t pol) {
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-      " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst_smem)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      " [%0], [%1], %2, [%3], %4;" ::"r"(dst_smem),
+      "l"(src), "r"(bytes), "r"(bar), "l"(pol)
       : "memory");
 }
 // ------------------------------------------------------------------ row slots
@@ -129,18 +143,22 @@ __device__ __forceinline__ void mr_batch(const uint4 (&v)[NB], float k2, float& 
     r += s + (float)(neq - 1);
     return;
   }
-  float s0 = 0.f, s1 = 0.f;
+  // fast path: exp2 arguments two at a time (FFMA2) and two running sums (FADD2)
+  const f32x2 K2 = pk2(k2, k2), NMK = pk2(-mk, -mk);
+  f32x2 acc = pk2(0.f, 0.f);
 #pragma unroll
   for (int u = 0; u < NB; ++u) {
     float f[N];
     Traits<DT>::unpack(v[u], f);
 #pragma unroll
     for (int j = 0; j < N; j += 2) {
-      const float e0 = fmaf(f[j], k2, -mk), e1 = fmaf(f[j + 1], k2, -mk);
-      s0 += (j < NPF) ? ex2_poly4(e0) : ex2(e0);
-      s1 += (j + 1 < NPF) ? ex2_poly4(e1) : ex2(e1);
+      float e0, e1;
+      upk2(ffma2(pk2(f[j], f[j + 1]), K2, NMK), e0, e1);
+      acc = fadd2(acc, pk2((j < NPF) ? ex2_poly4(e0) : ex2(e0), (j + 1 < NPF) ? ex2_poly4(e1) : ex2(e1)));
     }
   }
+  float s0, s1;
+  upk2(acc, s0, s1);
   float s = s0 + s1;
   if (DT == 1 && rec) s -= ex2(fmaf(m, k2, -mk));
   r += s;
