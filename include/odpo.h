@@ -104,7 +104,8 @@ enum {
 
 typedef struct {
   int32_t schedule;     /* ODPO_SCHED_*                                            */
-  int32_t lag_pairs;    /* reserved (the fused dispatch adapts its lag); ignored             */
+  int32_t lag_pairs;    /* FUSED: cap, in pairs, on how far the forward pass may run ahead of
+                           the backward pass (0 = no cap)                             */
   int32_t ctas_per_sm;  /* FUSED: persistent CTAs per SM (0 = auto)               */
   int32_t launches;     /* OUT: number of kernels this call launched               */
   int32_t exp2_split;   /* bf16 only: index of the MUFU/FMA-polynomial exp2 split

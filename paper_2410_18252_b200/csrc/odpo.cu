@@ -15,6 +15,7 @@
 #include <math.h>
 #include <stdint.h>
 
+#include <cstdio>
 #include <mutex>
 
 #include "odpo.h"
@@ -40,7 +41,8 @@ struct Workspace {
   unsigned* counters;  // [0] ticket, [1] pairs done, [2] n_unref
 };
 
-enum { C_TICKET = 0, C_PAIRS_DONE = 1, C_NUNREF = 2, C_BTICKET = 3, C_COUNT = 8 };
+enum { C_TICKET = 0, C_PAIRS_DONE = 1, C_NUNREF = 2, C_BTICKET = 3, C_DBG_SUM = 4, C_DBG_N = 5,
+       C_DBG_MAX = 6, C_DBG_DONE = 7, C_COUNT = 8 };
 
 static inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
@@ -212,6 +214,7 @@ struct LossArgs {
   int seqsum;       // SEQ: sum sequences (seq_logprobs) or only write row stats (TWO_PASS)
   Workspace w;
   int lag;
+  int64_t max_lead;  // FUSED: cap on forward rows dispensed ahead of the backward frontier
   int look;         // producer decode lookahead (rows), <= kSlots - 2
   int esize;
 };
@@ -328,12 +331,13 @@ enum { M_SEQ = 0, M_FUSED = 1 };
 // rows followed by zero rows of unreferenced sequences (C_BTICKET).  A producer claims the
 // next backward row whenever the peeked row's pair has completed its forward pass (ready
 // flag); otherwise it claims a forward row.  Concurrent claims can overshoot the peeked row
-// into a pair whose forward rows are not all dispensed yet; such a claim is HELD by its
-// producer, which keeps dispensing forward rows itself until that pair's forward rows are all
-// dispensed, and only then queues the backward row.  Hence a queued backward row waits only on
-// forward rows that are already dispensed, forward rows never wait, and the kernel cannot
-// deadlock (no co-residency assumption).  The backward pass trails the forward pass by the
-// completion latency only, which keeps each pair's logits L2-resident for the re-read.
+// into a pair that is not complete yet; such a claim is HELD by its producer, which keeps
+// dispensing forward rows itself until that pair is ready, and only then queues the backward
+// row.  Hence a queued backward row never waits (except after every forward row has been
+// dispensed, when the wait is for dispensed rows only), forward rows never wait, and the
+// kernel cannot deadlock (no co-residency assumption).  The backward pass trails the forward
+// pass by the completion latency only, which keeps each pair's logits L2-resident for the
+// backward re-read.
 struct Dispatch {
   bool f_exh;
   int64_t ready_pair;  // a pair known ready (cache; readiness is monotone)
@@ -341,8 +345,11 @@ struct Dispatch {
   int64_t ft_seen;     // lower bound of the forward counter (it only grows)
 };
 
-__device__ __forceinline__ bool fused_next(const LossArgs& a, int64_t totalF, int64_t totalB,
-                                           Dispatch& D, bool& fwd, int64_t& idx) {
+// Returns 1 (a row was claimed), 0 (everything dispensed) or -1 (nothing to claim right now;
+// only when may_block is false -- the producer then streams the rows it already holds, which
+// is what lets the rows it is waiting for complete).
+__device__ __forceinline__ int fused_next(const LossArgs& a, int64_t totalF, int64_t totalB,
+                                          Dispatch& D, bool may_block, bool& fwd, int64_t& idx) {
   const int64_t R = 2 * a.T;
   unsigned* cnt = a.w.counters;
   auto take_f = [&](int64_t& f) -> bool {
@@ -355,19 +362,29 @@ __device__ __forceinline__ bool fused_next(const LossArgs& a, int64_t totalF, in
   };
   for (;;) {
     if (D.held >= 0) {
-      const int64_t need = (D.held / R + 1) * R;  // forward rows dispensed once ft >= need
-      bool disp = D.f_exh || D.ft_seen >= need;
-      if (!disp) {
-        const int64_t ft = (int64_t)ld_relaxed(&cnt[C_TICKET]);
-        if (ft > D.ft_seen) D.ft_seen = ft;
-        disp = ft >= need;
+      // queue the held backward row once its pair is READY (then it never waits); until
+      // then keep this producer busy with forward rows
+      const int64_t hp = D.held / R;
+      bool rdy = D.f_exh || hp == D.ready_pair;
+      if (!rdy && ld_relaxed(&a.w.pair_ready[hp]) != 0u) {
+        D.ready_pair = hp;
+        rdy = true;
       }
       int64_t f;
-      if (!disp && take_f(f)) { fwd = true; idx = f; return true; }
+      if (!rdy && take_f(f)) { fwd = true; idx = f; return 1; }
       fwd = false;
       idx = D.held;
       D.held = -1;
-      return true;
+#ifdef ODPO_DEBUG_LEAD
+      if (idx < totalF) {
+        const int64_t ft = (int64_t)ld_relaxed(&cnt[C_TICKET]);
+        const unsigned lead = (unsigned)(ft > idx ? ft - idx : 0);
+        atomicAdd(&cnt[C_DBG_SUM], lead);
+        atomicAdd(&cnt[C_DBG_N], 1u);
+        atomicMax(&cnt[C_DBG_MAX], lead);
+      }
+#endif
+      return 1;
     }
     const int64_t bt = (int64_t)ld_relaxed(&cnt[C_BTICKET]);
     bool takeB = false;
@@ -387,13 +404,27 @@ __device__ __forceinline__ bool fused_next(const LossArgs& a, int64_t totalF, in
     if (takeB) {
       const int64_t b = (int64_t)atomicAdd(&cnt[C_BTICKET], 1u);
       if (b >= totalB) continue;
-      if (b >= totalF || D.f_exh) { fwd = false; idx = b; return true; }
+      if (b >= totalF || D.f_exh) { fwd = false; idx = b; return 1; }
       D.held = b;  // resolved at the top of the loop (queued now if its pair is dispensed)
       continue;
     }
+    // forward rows, unless the forward frontier already leads the backward frontier by the
+    // L2 budget (max_lead rows): then wait for the next backward pair instead, so that the
+    // logits between the two frontiers stay L2-resident.  max_lead >= 2R keeps the next
+    // backward pair fully dispensed, so this wait always terminates.
+    if (!D.f_exh && bt < totalF && D.ft_seen - bt >= a.max_lead) {
+      const int64_t ft = (int64_t)ld_relaxed(&cnt[C_TICKET]);
+      if (ft > D.ft_seen) D.ft_seen = ft;
+      if (ft - bt >= a.max_lead) {
+        if (!may_block) return -1;
+        __nanosleep(64);
+        continue;
+      }
+    }
     int64_t f;
-    if (take_f(f)) { fwd = true; idx = f; return true; }
-    if (bt >= totalB) return false;  // everything dispensed
+    if (take_f(f)) { fwd = true; idx = f; return 1; }
+    if (bt >= totalB) return 0;  // everything dispensed
+    if (!may_block) return -1;
     __nanosleep(128);                 // forward exhausted; wait for the next pair to complete
   }
 }
@@ -573,7 +604,9 @@ __global__ void __launch_bounds__(kEngThreads, ODPO_CTAS_PER_SM) k_engine(LossAr
         int64_t tk;
         bool fwd = true, more;
         if (MODE == M_FUSED) {
-          more = fused_next(a, totalF, totalB, D, fwd, tk);
+          const int r = fused_next(a, totalF, totalB, D, ahead == 0, fwd, tk);
+          if (r < 0) break;  // stream the rows already held, then retry
+          more = r > 0;
         } else {
           tk = (int64_t)atomicAdd(&a.w.counters[C_TICKET], 1u);
           more = tk < total;
@@ -621,6 +654,14 @@ __global__ void __launch_bounds__(kEngThreads, ODPO_CTAS_PER_SM) k_engine(LossAr
       if (++psl == kSlots) psl = 0;
       if (kind == K_END) break;
     }
+#ifdef ODPO_DEBUG_LEAD
+    if (MODE == M_FUSED && atomicAdd(&a.w.counters[C_DBG_DONE], 1u) == gridDim.x - 1) {
+      const unsigned n = ld_relaxed(&a.w.counters[C_DBG_N]);
+      printf("ODPO_DEBUG_LEAD: backward claims %u, mean forward lead %.1f rows, max %u rows (2T=%d)\n",
+             n, n ? (double)ld_relaxed(&a.w.counters[C_DBG_SUM]) / n : 0.0,
+             ld_relaxed(&a.w.counters[C_DBG_MAX]), (int)(2 * T));
+    }
+#endif
     return;
   }
 
@@ -977,7 +1018,7 @@ static void base_args(LossArgs& a, const void* logits, int64_t B, int64_t T, int
   a.dl = nullptr; a.dsb = 0; a.dst = 0;
   a.seq_logp = nullptr; a.z_out = nullptr; a.stats = nullptr; a.status = status;
   a.tok_out = nullptr; a.lse_out = nullptr; a.seqsum = 0;
-  a.w = w; a.lag = 1; a.look = kLook; a.esize = es;
+  a.w = w; a.lag = 1; a.max_lead = 1; a.look = kLook; a.esize = es;
 }
 
 odpo_status odpo_seq_logprobs(const void* logits, odpo_dtype dt, int64_t B, int64_t T, int64_t V,
@@ -1073,6 +1114,18 @@ odpo_status odpo_online_dpo_loss_fwd_bwd_ex(const void* policy_logits, odpo_dtyp
     if (cps < 1) cps = 1;
     const int grid = di.sms * cps;
     a.look = (opts && opts->lookahead >= 0) ? (opts->lookahead < kSlots - 2 ? opts->lookahead : kSlots - 2) : kLook;
+    {
+      // L2 budget for logits kept between the forward and backward frontiers
+      const int64_t row_bytes = V * es;
+      const int64_t R = 2 * T;
+      // default: no cap (measured: capping the lead idles CTAs more than it saves in L2
+      // misses with row-granular work units)
+      int64_t lead = (opts && opts->lag_pairs > 0) ? (int64_t)opts->lag_pairs * R
+                                                   : (int64_t)INT32_MAX;
+      (void)row_bytes;
+      if (lead < 2 * R) lead = 2 * R;
+      a.max_lead = lead;
+    }
     if ((e = launch_engine(dti, M_FUSED, pv, a, cps, s, nullptr)) != ODPO_OK) return e;
     launches += 1;
   }

@@ -13,17 +13,19 @@
 
 namespace odpo {
 
+// Engine geometry (tuned on B200 for the BASELINE shapes; see profiles/ and DESIGN.md):
+// 4 consumer warps per CTA, a 3 x 16 KB TMA ring, 4 CTAs per SM.
 #ifndef ODPO_NCW
-#define ODPO_NCW 8
+#define ODPO_NCW 4
 #endif
 #ifndef ODPO_STAGES
-#define ODPO_STAGES 6
+#define ODPO_STAGES 3
 #endif
 #ifndef ODPO_CHUNK
 #define ODPO_CHUNK 16384
 #endif
 #ifndef ODPO_CTAS_PER_SM
-#define ODPO_CTAS_PER_SM 2
+#define ODPO_CTAS_PER_SM 4
 #endif
 constexpr int kNCW = ODPO_NCW;             // consumer warps (warps 0..kNCW-1)
 constexpr int kNCT = kNCW * 32;            // consumer threads
