@@ -51,6 +51,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
     return ap.parse_args()
 
 
@@ -146,7 +147,7 @@ def run_reference(args, rank, world):
         return
     w = workload(args.config)
     cores = os.cpu_count() or 1
-    npairs = max(1, min(w.P, cores // 2 if w.T * w.V < 1e7 else 1))
+    npairs = max(1, min(w.P, cores // 2)) if w.T * w.V < 1e7 else 1
     threads = min(cores, 2 * npairs)
     for _ in range(max(0, min(args.warmup, 1))):
         oracle_sample(w, args.seed, npairs, args.mask, threads)
@@ -337,13 +338,21 @@ def run_ours(args, rank, world, local_rank):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
+        # the oracle as it stands, on successive blocks of this workload's pairs until about
+        # args.cpu_seconds of CPU work have been timed (a bounded sample)
         cores = os.cpu_count() or 1
-        npairs = max(1, min(P, max(2, cores // 4))) if w.T * w.V < 1e7 else 1
+        npairs = max(1, min(P, cores // 2)) if w.T * w.V < 1e7 else 1
         threads = min(cores, 2 * npairs)
-        dt, _ = oracle_sample(w, args.seed, npairs, args.mask, threads)
-        cpu = {"value": npairs / dt, "unit": "pairs/s", "cores": threads, "kind": "oracle",
-               "sample": f"{npairs} pairs of the {args.config} workload (pair_select + fp64 loss + "
-                         f"full dlogits), {dt:.1f} s on {threads} host threads"}
+        done, spent, p0c = 0, 0.0, 0
+        while spent < args.cpu_seconds and done < 64 * P:
+            dt, _ = oracle_sample(w, args.seed, npairs, args.mask, threads, p0=p0c % P)
+            spent += dt
+            done += npairs
+            p0c += npairs
+        cpu = {"value": done / spent, "unit": "pairs/s", "cores": threads, "kind": "oracle",
+               "sample": f"{done} pairs of the {args.config} workload in blocks of {npairs} "
+                         f"(pair_select + fp64 loss + full dlogits), {spent:.1f} s on {threads} "
+                         f"host threads"}
 
     if rank == 0:
         line = {

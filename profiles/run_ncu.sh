@@ -9,7 +9,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file gpurun_out/${TAG}_launches.csv \
     python bench.py --steps 3 --warmup 1 --no-e2e --no-cpu "$@" > gpurun_out/${TAG}_launches_bench.log 2>&1
 # 2) one full capture of the top kernels
-ncu --set full --clock-control none --import-source on -k regex:"k_fused|k_row_fwd|k_row_bwd" -s 1 -c 3 \
+ncu --set full --clock-control none --import-source on -k regex:"k_engine|k_row_bwd" -s 2 -c 2 \
     -o gpurun_out/${TAG}_prof -f \
     python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu "$@" > gpurun_out/${TAG}_prof_bench.log 2>&1
 ls -la gpurun_out
