@@ -37,12 +37,14 @@ struct Workspace {
   unsigned* seq_cnt;   // forward rows done per sequence (SEQ mode)
   unsigned* pair_cnt;  // forward rows done per pair (FUSED)
   unsigned* pair_ready;
+  unsigned* pair_bcnt; // backward rows dispensed per pair (FUSED dispatch)
   double* pair_vals;   // [P][ODPO_NSTATS]
+  unsigned long long* dbg_t;  // debug builds: [P][4] timestamps
   unsigned* counters;  // [0] ticket, [1] pairs done, [2] n_unref
 };
 
-enum { C_TICKET = 0, C_PAIRS_DONE = 1, C_NUNREF = 2, C_BTICKET = 3, C_DBG_SUM = 4, C_DBG_N = 5,
-       C_DBG_MAX = 6, C_DBG_DONE = 7, C_COUNT = 8 };
+enum { C_TICKET = 0, C_PAIRS_DONE = 1, C_NUNREF = 2, C_BPAIR = 3, C_ZTICKET = 4, C_DBG_SUM = 5,
+       C_DBG_N = 6, C_DBG_MAX = 7, C_DBG_DONE = 8, C_COUNT = 16 };
 
 static inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
@@ -63,9 +65,16 @@ static size_t ws_layout(int64_t B, int64_t T, int64_t P, char* base, Workspace* 
   char* p_sc = take((size_t)B * 4);
   char* p_pc = take((size_t)P * 4);
   char* p_pr = take((size_t)P * 4);
+  char* p_pb = take((size_t)P * 4);
   char* p_pv = take((size_t)P * ODPO_NSTATS * 8);
   char* p_ct = take(C_COUNT * 4);
+#ifdef ODPO_DEBUG_LEAD
+  char* p_dt = take((size_t)P * 4 * 8);
+#else
+  char* p_dt = nullptr;
+#endif
   if (w) {
+    w->dbg_t = (unsigned long long*)p_dt;
     w->row_m = (float*)p_m;
     w->row_l1p = (float*)p_l;
     w->row_logp = (float*)p_lp;
@@ -75,12 +84,18 @@ static size_t ws_layout(int64_t B, int64_t T, int64_t P, char* base, Workspace* 
     w->seq_cnt = (unsigned*)p_sc;
     w->pair_cnt = (unsigned*)p_pc;
     w->pair_ready = (unsigned*)p_pr;
+    w->pair_bcnt = (unsigned*)p_pb;
     w->pair_vals = (double*)p_pv;
     w->counters = (unsigned*)p_ct;
   }
   return off;
 }
 
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 __device__ __forceinline__ void flag(uint32_t* status, uint32_t f) {
   if (f && status) atomicOr(status, f);
 }
@@ -160,6 +175,7 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep(const int32_t* __restrict
   for (int64_t p = tid; p < P; p += kPrepThreads) {
     w.pair_cnt[p] = 0;
     w.pair_ready[p] = 0;
+    w.pair_bcnt[p] = 0;
   }
   if (tid < C_COUNT) w.counters[tid] = 0;
   __syncthreads();
@@ -279,14 +295,16 @@ __device__ __noinline__ void pair_reduce_warp(const LossArgs& a, int64_t p) {
       pv[ODPO_ST_NTOK_REJ] = (double)nr;
     }
     flag(a.status, fl);
-    __threadfence();
-    st_release(&a.w.pair_ready[p], 1u);
-    const unsigned done = atomicAdd(&a.w.counters[C_PAIRS_DONE], 1u);
+#ifdef ODPO_DEBUG_LEAD
+    if (a.w.dbg_t) a.w.dbg_t[p * 4 + 2] = gtimer();
+#endif
+    st_release(&a.w.pair_ready[p], 1u);  // publishes this lane's coef / stats writes
+    const unsigned done = atom_add_acq_rel(&a.w.counters[C_PAIRS_DONE], 1u);
     last = (done == (unsigned)(a.P - 1));
   }
   last = __shfl_sync(kFull, last, 0);
   if (!last) return;
-  __threadfence();
+  fence_acq_rel_gpu();
   double acc[ODPO_NSTATS];
 #pragma unroll
   for (int k = 0; k < ODPO_NSTATS; ++k) acc[k] = 0.0;
@@ -327,105 +345,87 @@ __global__ void __launch_bounds__(kRowThreads, 2) k_row_bwd(LossArgs a) {
 // ------------------------------------------------------------------ the TMA-ring engine
 enum { M_SEQ = 0, M_FUSED = 1 };
 
-// Fused dispatch (adaptive).  Two counters: forward rows in pair order (C_TICKET) and backward
-// rows followed by zero rows of unreferenced sequences (C_BTICKET).  A producer claims the
-// next backward row whenever the peeked row's pair has completed its forward pass (ready
-// flag); otherwise it claims a forward row.  Concurrent claims can overshoot the peeked row
-// into a pair that is not complete yet; such a claim is HELD by its producer, which keeps
-// dispensing forward rows itself until that pair is ready, and only then queues the backward
-// row.  Hence a queued backward row never waits (except after every forward row has been
-// dispensed, when the wait is for dispensed rows only), forward rows never wait, and the
-// kernel cannot deadlock (no co-residency assumption).  The backward pass trails the forward
-// pass by the completion latency only, which keeps each pair's logits L2-resident for the
-// backward re-read.
+// Fused dispatch (adaptive, per-pair backward counters).  Forward rows are dispensed in pair
+// order from one counter (C_TICKET).  Backward rows are dispensed pair by pair: C_BPAIR is the
+// oldest pair with undispensed backward rows, and pair_bcnt[p] hands out that pair's 2T rows.
+// A producer takes a backward row only from a pair whose forward pass has completed (ready
+// flag), so a queued backward row never waits; otherwise it takes a forward row, and forward
+// rows never wait.  Once every forward row is dispensed a producer with nothing queued may
+// wait for the next pair to complete -- its forward rows are all dispensed and progressing --
+// so the kernel cannot deadlock (no co-residency assumption).  The backward pass trails the
+// forward pass by the completion latency only, which keeps a pair's logits L2-resident for
+// the backward re-read.  Zero rows of unreferenced sequences (C_ZTICKET) come last.
 struct Dispatch {
   bool f_exh;
   int64_t ready_pair;  // a pair known ready (cache; readiness is monotone)
-  int64_t held;        // held backward claim, -1 if none
-  int64_t ft_seen;     // lower bound of the forward counter (it only grows)
 };
 
 // Returns 1 (a row was claimed), 0 (everything dispensed) or -1 (nothing to claim right now;
-// only when may_block is false -- the producer then streams the rows it already holds, which
-// is what lets the rows it is waiting for complete).
-__device__ __forceinline__ int fused_next(const LossArgs& a, int64_t totalF, int64_t totalB,
+// only when may_block is false -- the producer then streams the rows it already holds).
+__device__ __forceinline__ int fused_next(const LossArgs& a, int64_t totalF, int64_t nzero,
                                           Dispatch& D, bool may_block, bool& fwd, int64_t& idx) {
   const int64_t R = 2 * a.T;
   unsigned* cnt = a.w.counters;
-  auto take_f = [&](int64_t& f) -> bool {
-    if (D.f_exh) return false;
-    f = (int64_t)atomicAdd(&cnt[C_TICKET], 1u);
-    if (f + 1 > D.ft_seen) D.ft_seen = f + 1;
-    if (f < totalF) return true;
-    D.f_exh = true;
-    return false;
-  };
   for (;;) {
-    if (D.held >= 0) {
-      // queue the held backward row once its pair is READY (then it never waits); until
-      // then keep this producer busy with forward rows
-      const int64_t hp = D.held / R;
-      bool rdy = D.f_exh || hp == D.ready_pair;
-      if (!rdy && ld_relaxed(&a.w.pair_ready[hp]) != 0u) {
-        D.ready_pair = hp;
+    const int64_t pb = (int64_t)ld_relaxed(&cnt[C_BPAIR]);
+    if (pb < a.P) {
+      bool rdy = pb == D.ready_pair;
+      if (!rdy && ld_relaxed(&a.w.pair_ready[pb]) != 0u) {
+        D.ready_pair = pb;
         rdy = true;
       }
-      int64_t f;
-      if (!rdy && take_f(f)) { fwd = true; idx = f; return 1; }
-      fwd = false;
-      idx = D.held;
-      D.held = -1;
+      if (rdy) {
+        const int64_t r = (int64_t)atomicAdd(&a.w.pair_bcnt[pb], 1u);
+        if (r < R) {
 #ifdef ODPO_DEBUG_LEAD
-      if (idx < totalF) {
-        const int64_t ft = (int64_t)ld_relaxed(&cnt[C_TICKET]);
-        const unsigned lead = (unsigned)(ft > idx ? ft - idx : 0);
-        atomicAdd(&cnt[C_DBG_SUM], lead);
-        atomicAdd(&cnt[C_DBG_N], 1u);
-        atomicMax(&cnt[C_DBG_MAX], lead);
-      }
+          if (r == 0) {
+            a.w.dbg_t[pb * 4 + 3] = gtimer();
+            const int64_t ft = (int64_t)ld_relaxed(&cnt[C_TICKET]);
+            const unsigned lead = (unsigned)(ft > pb * R ? ft - pb * R : 0);
+            atomicAdd(&cnt[C_DBG_SUM], lead);
+            atomicAdd(&cnt[C_DBG_N], 1u);
+            atomicMax(&cnt[C_DBG_MAX], lead);
+          }
 #endif
-      return 1;
-    }
-    const int64_t bt = (int64_t)ld_relaxed(&cnt[C_BTICKET]);
-    bool takeB = false;
-    if (bt < totalB) {
-      if (bt >= totalF || D.f_exh) {
-        takeB = true;
-      } else {
-        const int64_t p = bt / R;
-        if (p == D.ready_pair) {
-          takeB = true;
-        } else if (ld_relaxed(&a.w.pair_ready[p]) != 0u) {
-          D.ready_pair = p;
-          takeB = true;
+          fwd = false;
+          idx = pb * R + r;
+          return 1;
         }
-      }
-    }
-    if (takeB) {
-      const int64_t b = (int64_t)atomicAdd(&cnt[C_BTICKET], 1u);
-      if (b >= totalB) continue;
-      if (b >= totalF || D.f_exh) { fwd = false; idx = b; return 1; }
-      D.held = b;  // resolved at the top of the loop (queued now if its pair is dispensed)
-      continue;
-    }
-    // forward rows, unless the forward frontier already leads the backward frontier by the
-    // L2 budget (max_lead rows): then wait for the next backward pair instead, so that the
-    // logits between the two frontiers stay L2-resident.  max_lead >= 2R keeps the next
-    // backward pair fully dispensed, so this wait always terminates.
-    if (!D.f_exh && bt < totalF && D.ft_seen - bt >= a.max_lead) {
-      const int64_t ft = (int64_t)ld_relaxed(&cnt[C_TICKET]);
-      if (ft > D.ft_seen) D.ft_seen = ft;
-      if (ft - bt >= a.max_lead) {
-        if (!may_block) return -1;
-        __nanosleep(64);
+        atomicCAS(&cnt[C_BPAIR], (unsigned)pb, (unsigned)(pb + 1));  // pair exhausted
         continue;
       }
+    } else {
+      const int64_t z = (int64_t)atomicAdd(&cnt[C_ZTICKET], 1u);
+      if (z < nzero) {
+        fwd = false;
+        idx = totalF + z;
+        return 1;
+      }
+      return 0;  // every backward and zero row dispensed (so every forward row too)
     }
-    int64_t f;
-    if (take_f(f)) { fwd = true; idx = f; return 1; }
-    if (bt >= totalB) return 0;  // everything dispensed
+    // the next backward pair is not ready: a forward row, unless capped or exhausted
+    if (!D.f_exh) {
+      bool capped = false;
+      if (a.max_lead < (int64_t)INT32_MAX) {
+        const int64_t ft = (int64_t)ld_relaxed(&cnt[C_TICKET]);
+        capped = ft - pb * R >= a.max_lead;
+      }
+      if (!capped) {
+        const int64_t f = (int64_t)atomicAdd(&cnt[C_TICKET], 1u);
+        if (f < totalF) {
+          fwd = true;
+          idx = f;
+#ifdef ODPO_DEBUG_LEAD
+          if (f % R == 0) a.w.dbg_t[(f / R) * 4 + 0] = gtimer();
+          if (f % R == R - 1) a.w.dbg_t[(f / R) * 4 + 1] = gtimer();
+#endif
+          return 1;
+        }
+        D.f_exh = true;
+      }
+    }
     if (!may_block) return -1;
-    __nanosleep(128);                 // forward exhausted; wait for the next pair to complete
+    __nanosleep(128);
   }
 }
 
@@ -513,13 +513,13 @@ template <int MODE>
 __device__ __forceinline__ bool count_row(const LossArgs& a, const RowSlot& S, int lane) {
   unsigned last = 0;
   if (lane == 0 && (MODE == M_FUSED || a.seqsum)) {
-    __threadfence();
+    // release: this row's statistics before the count; acquire: the other rows' statistics
     unsigned* cnt = MODE == M_FUSED ? &a.w.pair_cnt[S.p] : &a.w.seq_cnt[S.s];
     const unsigned need = MODE == M_FUSED ? (unsigned)(2 * a.T) : (unsigned)a.T;
-    last = (atomicAdd(cnt, 1u) == need - 1u);
+    last = (atom_add_acq_rel(cnt, 1u) == need - 1u);
   }
   last = __shfl_sync(kFull, last, 0);
-  if (last) __threadfence();
+  if (last) fence_acq_rel_gpu();  // make the acquire visible to every lane of the warp
   return last != 0;
 }
 
@@ -589,9 +589,9 @@ __global__ void __launch_bounds__(kEngThreads, ODPO_CTAS_PER_SM) k_engine(LossAr
     const uint64_t pol_drop = policy_evict_first();
     const int nch = nvec > 0 ? (nvec + kCV - 1) / kCV : 1;
     const int64_t totalF = a.P * 2 * T;
-    const int64_t totalB = totalF + (int64_t)__ldcg(&a.w.counters[C_NUNREF]) * T;
+    const int64_t nzero = (int64_t)__ldcg(&a.w.counters[C_NUNREF]) * T;
     const int64_t total = a.B * T;  // SEQ
-    Dispatch D{false, -1, -1, 0};
+    Dispatch D{false, -1};
     // Rows are DECODED into slots up to kLook rows ahead of the row whose chunks are being
     // pushed, so the parameter warp sees backward rows early enough to hide the latency of
     // their pair-ready check and parameter loads.
@@ -604,7 +604,7 @@ __global__ void __launch_bounds__(kEngThreads, ODPO_CTAS_PER_SM) k_engine(LossAr
         int64_t tk;
         bool fwd = true, more;
         if (MODE == M_FUSED) {
-          const int r = fused_next(a, totalF, totalB, D, ahead == 0, fwd, tk);
+          const int r = fused_next(a, totalF, nzero, D, ahead == 0, fwd, tk);
           if (r < 0) break;  // stream the rows already held, then retry
           more = r > 0;
         } else {
@@ -618,6 +618,16 @@ __global__ void __launch_bounds__(kEngThreads, ODPO_CTAS_PER_SM) k_engine(LossAr
         if (!more) {
           S.kind = K_END;
           ended = true;
+          // every epilogue warp must see an END in one of its own slots: fill the next
+          // kNEpi-1 slots with END too (their previous uses are already released)
+          for (int q = 1; q < kNEpi; ++q) {
+            const int y = (dsl + q) % kSlots;
+            const uint32_t yph = dph ^ (uint32_t)((dsl + q) / kSlots);
+            mbar_wait(sempty_s + 8 * y, yph ^ 1u);
+            slots[y].kind = K_END;
+            slots[y].nchunk = 0;
+            mbar_arrive(sfull_s + 8 * y);
+          }
         } else {
           data = decode_row<DT, MODE>(a, tk, fwd, S, pol, pol_keep, pol_drop);
         }
@@ -660,6 +670,16 @@ __global__ void __launch_bounds__(kEngThreads, ODPO_CTAS_PER_SM) k_engine(LossAr
       printf("ODPO_DEBUG_LEAD: backward claims %u, mean forward lead %.1f rows, max %u rows (2T=%d)\n",
              n, n ? (double)ld_relaxed(&a.w.counters[C_DBG_SUM]) / n : 0.0,
              ld_relaxed(&a.w.counters[C_DBG_MAX]), (int)(2 * T));
+      double d01 = 0, d12 = 0, d23 = 0;
+      const unsigned long long* dt = a.w.dbg_t;
+      for (int64_t p = 0; p < a.P; ++p) {
+        d01 += (double)(dt[4 * p + 1] - dt[4 * p + 0]);
+        d12 += (double)(dt[4 * p + 2] - dt[4 * p + 1]);
+        d23 += (double)(dt[4 * p + 3] - dt[4 * p + 2]);
+      }
+      printf("ODPO_DEBUG_LEAD: per pair mean us: dispatch span %.2f, last F dispatch -> ready %.2f, "
+             "ready -> first B claim %.2f; total kernel span %.1f us\n", d01 / a.P / 1e3,
+             d12 / a.P / 1e3, d23 / a.P / 1e3, (double)(dt[4 * (a.P - 1) + 3] - dt[0]) / 1e3);
     }
 #endif
     return;
@@ -696,9 +716,12 @@ __global__ void __launch_bounds__(kEngThreads, ODPO_CTAS_PER_SM) k_engine(LossAr
     return;
   }
 
-  if (warp == kEpiWarp) {
-    // ================= row epilogue: merge partials, finalize, count, pair/sequence reduce
-    int sl = 0;
+  if (warp >= kEpiWarp) {
+    // ================= row epilogues: merge partials, finalize, count, pair/sequence reduce.
+    // Epilogue warp e owns slots e, e+kNEpi, ... (each in order), so the global-memory
+    // round trips of one row's counting overlap with the next rows'.
+    const int e = warp - kEpiWarp;
+    int sl = e;
     uint32_t lph = 0;
     uint32_t rmask = 0;  // per-slot parity of part_ready (advances only on consumer rows)
     for (;;) {
@@ -750,7 +773,8 @@ __global__ void __launch_bounds__(kEngThreads, ODPO_CTAS_PER_SM) k_engine(LossAr
       // rows the consumers never see also carry their kNCW arrivals
       if (lane == 0)
         mbar_arrive_n(sempty_s + 8 * sl, (kind == K_FSKIP || kind == K_NONE) ? 1u + kNCW : 1u);
-      if (++sl == kSlots) { sl = 0; lph ^= 1u; }
+      sl += kNEpi;
+      if (sl >= kSlots) { sl -= kSlots; lph ^= 1u; }
     }
     return;
   }

@@ -29,10 +29,14 @@ namespace odpo {
 #endif
 constexpr int kNCW = ODPO_NCW;             // consumer warps (warps 0..kNCW-1)
 constexpr int kNCT = kNCW * 32;            // consumer threads
+#ifndef ODPO_NEPI
+#define ODPO_NEPI 2
+#endif
 constexpr int kProdWarp = kNCW;            // TMA producer warp
-constexpr int kEpiWarp = kNCW + 1;         // row-epilogue warp
-constexpr int kParWarp = kNCW + 2;         // backward-parameter prefetch warp
-constexpr int kEngThreads = kNCT + 96;
+constexpr int kParWarp = kNCW + 1;         // backward-parameter prefetch warp
+constexpr int kEpiWarp = kNCW + 2;         // first row-epilogue warp
+constexpr int kNEpi = ODPO_NEPI;           // row-epilogue warps (slot s -> warp s % kNEpi)
+constexpr int kEngThreads = kNCT + 64 + 32 * kNEpi;
 constexpr int kStages = ODPO_STAGES;
 constexpr int kChunk = ODPO_CHUNK;         // bytes per stage
 constexpr int kCV = kChunk / 16;           // 16-byte vectors per chunk
@@ -40,6 +44,7 @@ constexpr int kUB = kCV / kNCT;            // vectors per consumer thread per ch
 constexpr int kSlots = 8;                  // rows in flight per CTA (row-slot ring)
 constexpr int kLook = 1;                   // default rows decoded ahead of the row being pushed
 static_assert(kCV % kNCT == 0, "chunk must split evenly over consumers");
+static_assert(kSlots % kNEpi == 0, "epilogue warps must tile the slot ring");
 constexpr int kEngSmem = kStages * kChunk;
 
 // ------------------------------------------------------------------ mbarrier / TMA PTX
