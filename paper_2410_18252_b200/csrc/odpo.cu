@@ -15,6 +15,7 @@
 #include <math.h>
 #include <stdint.h>
 
+#include <cstddef>
 #include <cstdio>
 #include <mutex>
 
@@ -538,12 +539,22 @@ __device__ __forceinline__ void complete_unit(const LossArgs& a, const RowSlot& 
   }
 }
 
-// ---- the engine: warps 0..7 consumers, warp 8 TMA producer, warp 9 row epilogue
-template <int DT, int MODE, int PV>
+// ---- the engine.  Warps 0..kNCW-1 consume, then the TMA producer, the parameter warp and the
+// epilogue warps.  With CS > 1 the kernel runs as thread-block clusters of CS CTAs on CS
+// different SMs: a row is split into CS contiguous vocabulary ranges, one per CTA, so it is
+// streamed with CS SMs' bandwidth; the cluster leader (rank 0) claims the work, broadcasts
+// each row slot to its peers through distributed shared memory, prefetches backward
+// parameters for all of them, and its epilogue merges the CS*kNCW per-warp partials (written
+// into its slot through DSMEM, in fixed (rank, warp) order).  Shorter per-row latency means a
+// pair completes sooner after its rows are dispensed, which keeps the forward/backward lead
+// inside L2.  CS = 1 is the plain single-CTA engine.
+template <int DT, int MODE, int PV, int CS>
 __global__ void __launch_bounds__(kEngThreads, ODPO_CTAS_PER_SM) k_engine(LossArgs a) {
   constexpr int NPF = DT == 1 ? kPoly[PV].npf : 0;
   constexpr int NPB = DT == 1 ? kPoly[PV].npb : 0;
   constexpr int N = Traits<DT>::N;
+  constexpr int NPART = CS * kNCW;  // partials per row
+  static_assert(NPART <= 32, "one warp merges the partials");
   extern __shared__ __align__(128) uint8_t ring[];
   __shared__ __align__(8) uint64_t full[kStages];
   __shared__ __align__(8) uint64_t empty[kStages];
@@ -553,8 +564,10 @@ __global__ void __launch_bounds__(kEngThreads, ODPO_CTAS_PER_SM) k_engine(LossAr
   __shared__ __align__(8) uint64_t param_ready[kSlots];
   __shared__ int32_t stage_slot[kStages];
   __shared__ int32_t stage_chunk[kStages];
-  __shared__ RowSlot slots[kSlots];
+  __shared__ __align__(16) RowSlot slots[kSlots];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t crank = CS > 1 ? cluster_rank() : 0u;
+  const bool leader = crank == 0;
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
@@ -562,347 +575,392 @@ __global__ void __launch_bounds__(kEngThreads, ODPO_CTAS_PER_SM) k_engine(LossAr
     }
     for (int s = 0; s < kSlots; ++s) {
       mbar_init(&slot_full[s], 1);
-      mbar_init(&slot_empty[s], kNCW + 2);   // consumer warps + epilogue + parameter warp
-      mbar_init(&part_ready[s], kNCW);
+      mbar_init(&slot_empty[s], NPART + 2);  // every consumer warp + epilogue + parameter warp
+      mbar_init(&part_ready[s], NPART);
       mbar_init(&param_ready[s], 1);
     }
     mbar_fence_init();
   }
-  __syncthreads();
+  if (CS > 1) cluster_sync_all();  // peers' barriers exist before any remote arrive
+  else __syncthreads();
   // 32-bit shared-window addresses, hoisted out of every loop
   const uint32_t ring_s = smem_u32(ring);
   const uint32_t full_s = smem_u32(full), empty_s = smem_u32(empty);
   const uint32_t sfull_s = smem_u32(slot_full), sempty_s = smem_u32(slot_empty);
   const uint32_t pready_s = smem_u32(part_ready), mready_s = smem_u32(param_ready);
+  const uint32_t slots_s = smem_u32(slots);
+  // the leader's copies (cluster addresses) of the barriers/slots the consumers report to
+  const uint32_t L_sempty = CS > 1 ? mapa(sempty_s, 0) : sempty_s;
+  const uint32_t L_pready = CS > 1 ? mapa(pready_s, 0) : pready_s;
+  const uint32_t L_slots = CS > 1 ? mapa(slots_s, 0) : slots_s;
+  auto wait = [&](uint32_t b, uint32_t par) {
+    if (CS > 1) mbar_wait_cl(b, par);
+    else mbar_wait(b, par);
+  };
+  auto arrive_leader = [&](uint32_t b_local_offset_addr_leader, uint32_t n) {
+    if (CS > 1) mbar_arrive_cl_n(b_local_offset_addr_leader, n);
+    else mbar_arrive_n(b_local_offset_addr_leader, n);
+  };
 
   const int64_t T = a.T;
   const int V = (int)a.V;
   const int nvec = V / N;
   const int tail = V - nvec * N;
-  const float invT = a.invT;
-  const float k2 = invT * kLog2e;
+  // this CTA's contiguous vector range of every row
+  const int v_lo = (int)((int64_t)nvec * crank / CS);
+  const int v_hi = (int)((int64_t)nvec * (crank + 1) / CS);
+  const int lch = v_hi > v_lo ? (v_hi - v_lo + kCV - 1) / kCV : 1;  // chunks per row (>= 1)
+  const bool tail_owner = crank == CS - 1;
+  const float k2 = a.invT * kLog2e;
 
   if (warp == kProdWarp) {
-    // ================= producer: tickets -> row slots -> TMA chunk stages
-    if (lane != 0) return;
-    const uint64_t pol_keep = policy_evict_last();
-    const uint64_t pol_drop = policy_evict_first();
-    const int nch = nvec > 0 ? (nvec + kCV - 1) / kCV : 1;
-    const int64_t totalF = a.P * 2 * T;
-    const int64_t nzero = (int64_t)__ldcg(&a.w.counters[C_NUNREF]) * T;
-    const int64_t total = a.B * T;  // SEQ
-    Dispatch D{false, -1};
-    // Rows are DECODED into slots up to kLook rows ahead of the row whose chunks are being
-    // pushed, so the parameter warp sees backward rows early enough to hide the latency of
-    // their pair-ready check and parameter loads.
-    int st = 0, dsl = 0, psl = 0, ahead = 0;
-    uint32_t sph = 0, dph = 0;
-    uint32_t pmask = 0;  // per-slot parity of param_ready (advances only on B rows)
-    bool ended = false;
-    for (;;) {
-      while (!ended && ahead <= a.look) {
-        int64_t tk;
-        bool fwd = true, more;
-        if (MODE == M_FUSED) {
-          const int r = fused_next(a, totalF, nzero, D, ahead == 0, fwd, tk);
-          if (r < 0) break;  // stream the rows already held, then retry
-          more = r > 0;
-        } else {
-          tk = (int64_t)atomicAdd(&a.w.counters[C_TICKET], 1u);
-          more = tk < total;
-        }
-        mbar_wait(sempty_s + 8 * dsl, dph ^ 1u);
-        RowSlot& S = slots[dsl];
-        uint64_t pol = pol_drop;
-        bool data = false;
-        if (!more) {
-          S.kind = K_END;
-          ended = true;
-          // every epilogue warp must see an END in one of its own slots: fill the next
-          // kNEpi-1 slots with END too (their previous uses are already released)
-          for (int q = 1; q < kNEpi; ++q) {
-            const int y = (dsl + q) % kSlots;
-            const uint32_t yph = dph ^ (uint32_t)((dsl + q) / kSlots);
-            mbar_wait(sempty_s + 8 * y, yph ^ 1u);
-            slots[y].kind = K_END;
-            slots[y].nchunk = 0;
-            mbar_arrive(sfull_s + 8 * y);
+    if (lane == 0) {
+      // ================= producer: (leader) tickets -> row slots, broadcast; every CTA streams
+      // its own vocabulary range of each row into its TMA ring
+      const uint64_t pol_keep = policy_evict_last();
+      const uint64_t pol_drop = policy_evict_first();
+      const int64_t totalF = a.P * 2 * T;
+      const int64_t nzero = (int64_t)__ldcg(&a.w.counters[C_NUNREF]) * T;
+      const int64_t total = a.B * T;  // SEQ
+      Dispatch D{false, -1};
+      int st = 0, dsl = 0, psl = 0, ahead = 0;
+      uint32_t sph = 0, dph = 0, pph = 0;
+      uint32_t pmask = 0;  // per-slot parity of param_ready (advances only on B rows)
+      bool ended = false;
+      for (;;) {
+        if (leader) {
+          // decode up to a.look rows ahead of the row being streamed
+          while (!ended && ahead <= a.look) {
+            int64_t tk;
+            bool fwd = true, more;
+            if (MODE == M_FUSED) {
+              const int r = fused_next(a, totalF, nzero, D, ahead == 0, fwd, tk);
+              if (r < 0) break;  // stream the rows already held, then retry
+              more = r > 0;
+            } else {
+              tk = (int64_t)atomicAdd(&a.w.counters[C_TICKET], 1u);
+              more = tk < total;
+            }
+            wait(sempty_s + 8 * dsl, dph ^ 1u);
+            RowSlot& S = slots[dsl];
+            uint64_t pol = pol_drop;
+            bool data = false;
+            if (!more) {
+              S.kind = K_END;
+              ended = true;
+            } else {
+              data = decode_row<DT, MODE>(a, tk, fwd, S, pol, pol_keep, pol_drop);
+            }
+            S.nchunk = data ? 1 : 0;
+            S.pphase = (pmask >> dsl) & 1u;
+            if (S.kind == K_B) pmask ^= 1u << dsl;
+            // broadcast the slot header to the peers, then signal slot_full everywhere
+            for (int r = 1; r < CS; ++r) {
+              const uint32_t dst = mapa(slots_s + dsl * (uint32_t)sizeof(RowSlot), r);
+              const uint64_t* src = reinterpret_cast<const uint64_t*>(&S);
+#pragma unroll
+              for (int q = 0; q < kSlotHeaderBytes / 8; ++q) st_cl_u64(dst + 8 * q, src[q]);
+            }
+            for (int r = 1; r < CS; ++r) mbar_arrive_cl(mapa(sfull_s + 8 * dsl, r));
+            mbar_arrive(sfull_s + 8 * dsl);
+            if (!more) {
+              // every epilogue warp must see an END in one of its own slots
+              for (int q = 1; q < kNEpi; ++q) {
+                const int y = (dsl + q) % kSlots;
+                const uint32_t yph = dph ^ (uint32_t)((dsl + q) / kSlots);
+                wait(sempty_s + 8 * y, yph ^ 1u);
+                slots[y].kind = K_END;
+                slots[y].nchunk = 0;
+                mbar_arrive(sfull_s + 8 * y);
+              }
+            }
+            ++ahead;
+            if (++dsl == kSlots) { dsl = 0; dph ^= 1u; }
           }
+          if (ahead == 0) break;
         } else {
-          data = decode_row<DT, MODE>(a, tk, fwd, S, pol, pol_keep, pol_drop);
+          wait(sfull_s + 8 * psl, pph);  // peers: the leader filled this slot
         }
-        S.nchunk = data ? nch : 0;
-        S.pphase = (pmask >> dsl) & 1u;
-        if (S.kind == K_B) pmask ^= 1u << dsl;
-        mbar_arrive(sfull_s + 8 * dsl);
-        ++ahead;
-        if (++dsl == kSlots) { dsl = 0; dph ^= 1u; }
-      }
-      if (ahead == 0) break;
-      const RowSlot& S = slots[psl];
-      const int kind = S.kind;
-      if (kind == K_F || kind == K_B || kind == K_ZERO || kind == K_END) {
-        const bool data = S.nchunk > 0;
-        const int nstage = data ? S.nchunk : 1;
-        const uint64_t pol = (MODE == M_FUSED && kind == K_F) ? pol_keep : pol_drop;
-        for (int c = 0; c < nstage; ++c) {
-          mbar_wait(empty_s + 8 * st, sph ^ 1u);
-          stage_slot[st] = kind == K_END ? -1 : psl;
-          stage_chunk[st] = c;
-          const int nv = data ? min(kCV, nvec - c * kCV) : 0;
-          if (nv > 0) {
-            const uint32_t bytes = (uint32_t)nv * 16u;
-            mbar_arrive_tx(full_s + 8 * st, bytes);
-            tma_load_1d(ring_s + st * kChunk, S.row + (size_t)c * kChunk, bytes, full_s + 8 * st, pol);
-          } else {
-            mbar_arrive(full_s + 8 * st);
+        const RowSlot& S = slots[psl];
+        const int kind = S.kind;
+        if (kind == K_F || kind == K_B || kind == K_ZERO || kind == K_END) {
+          const bool data = (kind == K_F || kind == K_B) && S.nchunk > 0 && v_hi > v_lo;
+          const int nstage = data ? lch : 1;
+          const uint64_t pol = (MODE == M_FUSED && kind == K_F) ? pol_keep : pol_drop;
+          for (int c = 0; c < nstage; ++c) {
+            wait(empty_s + 8 * st, sph ^ 1u);
+            stage_slot[st] = kind == K_END ? -1 : psl;
+            stage_chunk[st] = c;
+            const int vs = v_lo + c * kCV;
+            const int nv = data ? min(kCV, v_hi - vs) : 0;
+            if (nv > 0) {
+              const uint32_t bytes = (uint32_t)nv * 16u;
+              mbar_arrive_tx(full_s + 8 * st, bytes);
+              tma_load_1d(ring_s + st * kChunk, S.row + (size_t)vs * 16, bytes, full_s + 8 * st, pol);
+            } else {
+              mbar_arrive(full_s + 8 * st);
+            }
+            if (++st == kStages) { st = 0; sph ^= 1u; }
           }
-          if (++st == kStages) { st = 0; sph ^= 1u; }
         }
+        if (leader) --ahead;
+        if (++psl == kSlots) { psl = 0; pph ^= 1u; }
+        if (kind == K_END) break;
       }
-      --ahead;
-      if (++psl == kSlots) psl = 0;
-      if (kind == K_END) break;
-    }
 #ifdef ODPO_DEBUG_LEAD
-    if (MODE == M_FUSED && atomicAdd(&a.w.counters[C_DBG_DONE], 1u) == gridDim.x - 1) {
-      const unsigned n = ld_relaxed(&a.w.counters[C_DBG_N]);
-      printf("ODPO_DEBUG_LEAD: backward claims %u, mean forward lead %.1f rows, max %u rows (2T=%d)\n",
-             n, n ? (double)ld_relaxed(&a.w.counters[C_DBG_SUM]) / n : 0.0,
-             ld_relaxed(&a.w.counters[C_DBG_MAX]), (int)(2 * T));
-      double d01 = 0, d12 = 0, d23 = 0;
-      const unsigned long long* dt = a.w.dbg_t;
-      for (int64_t p = 0; p < a.P; ++p) {
-        d01 += (double)(dt[4 * p + 1] - dt[4 * p + 0]);
-        d12 += (double)(dt[4 * p + 2] - dt[4 * p + 1]);
-        d23 += (double)(dt[4 * p + 3] - dt[4 * p + 2]);
+      if (MODE == M_FUSED && leader &&
+          atomicAdd(&a.w.counters[C_DBG_DONE], 1u) == gridDim.x / CS - 1) {
+        const unsigned n = ld_relaxed(&a.w.counters[C_DBG_N]);
+        printf("ODPO_DEBUG_LEAD: backward claims %u, mean forward lead %.1f rows, max %u rows (2T=%d)\n",
+               n, n ? (double)ld_relaxed(&a.w.counters[C_DBG_SUM]) / n : 0.0,
+               ld_relaxed(&a.w.counters[C_DBG_MAX]), (int)(2 * T));
+        double d01 = 0, d12 = 0, d23 = 0;
+        const unsigned long long* dt = a.w.dbg_t;
+        for (int64_t p = 0; p < a.P; ++p) {
+          d01 += (double)(dt[4 * p + 1] - dt[4 * p + 0]);
+          d12 += (double)(dt[4 * p + 2] - dt[4 * p + 1]);
+          d23 += (double)(dt[4 * p + 3] - dt[4 * p + 2]);
+        }
+        printf("ODPO_DEBUG_LEAD: per pair mean us: dispatch span %.2f, last F dispatch -> ready %.2f, "
+               "ready -> first B claim %.2f\n", d01 / a.P / 1e3, d12 / a.P / 1e3, d23 / a.P / 1e3);
       }
-      printf("ODPO_DEBUG_LEAD: per pair mean us: dispatch span %.2f, last F dispatch -> ready %.2f, "
-             "ready -> first B claim %.2f; total kernel span %.1f us\n", d01 / a.P / 1e3,
-             d12 / a.P / 1e3, d23 / a.P / 1e3, (double)(dt[4 * (a.P - 1) + 3] - dt[0]) / 1e3);
-    }
 #endif
-    return;
-  }
-
-  if (warp == kParWarp) {
-    // ================= backward-parameter prefetch: for each backward row, wait (acquire) for
-    // its pair's coefficient, then publish the row constants to the consumers.  Runs ahead of
-    // the consumers by up to kSlots rows, so neither TMA issue nor compute waits on it.
-    if (lane != 0) return;
-    int sl = 0;
-    uint32_t lph = 0;
-    for (;;) {
-      mbar_wait(sfull_s + 8 * sl, lph);
-      RowSlot& S = slots[sl];
-      const int kind = S.kind;
-      if (kind == K_END) break;
-      if (kind == K_B) {
-        while (ld_relaxed(&a.w.pair_ready[S.p]) == 0u) __nanosleep(32);
-        fence_acq_rel_gpu();
-        const float m = __ldcg(a.w.row_m + S.g);
-        const float l1p = __ldcg(a.w.row_l1p + S.g);
-        const float logp = __ldcg(a.w.row_logp + S.g);
-        const float coef = __ldcg(a.w.seq_coef + S.s);
-        // coef folded into the exponent: coef * 2^e = sign * 2^(e + log2|coef|)
-        S.c = fmaf(l1p, kLog2e, m * k2) - log2f(fabsf(coef));
-        S.coef = coef;
-        S.gtok = coef * expm1f(logp);
-        mbar_arrive(mready_s + 8 * sl);
-      }
-      mbar_arrive(sempty_s + 8 * sl);
-      if (++sl == kSlots) { sl = 0; lph ^= 1u; }
     }
-    return;
-  }
-
-  if (warp >= kEpiWarp) {
-    // ================= row epilogues: merge partials, finalize, count, pair/sequence reduce.
-    // Epilogue warp e owns slots e, e+kNEpi, ... (each in order), so the global-memory
-    // round trips of one row's counting overlap with the next rows'.
-    const int e = warp - kEpiWarp;
-    int sl = e;
-    uint32_t lph = 0;
-    uint32_t rmask = 0;  // per-slot parity of part_ready (advances only on consumer rows)
-    for (;;) {
-      mbar_wait(sfull_s + 8 * sl, lph);
-      const RowSlot& S = slots[sl];
-      const int kind = S.kind;
-      if (kind == K_END) break;
-      // Only forward rows make the epilogue wait for the consumers; backward / zero rows are
-      // released by their consumers directly, so a backward row waiting for its pair never
-      // holds up the counting of later forward rows (no head-of-line blocking).
-      if (kind == K_F) {
-        mbar_wait(pready_s + 8 * sl, (rmask >> sl) & 1u);
-        rmask ^= 1u << sl;
-      }
-      if (kind == K_F) {
-        MR v;
-        v.m = lane < kNCW ? S.pm[lane] : -INFINITY;
-        v.r = lane < kNCW ? S.pr[lane] : 0.f;
-        v = warp_merge(v, k2);
-        if (lane == 0) {
-          uint32_t fl = 0;
-          const float l1p = log1pf(v.r);
-          float logp = 0.f;
-          if (S.tok < 0 || S.tok >= V) {
-            fl |= ODPO_FLAG_TOKEN_RANGE;
-          } else {
-            logp = __fsub_rn(__fmul_rn(__fsub_rn(S.xtok, v.m), invT), l1p);
-            if (!isfinite(logp)) fl |= ODPO_FLAG_NONFINITE_LOGIT;
+  } else if (warp == kParWarp) {
+    if (lane == 0 && leader) {
+      // ================= backward-parameter prefetch (leader): for each backward row, acquire
+      // its pair's coefficient, publish the row constants to every CTA of the cluster
+      int sl = 0;
+      uint32_t lph = 0;
+      for (;;) {
+        wait(sfull_s + 8 * sl, lph);
+        RowSlot& S = slots[sl];
+        const int kind = S.kind;
+        if (kind == K_END) break;
+        if (kind == K_B) {
+          while (ld_relaxed(&a.w.pair_ready[S.p]) == 0u) __nanosleep(32);
+          fence_acq_rel_gpu();
+          const float m = __ldcg(a.w.row_m + S.g);
+          const float l1p = __ldcg(a.w.row_l1p + S.g);
+          const float logp = __ldcg(a.w.row_logp + S.g);
+          const float coef = __ldcg(a.w.seq_coef + S.s);
+          // coef folded into the exponent: coef * 2^e = sign * 2^(e + log2|coef|)
+          const float c = fmaf(l1p, kLog2e, m * k2) - log2f(fabsf(coef));
+          const float gtok = coef * expm1f(logp);
+          S.c = c;
+          S.coef = coef;
+          S.gtok = gtok;
+          const uint32_t off_c = (uint32_t)offsetof(RowSlot, c);
+          for (int r = 1; r < CS; ++r) {
+            const uint32_t dst = mapa(slots_s + sl * (uint32_t)sizeof(RowSlot) + off_c, r);
+            st_cl_u32(dst, __float_as_uint(c));
+            st_cl_u32(dst + 4, __float_as_uint(coef));
+            st_cl_u32(dst + 8, __float_as_uint(gtok));
+            mbar_arrive_cl(mapa(mready_s + 8 * sl, r));
           }
-          if (!isfinite(v.m) || !isfinite(v.r)) fl |= ODPO_FLAG_NONFINITE_LOGIT;
-          a.w.row_m[S.g] = v.m;
-          a.w.row_l1p[S.g] = l1p;
-          a.w.row_logp[S.g] = logp;
-          if (MODE == M_SEQ) {
-            if (a.tok_out) a.tok_out[S.g] = logp;
-            if (a.lse_out) a.lse_out[S.g] = __fadd_rn(__fmul_rn(v.m, invT), l1p);
+          mbar_arrive(mready_s + 8 * sl);
+        }
+        mbar_arrive(sempty_s + 8 * sl);
+        if (++sl == kSlots) { sl = 0; lph ^= 1u; }
+      }
+    }
+  } else if (warp >= kEpiWarp) {
+    if (leader) {
+      // ================= row epilogues (leader): merge the cluster's partials, finalize, count,
+      // pair/sequence reduce.  Epilogue warp e owns slots e, e+kNEpi, ... (each in order).
+      const int e = warp - kEpiWarp;
+      int sl = e;
+      uint32_t lph = 0;
+      uint32_t rmask = 0;  // per-slot parity of part_ready (advances only on forward rows)
+      for (;;) {
+        wait(sfull_s + 8 * sl, lph);
+        const RowSlot& S = slots[sl];
+        const int kind = S.kind;
+        if (kind == K_END) break;
+        if (kind == K_F) {
+          wait(pready_s + 8 * sl, (rmask >> sl) & 1u);
+          rmask ^= 1u << sl;
+          MR v;
+          v.m = lane < NPART ? S.pm[lane] : -INFINITY;
+          v.r = lane < NPART ? S.pr[lane] : 0.f;
+          v = warp_merge(v, k2);
+          if (lane == 0) {
+            uint32_t fl = 0;
+            const float l1p = log1pf(v.r);
+            float logp = 0.f;
+            if (S.tok < 0 || S.tok >= V) {
+              fl |= ODPO_FLAG_TOKEN_RANGE;
+            } else {
+              logp = __fsub_rn(__fmul_rn(__fsub_rn(S.xtok, v.m), a.invT), l1p);
+              if (!isfinite(logp)) fl |= ODPO_FLAG_NONFINITE_LOGIT;
+            }
+            if (!isfinite(v.m) || !isfinite(v.r)) fl |= ODPO_FLAG_NONFINITE_LOGIT;
+            a.w.row_m[S.g] = v.m;
+            a.w.row_l1p[S.g] = l1p;
+            a.w.row_logp[S.g] = logp;
+            if (MODE == M_SEQ) {
+              if (a.tok_out) a.tok_out[S.g] = logp;
+              if (a.lse_out) a.lse_out[S.g] = __fadd_rn(__fmul_rn(v.m, a.invT), l1p);
+            }
+            flag(a.status, fl);
           }
-          flag(a.status, fl);
-        }
-        if (count_row<MODE>(a, S, lane)) complete_unit<MODE>(a, S, lane);
-      } else if (kind == K_FSKIP) {
-        if (lane == 0 && MODE == M_SEQ) {
-          if (a.tok_out) a.tok_out[S.g] = 0.f;
-          if (a.lse_out) a.lse_out[S.g] = 0.f;
-        }
-        if (count_row<MODE>(a, S, lane)) complete_unit<MODE>(a, S, lane);
-      }
-      __syncwarp();
-      // rows the consumers never see also carry their kNCW arrivals
-      if (lane == 0)
-        mbar_arrive_n(sempty_s + 8 * sl, (kind == K_FSKIP || kind == K_NONE) ? 1u + kNCW : 1u);
-      sl += kNEpi;
-      if (sl >= kSlots) { sl -= kSlots; lph ^= 1u; }
-    }
-    return;
-  }
-
-  // ================= consumers (warps 0..7)
-  const uint32_t NI = Traits<DT>::kNegInfWord;
-  int st = 0;
-  uint32_t sph = 0;
-  MR s{-INFINITY, 0.f};
-  float b_c = 0.f, b_coef = 0.f, b_gtok = 0.f;
-  int r_kind = K_NONE, r_tok = 0, r_nch = 1, r_tch = -1, r_tvl = -1;
-  const char* r_row = nullptr;
-  char* r_drow = nullptr;
-  for (;;) {
-    mbar_wait(full_s + 8 * st, sph);
-    const int sl = stage_slot[st];
-    if (sl < 0) break;
-    const int ch = stage_chunk[st];
-    RowSlot& S = slots[sl];
-    if (ch == 0) {  // a new row: cache its fields (a row's chunks occupy consecutive stages)
-      r_kind = S.kind;
-      r_tok = S.tok;
-      r_nch = S.nchunk > 0 ? S.nchunk : 1;
-      r_row = S.row;
-      r_drow = S.drow;
-      // the vector holding tok: its chunk and its chunk-local vector index (-1: none / tail)
-      const int tvec = (r_tok >= 0 && r_tok < nvec * N) ? r_tok / N : -1;
-      r_tch = tvec >= 0 ? tvec / kCV : -1;
-      r_tvl = tvec >= 0 ? tvec - r_tch * kCV : -1;
-    }
-    const int kind = r_kind;
-    const bool last_chunk = ch == r_nch - 1;
-    const uint4* sv = reinterpret_cast<const uint4*>(ring + (size_t)st * kChunk);
-    const int c0 = ch * kCV;
-    const int cnv = min(kCV, nvec - c0);
-    const bool own_tok = ch == r_tch && (r_tvl % kNCT) == tid;
-    if (kind == K_F) {
-      if (ch == 0) s = MR{-INFINITY, 0.f};
-      if (cnv == kCV) {  // full chunk: no predication
-        uint4 v[kUB];
-#pragma unroll
-        for (int u = 0; u < kUB; ++u) v[u] = sv[tid + u * kNCT];
-        mr_batch<DT, kUB, NPF>(v, k2, s.m, s.r);
-      } else if (tid < cnv) {
-        uint4 v[kUB];
-#pragma unroll
-        for (int u = 0; u < kUB; ++u) {
-          const int i = tid + u * kNCT;
-          v[u] = i < cnv ? sv[i] : make_uint4(NI, NI, NI, NI);
-        }
-        mr_batch<DT, kUB, NPF>(v, k2, s.m, s.r);
-      }
-      if (own_tok) {
-        float f[N];
-        Traits<DT>::unpack(sv[r_tvl], f);
-        float x = f[0];
-#pragma unroll
-        for (int j = 1; j < N; ++j) x = (r_tok % N == j) ? f[j] : x;
-        S.xtok = x;
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(empty_s + 8 * st);
-      if (last_chunk) {
-        if (tid < tail) {
-          const int64_t vv = (int64_t)nvec * N + tid;
-          const float x = Traits<DT>::load1(r_row, vv);
-          s = mr_push1(s, x, k2);
-          if (vv == r_tok) S.xtok = x;
-        }
-        const MR wv = warp_merge(s, k2);
-        if (lane == 0) {
-          S.pm[warp] = wv.m;
-          S.pr[warp] = wv.r;
-          mbar_arrive(pready_s + 8 * sl);
-          mbar_arrive(sempty_s + 8 * sl);
-        }
-      }
-    } else if (kind == K_B) {
-      if (ch == 0) {
-        mbar_wait(mready_s + 8 * sl, S.pphase);
-        b_c = S.c;
-        b_coef = S.coef;
-        b_gtok = S.gtok;
-      }
-      uint4* vout = reinterpret_cast<uint4*>(r_drow) + c0;
-      if (cnv == kCV) {
-        if (b_coef < 0.f) {
-#pragma unroll
-          for (int u = 0; u < kUB; ++u)
-            st16_stream(vout + tid + u * kNCT, bwd_vec<DT, NPB, true>(sv[tid + u * kNCT], k2, b_c));
-        } else {
-#pragma unroll
-          for (int u = 0; u < kUB; ++u)
-            st16_stream(vout + tid + u * kNCT, bwd_vec<DT, NPB, false>(sv[tid + u * kNCT], k2, b_c));
-        }
-      } else {
-#pragma unroll
-        for (int u = 0; u < kUB; ++u) {
-          const int i = tid + u * kNCT;
-          if (i < cnv)
-            st16_stream(vout + i, b_coef < 0.f ? bwd_vec<DT, NPB, true>(sv[i], k2, b_c)
-                                               : bwd_vec<DT, NPB, false>(sv[i], k2, b_c));
-        }
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(empty_s + 8 * st);
-      // onehot entry: the thread that stored tok's vector overwrites it (program order)
-      if (own_tok) Traits<DT>::store1(r_drow, r_tok, b_gtok);
-      if (last_chunk) {
-        if (tid < tail) {
-          const int64_t vv = (int64_t)nvec * N + tid;
-          const float x = Traits<DT>::load1(r_row, vv);
-          Traits<DT>::store1(r_drow, vv, vv == r_tok ? b_gtok : copysignf(ex2(fmaf(x, k2, -b_c)), b_coef));
+          if (count_row<MODE>(a, S, lane)) complete_unit<MODE>(a, S, lane);
+        } else if (kind == K_FSKIP) {
+          if (lane == 0 && MODE == M_SEQ) {
+            if (a.tok_out) a.tok_out[S.g] = 0.f;
+            if (a.lse_out) a.lse_out[S.g] = 0.f;
+          }
+          if (count_row<MODE>(a, S, lane)) complete_unit<MODE>(a, S, lane);
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(sempty_s + 8 * sl);
+        // rows the consumers never see also carry their NPART arrivals
+        if (lane == 0)
+          mbar_arrive_n(sempty_s + 8 * sl, (kind == K_FSKIP || kind == K_NONE) ? 1u + NPART : 1u);
+        sl += kNEpi;
+        if (sl >= kSlots) { sl -= kSlots; lph ^= 1u; }
       }
-    } else {  // K_ZERO
-      __syncwarp();
-      if (lane == 0) mbar_arrive(empty_s + 8 * st);
-      uint4* vout = reinterpret_cast<uint4*>(r_drow);
-      for (int i = tid; i < nvec; i += kNCT) st16_stream(vout + i, make_uint4(0, 0, 0, 0));
-      if (tid < tail) Traits<DT>::store1(r_drow, (int64_t)nvec * N + tid, 0.f);
-      __syncwarp();
-      if (lane == 0) mbar_arrive(sempty_s + 8 * sl);
     }
-    if (++st == kStages) { st = 0; sph ^= 1u; }
+  } else {
+    // ================= consumers (warps 0..kNCW-1): this CTA's vocabulary range of each row
+    const uint32_t NI = Traits<DT>::kNegInfWord;
+    const int pidx = (int)crank * kNCW + warp;  // this warp's partial index in the leader slot
+    int st = 0;
+    uint32_t sph = 0;
+    MR s{-INFINITY, 0.f};
+    float b_c = 0.f, b_coef = 0.f, b_gtok = 0.f;
+    int r_kind = K_NONE, r_tok = 0, r_nst = 1, r_tch = -1, r_tvl = -1;
+    const char* r_row = nullptr;
+    char* r_drow = nullptr;
+    for (;;) {
+      wait(full_s + 8 * st, sph);
+      const int sl = stage_slot[st];
+      if (sl < 0) break;
+      const int ch = stage_chunk[st];
+      RowSlot& S = slots[sl];
+      const uint32_t Lslot = L_slots + sl * (uint32_t)sizeof(RowSlot);
+      if (ch == 0) {  // a new row: cache its fields (a row's chunks occupy consecutive stages)
+        r_kind = S.kind;
+        r_tok = S.tok;
+        r_nst = ((r_kind == K_F || r_kind == K_B) && S.nchunk > 0 && v_hi > v_lo) ? lch : 1;
+        r_row = S.row;
+        r_drow = S.drow;
+        // the vector holding tok, if it is in this CTA's range: its chunk and chunk-local index
+        const int tvec = (r_tok >= 0 && r_tok < nvec * N) ? r_tok / N : -1;
+        const bool mine = tvec >= v_lo && tvec < v_hi;
+        r_tch = mine ? (tvec - v_lo) / kCV : -1;
+        r_tvl = mine ? (tvec - v_lo) - r_tch * kCV : -1;
+      }
+      const int kind = r_kind;
+      const bool last_chunk = ch == r_nst - 1;
+      const uint4* sv = reinterpret_cast<const uint4*>(ring + (size_t)st * kChunk);
+      const int c0 = v_lo + ch * kCV;  // first vector of this chunk within the row
+      const int cnv = v_hi > v_lo ? min(kCV, v_hi - c0) : 0;
+      const bool own_tok = ch == r_tch && (r_tvl % kNCT) == tid;
+      if (kind == K_F) {
+        if (ch == 0) s = MR{-INFINITY, 0.f};
+        if (cnv == kCV) {  // full chunk: no predication
+          uint4 v[kUB];
+#pragma unroll
+          for (int u = 0; u < kUB; ++u) v[u] = sv[tid + u * kNCT];
+          mr_batch<DT, kUB, NPF>(v, k2, s.m, s.r);
+        } else if (tid < cnv) {
+          uint4 v[kUB];
+#pragma unroll
+          for (int u = 0; u < kUB; ++u) {
+            const int i = tid + u * kNCT;
+            v[u] = i < cnv ? sv[i] : make_uint4(NI, NI, NI, NI);
+          }
+          mr_batch<DT, kUB, NPF>(v, k2, s.m, s.r);
+        }
+        if (own_tok) {
+          float f[N];
+          Traits<DT>::unpack(sv[r_tvl], f);
+          float x = f[0];
+#pragma unroll
+          for (int j = 1; j < N; ++j) x = (r_tok % N == j) ? f[j] : x;
+          if (CS > 1) st_cl_u32(Lslot + (uint32_t)offsetof(RowSlot, xtok), __float_as_uint(x));
+          else S.xtok = x;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty_s + 8 * st);
+        if (last_chunk) {
+          if (tail_owner && tid < tail) {
+            const int64_t vv = (int64_t)nvec * N + tid;
+            const float x = Traits<DT>::load1(r_row, vv);
+            s = mr_push1(s, x, k2);
+            if (vv == r_tok) {
+              if (CS > 1) st_cl_u32(Lslot + (uint32_t)offsetof(RowSlot, xtok), __float_as_uint(x));
+              else S.xtok = x;
+            }
+          }
+          const MR wv = warp_merge(s, k2);
+          __syncwarp();
+          if (lane == 0) {
+            if (CS > 1) {
+              st_cl_u32(Lslot + (uint32_t)offsetof(RowSlot, pm) + 4 * pidx, __float_as_uint(wv.m));
+              st_cl_u32(Lslot + (uint32_t)offsetof(RowSlot, pr) + 4 * pidx, __float_as_uint(wv.r));
+            } else {
+              S.pm[pidx] = wv.m;
+              S.pr[pidx] = wv.r;
+            }
+            arrive_leader(L_pready + 8 * sl, 1u);
+            arrive_leader(L_sempty + 8 * sl, 1u);
+          }
+        }
+      } else if (kind == K_B) {
+        if (ch == 0) {
+          wait(mready_s + 8 * sl, S.pphase);
+          b_c = S.c;
+          b_coef = S.coef;
+          b_gtok = S.gtok;
+        }
+        uint4* vout = reinterpret_cast<uint4*>(r_drow) + c0;
+        if (cnv == kCV) {
+          if (b_coef < 0.f) {
+#pragma unroll
+            for (int u = 0; u < kUB; ++u)
+              st16_stream(vout + tid + u * kNCT, bwd_vec<DT, NPB, true>(sv[tid + u * kNCT], k2, b_c));
+          } else {
+#pragma unroll
+            for (int u = 0; u < kUB; ++u)
+              st16_stream(vout + tid + u * kNCT, bwd_vec<DT, NPB, false>(sv[tid + u * kNCT], k2, b_c));
+          }
+        } else {
+#pragma unroll
+          for (int u = 0; u < kUB; ++u) {
+            const int i = tid + u * kNCT;
+            if (i < cnv)
+              st16_stream(vout + i, b_coef < 0.f ? bwd_vec<DT, NPB, true>(sv[i], k2, b_c)
+                                                 : bwd_vec<DT, NPB, false>(sv[i], k2, b_c));
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty_s + 8 * st);
+        // onehot entry: the thread that stored tok's vector overwrites it (program order)
+        if (own_tok) Traits<DT>::store1(r_drow, r_tok, b_gtok);
+        if (last_chunk) {
+          if (tail_owner && tid < tail) {
+            const int64_t vv = (int64_t)nvec * N + tid;
+            const float x = Traits<DT>::load1(r_row, vv);
+            Traits<DT>::store1(r_drow, vv, vv == r_tok ? b_gtok : copysignf(ex2(fmaf(x, k2, -b_c)), b_coef));
+          }
+          __syncwarp();
+          if (lane == 0) arrive_leader(L_sempty + 8 * sl, 1u);
+        }
+      } else {  // K_ZERO: this CTA's range of the row
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty_s + 8 * st);
+        uint4* vout = reinterpret_cast<uint4*>(r_drow);
+        for (int i = v_lo + tid; i < v_hi; i += kNCT) st16_stream(vout + i, make_uint4(0, 0, 0, 0));
+        if (tail_owner && tid < tail) Traits<DT>::store1(r_drow, (int64_t)nvec * N + tid, 0.f);
+        __syncwarp();
+        if (lane == 0) arrive_leader(L_sempty + 8 * sl, 1u);
+      }
+      if (++st == kStages) { st = 0; sph ^= 1u; }
+    }
   }
+  // no CTA may leave while a peer can still touch its shared memory
+  if (CS > 1) cluster_sync_all();
 }
 
 // ------------------------------------------------------------------ host side
@@ -916,8 +974,31 @@ static std::once_flag g_once[128];
 
 template <int DT, int MODE, int PV>
 static void setup_one(int* occ) {
-  cudaFuncSetAttribute(k_engine<DT, MODE, PV>, cudaFuncAttributeMaxDynamicSharedMemorySize, kEngSmem);
-  if (occ) cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, k_engine<DT, MODE, PV>, kEngThreads, kEngSmem);
+  cudaFuncSetAttribute(k_engine<DT, MODE, PV, kCS>, cudaFuncAttributeMaxDynamicSharedMemorySize, kEngSmem);
+  if (occ)
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, k_engine<DT, MODE, PV, kCS>, kEngThreads, kEngSmem);
+}
+
+// Launch an engine instantiation, as thread-block clusters of kCS CTAs when kCS > 1.
+template <typename Kern>
+static void launch_k(Kern kern, int grid, cudaStream_t s, const LossArgs& a) {
+  if (kCS == 1) {
+    kern<<<grid, kEngThreads, kEngSmem, s>>>(a);
+    return;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(kEngThreads);
+  cfg.dynamicSmemBytes = kEngSmem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = kCS;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, a);
 }
 template <int PV>
 static void setup_pv() {
@@ -963,7 +1044,7 @@ static odpo_status launched() {
 template <int MODE, int PV>
 static void launch_bf16(int pv, int grid, const LossArgs& a, cudaStream_t s) {
   if (pv == PV) {
-    k_engine<1, MODE, PV><<<grid, kEngThreads, kEngSmem, s>>>(a);
+    launch_k(k_engine<1, MODE, PV, kCS>, grid, s, a);
     return;
   }
   if constexpr (PV + 1 < kNumPoly) launch_bf16<MODE, PV + 1>(pv, grid, a, s);
@@ -985,10 +1066,10 @@ static odpo_status launch_engine(int dt, int mode, int pv, const LossArgs& a, in
   int occ = di.occ[dt][mode];
   if (occ < 1) occ = 1;
   if (cps <= 0 || cps > occ) cps = occ;
-  const int grid = di.sms * cps;
+  const int grid = (di.sms * cps / kCS) * kCS;
   if (grid_out) *grid_out = grid;
-  if (dt == 0 && mode == M_SEQ) k_engine<0, M_SEQ, 0><<<grid, kEngThreads, kEngSmem, s>>>(a);
-  if (dt == 0 && mode == M_FUSED) k_engine<0, M_FUSED, 0><<<grid, kEngThreads, kEngSmem, s>>>(a);
+  if (dt == 0 && mode == M_SEQ) launch_k(k_engine<0, M_SEQ, 0, kCS>, grid, s, a);
+  if (dt == 0 && mode == M_FUSED) launch_k(k_engine<0, M_FUSED, 0, kCS>, grid, s, a);
   if (dt == 1 && mode == M_SEQ) launch_bf16<M_SEQ, 0>(pv, grid, a, s);
   if (dt == 1 && mode == M_FUSED) launch_bf16<M_FUSED, 0>(pv, grid, a, s);
   return launched();

@@ -29,6 +29,10 @@ namespace odpo {
 #endif
 constexpr int kNCW = ODPO_NCW;             // consumer warps (warps 0..kNCW-1)
 constexpr int kNCT = kNCW * 32;            // consumer threads
+#ifndef ODPO_CLUSTER
+#define ODPO_CLUSTER 1
+#endif
+constexpr int kCS = ODPO_CLUSTER;          // CTAs per thread-block cluster (one row per cluster)
 #ifndef ODPO_NEPI
 #define ODPO_NEPI 2
 #endif
@@ -68,6 +72,48 @@ __device__ __forceinline__ void mbar_arrive_tx(uint32_t b, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes)
                : "memory");
 }
+// ---- thread-block cluster helpers (DSMEM): 32-bit shared::cluster addresses
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t mapa(uint32_t local_addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local_addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_cl_u32(uint32_t addr, uint32_t v) {
+  asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_cl_u64(uint32_t addr, uint64_t v) {
+  asm volatile("st.shared::cluster.u64 [%0], %1;" ::"r"(addr), "l"(v) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cl(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cl_n(uint32_t cluster_addr, uint32_t n) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(cluster_addr),
+               "r"(n)
+               : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release;\n\tbarrier.cluster.wait.acquire;" ::: "memory");
+}
+
+// Blocking wait on the phase with the given parity (cluster-scope acquire: a barrier may
+// receive arrivals, and the data they publish, from other CTAs of the cluster).
+__device__ __forceinline__ void mbar_wait_cl(uint32_t b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1, %2;\n\t"
+      "@!p bra WAIT%=;\n}" ::"r"(b),
+      "r"(parity), "r"(1000000u)
+      : "memory");
+}
+
 // Blocking wait on the phase with the given parity.  The suspend-time hint lets the hardware
 // park the warp until the phase completes instead of spinning through issue slots.
 __device__ __forceinline__ void mbar_wait(uint32_t b, uint32_t parity) {
@@ -104,8 +150,10 @@ struct RowSlot {
   const char* row;
   char* drow;
   float c, coef, gtok, xtok;
-  float pm[kNCW], pr[kNCW];
+  float pm[32], pr[32];  // per-warp (m, r) partials: [cluster rank * kNCW + warp]
 };
+// the header (kind .. drow) is what the cluster leader broadcasts to its peers
+constexpr int kSlotHeaderBytes = 56;
 
 // ------------------------------------------------------------------ per-batch online update
 // fp32 inputs (DT 0): exact exclusion of one max element (log1p form, 1e-5 contract).

@@ -1,5 +1,5 @@
 #!/bin/bash
-for lib in build_variants/libodpo_K4.so build_variants/libodpo_K8.so build_variants/libodpo_Q.so; do
+for lib in default build_variants/libodpo_C2.so build_variants/libodpo_C4.so build_variants/libodpo_C8.so; do
   for args in "--lookahead 1" "--lookahead 0" "--schedule two_pass"; do
     if [ "$lib" = default ]; then L=""; else L="ODPO_LIB=$PWD/$lib"; fi
     env $L timeout 60 python bench.py --config ${CFG:-pythia} --steps 10 --warmup 3 --no-cpu --no-e2e $args 2>&1 | tail -1 | python -c "
