@@ -47,6 +47,12 @@ def parse():
     ap.add_argument("--exp2-split", type=int, default=-1)
     ap.add_argument("--lookahead", type=int, default=-1)
     ap.add_argument("--mask", default="dense", choices=["dense", "prefix"])
+    ap.add_argument("--gradient", default="scaled", choices=["scaled", "unscaled"],
+                    help="scaled: dlogits (the north_star output); unscaled: G + row_scale")
+    ap.add_argument("--row-gap", type=int, default=-1)
+    ap.add_argument("--engine", type=int, default=-1, help="row-engine geometry (-1 auto)")
+    ap.add_argument("--no-aux", action="store_true",
+                    help="skip the auxiliary timing of the other gradient form")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -221,18 +227,28 @@ def run_ours(args, rank, world, local_rank):
 
     stats = torch.zeros(16, dtype=torch.float64, device=dev)
     status = torch.zeros(1, dtype=torch.int32, device=dev)
+    row_scale = torch.empty((B, T), dtype=torch.float32, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     launches = [0]
 
-    def step(timed_loss=None):
+    def loss_call(gradient, pair_rows, ref, tok, msk):
+        if gradient == "unscaled":
+            return odpo.online_dpo_loss_fwd_bwd_unscaled(
+                logits, ref, tok, msk, w.beta, pair_rows=pair_rows, p_global=Pg, G=dlogits,
+                row_scale=row_scale, ctas_per_sm=args.ctas_per_sm, exp2_split=args.exp2_split,
+                lookahead=args.lookahead, row_gap=args.row_gap, engine=args.engine, stats=stats,
+                status=status)
+        return odpo.online_dpo_loss_fwd_bwd(logits, ref, tok, msk, w.beta, pair_rows=pair_rows,
+                                            p_global=Pg, dlogits=dlogits, schedule=args.schedule,
+                                            lag_pairs=args.lag, ctas_per_sm=args.ctas_per_sm,
+                                            exp2_split=args.exp2_split, lookahead=args.lookahead,
+                                            engine=args.engine, stats=stats, status=status)
+
+    def step(timed_loss=None, gradient=args.gradient):
         sel = odpo.pair_select(rewards, eos, pen, status=status, sel_stats=stats[10:13])
         if timed_loss is not None:
             timed_loss[0].record()
-        out = odpo.online_dpo_loss_fwd_bwd(logits, ref_logp, tokens, mask, w.beta,
-                                           pair_rows=sel.pair_rows, p_global=Pg, dlogits=dlogits,
-                                           schedule=args.schedule, lag_pairs=args.lag,
-                                           ctas_per_sm=args.ctas_per_sm, exp2_split=args.exp2_split,
-                                           lookahead=args.lookahead, stats=stats, status=status)
+        out = loss_call(gradient, sel.pair_rows, ref_logp, tokens, mask)
         if timed_loss is not None:
             timed_loss[1].record()
         odpo.allreduce_stats(stats)
@@ -259,6 +275,7 @@ def run_ours(args, rank, world, local_rank):
         torch.cuda.synchronize()
     step_ms = np.array([a.elapsed_time(b) for a, b in ev])
     loss_ms = np.array([a.elapsed_time(b) for a, b in lev])
+    n_launch = launches[0]
     tot = torch.tensor([step_ms.sum()], dtype=torch.float64, device=dev)
     if world > 1:
         dist.barrier()
@@ -271,8 +288,28 @@ def run_ours(args, rank, world, local_rank):
     alg_bytes = rho * B * T * V * s_in + B * T * V * s_in
     achieved = alg_bytes / (loss_ms.mean() / 1e3) / 1e9
     peak, peak_src = peaks()
+
+    # auxiliary: the other gradient form on the same inputs (same bytes, not the headline)
+    aux = None
+    if not args.no_aux:
+        other = "unscaled" if args.gradient == "scaled" else "scaled"
+        for _ in range(2):
+            step(gradient=other)
+        aev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(K)]
+        for k in range(K):
+            flush.zero_()
+            torch.cuda.synchronize()
+            step(aev[k], gradient=other)
+        torch.cuda.synchronize()
+        ams = np.array([a.elapsed_time(b) for a, b in aev])
+        aach = alg_bytes / (ams.mean() / 1e3) / 1e9
+        aux = {"gradient": other, "loss_ms_mean": float(ams.mean()), "achieved": aach,
+               "frac": aach / peak, "pairs_per_s_loss_only": world * P / (ams.mean() / 1e3),
+               "status": int(status.item())}
     traffic = None
-    tp = os.path.join(ROOT, "profiles", f"ncu_traffic_{args.config}.json")
+    sfx = "" if args.gradient == "scaled" else "_unscaled"
+    tp = os.path.join(ROOT, "profiles", f"ncu_traffic_{args.config}{sfx}.json")
     if os.path.exists(tp):
         try:
             traffic = json.load(open(tp)).get("dram_bytes_per_launch")
@@ -307,10 +344,7 @@ def run_ours(args, rank, world, local_rank):
             d_mask.copy_(h_mask, non_blocking=True)
             d_ref.copy_(h_ref, non_blocking=True)
             sel = odpo.pair_select(d_rew, d_eos, pen, status=status, sel_stats=stats[10:13])
-            out = odpo.online_dpo_loss_fwd_bwd(logits, d_ref, d_tok, d_mask, w.beta,
-                                               pair_rows=sel.pair_rows, p_global=Pg,
-                                               dlogits=dlogits, schedule=args.schedule,
-                                               lag_pairs=args.lag, stats=stats, status=status)
+            out = loss_call(args.gradient, sel.pair_rows, d_ref, d_tok, d_mask)
             odpo.allreduce_stats(stats)
             h_stats.copy_(stats, non_blocking=True)
             h_z.copy_(out.z, non_blocking=True)
@@ -363,17 +397,21 @@ def run_ours(args, rank, world, local_rank):
                        "K": 2, "T": T, "V": V, "beta": w.beta, "mask": args.mask,
                        "ref_logp": "seq_logprobs over independent reference logits (setup)",
                        "schedule": args.schedule, "exp2_split": args.exp2_split,
+                       "gradient": args.gradient, "engine": args.engine,
                        "parallelism": f"dp{world}",
                        "l2": "inputs (%.2f GB) > L2; plus 256 MiB L2 flush between timed steps"
                              % (B * T * V * s_in / 1e9)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                         "kernel": "odpo_online_dpo_loss_fwd_bwd (prep + fused fwd/bwd)",
+                         "kernel": ("odpo_online_dpo_loss_fwd_bwd (prep + fused fwd/bwd)"
+                                    if args.gradient == "scaled" else
+                                    "odpo_online_dpo_loss_fwd_bwd_unscaled (prep + fwd/bwd)"),
                          "alg_bytes_per_launch": alg_bytes,
                          "loss_ms_mean": float(loss_ms.mean())},
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": int(launches[0] * K),
+            "gpu_launches": int(n_launch * K),
+            "aux_gradient_form": aux,
             "clocks": clk.summary(),
             "tokens_vocab_per_s": world * B * T * V * K / (tot_ms / 1e3),
             "eff_gbs_step": world * alg_bytes * K / (tot_ms / 1e3) / 1e9,

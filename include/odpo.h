@@ -111,6 +111,11 @@ typedef struct {
   int32_t exp2_split;   /* bf16 only: index of the MUFU/FMA-polynomial exp2 split
                            (-1 = library default)        */
   int32_t lookahead;    /* FUSED: rows a CTA decodes ahead of the row it streams (-1 = default) */
+  int32_t row_gap;      /* UNSCALED: forward rows a CTA streams between a row's forward and its
+                           backward, 0 or 1 (-1 = default 0)                          */
+  int32_t engine;       /* row-engine geometry: -1 auto, 0 = 4 consumer warps x 3-stage ring x
+                           4 CTAs/SM, 1 = 8 warps x 6 stages x 2 CTAs/SM;
+                           geometry 1 requires exp2_split -1 or 0                   */
 } odpo_launch_opts;
 
 /*
@@ -199,6 +204,33 @@ odpo_status odpo_online_dpo_loss_fwd_bwd_ex(const void* policy_logits, odpo_dtyp
                                             float* pair_logit, double* stats, uint32_t* status,
                                             void* workspace, size_t workspace_bytes,
                                             odpo_launch_opts* opts, void* stream);
+
+/*
+ * odpo_online_dpo_loss_fwd_bwd_unscaled -- the same loss, seq_logp, pair_logit, stats and
+ * status as odpo_online_dpo_loss_fwd_bwd, with the gradient returned FACTORED per row
+ * (performance tier; the gradient of PAPER.md:83's objective):
+ *
+ *   G          [B,T,V] device out, same dtype as the logits, strides (gstride_b, gstride_t);
+ *              may EQUAL policy_logits (in place) only with identical strides.
+ *              G[b,t,:] = softmax(invT x[b,t,:]) - onehot(tok[b,t]) for mask = 1 rows of
+ *              sequences referenced by a pair, 0 elsewhere.
+ *   row_scale  [B][T] f32 device out: coef_b * mask[b,t] (0 for unreferenced sequences), with
+ *              coef_c = +beta sigma(-z) invT / P_global, coef_r = -coef_c.
+ *
+ *   dlogits[b,t,:] = row_scale[b,t] * G[b,t,:]; a consumer such as the LM-head backward GEMM
+ *   folds row_scale into its epilogue / prologue.  G does not depend on the pair outcome, so
+ *   each row's backward follows its own forward in the same CTA and re-reads the row from L2:
+ *   one HBM read and one HBM write of [B,T,V] for every shape.
+ *   opts (may be NULL): schedule must be AUTO; ctas_per_sm, exp2_split, lookahead, row_gap apply;
+ *   opts->launches returns 2.  Other arguments and errors as odpo_online_dpo_loss_fwd_bwd.
+ */
+odpo_status odpo_online_dpo_loss_fwd_bwd_unscaled(
+    const void* policy_logits, odpo_dtype dt, int64_t B, int64_t T, int64_t V, int64_t stride_b,
+    int64_t stride_t, const float* ref_logp, const int32_t* tokens, const uint8_t* mask,
+    const int32_t* pair_rows, int64_t P, int64_t P_global, float beta, float inv_temperature,
+    void* G, int64_t gstride_b, int64_t gstride_t, float* row_scale, float* seq_logp,
+    float* pair_logit, double* stats, uint32_t* status, void* workspace, size_t workspace_bytes,
+    odpo_launch_opts* opts, void* stream);
 
 /* Host-only: device scratch bytes needed by the calls above for B sequences of T tokens
    and P pairs (about 13 bytes per row + 80 bytes per pair + small). */

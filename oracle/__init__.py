@@ -51,7 +51,11 @@ def lib():
                                        C.c_int]
         L.orc_online_dpo_loss_fwd_bwd.argtypes = [P, C.c_int, i64, i64, i64, i64, i64, P, P, P, P,
                                                   i64, i64, f32, f32, P, P, i64, P, P, P, P, C.c_int]
-        for f in (L.orc_pair_select, L.orc_seq_logprobs, L.orc_online_dpo_loss_fwd_bwd):
+        L.orc_online_dpo_loss_fwd_bwd_unscaled.argtypes = [
+            P, C.c_int, i64, i64, i64, i64, i64, P, P, P, P, i64, i64, f32, f32, P, P, i64, P, P, P,
+            P, P, C.c_int]
+        for f in (L.orc_pair_select, L.orc_seq_logprobs, L.orc_online_dpo_loss_fwd_bwd,
+                  L.orc_online_dpo_loss_fwd_bwd_unscaled):
             f.restype = C.c_int
         _lib = L
     return _lib
@@ -117,8 +121,12 @@ def seq_logprobs(logits, tokens, mask, inv_temperature=1.0, n_threads=1):
 
 
 def online_dpo_loss_fwd_bwd(logits, ref_logp, tokens, mask, beta, pair_rows=None, p_global=None,
-                            inv_temperature=1.0, want_dlogits=False, dl_rows=None, n_threads=1):
-    """Returns dict(seq_logp[B], z[P], stats[10], status, dlogits[n, V] or None)."""
+                            inv_temperature=1.0, want_dlogits=False, dl_rows=None, n_threads=1,
+                            unscaled=False):
+    """Returns dict(seq_logp[B], z[P], stats[10], status, dlogits[n, V] or None).
+
+    unscaled=True: 'dlogits' holds G = mask (softmax - onehot) (no coef_b) and 'row_scale'[B, T]
+    holds coef_b * mask, so the gradient is row_scale[..., None] * G."""
     a, dt, sb, st = _logits_args(logits)
     B, T, V = a.shape
     tok = np.ascontiguousarray(tokens, dtype=np.int32).reshape(B, T)
@@ -141,15 +149,21 @@ def online_dpo_loss_fwd_bwd(logits, ref_logp, tokens, mask, beta, pair_rows=None
     z = np.zeros(P, np.float64)
     stats = np.zeros(10, np.float64)
     status = np.zeros(1, np.uint32)
-    rc = lib().orc_online_dpo_loss_fwd_bwd(
-        _ptr(a), dt, B, T, V, sb, st, _ptr(ref), _ptr(tok), _ptr(msk), _ptr(pr), P, Pg,
-        float(np.float32(beta)), float(np.float32(inv_temperature)), _ptr(dl), _ptr(rows), n_rows,
-        _ptr(S), _ptr(z), _ptr(stats), _ptr(status), int(n_threads))
+    rs = np.zeros((B, T), np.float64) if unscaled else None
+    args = [_ptr(a), dt, B, T, V, sb, st, _ptr(ref), _ptr(tok), _ptr(msk), _ptr(pr), P, Pg,
+            float(np.float32(beta)), float(np.float32(inv_temperature)), _ptr(dl), _ptr(rows),
+            n_rows]
+    if unscaled:
+        rc = lib().orc_online_dpo_loss_fwd_bwd_unscaled(
+            *args, _ptr(rs), _ptr(S), _ptr(z), _ptr(stats), _ptr(status), int(n_threads))
+    else:
+        rc = lib().orc_online_dpo_loss_fwd_bwd(
+            *args, _ptr(S), _ptr(z), _ptr(stats), _ptr(status), int(n_threads))
     if rc:
         raise ValueError("orc_online_dpo_loss_fwd_bwd: invalid argument")
     if dl is not None and dl_rows is None:
         dl = dl.reshape(B, T, V)
-    return dict(seq_logp=S, z=z, stats=stats, status=int(status[0]), dlogits=dl)
+    return dict(seq_logp=S, z=z, stats=stats, status=int(status[0]), dlogits=dl, row_scale=rs)
 
 
 def to_bf16_bits(x) -> np.ndarray:

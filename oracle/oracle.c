@@ -24,6 +24,9 @@
  *                       max E log sigma(beta log pi(y+)/pi_init(y+) - beta log pi(y-)/pi_init(y-)))
  *                     as a mean over pairs of -log sigma(z) (reading R3), and its exact
  *                     gradient w.r.t. the logits, dL/dx = coef_b (softmax - onehot).
+ *   orc_online_dpo_loss_fwd_bwd_unscaled
+ *                     the same, with the gradient returned factored per row:
+ *                     G = softmax - onehot and row_scale = coef_b (dL/dx = row_scale * G).
  *
  * Every step follows the plain definition: y = x * invT; m = max_v y_v;
  * s = sum_v exp(y_v - m) (sequential); logp = (y_tok - m) - log(s); S_b = sum_t logp
@@ -242,6 +245,7 @@ typedef struct {
   const uint8_t* refd;  /* [B] referenced by a pair */
   const int64_t* rows;  /* rows to emit (NULL = all) */
   int64_t n0, n1;
+  int unscaled;         /* emit G = softmax - onehot (without coef_b) */
   double* out;          /* [n][V] */
 } grad_job;
 
@@ -264,19 +268,20 @@ static void* grad_worker(void* arg) {
     int64_t base = b * in->sb + t * in->stt;
     for (int64_t v = 0; v < V; ++v) {
       double y = load_x(in->logits, in->dtype, base + v) * in->invT;
-      o[v] = j->coef[b] * (exp(y - lse) - (v == tok ? 1.0 : 0.0));
+      double gv = exp(y - lse) - (v == tok ? 1.0 : 0.0);
+      o[v] = j->unscaled ? gv : j->coef[b] * gv;
     }
   }
   return NULL;
 }
 
-int orc_online_dpo_loss_fwd_bwd(const void* logits, int dtype, int64_t B, int64_t T, int64_t V,
-                                int64_t stride_b, int64_t stride_t, const float* ref_logp,
-                                const int32_t* tokens, const uint8_t* mask,
-                                const int32_t* pair_rows, int64_t P, int64_t P_global,
-                                float beta, float inv_temperature, double* dlogits,
-                                const int64_t* dl_rows, int64_t n_dl_rows, double* seq_logp,
-                                double* z_out, double* stats, uint32_t* status, int n_threads) {
+static int loss_core(const void* logits, int dtype, int64_t B, int64_t T, int64_t V,
+                     int64_t stride_b, int64_t stride_t, const float* ref_logp,
+                     const int32_t* tokens, const uint8_t* mask, const int32_t* pair_rows,
+                     int64_t P, int64_t P_global, float beta, float inv_temperature,
+                     double* dlogits, const int64_t* dl_rows, int64_t n_dl_rows,
+                     double* seq_logp, double* z_out, double* stats, uint32_t* status,
+                     int n_threads, int unscaled, double* row_scale) {
   if (!logits || !ref_logp || !tokens || !mask || !seq_logp || !stats) return 1;
   if (B <= 0 || T <= 0 || V <= 0 || P <= 0 || P_global < P) return 1;
   if (!pair_rows && B != 2 * P) return 1;
@@ -335,6 +340,7 @@ int orc_online_dpo_loss_fwd_bwd(const void* logits, int dtype, int64_t B, int64_
       jobs[i].rows = dl_rows;
       jobs[i].n0 = n * i / nt;
       jobs[i].n1 = n * (i + 1) / nt;
+      jobs[i].unscaled = unscaled;
       jobs[i].out = dlogits;
     }
     if (nt == 1) {
@@ -346,9 +352,44 @@ int orc_online_dpo_loss_fwd_bwd(const void* logits, int dtype, int64_t B, int64_
     free(jobs);
     free(th);
   }
+  if (row_scale) {
+    /* dlogits[b,t,:] = row_scale[b,t] * G[b,t,:] */
+    for (int64_t g = 0; g < B * T; ++g) {
+      int64_t b = g / T;
+      row_scale[g] = (refd[b] && mask[g]) ? coef[b] : 0.0;
+    }
+  }
   free(ntok);
   free(coef);
   free(refd);
   if (status) *status |= st;
   return 0;
+}
+
+int orc_online_dpo_loss_fwd_bwd(const void* logits, int dtype, int64_t B, int64_t T, int64_t V,
+                                int64_t stride_b, int64_t stride_t, const float* ref_logp,
+                                const int32_t* tokens, const uint8_t* mask,
+                                const int32_t* pair_rows, int64_t P, int64_t P_global,
+                                float beta, float inv_temperature, double* dlogits,
+                                const int64_t* dl_rows, int64_t n_dl_rows, double* seq_logp,
+                                double* z_out, double* stats, uint32_t* status, int n_threads) {
+  return loss_core(logits, dtype, B, T, V, stride_b, stride_t, ref_logp, tokens, mask, pair_rows,
+                   P, P_global, beta, inv_temperature, dlogits, dl_rows, n_dl_rows, seq_logp,
+                   z_out, stats, status, n_threads, 0, NULL);
+}
+
+/* The same loss with the gradient factored per row (performance tier):
+   G[b,t,:] = mask[b,t] * [b referenced] * (softmax(invT x) - onehot(tok)) and
+   row_scale[b,t] = mask[b,t] * [b referenced] * coef_b, so dL/dx = row_scale * G. */
+int orc_online_dpo_loss_fwd_bwd_unscaled(const void* logits, int dtype, int64_t B, int64_t T,
+                                         int64_t V, int64_t stride_b, int64_t stride_t,
+                                         const float* ref_logp, const int32_t* tokens,
+                                         const uint8_t* mask, const int32_t* pair_rows, int64_t P,
+                                         int64_t P_global, float beta, float inv_temperature,
+                                         double* G, const int64_t* g_rows, int64_t n_g_rows,
+                                         double* row_scale, double* seq_logp, double* z_out,
+                                         double* stats, uint32_t* status, int n_threads) {
+  return loss_core(logits, dtype, B, T, V, stride_b, stride_t, ref_logp, tokens, mask, pair_rows,
+                   P, P_global, beta, inv_temperature, G, g_rows, n_g_rows, seq_logp, z_out,
+                   stats, status, n_threads, 1, row_scale);
 }

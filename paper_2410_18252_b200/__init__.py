@@ -44,7 +44,8 @@ class OdpoError(RuntimeError):
 
 class _Opts(C.Structure):
     _fields_ = [("schedule", C.c_int32), ("lag_pairs", C.c_int32), ("ctas_per_sm", C.c_int32),
-                ("launches", C.c_int32), ("exp2_split", C.c_int32), ("lookahead", C.c_int32)]
+                ("launches", C.c_int32), ("exp2_split", C.c_int32), ("lookahead", C.c_int32),
+                ("row_gap", C.c_int32), ("engine", C.c_int32)]
 
 
 _lib = None
@@ -69,8 +70,11 @@ def _L():
                                                    sz, P]
         L.odpo_online_dpo_loss_fwd_bwd_ex.argtypes = (L.odpo_online_dpo_loss_fwd_bwd.argtypes[:-1]
                                                       + [C.POINTER(_Opts), P])
+        L.odpo_online_dpo_loss_fwd_bwd_unscaled.argtypes = [
+            P, C.c_int, i64, i64, i64, i64, i64, P, P, P, P, i64, i64, f32, f32, P, i64, i64, P, P,
+            P, P, P, P, sz, C.POINTER(_Opts), P]
         for f in (L.odpo_pair_select, L.odpo_seq_logprobs, L.odpo_online_dpo_loss_fwd_bwd,
-                  L.odpo_online_dpo_loss_fwd_bwd_ex):
+                  L.odpo_online_dpo_loss_fwd_bwd_ex, L.odpo_online_dpo_loss_fwd_bwd_unscaled):
             f.restype = C.c_int
         L.odpo_workspace_bytes.argtypes = [i64, i64, i64]
         L.odpo_workspace_bytes.restype = sz
@@ -194,6 +198,7 @@ class LossOutput:
     z: torch.Tensor
     status: torch.Tensor
     launches: int
+    row_scale: torch.Tensor | None = None  # unscaled call: dlogits holds G, grad = row_scale * G
 
     def named(self) -> dict:
         s = self.stats.tolist()
@@ -206,7 +211,7 @@ def online_dpo_loss_fwd_bwd(policy_logits: torch.Tensor, ref_logp: torch.Tensor,
                             inv_temperature: float = 1.0, inplace: bool = False,
                             dlogits: torch.Tensor | None = None, schedule: str = "auto",
                             lag_pairs: int = 0, ctas_per_sm: int = 0, exp2_split: int = -1,
-                            lookahead: int = -1,
+                            lookahead: int = -1, engine: int = -1,
                             stats: torch.Tensor | None = None,
                             status: torch.Tensor | None = None) -> LossOutput:
     """Online DPO loss, statistics and dlogits in one call.
@@ -241,13 +246,67 @@ def online_dpo_loss_fwd_bwd(policy_logits: torch.Tensor, ref_logp: torch.Tensor,
     nb = workspace_bytes(B, T, max(P, 1))
     ws = _workspace(dev, nb)
     opts = _Opts(SCHEDULES[schedule], int(lag_pairs), int(ctas_per_sm), 0, int(exp2_split),
-                 int(lookahead))
+                 int(lookahead), -1, int(engine))
     _check(_L().odpo_online_dpo_loss_fwd_bwd_ex(
         _p(policy_logits), dt, B, T, V, sb, st, _p(ref_logp), _p(tokens), _p(mask), _p(pair_rows),
         P, Pg, float(beta), float(inv_temperature), _p(dl), dl.stride(0), dl.stride(1), _p(seq),
         _p(z), _p(stats), _p(status), _p(ws), ws.numel(), C.byref(opts), _stream()),
         "odpo_online_dpo_loss_fwd_bwd")
     return LossOutput(stats, dl, seq, z[:P], status, int(opts.launches))
+
+
+def online_dpo_loss_fwd_bwd_unscaled(policy_logits: torch.Tensor, ref_logp: torch.Tensor,
+                                     tokens: torch.Tensor, mask: torch.Tensor, beta: float,
+                                     pair_rows: torch.Tensor | None = None,
+                                     p_global: int | None = None, inv_temperature: float = 1.0,
+                                     inplace: bool = False, G: torch.Tensor | None = None,
+                                     row_scale: torch.Tensor | None = None, ctas_per_sm: int = 0,
+                                     exp2_split: int = -1, lookahead: int = -1, row_gap: int = -1,
+                                     engine: int = -1,
+                                     stats: torch.Tensor | None = None,
+                                     status: torch.Tensor | None = None) -> LossOutput:
+    """The loss call with the gradient factored per row: out.dlogits holds
+    G = mask (softmax - onehot) and out.row_scale [B, T] holds coef_b * mask, so the gradient
+    is out.row_scale[..., None] * out.dlogits (one HBM read and one write of the logits)."""
+    dt, B, T, V, sb, st = _logits_meta(policy_logits, "policy_logits")
+    ref_logp = _dev(ref_logp, "ref_logp", torch.float32).contiguous()
+    tokens = _dev(tokens, "tokens", torch.int32).contiguous()
+    mask = _dev(mask, "mask", torch.uint8).contiguous()
+    dev = policy_logits.device
+    if pair_rows is not None:
+        pair_rows = _dev(pair_rows, "pair_rows", torch.int32).contiguous()
+        P = pair_rows.shape[0]
+    else:
+        P = B // 2
+    Pg = P if p_global is None else int(p_global)
+    if inplace:
+        g = policy_logits
+    elif G is not None:
+        g = _dev(G, "G", policy_logits.dtype)
+    else:
+        g = torch.empty_like(policy_logits)
+    if g.dim() != 3 or g.stride(2) != 1:
+        raise OdpoError("G must be [B, T, V] with a contiguous last dimension")
+    if row_scale is None:
+        row_scale = torch.empty((B, T), dtype=torch.float32, device=dev)
+    row_scale = _dev(row_scale, "row_scale", torch.float32)
+    if not row_scale.is_contiguous() or row_scale.numel() != B * T:
+        raise OdpoError("row_scale must be a contiguous [B, T] f32 tensor")
+    seq = torch.empty(B, dtype=torch.float32, device=dev)
+    z = torch.empty(max(P, 1), dtype=torch.float32, device=dev)
+    if stats is None:
+        stats = torch.zeros(STATS_BUF, dtype=torch.float64, device=dev)
+    if status is None:
+        status = torch.zeros(1, dtype=torch.int32, device=dev)
+    ws = _workspace(dev, workspace_bytes(B, T, max(P, 1)))
+    opts = _Opts(SCHEDULES["auto"], 0, int(ctas_per_sm), 0, int(exp2_split), int(lookahead),
+                 int(row_gap), int(engine))
+    _check(_L().odpo_online_dpo_loss_fwd_bwd_unscaled(
+        _p(policy_logits), dt, B, T, V, sb, st, _p(ref_logp), _p(tokens), _p(mask), _p(pair_rows),
+        P, Pg, float(beta), float(inv_temperature), _p(g), g.stride(0), g.stride(1), _p(row_scale),
+        _p(seq), _p(z), _p(stats), _p(status), _p(ws), ws.numel(), C.byref(opts), _stream()),
+        "odpo_online_dpo_loss_fwd_bwd_unscaled")
+    return LossOutput(stats, g, seq, z[:P], status, int(opts.launches), row_scale)
 
 
 def allreduce_stats(stats: torch.Tensor, group=None) -> torch.Tensor:

@@ -234,6 +234,8 @@ struct LossArgs {
   int64_t max_lead;  // FUSED: cap on forward rows dispensed ahead of the backward frontier
   int look;         // producer decode lookahead (rows), <= kSlots - 2
   int esize;
+  float* row_scale;  // UNSC: [B*T] out, coef_b * mask (dlogits = row_scale * G)
+  int row_gap;       // UNSC: forward rows streamed between a row's forward and its backward
 };
 
 __device__ __forceinline__ const char* row_ptr(const LossArgs& a, int64_t b, int64_t t) {
@@ -304,6 +306,16 @@ __device__ __noinline__ void pair_reduce_warp(const LossArgs& a, int64_t p) {
     last = (done == (unsigned)(a.P - 1));
   }
   last = __shfl_sync(kFull, last, 0);
+  if (a.row_scale) {
+    // UNSC: the row scales of both sequences, coef_b * mask (0 for an invalid pair)
+    float coef = 0.f;
+    if (lane == 0 && c >= 0 && r >= 0) coef = a.w.seq_coef[c];
+    coef = __shfl_sync(kFull, coef, 0);
+    for (int64_t t = lane; t < a.T; t += 32) {
+      if (c >= 0) a.row_scale[c * a.T + t] = a.mask[c * a.T + t] ? coef : 0.f;
+      if (r >= 0) a.row_scale[r * a.T + t] = a.mask[r * a.T + t] ? -coef : 0.f;
+    }
+  }
   if (!last) return;
   fence_acq_rel_gpu();
   double acc[ODPO_NSTATS];
@@ -344,7 +356,10 @@ __global__ void __launch_bounds__(kRowThreads, 2) k_row_bwd(LossArgs a) {
 }
 
 // ------------------------------------------------------------------ the TMA-ring engine
-enum { M_SEQ = 0, M_FUSED = 1 };
+// M_SEQ: forward rows only.  M_FUSED: pair-scheduled forward + scaled backward.  M_UNSC: each
+// row's forward pass and then its unscaled backward G = softmax - onehot in the same CTA (the
+// re-read is one row behind, so it is served from L2); the pair reducer writes row_scale.
+enum { M_SEQ = 0, M_FUSED = 1, M_UNSC = 2, M_NMODES = 3 };
 
 // Fused dispatch (adaptive, per-pair backward counters).  Forward rows are dispensed in pair
 // order from one counter (C_TICKET).  Backward rows are dispensed pair by pair: C_BPAIR is the
@@ -505,6 +520,7 @@ __device__ __forceinline__ bool decode_row(const LossArgs& a, int64_t tk, bool f
   const int64_t s = __ldcg(a.w.unref + k);
   S.kind = K_ZERO;
   S.s = s;
+  S.g = s * T + t;
   S.drow = drow_ptr(a, s, t);
   return false;
 }
@@ -513,10 +529,10 @@ __device__ __forceinline__ bool decode_row(const LossArgs& a, int64_t tk, bool f
 template <int MODE>
 __device__ __forceinline__ bool count_row(const LossArgs& a, const RowSlot& S, int lane) {
   unsigned last = 0;
-  if (lane == 0 && (MODE == M_FUSED || a.seqsum)) {
+  if (lane == 0 && (MODE != M_SEQ || a.seqsum)) {
     // release: this row's statistics before the count; acquire: the other rows' statistics
-    unsigned* cnt = MODE == M_FUSED ? &a.w.pair_cnt[S.p] : &a.w.seq_cnt[S.s];
-    const unsigned need = MODE == M_FUSED ? (unsigned)(2 * a.T) : (unsigned)a.T;
+    unsigned* cnt = MODE != M_SEQ ? &a.w.pair_cnt[S.p] : &a.w.seq_cnt[S.s];
+    const unsigned need = MODE != M_SEQ ? (unsigned)(2 * a.T) : (unsigned)a.T;
     last = (atom_add_acq_rel(cnt, 1u) == need - 1u);
   }
   last = __shfl_sync(kFull, last, 0);
@@ -526,7 +542,7 @@ __device__ __forceinline__ bool count_row(const LossArgs& a, const RowSlot& S, i
 
 template <int MODE>
 __device__ __forceinline__ void complete_unit(const LossArgs& a, const RowSlot& S, int lane) {
-  if (MODE == M_FUSED) {
+  if (MODE != M_SEQ) {
     pair_reduce_warp(a, S.p);
   } else {
     double Sq;
@@ -548,13 +564,16 @@ __device__ __forceinline__ void complete_unit(const LossArgs& a, const RowSlot& 
 // into its slot through DSMEM, in fixed (rank, warp) order).  Shorter per-row latency means a
 // pair completes sooner after its rows are dispensed, which keeps the forward/backward lead
 // inside L2.  CS = 1 is the plain single-CTA engine.
-template <int DT, int MODE, int PV, int CS>
-__global__ void __launch_bounds__(kEngThreads, ODPO_CTAS_PER_SM) k_engine(LossArgs a) {
+template <int DT, int MODE, int PV, int CS, class GE>
+__global__ void __launch_bounds__(GE::THREADS, GE::CPS) k_engine(LossArgs a) {
+  constexpr int kNCW = GE::NCW, kNCT = GE::NCT, kUB = GE::UB, kStages = GE::STAGES;
+  constexpr int kProdWarp = GE::PROD, kParWarp = GE::PAR, kEpiWarp = GE::EPI;
   constexpr int NPF = DT == 1 ? kPoly[PV].npf : 0;
   constexpr int NPB = DT == 1 ? kPoly[PV].npb : 0;
   constexpr int N = Traits<DT>::N;
   constexpr int NPART = CS * kNCW;  // partials per row
   static_assert(NPART <= 32, "one warp merges the partials");
+  static_assert(MODE != M_UNSC || CS == 1, "the unscaled mode runs on single-CTA clusters");
   extern __shared__ __align__(128) uint8_t ring[];
   __shared__ __align__(8) uint64_t full[kStages];
   __shared__ __align__(8) uint64_t empty[kStages];
@@ -625,22 +644,15 @@ __global__ void __launch_bounds__(kEngThreads, ODPO_CTAS_PER_SM) k_engine(LossAr
       Dispatch D{false, -1};
       int st = 0, dsl = 0, psl = 0, ahead = 0;
       uint32_t sph = 0, dph = 0, pph = 0;
-      uint32_t pmask = 0;  // per-slot parity of param_ready (advances only on B rows)
+      uint32_t pmask = 0;  // per-slot parity of param_ready (advances once per use)
       bool ended = false;
+      int64_t u_tk = -1;   // UNSC: the row whose backward is still to be emitted
+      int u_slot = -1;
+      uint32_t u_ph = 0;
       for (;;) {
         if (leader) {
-          // decode up to a.look rows ahead of the row being streamed
-          while (!ended && ahead <= a.look) {
-            int64_t tk;
-            bool fwd = true, more;
-            if (MODE == M_FUSED) {
-              const int r = fused_next(a, totalF, nzero, D, ahead == 0, fwd, tk);
-              if (r < 0) break;  // stream the rows already held, then retry
-              more = r > 0;
-            } else {
-              tk = (int64_t)atomicAdd(&a.w.counters[C_TICKET], 1u);
-              more = tk < total;
-            }
+          // fill slot dsl: a decoded row (more) or END (!more); fs/fph: UNSC backward rows
+          auto emit = [&](bool more, int64_t tk, bool fwd, int fs, uint32_t fph) {
             wait(sempty_s + 8 * dsl, dph ^ 1u);
             RowSlot& S = slots[dsl];
             uint64_t pol = pol_drop;
@@ -652,8 +664,15 @@ __global__ void __launch_bounds__(kEngThreads, ODPO_CTAS_PER_SM) k_engine(LossAr
               data = decode_row<DT, MODE>(a, tk, fwd, S, pol, pol_keep, pol_drop);
             }
             S.nchunk = data ? 1 : 0;
-            S.pphase = (pmask >> dsl) & 1u;
-            if (S.kind == K_B) pmask ^= 1u << dsl;
+            if (MODE == M_UNSC) {
+              // param_ready[slot] is published by the forward row's epilogue
+              S.fslot = fs;
+              S.pphase = fs >= 0 ? fph : (pmask >> dsl) & 1u;
+              if (S.kind == K_F) pmask ^= 1u << dsl;
+            } else {
+              S.pphase = (pmask >> dsl) & 1u;
+              if (S.kind == K_B) pmask ^= 1u << dsl;
+            }
             // broadcast the slot header to the peers, then signal slot_full everywhere
             for (int r = 1; r < CS; ++r) {
               const uint32_t dst = mapa(slots_s + dsl * (uint32_t)sizeof(RowSlot), r);
@@ -674,8 +693,47 @@ __global__ void __launch_bounds__(kEngThreads, ODPO_CTAS_PER_SM) k_engine(LossAr
                 mbar_arrive(sfull_s + 8 * y);
               }
             }
+            const int me = dsl;
             ++ahead;
             if (++dsl == kSlots) { dsl = 0; dph ^= 1u; }
+            return me;
+          };
+          // decode up to a.look rows ahead of the row being streamed
+          while (!ended && ahead <= a.look) {
+            int64_t tk;
+            bool fwd = true, more;
+            if (MODE == M_UNSC) {
+              // slot order F(k), U(k-1), F(k+1), U(k), ...: a row's backward streams one
+              // forward row after its own forward, so its epilogue has time to publish (m, l)
+              tk = (int64_t)atomicAdd(&a.w.counters[C_TICKET], 1u);
+              more = tk < totalF + nzero;
+              if (more && tk < totalF) {
+                const uint32_t fph = (pmask >> dsl) & 1u;
+                const int fs = emit(true, tk, true, -1, 0u);
+                if (a.row_gap == 0) {
+                  emit(true, tk, false, fs, fph);
+                  continue;
+                }
+                if (u_tk >= 0) emit(true, u_tk, false, u_slot, u_ph);
+                u_tk = tk;
+                u_slot = fs;
+                u_ph = fph;
+              } else {
+                if (u_tk >= 0) emit(true, u_tk, false, u_slot, u_ph);
+                u_tk = -1;
+                emit(more, tk, false, -1, 0u);
+              }
+              continue;
+            }
+            if (MODE == M_FUSED) {
+              const int r = fused_next(a, totalF, nzero, D, ahead == 0, fwd, tk);
+              if (r < 0) break;  // stream the rows already held, then retry
+              more = r > 0;
+            } else {
+              tk = (int64_t)atomicAdd(&a.w.counters[C_TICKET], 1u);
+              more = tk < total;
+            }
+            emit(more, tk, fwd, -1, 0u);
           }
           if (ahead == 0) break;
         } else {
@@ -686,7 +744,7 @@ __global__ void __launch_bounds__(kEngThreads, ODPO_CTAS_PER_SM) k_engine(LossAr
         if (kind == K_F || kind == K_B || kind == K_ZERO || kind == K_END) {
           const bool data = (kind == K_F || kind == K_B) && S.nchunk > 0 && v_hi > v_lo;
           const int nstage = data ? lch : 1;
-          const uint64_t pol = (MODE == M_FUSED && kind == K_F) ? pol_keep : pol_drop;
+          const uint64_t pol = (MODE != M_SEQ && kind == K_F) ? pol_keep : pol_drop;
           for (int c = 0; c < nstage; ++c) {
             wait(empty_s + 8 * st, sph ^ 1u);
             stage_slot[st] = kind == K_END ? -1 : psl;
@@ -737,7 +795,7 @@ __global__ void __launch_bounds__(kEngThreads, ODPO_CTAS_PER_SM) k_engine(LossAr
         RowSlot& S = slots[sl];
         const int kind = S.kind;
         if (kind == K_END) break;
-        if (kind == K_B) {
+        if (MODE == M_FUSED && kind == K_B) {
           while (ld_relaxed(&a.w.pair_ready[S.p]) == 0u) __nanosleep(32);
           fence_acq_rel_gpu();
           const float m = __ldcg(a.w.row_m + S.g);
@@ -802,6 +860,14 @@ __global__ void __launch_bounds__(kEngThreads, ODPO_CTAS_PER_SM) k_engine(LossAr
               if (a.tok_out) a.tok_out[S.g] = logp;
               if (a.lse_out) a.lse_out[S.g] = __fadd_rn(__fmul_rn(v.m, a.invT), l1p);
             }
+            if (MODE == M_UNSC) {
+              // the row's backward (G = softmax - onehot) constants, for this CTA's consumers
+              RowSlot& W = slots[sl];
+              W.c = fmaf(l1p, kLog2e, v.m * k2);
+              W.coef = 1.f;
+              W.gtok = expm1f(logp);
+              mbar_arrive(mready_s + 8 * sl);
+            }
             flag(a.status, fl);
           }
           if (count_row<MODE>(a, S, lane)) complete_unit<MODE>(a, S, lane);
@@ -811,6 +877,8 @@ __global__ void __launch_bounds__(kEngThreads, ODPO_CTAS_PER_SM) k_engine(LossAr
             if (a.lse_out) a.lse_out[S.g] = 0.f;
           }
           if (count_row<MODE>(a, S, lane)) complete_unit<MODE>(a, S, lane);
+        } else if (MODE == M_UNSC && kind == K_ZERO) {
+          if (lane == 0) a.row_scale[S.g] = 0.f;
         }
         __syncwarp();
         // rows the consumers never see also carry their NPART arrivals
@@ -904,15 +972,21 @@ __global__ void __launch_bounds__(kEngThreads, ODPO_CTAS_PER_SM) k_engine(LossAr
               S.pr[pidx] = wv.r;
             }
             arrive_leader(L_pready + 8 * sl, 1u);
-            arrive_leader(L_sempty + 8 * sl, 1u);
+            // UNSC: the slot is released when the row's backward has read its constants
+            if (MODE != M_UNSC) arrive_leader(L_sempty + 8 * sl, 1u);
           }
         }
       } else if (kind == K_B) {
         if (ch == 0) {
-          wait(mready_s + 8 * sl, S.pphase);
-          b_c = S.c;
-          b_coef = S.coef;
-          b_gtok = S.gtok;
+          const int fs = MODE == M_UNSC ? S.fslot : sl;
+          wait(mready_s + 8 * fs, S.pphase);
+          b_c = slots[fs].c;
+          b_coef = slots[fs].coef;
+          b_gtok = slots[fs].gtok;
+          if (MODE == M_UNSC) {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(sempty_s + 8 * fs);
+          }
         }
         uint4* vout = reinterpret_cast<uint4*>(r_drow) + c0;
         if (cnv == kCV) {
@@ -967,33 +1041,41 @@ __global__ void __launch_bounds__(kEngThreads, ODPO_CTAS_PER_SM) k_engine(LossAr
 struct DevInfo {
   int sms = 0;
   int l2 = 0;
-  int occ[2][2] = {{0, 0}, {0, 0}};  // [dtype][mode] (same for every poly variant)
+  int occ[2][2][M_NMODES] = {};  // [geometry][dtype][mode] (same for every poly variant)
 };
+// cluster size per mode: the unscaled mode always runs single-CTA
+template <int MODE>
+constexpr int mode_cs() { return MODE == M_UNSC ? 1 : kCS; }
 static DevInfo g_dev[128];
 static std::once_flag g_once[128];
 
-template <int DT, int MODE, int PV>
+template <int DT, int MODE, int PV, class GE>
 static void setup_one(int* occ) {
-  cudaFuncSetAttribute(k_engine<DT, MODE, PV, kCS>, cudaFuncAttributeMaxDynamicSharedMemorySize, kEngSmem);
+  constexpr int CS = mode_cs<MODE>();
+  cudaFuncSetAttribute(k_engine<DT, MODE, PV, CS, GE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       GE::SMEM);
   if (occ)
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, k_engine<DT, MODE, PV, kCS>, kEngThreads, kEngSmem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, k_engine<DT, MODE, PV, CS, GE>, GE::THREADS,
+                                                  GE::SMEM);
 }
 
-// Launch an engine instantiation, as thread-block clusters of kCS CTAs when kCS > 1.
-template <typename Kern>
-static void launch_k(Kern kern, int grid, cudaStream_t s, const LossArgs& a) {
-  if (kCS == 1) {
-    kern<<<grid, kEngThreads, kEngSmem, s>>>(a);
+// Launch an engine instantiation, as thread-block clusters of CS CTAs when CS > 1.
+template <int DT, int MODE, int PV, class GE>
+static void launch_k(int grid, cudaStream_t s, const LossArgs& a) {
+  constexpr int CS = mode_cs<MODE>();
+  auto kern = k_engine<DT, MODE, PV, CS, GE>;
+  if (CS == 1) {
+    kern<<<grid, GE::THREADS, GE::SMEM, s>>>(a);
     return;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)grid);
-  cfg.blockDim = dim3(kEngThreads);
-  cfg.dynamicSmemBytes = kEngSmem;
+  cfg.blockDim = dim3(GE::THREADS);
+  cfg.dynamicSmemBytes = GE::SMEM;
   cfg.stream = s;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = kCS;
+  at[0].val.clusterDim.x = (unsigned)CS;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
@@ -1002,9 +1084,19 @@ static void launch_k(Kern kern, int grid, cudaStream_t s, const LossArgs& a) {
 }
 template <int PV>
 static void setup_pv() {
-  setup_one<1, M_SEQ, PV>(nullptr);
-  setup_one<1, M_FUSED, PV>(nullptr);
+  setup_one<1, M_SEQ, PV, Geo0>(nullptr);
+  setup_one<1, M_FUSED, PV, Geo0>(nullptr);
+  setup_one<1, M_UNSC, PV, Geo0>(nullptr);
   if constexpr (PV + 1 < kNumPoly) setup_pv<PV + 1>();
+}
+template <class GE>
+static void setup_geo(DevInfo& d, int g) {
+  setup_one<0, M_SEQ, 0, GE>(&d.occ[g][0][M_SEQ]);
+  setup_one<0, M_FUSED, 0, GE>(&d.occ[g][0][M_FUSED]);
+  setup_one<0, M_UNSC, 0, GE>(&d.occ[g][0][M_UNSC]);
+  setup_one<1, M_SEQ, 0, GE>(&d.occ[g][1][M_SEQ]);
+  setup_one<1, M_FUSED, 0, GE>(&d.occ[g][1][M_FUSED]);
+  setup_one<1, M_UNSC, 0, GE>(&d.occ[g][1][M_UNSC]);
 }
 
 static const DevInfo& dev_info(int dev) {
@@ -1012,10 +1104,8 @@ static const DevInfo& dev_info(int dev) {
     DevInfo& d = g_dev[dev];
     cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev);
     cudaDeviceGetAttribute(&d.l2, cudaDevAttrL2CacheSize, dev);
-    setup_one<0, M_SEQ, 0>(&d.occ[0][M_SEQ]);
-    setup_one<0, M_FUSED, 0>(&d.occ[0][M_FUSED]);
-    setup_one<1, M_SEQ, 0>(&d.occ[1][M_SEQ]);
-    setup_one<1, M_FUSED, 0>(&d.occ[1][M_FUSED]);
+    setup_geo<Geo0>(d, 0);
+    setup_geo<Geo1>(d, 1);
     setup_pv<1>();
   });
   return g_dev[dev];
@@ -1044,7 +1134,7 @@ static odpo_status launched() {
 template <int MODE, int PV>
 static void launch_bf16(int pv, int grid, const LossArgs& a, cudaStream_t s) {
   if (pv == PV) {
-    launch_k(k_engine<1, MODE, PV, kCS>, grid, s, a);
+    launch_k<1, MODE, PV, Geo0>(grid, s, a);
     return;
   }
   if constexpr (PV + 1 < kNumPoly) launch_bf16<MODE, PV + 1>(pv, grid, a, s);
@@ -1058,20 +1148,41 @@ static void launch_bwd_bf16(int pv, unsigned rows, const LossArgs& a, cudaStream
   if constexpr (PV + 1 < kNumPoly) launch_bwd_bf16<PV + 1>(pv, rows, a, s);
 }
 
+// Geometry choice: geometry 1 for the unscaled mode on rows longer
+// than 128 KB (its re-read must stay in L2); geometry 0 elsewhere.  geo >= 0 forces one.
+static int pick_geo(int mode, int64_t row_bytes, int pv, int geo) {
+  if (geo >= 0) return geo;
+  if (pv != 0) return 0;
+  return (mode == M_UNSC && row_bytes > (128 << 10)) ? 1 : 0;
+}
+
 static odpo_status launch_engine(int dt, int mode, int pv, const LossArgs& a, int cps,
-                                 cudaStream_t s, int* grid_out) {
+                                 cudaStream_t s, int geo) {
   int dev = 0;
   cudaGetDevice(&dev);
   const DevInfo& di = dev_info(dev);
-  int occ = di.occ[dt][mode];
+  geo = pick_geo(mode, a.V * a.esize, pv, geo);
+  if (geo > 1 || (geo == 1 && pv != 0)) return ODPO_ERR_UNSUPPORTED;
+  int occ = di.occ[geo][dt][mode];
   if (occ < 1) occ = 1;
   if (cps <= 0 || cps > occ) cps = occ;
-  const int grid = (di.sms * cps / kCS) * kCS;
-  if (grid_out) *grid_out = grid;
-  if (dt == 0 && mode == M_SEQ) launch_k(k_engine<0, M_SEQ, 0, kCS>, grid, s, a);
-  if (dt == 0 && mode == M_FUSED) launch_k(k_engine<0, M_FUSED, 0, kCS>, grid, s, a);
+  const int cs = mode == M_UNSC ? 1 : kCS;
+  const int grid = (di.sms * cps / cs) * cs;
+  if (geo == 1) {
+    if (dt == 0 && mode == M_SEQ) launch_k<0, M_SEQ, 0, Geo1>(grid, s, a);
+    if (dt == 0 && mode == M_FUSED) launch_k<0, M_FUSED, 0, Geo1>(grid, s, a);
+    if (dt == 0 && mode == M_UNSC) launch_k<0, M_UNSC, 0, Geo1>(grid, s, a);
+    if (dt == 1 && mode == M_SEQ) launch_k<1, M_SEQ, 0, Geo1>(grid, s, a);
+    if (dt == 1 && mode == M_FUSED) launch_k<1, M_FUSED, 0, Geo1>(grid, s, a);
+    if (dt == 1 && mode == M_UNSC) launch_k<1, M_UNSC, 0, Geo1>(grid, s, a);
+    return launched();
+  }
+  if (dt == 0 && mode == M_SEQ) launch_k<0, M_SEQ, 0, Geo0>(grid, s, a);
+  if (dt == 0 && mode == M_FUSED) launch_k<0, M_FUSED, 0, Geo0>(grid, s, a);
+  if (dt == 0 && mode == M_UNSC) launch_k<0, M_UNSC, 0, Geo0>(grid, s, a);
   if (dt == 1 && mode == M_SEQ) launch_bf16<M_SEQ, 0>(pv, grid, a, s);
   if (dt == 1 && mode == M_FUSED) launch_bf16<M_FUSED, 0>(pv, grid, a, s);
+  if (dt == 1 && mode == M_UNSC) launch_bf16<M_UNSC, 0>(pv, grid, a, s);
   return launched();
 }
 
@@ -1124,6 +1235,8 @@ static void base_args(LossArgs& a, const void* logits, int64_t B, int64_t T, int
   a.seq_logp = nullptr; a.z_out = nullptr; a.stats = nullptr; a.status = status;
   a.tok_out = nullptr; a.lse_out = nullptr; a.seqsum = 0;
   a.w = w; a.lag = 1; a.max_lead = 1; a.look = kLook; a.esize = es;
+  a.row_scale = nullptr;
+  a.row_gap = 0;
 }
 
 odpo_status odpo_seq_logprobs(const void* logits, odpo_dtype dt, int64_t B, int64_t T, int64_t V,
@@ -1148,7 +1261,31 @@ odpo_status odpo_seq_logprobs(const void* logits, odpo_dtype dt, int64_t B, int6
   a.seqsum = 1;
   k_prep<<<1, kPrepThreads, 0, s>>>(nullptr, B, 0, w, nullptr);
   if ((e = launched()) != ODPO_OK) return e;
-  return launch_engine(dt == ODPO_F32 ? 0 : 1, M_SEQ, kPolyDefault, a, 0, s, nullptr);
+  return launch_engine(dt == ODPO_F32 ? 0 : 1, M_SEQ, kPolyDefault, a, 0, s, -1);
+}
+
+// Shared argument checks of the two loss entry points (dl = dlogits or G).
+static odpo_status check_loss(const void* logits, odpo_dtype dt, int64_t B, int64_t T, int64_t V,
+                              int64_t sb, int64_t st, const float* ref_logp,
+                              const int32_t* tokens, const uint8_t* mask,
+                              const int32_t* pair_rows, int64_t P, int64_t P_global, float beta,
+                              float invT, const void* dl, int64_t dsb, int64_t dst,
+                              const float* seq_logp, const double* stats, const void* workspace,
+                              size_t workspace_bytes) {
+  odpo_status e = check_logits(logits, dt, B, T, V, sb, st);
+  if (e != ODPO_OK) return e;
+  if (!ref_logp || !tokens || !mask || !dl || !seq_logp || !stats) return ODPO_ERR_INVALID_ARG;
+  if (P <= 0 || P_global < P || !finite_pos(beta) || !finite_pos(invT)) return ODPO_ERR_INVALID_ARG;
+  if (!pair_rows && B != 2 * P) return ODPO_ERR_INVALID_ARG;
+  if (dst < V || dsb < 0) return ODPO_ERR_INVALID_ARG;
+  if (B > 1 && dsb < (T - 1) * dst + V) return ODPO_ERR_INVALID_ARG;
+  if (dl == logits && (dsb != sb || dst != st)) return ODPO_ERR_INVALID_ARG;
+  const int64_t es = dt == ODPO_F32 ? 4 : 2;
+  if (!aligned16(dl) || (dsb * es) % 16 || (dst * es) % 16) return ODPO_ERR_ALIGNMENT;
+  if (4 * P * T + B * T >= (int64_t)UINT32_MAX / 2 || P > (int64_t)INT32_MAX / 2)
+    return ODPO_ERR_UNSUPPORTED;
+  if (!workspace || workspace_bytes < ws_layout(B, T, P, nullptr, nullptr)) return ODPO_ERR_WORKSPACE;
+  return ODPO_OK;
 }
 
 odpo_status odpo_online_dpo_loss_fwd_bwd_ex(const void* policy_logits, odpo_dtype dt, int64_t B,
@@ -1161,21 +1298,11 @@ odpo_status odpo_online_dpo_loss_fwd_bwd_ex(const void* policy_logits, odpo_dtyp
                                             float* pair_logit, double* stats, uint32_t* status,
                                             void* workspace, size_t workspace_bytes,
                                             odpo_launch_opts* opts, void* stream) {
-  odpo_status e = check_logits(policy_logits, dt, B, T, V, stride_b, stride_t);
+  odpo_status e = check_loss(policy_logits, dt, B, T, V, stride_b, stride_t, ref_logp, tokens,
+                             mask, pair_rows, P, P_global, beta, inv_temperature, dlogits,
+                             dstride_b, dstride_t, seq_logp, stats, workspace, workspace_bytes);
   if (e != ODPO_OK) return e;
-  if (!ref_logp || !tokens || !mask || !dlogits || !seq_logp || !stats) return ODPO_ERR_INVALID_ARG;
-  if (P <= 0 || P_global < P || !finite_pos(beta) || !finite_pos(inv_temperature))
-    return ODPO_ERR_INVALID_ARG;
-  if (!pair_rows && B != 2 * P) return ODPO_ERR_INVALID_ARG;
-  if (dstride_t < V || dstride_b < 0) return ODPO_ERR_INVALID_ARG;
-  if (B > 1 && dstride_b < (T - 1) * dstride_t + V) return ODPO_ERR_INVALID_ARG;
-  if (dlogits == policy_logits && (dstride_b != stride_b || dstride_t != stride_t))
-    return ODPO_ERR_INVALID_ARG;
   const int64_t es = dt == ODPO_F32 ? 4 : 2;
-  if (!aligned16(dlogits) || (dstride_b * es) % 16 || (dstride_t * es) % 16) return ODPO_ERR_ALIGNMENT;
-  if (4 * P * T + B * T >= (int64_t)UINT32_MAX / 2 || P > (int64_t)INT32_MAX / 2)
-    return ODPO_ERR_UNSUPPORTED;
-  if (!workspace || workspace_bytes < ws_layout(B, T, P, nullptr, nullptr)) return ODPO_ERR_WORKSPACE;
   const int sched = opts ? opts->schedule : ODPO_SCHED_AUTO;
   if (sched < ODPO_SCHED_AUTO || sched > ODPO_SCHED_TWO_PASS) return ODPO_ERR_UNSUPPORTED;
   const int pv = (opts && opts->exp2_split >= 0) ? opts->exp2_split : kPolyDefault;
@@ -1200,10 +1327,11 @@ odpo_status odpo_online_dpo_loss_fwd_bwd_ex(const void* policy_logits, odpo_dtyp
   if ((e = launched()) != ODPO_OK) return e;
   int launches = 1;
   const int dti = dt == ODPO_F32 ? 0 : 1;
+  const int geo = opts ? opts->engine : -1;
 
   if (sched == ODPO_SCHED_TWO_PASS) {
     a.seqsum = 0;   // forward rows only; k_pair_reduce sums the sequences
-    if ((e = launch_engine(dti, M_SEQ, pv, a, opts ? opts->ctas_per_sm : 0, s, nullptr)) != ODPO_OK)
+    if ((e = launch_engine(dti, M_SEQ, pv, a, opts ? opts->ctas_per_sm : 0, s, geo)) != ODPO_OK)
       return e;
     k_pair_reduce<<<(unsigned)P, 32, 0, s>>>(a);
     if ((e = launched()) != ODPO_OK) return e;
@@ -1213,25 +1341,15 @@ odpo_status odpo_online_dpo_loss_fwd_bwd_ex(const void* policy_logits, odpo_dtyp
     if ((e = launched()) != ODPO_OK) return e;
     launches += 3;
   } else {
-    int occ = di.occ[dti][M_FUSED];
-    int cps = (opts && opts->ctas_per_sm > 0) ? opts->ctas_per_sm : occ;
-    if (cps > occ) cps = occ;
-    if (cps < 1) cps = 1;
-    const int grid = di.sms * cps;
     a.look = (opts && opts->lookahead >= 0) ? (opts->lookahead < kSlots - 2 ? opts->lookahead : kSlots - 2) : kLook;
-    {
-      // L2 budget for logits kept between the forward and backward frontiers
-      const int64_t row_bytes = V * es;
-      const int64_t R = 2 * T;
-      // default: no cap (measured: capping the lead idles CTAs more than it saves in L2
-      // misses with row-granular work units)
-      int64_t lead = (opts && opts->lag_pairs > 0) ? (int64_t)opts->lag_pairs * R
-                                                   : (int64_t)INT32_MAX;
-      (void)row_bytes;
-      if (lead < 2 * R) lead = 2 * R;
-      a.max_lead = lead;
-    }
-    if ((e = launch_engine(dti, M_FUSED, pv, a, cps, s, nullptr)) != ODPO_OK) return e;
+    // optional cap on the forward lead (default none: measured, capping idles CTAs more than
+    // it saves in L2 misses with row-granular work units)
+    const int64_t R = 2 * T;
+    int64_t lead = (opts && opts->lag_pairs > 0) ? (int64_t)opts->lag_pairs * R : (int64_t)INT32_MAX;
+    if (lead < 2 * R) lead = 2 * R;
+    a.max_lead = lead;
+    const int cps = opts ? opts->ctas_per_sm : 0;
+    if ((e = launch_engine(dti, M_FUSED, pv, a, cps, s, geo)) != ODPO_OK) return e;
     launches += 1;
   }
   if (opts) opts->launches = launches;
@@ -1252,6 +1370,47 @@ odpo_status odpo_online_dpo_loss_fwd_bwd(const void* policy_logits, odpo_dtype d
                                          inv_temperature, dlogits, dstride_b, dstride_t, seq_logp,
                                          pair_logit, stats, status, workspace, workspace_bytes,
                                          nullptr, stream);
+}
+
+odpo_status odpo_online_dpo_loss_fwd_bwd_unscaled(
+    const void* policy_logits, odpo_dtype dt, int64_t B, int64_t T, int64_t V, int64_t stride_b,
+    int64_t stride_t, const float* ref_logp, const int32_t* tokens, const uint8_t* mask,
+    const int32_t* pair_rows, int64_t P, int64_t P_global, float beta, float inv_temperature,
+    void* G, int64_t gstride_b, int64_t gstride_t, float* row_scale, float* seq_logp,
+    float* pair_logit, double* stats, uint32_t* status, void* workspace, size_t workspace_bytes,
+    odpo_launch_opts* opts, void* stream) {
+  odpo_status e = check_loss(policy_logits, dt, B, T, V, stride_b, stride_t, ref_logp, tokens,
+                             mask, pair_rows, P, P_global, beta, inv_temperature, G, gstride_b,
+                             gstride_t, seq_logp, stats, workspace, workspace_bytes);
+  if (e != ODPO_OK) return e;
+  if (!row_scale) return ODPO_ERR_INVALID_ARG;
+  if (opts && opts->schedule != ODPO_SCHED_AUTO) return ODPO_ERR_UNSUPPORTED;
+  const int pv = (opts && opts->exp2_split >= 0) ? opts->exp2_split : kPolyDefault;
+  if (pv >= kNumPoly) return ODPO_ERR_UNSUPPORTED;
+  Workspace w;
+  ws_layout(B, T, P, (char*)workspace, &w);
+  cudaStream_t s = (cudaStream_t)stream;
+  LossArgs a;
+  base_args(a, policy_logits, B, T, V, stride_b, stride_t, tokens, mask, inv_temperature, status,
+            w, dt == ODPO_F32 ? 4 : 2);
+  a.ref = ref_logp; a.pair_rows = pair_rows;
+  a.P = P; a.Pg = (double)P_global; a.beta = beta;
+  a.dl = G; a.dsb = gstride_b; a.dst = gstride_t;
+  a.seq_logp = seq_logp; a.z_out = pair_logit; a.stats = stats;
+  a.row_scale = row_scale;
+  // the producer emits up to three slots per ticket; keep the decode window inside the ring
+  const int look = (opts && opts->lookahead >= 0) ? opts->lookahead : kLook;
+  a.look = look < kSlots - 6 ? look : kSlots - 6;
+  if (opts && opts->row_gap > 1) return ODPO_ERR_UNSUPPORTED;
+  a.row_gap = (opts && opts->row_gap >= 0) ? opts->row_gap : 0;
+  k_prep<<<1, kPrepThreads, 0, s>>>(pair_rows, B, P, w, status);
+  if ((e = launched()) != ODPO_OK) return e;
+  const int geo = opts ? opts->engine : -1;
+  if ((e = launch_engine(dt == ODPO_F32 ? 0 : 1, M_UNSC, pv, a, opts ? opts->ctas_per_sm : 0, s,
+                         geo)) != ODPO_OK)
+    return e;
+  if (opts) opts->launches = 2;
+  return ODPO_OK;
 }
 
 }  // extern "C"

@@ -9,12 +9,16 @@
 // while the current row is reduced.
 #pragma once
 
+#include <cstddef>
+
 #include "odpo_device.cuh"
 
 namespace odpo {
 
-// Engine geometry (tuned on B200 for the BASELINE shapes; see profiles/ and DESIGN.md):
-// 4 consumer warps per CTA, a 3 x 16 KB TMA ring, 4 CTAs per SM.
+// Engine geometry (tuned on B200 for the BASELINE shapes; see profiles/ and DESIGN.md).
+// Geometry 0 (default): 4 consumer warps per CTA, a 3 x 16 KB TMA ring, 4 CTAs per SM.
+// Geometry 1 (large rows): 8 consumer warps, a 6 x 16 KB ring, 2 CTAs per SM -- half as many
+// rows in flight, so a row's unscaled backward re-read stays in L2 for 256 KB rows.
 #ifndef ODPO_NCW
 #define ODPO_NCW 4
 #endif
@@ -27,8 +31,6 @@ namespace odpo {
 #ifndef ODPO_CTAS_PER_SM
 #define ODPO_CTAS_PER_SM 4
 #endif
-constexpr int kNCW = ODPO_NCW;             // consumer warps (warps 0..kNCW-1)
-constexpr int kNCT = kNCW * 32;            // consumer threads
 #ifndef ODPO_CLUSTER
 #define ODPO_CLUSTER 1
 #endif
@@ -36,20 +38,29 @@ constexpr int kCS = ODPO_CLUSTER;          // CTAs per thread-block cluster (one
 #ifndef ODPO_NEPI
 #define ODPO_NEPI 2
 #endif
-constexpr int kProdWarp = kNCW;            // TMA producer warp
-constexpr int kParWarp = kNCW + 1;         // backward-parameter prefetch warp
-constexpr int kEpiWarp = kNCW + 2;         // first row-epilogue warp
 constexpr int kNEpi = ODPO_NEPI;           // row-epilogue warps (slot s -> warp s % kNEpi)
-constexpr int kEngThreads = kNCT + 64 + 32 * kNEpi;
-constexpr int kStages = ODPO_STAGES;
 constexpr int kChunk = ODPO_CHUNK;         // bytes per stage
 constexpr int kCV = kChunk / 16;           // 16-byte vectors per chunk
-constexpr int kUB = kCV / kNCT;            // vectors per consumer thread per chunk
 constexpr int kSlots = 8;                  // rows in flight per CTA (row-slot ring)
 constexpr int kLook = 1;                   // default rows decoded ahead of the row being pushed
-static_assert(kCV % kNCT == 0, "chunk must split evenly over consumers");
 static_assert(kSlots % kNEpi == 0, "epilogue warps must tile the slot ring");
-constexpr int kEngSmem = kStages * kChunk;
+
+template <int NCW_, int STAGES_, int CPS_>
+struct Geo {
+  static constexpr int NCW = NCW_;         // consumer warps (warps 0..NCW-1)
+  static constexpr int NCT = NCW * 32;     // consumer threads
+  static constexpr int STAGES = STAGES_;   // TMA ring stages of kChunk bytes
+  static constexpr int CPS = CPS_;         // CTAs per SM (launch bounds)
+  static constexpr int UB = kCV / NCT;     // vectors per consumer thread per chunk
+  static constexpr int PROD = NCW;         // TMA producer warp
+  static constexpr int PAR = NCW + 1;      // backward-parameter prefetch warp
+  static constexpr int EPI = NCW + 2;      // first row-epilogue warp
+  static constexpr int THREADS = NCT + 64 + 32 * kNEpi;
+  static constexpr int SMEM = STAGES * kChunk;
+  static_assert(kCV % NCT == 0, "chunk must split evenly over consumers");
+};
+using Geo0 = Geo<ODPO_NCW, ODPO_STAGES, ODPO_CTAS_PER_SM>;
+using Geo1 = Geo<8, 6, 2>;
 
 // ------------------------------------------------------------------ mbarrier / TMA PTX
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -143,7 +154,9 @@ struct RowSlot {
   int32_t kind;
   int32_t tok;
   int32_t nchunk;
-  uint32_t pphase;  // parity of this slot's param_ready phase for this (B) row
+  uint32_t pphase;  // parity of the param_ready phase this (B) row waits for
+  int32_t fslot;    // UNSC backward rows: the slot holding the same row's forward pass
+  int32_t pad_;
   int64_t p;       // pair (FUSED) or sequence (SEQ)
   int64_t s;       // sequence
   int64_t g;       // row = s*T + t
@@ -153,7 +166,8 @@ struct RowSlot {
   float pm[32], pr[32];  // per-warp (m, r) partials: [cluster rank * kNCW + warp]
 };
 // the header (kind .. drow) is what the cluster leader broadcasts to its peers
-constexpr int kSlotHeaderBytes = 56;
+constexpr int kSlotHeaderBytes = 64;
+static_assert(offsetof(RowSlot, c) == kSlotHeaderBytes, "slot header layout");
 
 // ------------------------------------------------------------------ per-batch online update
 // fp32 inputs (DT 0): exact exclusion of one max element (log1p form, 1e-5 contract).

@@ -40,6 +40,8 @@ def main():
         for _ in range(a.reps):
             if v == "seq":
                 odpo.seq_logprobs(logits, tokens, mask)
+            elif v == "unsc":
+                odpo.online_dpo_loss_fwd_bwd_unscaled(logits, ref, tokens, mask, w.beta, G=dl)
             else:
                 parts = v.split(":")
                 sched, split = parts[0], int(parts[1]) if len(parts) > 1 else -1

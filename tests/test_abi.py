@@ -102,6 +102,30 @@ def test_argument_errors_are_synchronous(lib):
                                  None, FAKE, 8, None) == 3
 
 
+def _unscaled(lib, row_scale=FAKE, sched=0, **kw):
+    a = dict(logits=FAKE, dt=1, B=4, T=3, V=64, sb=192, st=64, ref=FAKE, tok=FAKE, mask=FAKE,
+             pr=None, P=2, Pg=2, beta=0.1, invT=1.0, dl=FAKE, dsb=192, dst=64, seq=FAKE, z=None,
+             stats=FAKE, status=None, ws=FAKE, wsb=1 << 20)
+    a.update(kw)
+    import paper_2410_18252_b200 as odpo
+    opts = odpo._Opts(sched, 0, 0, 0, -1, -1, -1, -1)
+    return lib.odpo_online_dpo_loss_fwd_bwd_unscaled(
+        a["logits"], a["dt"], a["B"], a["T"], a["V"], a["sb"], a["st"], a["ref"], a["tok"],
+        a["mask"], a["pr"], a["P"], a["Pg"], a["beta"], a["invT"], a["dl"], a["dsb"], a["dst"],
+        row_scale, a["seq"], a["z"], a["stats"], a["status"], a["ws"], a["wsb"], C.byref(opts),
+        None)
+
+
+def test_unscaled_argument_errors_are_synchronous(lib):
+    assert _unscaled(lib, row_scale=None) == 1
+    assert _unscaled(lib, beta=0.0) == 1
+    assert _unscaled(lib, dl=None) == 1
+    assert _unscaled(lib, dl=FAKE_MIS) == 2
+    assert _unscaled(lib, wsb=16) == 3
+    assert _unscaled(lib, sched=2) == 4    # only the AUTO schedule exists for this call
+    assert _unscaled(lib, dl=FAKE, logits=FAKE, dsb=256, dst=64) == 1
+
+
 def test_product_has_no_oracle_or_cpu_fallback():
     """The product package never imports the oracle and refuses CPU tensors."""
     pkg = os.path.join(ROOT, "paper_2410_18252_b200")

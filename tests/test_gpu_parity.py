@@ -183,6 +183,26 @@ def test_loss_parity_small(odpo, case, sched):
     check_dlogits(to_f64(out.dlogits), o["dlogits"], coef[:, None, None], dt)
 
 
+@pytest.mark.parametrize("case", CASES[:2] + CASES[3:4], ids=lambda c: f"P{c[0]}V{c[2]}{c[3]}")
+@pytest.mark.parametrize("sched", SCHEDS)
+def test_loss_parity_engine_geometry1(odpo, case, sched):
+    """The same parity with the large-row engine geometry (8 warps x 6 stages x 2 CTAs/SM)."""
+    P, T, V, dt, mk, extra, invT = case
+    b = Batch(P, T, V, dt, seed=5, mask_kind=mk, lbar=max(1, T // 2), extra_seqs=extra, invT=invT)
+    ref = (synth.rewards_for(5, b.B, 1).reshape(-1) - 30.0).astype(np.float32)
+    out = run_loss(odpo, b, torch.from_numpy(ref).cuda(), 0.1, sched, engine=1)
+    o = oracle_loss(b, ref, 0.1)
+    live = np.arange(b.B) if b.pair_rows is None else b.pair_rows.reshape(-1)
+    check_seq(out.seq_logp.cpu().numpy()[live], o["seq_logp"][live], dt)
+    coef = coef_from_oracle(o, P, P, 0.1, invT, b.pair_rows, b.B)
+    check_dlogits(to_f64(out.dlogits), o["dlogits"], coef[:, None, None], dt)
+    # the geometry fixes the per-row reduction tree (warps per CTA): deterministic per geometry
+    again = run_loss(odpo, b, torch.from_numpy(ref).cuda(), 0.1, sched, engine=1)
+    li = torch.from_numpy(live).cuda()
+    assert torch.equal(again.seq_logp[li], out.seq_logp[li])
+    assert torch.equal(again.dlogits, out.dlogits)
+
+
 @pytest.mark.parametrize("sched", SCHEDS)
 def test_tiny_config_full_parity(odpo, sched):
     """BASELINE.json configs[0]: 4 prompts x 2, T=53, V=50304, fp32, beta=0.05 (full dlogits)."""

@@ -311,6 +311,54 @@ def test_gradient_finite_differences(orc, beta, invT):
     assert np.all(g[1, 2] == 0.0)
 
 
+# ------------------------------------------------------- O-8b factored (unscaled) gradient
+def test_unscaled_factorisation_finite_differences(orc):
+    """row_scale * G is the loss gradient (central differences, as O-8), G is the plain
+    softmax - onehot of invT x (scipy), and masked / unreferenced rows are 0 in both."""
+    from scipy.special import softmax
+    rng = np.random.default_rng(11)
+    B, T, V, invT, beta = 6, 3, 5, 1 / 0.7, 0.3
+    x = rng.normal(0, 1.5, size=(B, T, V))
+    tok = rng.integers(0, V, size=(B, T)).astype(np.int32)
+    mask = np.ones((B, T), np.uint8)
+    mask[1, 2] = 0
+    ref = rng.normal(-3, 1, size=B).astype(np.float32)
+    pr = np.array([[2, 1], [0, 3]], np.int32)   # rows 4, 5 unreferenced
+    Pg = 3
+    u = orc.online_dpo_loss_fwd_bwd(x, ref, tok, mask, beta, pair_rows=pr, p_global=Pg,
+                                    inv_temperature=invT, want_dlogits=True, unscaled=True)
+    G, rs = u["dlogits"], u["row_scale"]
+    h = 1e-6
+    worst = 0.0
+    for b in range(4):
+        for t in range(T):
+            for v in range(V):
+                xp = x.copy()
+                xp[b, t, v] += h
+                xm = x.copy()
+                xm[b, t, v] -= h
+                lp = orc.online_dpo_loss_fwd_bwd(xp, ref, tok, mask, beta, pair_rows=pr,
+                                                 p_global=Pg, inv_temperature=invT)["stats"][1]
+                lm = orc.online_dpo_loss_fwd_bwd(xm, ref, tok, mask, beta, pair_rows=pr,
+                                                 p_global=Pg, inv_temperature=invT)["stats"][1]
+                worst = max(worst, abs((lp - lm) / (2 * h) - rs[b, t] * G[b, t, v]))
+    assert worst <= 1e-8, worst
+    sm = softmax(x * np.float64(np.float32(invT)), axis=2)
+    oh = np.zeros_like(sm)
+    np.put_along_axis(oh, tok[..., None].astype(np.int64), 1.0, axis=2)
+    live = np.zeros((B, T), bool)
+    live[:4] = mask[:4] == 1
+    assert np.max(np.abs(G[live] - (sm - oh)[live])) < 1e-15
+    assert np.all(G[~live] == 0.0) and np.all(rs[~live] == 0.0)
+    # chosen / rejected scales are opposite: coef_r = -coef_c
+    assert rs[2, 0] == -rs[1, 0] and rs[0, 0] == -rs[3, 0] and rs[2, 0] > 0
+    # the unscaled call's loss outputs are the scaled call's
+    s_ = orc.online_dpo_loss_fwd_bwd(x, ref, tok, mask, beta, pair_rows=pr, p_global=Pg,
+                                     inv_temperature=invT, want_dlogits=True)
+    for k in ("seq_logp", "z", "stats"):
+        assert np.array_equal(s_[k], u[k])
+
+
 # ------------------------------------------------------------------------ O-9 invariants
 def test_gradient_invariants(orc):
     x, tok, mask, rng = _random_batch(7, P=6, T=5, V=11)
