@@ -54,8 +54,10 @@ def lib():
         L.orc_online_dpo_loss_fwd_bwd_unscaled.argtypes = [
             P, C.c_int, i64, i64, i64, i64, i64, P, P, P, P, i64, i64, f32, f32, P, P, i64, P, P, P,
             P, P, C.c_int]
+        L.orc_pg_loss_fwd_bwd.argtypes = [P, C.c_int, i64, i64, i64, i64, i64, P, P, P, i64, i64,
+                                          C.c_int, P, P, f32, f32, P, P, i64, P, P, P, C.c_int]
         for f in (L.orc_pair_select, L.orc_seq_logprobs, L.orc_online_dpo_loss_fwd_bwd,
-                  L.orc_online_dpo_loss_fwd_bwd_unscaled):
+                  L.orc_online_dpo_loss_fwd_bwd_unscaled, L.orc_pg_loss_fwd_bwd):
             f.restype = C.c_int
         _lib = L
     return _lib
@@ -164,6 +166,45 @@ def online_dpo_loss_fwd_bwd(logits, ref_logp, tokens, mask, beta, pair_rows=None
     if dl is not None and dl_rows is None:
         dl = dl.reshape(B, T, V)
     return dict(seq_logp=S, z=z, stats=stats, status=int(status[0]), dlogits=dl, row_scale=rs)
+
+
+PG_KINDS = {"rloo": 0, "copg": 1, "prox_rloo": 2, "sft": 3}
+
+
+def pg_loss_fwd_bwd(logits, tokens, mask, kind, rewards, old_logp=None, clip_eps=0.2,
+                    pair_rows=None, p_global=None, inv_temperature=1.0, want_dlogits=False,
+                    dl_rows=None, n_threads=1):
+    """Coefficient-variant losses (App B): returns dict(seq_logp[B], stats[10], status,
+    dlogits[n, V] or None).  rewards[B] and old_logp[B] are per sequence."""
+    a, dt, sb, st = _logits_args(logits)
+    B, T, V = a.shape
+    tok = np.ascontiguousarray(tokens, dtype=np.int32).reshape(B, T)
+    msk = np.ascontiguousarray(mask, dtype=np.uint8).reshape(B, T)
+    rew = np.ascontiguousarray(rewards, dtype=np.float32).reshape(B)
+    old = None if old_logp is None else np.ascontiguousarray(old_logp, dtype=np.float32).reshape(B)
+    pr = None if pair_rows is None else np.ascontiguousarray(pair_rows, dtype=np.int32).reshape(-1, 2)
+    P = B // 2 if pr is None else pr.shape[0]
+    Pg = P if p_global is None else int(p_global)
+    dl, rows, n_rows = None, None, 0
+    if want_dlogits or dl_rows is not None:
+        if dl_rows is not None:
+            rows = np.ascontiguousarray(dl_rows, dtype=np.int64).reshape(-1)
+            n_rows = rows.size
+        else:
+            n_rows = B * T
+        dl = np.zeros((n_rows, V), np.float64)
+    S = np.zeros(B, np.float64)
+    stats = np.zeros(10, np.float64)
+    status = np.zeros(1, np.uint32)
+    rc = lib().orc_pg_loss_fwd_bwd(
+        _ptr(a), dt, B, T, V, sb, st, _ptr(tok), _ptr(msk), _ptr(pr), P, Pg, PG_KINDS[kind],
+        _ptr(rew), _ptr(old), float(np.float32(clip_eps)), float(np.float32(inv_temperature)),
+        _ptr(dl), _ptr(rows), n_rows, _ptr(S), _ptr(stats), _ptr(status), int(n_threads))
+    if rc:
+        raise ValueError("orc_pg_loss_fwd_bwd: invalid argument")
+    if dl is not None and dl_rows is None:
+        dl = dl.reshape(B, T, V)
+    return dict(seq_logp=S, stats=stats, status=int(status[0]), dlogits=dl)
 
 
 def to_bf16_bits(x) -> np.ndarray:

@@ -24,6 +24,11 @@
  *                       max E log sigma(beta log pi(y+)/pi_init(y+) - beta log pi(y-)/pi_init(y-)))
  *                     as a mean over pairs of -log sigma(z) (reading R3), and its exact
  *                     gradient w.r.t. the logits, dL/dx = coef_b (softmax - onehot).
+ *   orc_pg_loss_fwd_bwd
+ *                     the coefficient-variant losses of App B on the same
+ *                     token log-probs: RLOO with k = 2, CoPG
+ *                     (PAPER.md:716-719), Proximal RLOO and the Best-of-2
+ *                     SFT baseline; see that function's comment.
  *   orc_online_dpo_loss_fwd_bwd_unscaled
  *                     the same, with the gradient returned factored per row:
  *                     G = softmax - onehot and row_scale = coef_b (dL/dx = row_scale * G).
@@ -392,4 +397,123 @@ int orc_online_dpo_loss_fwd_bwd_unscaled(const void* logits, int dtype, int64_t 
   return loss_core(logits, dtype, B, T, V, stride_b, stride_t, ref_logp, tokens, mask, pair_rows,
                    P, P_global, beta, inv_temperature, G, g_rows, n_g_rows, seq_logp, z_out,
                    stats, status, n_threads, 1, row_scale);
+}
+
+/* ----------------------------------------------------------- coefficient-variant losses
+ * Each pair p = (y1, y2) = pair_rows[p] with per-sequence rewards R and advantages
+ * A1 = R1 - R2, A2 = R2 - R1 (k = 2).  Losses are MINIMISED, as the negated
+ * objectives, averaged over P_global pairs:
+ *   kind 0 RLOO       l_p = -1/2 [S1 A1 + S2 A2]                       (
+ *                     reading: each sample carries its own leave-one-out advantage)
+ *   kind 1 CoPG       l_p = -1/2 [(S1 - O1) A1 + (S2 - O2) A2]
+ *   kind 2 Prox RLOO  l_p = -1/2 [min(r1 A1, clip(r1) A1) + min(r2 A2, clip(r2) A2)],
+ *                     r = exp(S - O), clip to [1 - eps, 1 + eps]
+ *   kind 3 Best-of-2 SFT  l_p = -S1 (y1 = the chosen completion)
+ * with S = log pi_theta(y|x) (R1) and O = log pi_old(y|x) (old_logp).  The gradient is
+ * dl/dx = coef_b (softmax(invT x) - onehot), coef_b = -(dL/dS_b) invT:
+ *   RLOO, CoPG: coef_b = A_b invT / (2 P_global)
+ *   Prox: coef_b = r_b A_b invT / (2 P_global) where min() takes the unclipped term
+ *         (r A <= clip(r) A), else 0
+ *   SFT: coef_1 = invT / P_global, coef_2 = 0.
+ * stats[10]: pairs, mean loss, sequences with a nonzero coefficient, sum r (Prox only),
+ * sum A1, sum |A1|, sum S1, sum S2, tokens of y1, tokens of y2. */
+int orc_pg_loss_fwd_bwd(const void* logits, int dtype, int64_t B, int64_t T, int64_t V,
+                        int64_t stride_b, int64_t stride_t, const int32_t* tokens,
+                        const uint8_t* mask, const int32_t* pair_rows, int64_t P,
+                        int64_t P_global, int kind, const float* rewards,
+                        const float* old_logp, float clip_eps, float inv_temperature,
+                        double* dlogits, const int64_t* dl_rows, int64_t n_dl_rows,
+                        double* seq_logp, double* stats, uint32_t* status, int n_threads) {
+  if (!logits || !tokens || !mask || !seq_logp || !stats || !rewards) return 1;
+  if (B <= 0 || T <= 0 || V <= 0 || P <= 0 || P_global < P || kind < 0 || kind > 3) return 1;
+  if ((kind == 1 || kind == 2) && !old_logp) return 1;
+  if (!pair_rows && B != 2 * P) return 1;
+  rows_in in = {logits, dtype, B, T, V, stride_b, stride_t, tokens, mask, (double)inv_temperature};
+  double* ntok = (double*)calloc((size_t)B, sizeof(double));
+  double* coef = (double*)calloc((size_t)B, sizeof(double));
+  uint8_t* refd = (uint8_t*)calloc((size_t)B, 1);
+  uint32_t st = run_seqs(&in, seq_logp, ntok, NULL, NULL, n_threads);
+  double invT = (double)inv_temperature, Pg = (double)P_global, eps = (double)clip_eps;
+  double acc[ORC_NSTATS];
+  for (int i = 0; i < ORC_NSTATS; ++i) acc[i] = 0.0;
+  for (int64_t p = 0; p < P; ++p) {
+    int64_t y[2];
+    y[0] = pair_rows ? pair_rows[2 * p] : 2 * p;
+    y[1] = pair_rows ? pair_rows[2 * p + 1] : 2 * p + 1;
+    if (y[0] < 0 || y[0] >= B || y[1] < 0 || y[1] >= B) {
+      st |= ORC_FLAG_PAIR_RANGE;
+      continue;
+    }
+    if (y[0] == y[1] || refd[y[0]] || refd[y[1]]) st |= ORC_FLAG_DUP_ROW;
+    refd[y[0]] = refd[y[1]] = 1;
+    double A[2], loss = 0.0;
+    A[0] = (double)rewards[y[0]] - (double)rewards[y[1]];
+    A[1] = -A[0];
+    for (int k = 0; k < 2; ++k) {
+      int64_t b = y[k];
+      double S = seq_logp[b];
+      double c = 0.0;
+      if (kind == 0) {
+        loss += -0.5 * S * A[k];
+        c = A[k] * invT / (2.0 * Pg);
+      } else if (kind == 1) {
+        loss += -0.5 * (S - (double)old_logp[b]) * A[k];
+        c = A[k] * invT / (2.0 * Pg);
+      } else if (kind == 2) {
+        double r = exp(S - (double)old_logp[b]);
+        double rc = r < 1.0 - eps ? 1.0 - eps : (r > 1.0 + eps ? 1.0 + eps : r);
+        double u = r * A[k], v = rc * A[k];
+        loss += -0.5 * (u <= v ? u : v);
+        c = (u <= v) ? r * A[k] * invT / (2.0 * Pg) : 0.0;
+        acc[ORC_ST_Z] += r;
+      } else {
+        if (k == 0) {
+          loss += -S;
+          c = invT / Pg;
+        }
+      }
+      coef[b] = c;
+      if (c != 0.0) acc[ORC_ST_NCORRECT] += 1.0;
+    }
+    acc[ORC_ST_NPAIRS] += 1.0;
+    acc[ORC_ST_LOSS] += loss;
+    acc[ORC_ST_RCHOSEN] += A[0];
+    acc[ORC_ST_RREJ] += fabs(A[0]);
+    acc[ORC_ST_SCHOSEN] += seq_logp[y[0]];
+    acc[ORC_ST_SREJ] += seq_logp[y[1]];
+    acc[ORC_ST_NTOK_CHOSEN] += ntok[y[0]];
+    acc[ORC_ST_NTOK_REJ] += ntok[y[1]];
+  }
+  acc[ORC_ST_LOSS] /= Pg;
+  for (int i = 0; i < ORC_NSTATS; ++i) stats[i] = acc[i];
+  if (dlogits) {
+    int64_t n = dl_rows ? n_dl_rows : B * T;
+    int nt = n_threads < 1 ? 1 : n_threads;
+    if (nt > n) nt = (int)(n > 0 ? n : 1);
+    grad_job* jobs = (grad_job*)calloc((size_t)nt, sizeof(grad_job));
+    pthread_t* th = (pthread_t*)calloc((size_t)nt, sizeof(pthread_t));
+    for (int i = 0; i < nt; ++i) {
+      jobs[i].in = &in;
+      jobs[i].coef = coef;
+      jobs[i].refd = refd;
+      jobs[i].rows = dl_rows;
+      jobs[i].n0 = n * i / nt;
+      jobs[i].n1 = n * (i + 1) / nt;
+      jobs[i].unscaled = 0;
+      jobs[i].out = dlogits;
+    }
+    if (nt == 1) {
+      grad_worker(&jobs[0]);
+    } else {
+      for (int i = 0; i < nt; ++i) pthread_create(&th[i], NULL, grad_worker, &jobs[i]);
+      for (int i = 0; i < nt; ++i) pthread_join(th[i], NULL);
+    }
+    free(jobs);
+    free(th);
+  }
+  free(ntok);
+  free(coef);
+  free(refd);
+  if (status) *status |= st;
+  return 0;
 }

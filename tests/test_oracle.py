@@ -463,3 +463,106 @@ def test_neg_inf_reading_r14(orc):
     x3 = np.array([[[0.0, np.inf, 1.0]]])
     assert orc.seq_logprobs(x3, np.array([[0]], np.int32), np.ones((1, 1), np.uint8))["status"] \
         & orc.FLAG_NONFINITE_LOGIT
+
+
+# --------------------------------------------- O-10 coefficient-variant losses (App B, NEXT-3)
+def _pg_batch(seed, B=6, T=3, V=5):
+    rng = np.random.default_rng(seed)
+    x = rng.normal(0, 1.5, size=(B, T, V))
+    tok = rng.integers(0, V, size=(B, T)).astype(np.int32)
+    mask = np.ones((B, T), np.uint8)
+    mask[1, 2] = 0
+    rew = rng.normal(0, 1, size=B).astype(np.float32)
+    pr = np.array([[2, 1], [0, 3]], np.int32)    # rows 4, 5 unreferenced
+    return x, tok, mask, rew, pr
+
+
+def _pg_fd(orc, x, tok, mask, kind, rew, old, pr, Pg, invT, eps, g, rows_b):
+    h = 1e-6
+    worst = 0.0
+    B, T, V = x.shape
+    for b in rows_b:
+        for t in range(T):
+            for v in range(V):
+                xp = x.copy()
+                xp[b, t, v] += h
+                xm = x.copy()
+                xm[b, t, v] -= h
+                lp = orc.pg_loss_fwd_bwd(xp, tok, mask, kind, rew, old, eps, pr, Pg, invT)["stats"][1]
+                lm = orc.pg_loss_fwd_bwd(xm, tok, mask, kind, rew, old, eps, pr, Pg, invT)["stats"][1]
+                worst = max(worst, abs((lp - lm) / (2 * h) - g[b, t, v]))
+    return worst
+
+
+@pytest.mark.parametrize("kind", ["rloo", "copg", "prox_rloo", "sft"])
+def test_pg_gradient_finite_differences(orc, kind):
+    """dlogits of every App B loss is the central-difference gradient of its loss value."""
+    x, tok, mask, rew, pr = _pg_batch(21)
+    invT, Pg, eps = 1 / 0.7, 3, 0.2
+    S = orc.seq_logprobs(x, tok, mask, inv_temperature=invT)["seq_logp"]
+    # old log-probs: sequence 2 inside the clip range, 1 above it, 0 and 3 below it
+    # (differentiable points: |log r - log(1 +- eps)| >= 0.05)
+    old = S.copy()
+    old[2] -= 0.05
+    old[1] -= 0.6
+    old[0] += 0.6
+    old[3] += 0.7
+    old = old.astype(np.float32)
+    out = orc.pg_loss_fwd_bwd(x, tok, mask, kind, rew, old, eps, pr, Pg, invT, want_dlogits=True)
+    g = out["dlogits"]
+    assert _pg_fd(orc, x, tok, mask, kind, rew, old, pr, Pg, invT, eps, g, range(4)) <= 1e-8
+    assert np.all(g[4:] == 0.0) and np.all(g[1, 2] == 0.0)
+    if kind == "sft":
+        assert np.all(g[[1, 3]] == 0.0)     # rejected completions carry no gradient
+        assert abs(out["stats"][1] + (S[2] + S[0]) / Pg) < 1e-12
+
+
+def test_copg_has_the_rloo_gradient(orc):
+    """CoPG and RLOO have the same gradient; their losses differ by the
+    old-policy term."""
+    x, tok, mask, rew, pr = _pg_batch(22)
+    old = np.array([-3.0, -4.0, -5.0, -6.0, 0.0, 0.0], np.float32)
+    a = orc.pg_loss_fwd_bwd(x, tok, mask, "rloo", rew, None, 0.2, pr, want_dlogits=True)
+    b = orc.pg_loss_fwd_bwd(x, tok, mask, "copg", rew, old, 0.2, pr, want_dlogits=True)
+    assert np.array_equal(a["dlogits"], b["dlogits"])
+    r64, o64 = rew.astype(np.float64), old.astype(np.float64)
+    A = [r64[2] - r64[1], r64[0] - r64[3]]
+    shift = 0.5 * sum(A[i] * (o64[pr[i, 0]] - o64[pr[i, 1]]) for i in range(2)) / 2
+    assert abs((b["stats"][1] - a["stats"][1]) - shift) < 1e-12
+
+
+def test_prox_rloo_special_cases(orc):
+    """r = 1 (pi_old = pi_theta): the RLOO gradient and a zero loss (A2 = -A1); a ratio
+    outside the clip range on the improving side: zero gradient, loss at the clipped value."""
+    x, tok, mask, rew, pr = _pg_batch(23)
+    S = orc.seq_logprobs(x, tok, mask)["seq_logp"]
+    old = S.astype(np.float32)
+    S32 = old.astype(np.float64)
+    r = orc.pg_loss_fwd_bwd(x, tok, mask, "rloo", rew, None, 0.2, pr, want_dlogits=True)
+    p = orc.pg_loss_fwd_bwd(x, tok, mask, "prox_rloo", rew, old, 0.2, pr, want_dlogits=True)
+    ratio = np.exp(S - S32)           # 1 up to the f32 rounding of old_logp
+    assert np.max(np.abs(ratio - 1)) < 1e-6
+    assert np.max(np.abs(p["dlogits"] - r["dlogits"])) < 1e-6 * np.max(np.abs(r["dlogits"]))
+    assert abs(p["stats"][1]) < 1e-6 and p["stats"][2] == 4
+    # sequence 2 (chosen of pair 0) with A > 0 and r = e^0.5 > 1.2: clipped, no gradient
+    A0 = float(rew[2]) - float(rew[1])
+    old2 = old.copy()
+    old2[2] = np.float32(S[2] - 0.5) if A0 > 0 else np.float32(S[2] + 0.5)
+    q = orc.pg_loss_fwd_bwd(x, tok, mask, "prox_rloo", rew, old2, 0.2, pr, want_dlogits=True)
+    assert np.all(q["dlogits"][2] == 0.0) and q["stats"][2] == 3
+    assert np.array_equal(q["dlogits"][[0, 1, 3]], p["dlogits"][[0, 1, 3]]) or \
+        np.max(np.abs(q["dlogits"][[0, 1, 3]] - p["dlogits"][[0, 1, 3]])) < 1e-15
+
+
+def test_rloo_uniform_rows_closed_form(orc):
+    """Uniform rows: S_b = -n_b log V, so the RLOO loss is -1/2 sum_p A_p (S_1 - S_2) / P."""
+    B, T, V = 4, 3, 7
+    x = np.zeros((B, T, V))
+    tok = np.zeros((B, T), np.int32)
+    mask = np.array([[1, 1, 1], [1, 0, 0], [1, 1, 0], [1, 1, 1]], np.uint8)
+    rew = np.array([1.0, -0.5, 0.25, 2.0], np.float32)
+    out = orc.pg_loss_fwd_bwd(x, tok, mask, "rloo", rew, None, 0.2)
+    S = -mask.sum(1).astype(np.float64) * np.log(V)
+    A = [1.5, -1.75]
+    want = (-0.5 * (A[0] * (S[0] - S[1]) + A[1] * (S[2] - S[3]))) / 2
+    assert abs(out["stats"][1] - want) < 1e-12
