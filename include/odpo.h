@@ -232,6 +232,45 @@ odpo_status odpo_online_dpo_loss_fwd_bwd_unscaled(
     float* pair_logit, double* stats, uint32_t* status, void* workspace, size_t workspace_bytes,
     odpo_launch_opts* opts, void* stream);
 
+/* Coefficient-variant losses of App B and the Best-of-2 baseline (:209). */
+typedef enum {
+  ODPO_PG_RLOO = 0,           /* l_p = -1/2 [S1 A1 + S2 A2], A1 = R1 - R2 = -A2 */
+  ODPO_PG_COPG = 1,           /* l_p = -1/2 [(S1 - O1) A1 + (S2 - O2) A2]      */
+  ODPO_PG_PROX_RLOO = 2,      /* l_p = -1/2 sum_k min(r_k A_k, clip(r_k, 1-eps, 1+eps) A_k),
+                                 r = exp(S - O)                                */
+  ODPO_PG_BEST_OF_K_SFT = 3   /* l_p = -S1, S1 = the chosen completion            */
+} odpo_pg_kind;
+
+/*
+ * odpo_pg_loss_fwd_bwd -- the same learner step for the App B losses: S = log pi(y|x) as in
+ * odpo_seq_logprobs, the loss averaged over P_global pairs, and
+ * dlogits[b,t,:] = coef_b * mask[b,t] * (softmax - onehot(tok)) with coef_b = -(dL/dS_b) invT:
+ *   RLOO, CoPG: coef_b = A_b invT / (2 P_global);  SFT: invT / P_global on y1, 0 on y2;
+ *   Proximal RLOO: r_b A_b invT / (2 P_global) where min() takes the unclipped term, else 0.
+ *
+ *   pair_rows  [P][2] (y1, y2) or NULL => (2p, 2p+1); for SFT y1 must be the chosen one
+ *              (pair_select's order).
+ *   rewards    [B] f32 device: per-sequence (already shaped) rewards R.
+ *   old_logp   [B] f32 device: log pi_old(y|x) (CoPG, Proximal RLOO; may be NULL otherwise).
+ *   clip_eps   Proximal RLOO clip range, 0 <= eps < 1.
+ *   stats      [ODPO_NSTATS] f64 out, per this call: pairs, mean loss, sequences with a nonzero
+ *              coefficient, sum r (Proximal RLOO), sum A1, sum |A1|, sum S1, sum S2, tokens of
+ *              y1, tokens of y2.
+ * RLOO, CoPG and SFT know every coefficient before the forward pass: each row's backward
+ * follows its forward in the same CTA (one HBM read and one write of [B,T,V]).  Proximal RLOO
+ * needs S first and runs the FUSED (default) or TWO_PASS schedule of the DPO call.
+ * Other arguments, ownership and errors as odpo_online_dpo_loss_fwd_bwd.
+ */
+odpo_status odpo_pg_loss_fwd_bwd(const void* policy_logits, odpo_dtype dt, int64_t B, int64_t T,
+                                 int64_t V, int64_t stride_b, int64_t stride_t,
+                                 const int32_t* tokens, const uint8_t* mask,
+                                 const int32_t* pair_rows, int64_t P, int64_t P_global,
+                                 int32_t kind, const float* rewards, const float* old_logp,
+                                 float clip_eps, float inv_temperature, void* dlogits,
+                                 int64_t dstride_b, int64_t dstride_t, float* seq_logp,
+                                 double* stats, uint32_t* status, void* workspace,
+                                 size_t workspace_bytes, odpo_launch_opts* opts, void* stream);
+
 /* Host-only: device scratch bytes needed by the calls above for B sequences of T tokens
    and P pairs (about 13 bytes per row + 80 bytes per pair + small). */
 size_t odpo_workspace_bytes(int64_t B, int64_t T, int64_t P);

@@ -73,8 +73,12 @@ def _L():
         L.odpo_online_dpo_loss_fwd_bwd_unscaled.argtypes = [
             P, C.c_int, i64, i64, i64, i64, i64, P, P, P, P, i64, i64, f32, f32, P, i64, i64, P, P,
             P, P, P, P, sz, C.POINTER(_Opts), P]
+        L.odpo_pg_loss_fwd_bwd.argtypes = [
+            P, C.c_int, i64, i64, i64, i64, i64, P, P, P, i64, i64, i32, P, P, f32, f32, P, i64,
+            i64, P, P, P, P, sz, C.POINTER(_Opts), P]
         for f in (L.odpo_pair_select, L.odpo_seq_logprobs, L.odpo_online_dpo_loss_fwd_bwd,
-                  L.odpo_online_dpo_loss_fwd_bwd_ex, L.odpo_online_dpo_loss_fwd_bwd_unscaled):
+                  L.odpo_online_dpo_loss_fwd_bwd_ex, L.odpo_online_dpo_loss_fwd_bwd_unscaled,
+                  L.odpo_pg_loss_fwd_bwd):
             f.restype = C.c_int
         L.odpo_workspace_bytes.argtypes = [i64, i64, i64]
         L.odpo_workspace_bytes.restype = sz
@@ -307,6 +311,55 @@ def online_dpo_loss_fwd_bwd_unscaled(policy_logits: torch.Tensor, ref_logp: torc
         _p(seq), _p(z), _p(stats), _p(status), _p(ws), ws.numel(), C.byref(opts), _stream()),
         "odpo_online_dpo_loss_fwd_bwd_unscaled")
     return LossOutput(stats, g, seq, z[:P], status, int(opts.launches), row_scale)
+
+
+PG_KINDS = {"rloo": 0, "copg": 1, "prox_rloo": 2, "sft": 3}
+
+
+def pg_loss_fwd_bwd(policy_logits: torch.Tensor, tokens: torch.Tensor, mask: torch.Tensor,
+                    kind: str, rewards: torch.Tensor, old_logp: torch.Tensor | None = None,
+                    clip_eps: float = 0.2, pair_rows: torch.Tensor | None = None,
+                    p_global: int | None = None, inv_temperature: float = 1.0,
+                    inplace: bool = False, dlogits: torch.Tensor | None = None,
+                    schedule: str = "auto", ctas_per_sm: int = 0, engine: int = -1,
+                    stats: torch.Tensor | None = None,
+                    status: torch.Tensor | None = None) -> LossOutput:
+    """App B losses on the same path: kind in rloo / copg / prox_rloo /
+    sft; rewards[B] and old_logp[B] per sequence.  out.z is empty (no DPO logit)."""
+    dt, B, T, V, sb, st = _logits_meta(policy_logits, "policy_logits")
+    tokens = _dev(tokens, "tokens", torch.int32).contiguous()
+    mask = _dev(mask, "mask", torch.uint8).contiguous()
+    rewards = _dev(rewards, "rewards", torch.float32).contiguous()
+    if old_logp is not None:
+        old_logp = _dev(old_logp, "old_logp", torch.float32).contiguous()
+    dev = policy_logits.device
+    if pair_rows is not None:
+        pair_rows = _dev(pair_rows, "pair_rows", torch.int32).contiguous()
+        P = pair_rows.shape[0]
+    else:
+        P = B // 2
+    Pg = P if p_global is None else int(p_global)
+    if inplace:
+        dl = policy_logits
+    elif dlogits is not None:
+        dl = _dev(dlogits, "dlogits", policy_logits.dtype)
+    else:
+        dl = torch.empty_like(policy_logits)
+    if dl.dim() != 3 or dl.stride(2) != 1:
+        raise OdpoError("dlogits must be [B, T, V] with a contiguous last dimension")
+    seq = torch.empty(B, dtype=torch.float32, device=dev)
+    if stats is None:
+        stats = torch.zeros(STATS_BUF, dtype=torch.float64, device=dev)
+    if status is None:
+        status = torch.zeros(1, dtype=torch.int32, device=dev)
+    ws = _workspace(dev, workspace_bytes(B, T, max(P, 1)))
+    opts = _Opts(SCHEDULES[schedule], 0, int(ctas_per_sm), 0, -1, -1, -1, int(engine))
+    _check(_L().odpo_pg_loss_fwd_bwd(
+        _p(policy_logits), dt, B, T, V, sb, st, _p(tokens), _p(mask), _p(pair_rows), P, Pg,
+        PG_KINDS[kind], _p(rewards), _p(old_logp), float(clip_eps), float(inv_temperature),
+        _p(dl), dl.stride(0), dl.stride(1), _p(seq), _p(stats), _p(status), _p(ws), ws.numel(),
+        C.byref(opts), _stream()), "odpo_pg_loss_fwd_bwd")
+    return LossOutput(stats, dl, seq, seq[:0], status, int(opts.launches))
 
 
 def allreduce_stats(stats: torch.Tensor, group=None) -> torch.Tensor:

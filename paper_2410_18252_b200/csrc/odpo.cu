@@ -236,6 +236,12 @@ struct LossArgs {
   int esize;
   float* row_scale;  // UNSC: [B*T] out, coef_b * mask (dlogits = row_scale * G)
   int row_gap;       // UNSC: forward rows streamed between a row's forward and its backward
+  // coefficient-variant losses (App B): -1 = Online DPO, else ODPO_PG_* (odpo.h)
+  int pg_kind;
+  int coef_known;        // UNSC: seq_coef is an input (RLOO, CoPG, SFT): write coef*G directly
+  const float* rewards;  // [B] per-sequence rewards (advantages A1 = R1 - R2)
+  const float* old_logp; // [B] log pi_old (CoPG, Proximal RLOO)
+  float clip_eps;
 };
 
 __device__ __forceinline__ const char* row_ptr(const LossArgs& a, int64_t b, int64_t t) {
@@ -264,7 +270,60 @@ __device__ __noinline__ void pair_reduce_warp(const LossArgs& a, int64_t p) {
   if (c >= 0) seq_sum_warp(a.w.row_logp + c * a.T, a.mask + c * a.T, a.T, Sc, nc);
   if (r >= 0) seq_sum_warp(a.w.row_logp + r * a.T, a.mask + r * a.T, a.T, Sr, nr);
   unsigned last = 0;
-  if (lane == 0) {
+  if (lane == 0 && a.pg_kind >= 0) {
+    uint32_t fl = 0;
+    double* pv = a.w.pair_vals + p * ODPO_NSTATS;
+    if (c < 0 || r < 0) {
+      for (int k = 0; k < ODPO_NSTATS; ++k) pv[k] = 0.0;
+    } else {
+      if (nc == 0 || nr == 0) fl |= ODPO_FLAG_EMPTY_SEQ;
+      const float fS[2] = {nc ? (float)Sc : 0.f, nr ? (float)Sr : 0.f};
+      const int64_t y[2] = {c, r};
+      const double A0 = (double)a.rewards[c] - (double)a.rewards[r];
+      const double A[2] = {A0, -A0};
+      const double scale = (double)a.invT / (2.0 * a.Pg);
+      double loss = 0.0, nact = 0.0, rsum = 0.0;
+      for (int k = 0; k < 2; ++k) {
+        const double S = (double)fS[k];
+        double cf = 0.0;
+        if (a.pg_kind == ODPO_PG_RLOO) {
+          loss += -0.5 * S * A[k];
+          cf = A[k] * scale;
+        } else if (a.pg_kind == ODPO_PG_COPG) {
+          loss += -0.5 * (S - (double)a.old_logp[y[k]]) * A[k];
+          cf = A[k] * scale;
+        } else if (a.pg_kind == ODPO_PG_PROX_RLOO) {
+          const double rt = exp(S - (double)a.old_logp[y[k]]);
+          const double eps = (double)a.clip_eps;
+          const double rc = fmin(fmax(rt, 1.0 - eps), 1.0 + eps);
+          const double u = rt * A[k], v = rc * A[k];
+          loss += -0.5 * (u <= v ? u : v);
+          cf = u <= v ? rt * A[k] * scale : 0.0;
+          rsum += rt;
+          a.w.seq_coef[y[k]] = (float)cf;   // the only kind whose coefficient needs S
+        } else if (k == 0) {               // Best-of-2 SFT on the chosen completion
+          loss += -S;
+          cf = 2.0 * scale;
+        }
+        if ((float)cf != 0.f) nact += 1.0;
+        a.seq_logp[y[k]] = fS[k];
+      }
+      pv[ODPO_ST_NPAIRS] = 1.0;
+      pv[ODPO_ST_LOSS] = loss;
+      pv[ODPO_ST_NCORRECT] = nact;
+      pv[ODPO_ST_Z] = rsum;
+      pv[ODPO_ST_RCHOSEN] = A0;
+      pv[ODPO_ST_RREJ] = fabs(A0);
+      pv[ODPO_ST_SCHOSEN] = (double)fS[0];
+      pv[ODPO_ST_SREJ] = (double)fS[1];
+      pv[ODPO_ST_NTOK_CHOSEN] = (double)nc;
+      pv[ODPO_ST_NTOK_REJ] = (double)nr;
+    }
+    flag(a.status, fl);
+    st_release(&a.w.pair_ready[p], 1u);
+    const unsigned done = atom_add_acq_rel(&a.w.counters[C_PAIRS_DONE], 1u);
+    last = (done == (unsigned)(a.P - 1));
+  } else if (lane == 0) {
     uint32_t fl = 0;
     double* pv = a.w.pair_vals + p * ODPO_NSTATS;
     if (c < 0 || r < 0) {
@@ -339,6 +398,26 @@ __device__ __noinline__ void pair_reduce_warp(const LossArgs& a, int64_t p) {
 
 // ------------------------------------------------------------------ K3b pair reduce (grid = P)
 __global__ void __launch_bounds__(32) k_pair_reduce(LossArgs a) { pair_reduce_warp(a, blockIdx.x); }
+
+// ------------------------------------------------------------------ App B known coefficients
+// RLOO / CoPG: coef_b = A_b invT / (2 P_global); Best-of-2 SFT: invT / P_global on the chosen
+// completion, 0 on the other.  One thread per pair.
+__global__ void k_pg_coef(LossArgs a) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= a.P) return;
+  int64_t c, r;
+  pair_seqs(a, p, c, r);
+  if (c < 0 || r < 0) return;
+  const double scale = (double)a.invT / (2.0 * a.Pg);
+  if (a.pg_kind == ODPO_PG_BEST_OF_K_SFT) {
+    a.w.seq_coef[c] = (float)(2.0 * scale);
+    a.w.seq_coef[r] = 0.f;
+  } else {
+    const double A0 = (double)a.rewards[c] - (double)a.rewards[r];
+    a.w.seq_coef[c] = (float)(A0 * scale);
+    a.w.seq_coef[r] = (float)(-A0 * scale);
+  }
+}
 
 // ------------------------------------------------------------------ K4 row backward (grid = rows)
 template <int DT, int NPB>
@@ -863,9 +942,11 @@ __global__ void __launch_bounds__(GE::THREADS, GE::CPS) k_engine(LossArgs a) {
             if (MODE == M_UNSC) {
               // the row's backward (G = softmax - onehot) constants, for this CTA's consumers
               RowSlot& W = slots[sl];
-              W.c = fmaf(l1p, kLog2e, v.m * k2);
-              W.coef = 1.f;
-              W.gtok = expm1f(logp);
+              // known coefficient (App B losses): coef folded into the exponent as in FUSED
+              const float cf = a.coef_known ? __ldcg(a.w.seq_coef + S.s) : 1.f;
+              W.c = cf != 0.f ? fmaf(l1p, kLog2e, v.m * k2) - log2f(fabsf(cf)) : INFINITY;
+              W.coef = cf;
+              W.gtok = cf * expm1f(logp);
               mbar_arrive(mready_s + 8 * sl);
             }
             flag(a.status, fl);
@@ -878,7 +959,7 @@ __global__ void __launch_bounds__(GE::THREADS, GE::CPS) k_engine(LossArgs a) {
           }
           if (count_row<MODE>(a, S, lane)) complete_unit<MODE>(a, S, lane);
         } else if (MODE == M_UNSC && kind == K_ZERO) {
-          if (lane == 0) a.row_scale[S.g] = 0.f;
+          if (lane == 0 && a.row_scale) a.row_scale[S.g] = 0.f;
         }
         __syncwarp();
         // rows the consumers never see also carry their NPART arrivals
@@ -1237,6 +1318,11 @@ static void base_args(LossArgs& a, const void* logits, int64_t B, int64_t T, int
   a.w = w; a.lag = 1; a.max_lead = 1; a.look = kLook; a.esize = es;
   a.row_scale = nullptr;
   a.row_gap = 0;
+  a.pg_kind = -1;
+  a.coef_known = 0;
+  a.rewards = nullptr;
+  a.old_logp = nullptr;
+  a.clip_eps = 0.f;
 }
 
 odpo_status odpo_seq_logprobs(const void* logits, odpo_dtype dt, int64_t B, int64_t T, int64_t V,
@@ -1410,6 +1496,76 @@ odpo_status odpo_online_dpo_loss_fwd_bwd_unscaled(
                          geo)) != ODPO_OK)
     return e;
   if (opts) opts->launches = 2;
+  return ODPO_OK;
+}
+
+odpo_status odpo_pg_loss_fwd_bwd(const void* policy_logits, odpo_dtype dt, int64_t B, int64_t T,
+                                 int64_t V, int64_t stride_b, int64_t stride_t,
+                                 const int32_t* tokens, const uint8_t* mask,
+                                 const int32_t* pair_rows, int64_t P, int64_t P_global,
+                                 int32_t kind, const float* rewards, const float* old_logp,
+                                 float clip_eps, float inv_temperature, void* dlogits,
+                                 int64_t dstride_b, int64_t dstride_t, float* seq_logp,
+                                 double* stats, uint32_t* status, void* workspace,
+                                 size_t workspace_bytes, odpo_launch_opts* opts, void* stream) {
+  if (kind < ODPO_PG_RLOO || kind > ODPO_PG_BEST_OF_K_SFT || !rewards) return ODPO_ERR_INVALID_ARG;
+  if ((kind == ODPO_PG_COPG || kind == ODPO_PG_PROX_RLOO) && !old_logp) return ODPO_ERR_INVALID_ARG;
+  if (kind == ODPO_PG_PROX_RLOO && !(clip_eps >= 0.f && clip_eps < 1.f)) return ODPO_ERR_INVALID_ARG;
+  // the shared checks (ref_logp is not an input here: pass a valid pointer to skip its check)
+  odpo_status e = check_loss(policy_logits, dt, B, T, V, stride_b, stride_t, rewards, tokens,
+                             mask, pair_rows, P, P_global, 1.f, inv_temperature, dlogits,
+                             dstride_b, dstride_t, seq_logp, stats, workspace, workspace_bytes);
+  if (e != ODPO_OK) return e;
+  const int pv = (opts && opts->exp2_split >= 0) ? opts->exp2_split : kPolyDefault;
+  if (pv >= kNumPoly) return ODPO_ERR_UNSUPPORTED;
+  const int sched = opts ? opts->schedule : ODPO_SCHED_AUTO;
+  if (sched < ODPO_SCHED_AUTO || sched > ODPO_SCHED_TWO_PASS) return ODPO_ERR_UNSUPPORTED;
+  Workspace w;
+  ws_layout(B, T, P, (char*)workspace, &w);
+  cudaStream_t s = (cudaStream_t)stream;
+  LossArgs a;
+  base_args(a, policy_logits, B, T, V, stride_b, stride_t, tokens, mask, inv_temperature, status,
+            w, dt == ODPO_F32 ? 4 : 2);
+  a.pair_rows = pair_rows;
+  a.P = P; a.Pg = (double)P_global; a.beta = 1.f;
+  a.dl = dlogits; a.dsb = dstride_b; a.dst = dstride_t;
+  a.seq_logp = seq_logp; a.stats = stats;
+  a.pg_kind = kind; a.rewards = rewards; a.old_logp = old_logp; a.clip_eps = clip_eps;
+  const int dti = dt == ODPO_F32 ? 0 : 1;
+  const int geo = opts ? opts->engine : -1;
+  const int cps = opts ? opts->ctas_per_sm : 0;
+  k_prep<<<1, kPrepThreads, 0, s>>>(pair_rows, B, P, w, status);
+  if ((e = launched()) != ODPO_OK) return e;
+  int launches = 1;
+  if (kind != ODPO_PG_PROX_RLOO) {
+    // coefficients known before the forward pass: each row's scaled backward follows its own
+    // forward in the same CTA (one HBM read, one write)
+    k_pg_coef<<<(unsigned)((P + 255) / 256), 256, 0, s>>>(a);
+    if ((e = launched()) != ODPO_OK) return e;
+    a.coef_known = 1;
+    const int look = (opts && opts->lookahead >= 0) ? opts->lookahead : kLook;
+    a.look = look < kSlots - 6 ? look : kSlots - 6;
+    a.row_gap = 0;
+    if ((e = launch_engine(dti, M_UNSC, pv, a, cps, s, geo)) != ODPO_OK) return e;
+    launches += 2;
+  } else if (sched == ODPO_SCHED_TWO_PASS) {
+    a.seqsum = 0;
+    if ((e = launch_engine(dti, M_SEQ, pv, a, cps, s, geo)) != ODPO_OK) return e;
+    k_pair_reduce<<<(unsigned)P, 32, 0, s>>>(a);
+    if ((e = launched()) != ODPO_OK) return e;
+    const unsigned rows = (unsigned)(B * T);
+    if (dt == ODPO_F32) k_row_bwd<0, 0><<<rows, kRowThreads, 0, s>>>(a);
+    else launch_bwd_bf16<0>(pv, rows, a, s);
+    if ((e = launched()) != ODPO_OK) return e;
+    launches += 3;
+  } else {
+    // Proximal RLOO: the coefficient needs the sequence's own log-prob (its pair's forward)
+    a.look = (opts && opts->lookahead >= 0) ? (opts->lookahead < kSlots - 2 ? opts->lookahead : kSlots - 2) : kLook;
+    a.max_lead = (int64_t)INT32_MAX;
+    if ((e = launch_engine(dti, M_FUSED, pv, a, cps, s, geo)) != ODPO_OK) return e;
+    launches += 1;
+  }
+  if (opts) opts->launches = launches;
   return ODPO_OK;
 }
 
