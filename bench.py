@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--mask", default="dense", choices=["dense", "prefix"])
     ap.add_argument("--gradient", default="scaled", choices=["scaled", "unscaled"],
                     help="scaled: dlogits (the north_star output); unscaled: G + row_scale")
+    ap.add_argument("--loss", default="dpo", choices=["dpo", "rloo", "copg", "prox_rloo", "sft"],
+                    help="dpo: Online DPO (the north_star); others: App B losses on the same path")
     ap.add_argument("--row-gap", type=int, default=-1)
     ap.add_argument("--engine", type=int, default=-1, help="row-engine geometry (-1 auto)")
     ap.add_argument("--no-aux", action="store_true",
@@ -231,7 +233,15 @@ def run_ours(args, rank, world, local_rank):
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     launches = [0]
 
+    rew_seq = rewards.reshape(-1).contiguous()   # per-sequence rewards (App B losses)
+
     def loss_call(gradient, pair_rows, ref, tok, msk):
+        if args.loss != "dpo":
+            # ref doubles as log pi_old for CoPG / Proximal RLOO
+            return odpo.pg_loss_fwd_bwd(logits, tok, msk, args.loss, rew_seq, ref, 0.2,
+                                        pair_rows=pair_rows, p_global=Pg, dlogits=dlogits,
+                                        schedule=args.schedule, ctas_per_sm=args.ctas_per_sm,
+                                        engine=args.engine, stats=stats, status=status)
         if gradient == "unscaled":
             return odpo.online_dpo_loss_fwd_bwd_unscaled(
                 logits, ref, tok, msk, w.beta, pair_rows=pair_rows, p_global=Pg, G=dlogits,
@@ -291,7 +301,7 @@ def run_ours(args, rank, world, local_rank):
 
     # auxiliary: the other gradient form on the same inputs (same bytes, not the headline)
     aux = None
-    if not args.no_aux:
+    if not args.no_aux and args.loss == "dpo":
         other = "unscaled" if args.gradient == "scaled" else "scaled"
         for _ in range(2):
             step(gradient=other)
@@ -308,7 +318,7 @@ def run_ours(args, rank, world, local_rank):
                "frac": aach / peak, "pairs_per_s_loss_only": world * P / (ams.mean() / 1e3),
                "status": int(status.item())}
     traffic = None
-    sfx = "" if args.gradient == "scaled" else "_unscaled"
+    sfx = ("" if args.gradient == "scaled" else "_unscaled") if args.loss == "dpo" else "_" + args.loss
     tp = os.path.join(ROOT, "profiles", f"ncu_traffic_{args.config}{sfx}.json")
     if os.path.exists(tp):
         try:
@@ -397,13 +407,14 @@ def run_ours(args, rank, world, local_rank):
                        "K": 2, "T": T, "V": V, "beta": w.beta, "mask": args.mask,
                        "ref_logp": "seq_logprobs over independent reference logits (setup)",
                        "schedule": args.schedule, "exp2_split": args.exp2_split,
-                       "gradient": args.gradient, "engine": args.engine,
+                       "loss": args.loss, "gradient": args.gradient, "engine": args.engine,
                        "parallelism": f"dp{world}",
                        "l2": "inputs (%.2f GB) > L2; plus 256 MiB L2 flush between timed steps"
                              % (B * T * V * s_in / 1e9)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                         "kernel": ("odpo_online_dpo_loss_fwd_bwd (prep + fused fwd/bwd)"
+                         "kernel": ("odpo_pg_loss_fwd_bwd (%s)" % args.loss if args.loss != "dpo"
+                                    else "odpo_online_dpo_loss_fwd_bwd (prep + fused fwd/bwd)"
                                     if args.gradient == "scaled" else
                                     "odpo_online_dpo_loss_fwd_bwd_unscaled (prep + fwd/bwd)"),
                          "alg_bytes_per_launch": alg_bytes,
