@@ -41,7 +41,7 @@ def parse():
     ap.add_argument("--config", default="pythia", choices=["tiny", "pythia", "rho", "llama", "strong"])
     ap.add_argument("--chunk-pairs", type=int, default=64)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--schedule", default="auto", choices=["auto", "fused", "two_pass"])
+    ap.add_argument("--schedule", default="auto", choices=["auto", "fused", "two_pass", "wave"])
     ap.add_argument("--lag", type=int, default=0)
     ap.add_argument("--ctas-per-sm", type=int, default=0)
     ap.add_argument("--exp2-split", type=int, default=-1)
@@ -252,7 +252,8 @@ def run_ours(args, rank, world, local_rank):
                                             p_global=Pg, dlogits=dlogits, schedule=args.schedule,
                                             lag_pairs=args.lag, ctas_per_sm=args.ctas_per_sm,
                                             exp2_split=args.exp2_split, lookahead=args.lookahead,
-                                            engine=args.engine, stats=stats, status=status)
+                                            engine=args.engine, row_gap=args.row_gap, stats=stats,
+                                            status=status)
 
     def step(timed_loss=None, gradient=args.gradient):
         sel = odpo.pair_select(rewards, eos, pen, status=status, sel_stats=stats[10:13])

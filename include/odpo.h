@@ -97,9 +97,14 @@ enum {
   ODPO_SCHED_AUTO = 0,     /* = FUSED                                                   */
   ODPO_SCHED_FUSED = 1,    /* one persistent kernel: forward and backward rows dispatched
                               adaptively (a backward row is taken as soon as its pair's
-                              forward pass has completed), per-pair completion counters;
-                              the backward re-read of a pair is served from L2            */
-  ODPO_SCHED_TWO_PASS = 2  /* forward kernel, pair-reduce kernel, backward kernel (2R+1W) */
+                              forward pass has completed), per-pair completion counters  */
+  ODPO_SCHED_TWO_PASS = 2, /* forward kernel, pair-reduce kernel, backward kernel (2R+1W) */
+  ODPO_SCHED_WAVE = 3      /* one persistent kernel, pairs statically assigned to groups
+                              of 2T CTAs (one row per CTA per pair, forward then
+                              backward), few enough groups that every in-flight pair
+                              stays in L2 (1R+1W at HBM); needs 2T <= resident CTAs and
+                              all CTAs co-resident (UNSUPPORTED otherwise).  Measured
+                              slower than FUSED on B200          */
 };
 
 typedef struct {
@@ -112,7 +117,8 @@ typedef struct {
                            (-1 = library default)        */
   int32_t lookahead;    /* FUSED: rows a CTA decodes ahead of the row it streams (-1 = default) */
   int32_t row_gap;      /* UNSCALED: forward rows a CTA streams between a row's forward and its
-                           backward, 0 or 1 (-1 = default 0)                          */
+                           backward, 0 or 1 (-1 = default 0); WAVE: pair-steps between a
+                           pair's forward and backward rows, 0 or 1 (-1 = default 1)  */
   int32_t engine;       /* row-engine geometry: -1 auto, 0 = 4 consumer warps x 3-stage ring x
                            4 CTAs/SM, 1 = 8 warps x 6 stages x 2 CTAs/SM;
                            geometry 1 requires exp2_split -1 or 0                   */

@@ -34,7 +34,7 @@ SEL_NAMES = ["margin_sum", "ndegen", "ntrunc"]
 NSTATS, NSEL, STATS_BUF = 10, 3, 16
 FLAGS = {"TOKEN_RANGE": 1, "NONFINITE_LOGIT": 2, "EMPTY_SEQ": 4, "NONFINITE_REWARD": 8,
          "DUP_ROW": 16, "DEGENERATE_PAIR": 32, "PAIR_RANGE": 64}
-SCHEDULES = {"auto": 0, "fused": 1, "two_pass": 2}
+SCHEDULES = {"auto": 0, "fused": 1, "two_pass": 2, "wave": 3}
 _DT = {torch.float32: 0, torch.bfloat16: 1}
 
 
@@ -215,7 +215,7 @@ def online_dpo_loss_fwd_bwd(policy_logits: torch.Tensor, ref_logp: torch.Tensor,
                             inv_temperature: float = 1.0, inplace: bool = False,
                             dlogits: torch.Tensor | None = None, schedule: str = "auto",
                             lag_pairs: int = 0, ctas_per_sm: int = 0, exp2_split: int = -1,
-                            lookahead: int = -1, engine: int = -1,
+                            lookahead: int = -1, engine: int = -1, row_gap: int = -1,
                             stats: torch.Tensor | None = None,
                             status: torch.Tensor | None = None) -> LossOutput:
     """Online DPO loss, statistics and dlogits in one call.
@@ -250,7 +250,7 @@ def online_dpo_loss_fwd_bwd(policy_logits: torch.Tensor, ref_logp: torch.Tensor,
     nb = workspace_bytes(B, T, max(P, 1))
     ws = _workspace(dev, nb)
     opts = _Opts(SCHEDULES[schedule], int(lag_pairs), int(ctas_per_sm), 0, int(exp2_split),
-                 int(lookahead), -1, int(engine))
+                 int(lookahead), int(row_gap), int(engine))
     _check(_L().odpo_online_dpo_loss_fwd_bwd_ex(
         _p(policy_logits), dt, B, T, V, sb, st, _p(ref_logp), _p(tokens), _p(mask), _p(pair_rows),
         P, Pg, float(beta), float(inv_temperature), _p(dl), dl.stride(0), dl.stride(1), _p(seq),

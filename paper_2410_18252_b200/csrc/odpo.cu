@@ -234,6 +234,9 @@ struct LossArgs {
   int64_t max_lead;  // FUSED: cap on forward rows dispensed ahead of the backward frontier
   int look;         // producer decode lookahead (rows), <= kSlots - 2
   int esize;
+  int wave_ng;      // FUSED, wave schedule: groups (0 = adaptive dispatch)
+  int wave_gs;      // CTAs per group (= 2T)
+  int wave_gap;     // pair-steps between a pair's forward and backward rows (0 or 1)
   float* row_scale;  // UNSC: [B*T] out, coef_b * mask (dlogits = row_scale * G)
   int row_gap;       // UNSC: forward rows streamed between a row's forward and its backward
   // coefficient-variant losses (App B): -1 = Online DPO, else ODPO_PG_* (odpo.h)
@@ -524,6 +527,62 @@ __device__ __forceinline__ int fused_next(const LossArgs& a, int64_t totalF, int
   }
 }
 
+// Wave dispatch (ODPO_SCHED_WAVE).  CTA b belongs to group g = b % NG with rank b / NG; group
+// g owns pairs g, g + NG, ... and for each of them its CTA of rank j streams rows j, j + GS, ...
+// of the pair's 2T rows forward, then the same rows backward.  A pair's rows are all in flight
+// at once (one per CTA), so it completes about one row-time after it starts and NG pairs'
+// logits stay in L2 for the backward re-read.  Static assignment: a CTA's backward row waits
+// only on forward rows that other CTAs of its group stream before their own backward row, so
+// the schedule is deadlock-free when all CTAs are co-resident (the host checks the grid).
+struct Wave {
+  int g, rank;
+  int64_t k, i;
+  int phase;
+  bool pairs_done;
+};
+__device__ __forceinline__ int wave_next(const LossArgs& a, Wave& W, int64_t totalF, int64_t nzero,
+                                         bool& fwd, int64_t& idx) {
+  const int64_t R = 2 * a.T;
+  // per CTA: F(0), [F(1)], B(0), [F(2)], B(1), ... with wave_gap = 1 (the bracketed forward
+  // rows hide the wait for the previous pair); F(0), B(0), F(1), B(1), ... with wave_gap = 0
+  for (;;) {
+    if (!W.pairs_done) {
+      if (W.rank >= a.wave_gs) {
+        W.pairs_done = true;
+        continue;
+      }
+      // phase 0: forward rows of pair-step k; phase 1: backward rows of pair-step k - gap
+      const int64_t kk = W.phase == 0 ? W.k : W.k - a.wave_gap;
+      const int64_t p = W.g + kk * a.wave_ng;
+      const bool valid = kk >= 0 && p < a.P;
+      const int64_t j = W.rank + W.i * a.wave_gs;
+      if (valid && j < R) {
+        fwd = W.phase == 0;
+        idx = p * R + j;
+        ++W.i;
+        return 1;
+      }
+      W.i = 0;
+      if (W.phase == 0) {
+        W.phase = 1;
+      } else {
+        W.phase = 0;
+        ++W.k;
+        // done once the backward of the last pair-step has been emitted
+        if (W.g + (W.k - a.wave_gap) * a.wave_ng >= a.P) W.pairs_done = true;
+      }
+      continue;
+    }
+    const int64_t z = (int64_t)atomicAdd(&a.w.counters[C_ZTICKET], 1u);
+    if (z < nzero) {
+      fwd = false;
+      idx = totalF + z;
+      return 1;
+    }
+    return 0;
+  }
+}
+
 // exp2 split variants (bf16): NPF / NPB of every 8 elements use the FMA-pipe polynomial in the
 // forward / backward; the rest use MUFU.EX2.
 struct PolyVariant {
@@ -721,6 +780,8 @@ __global__ void __launch_bounds__(GE::THREADS, GE::CPS) k_engine(LossArgs a) {
       const int64_t nzero = (int64_t)__ldcg(&a.w.counters[C_NUNREF]) * T;
       const int64_t total = a.B * T;  // SEQ
       Dispatch D{false, -1};
+      Wave Wv{(int)(blockIdx.x % (a.wave_ng > 0 ? a.wave_ng : 1)),
+              (int)(blockIdx.x / (a.wave_ng > 0 ? a.wave_ng : 1)), 0, 0, 0, false};
       int st = 0, dsl = 0, psl = 0, ahead = 0;
       uint32_t sph = 0, dph = 0, pph = 0;
       uint32_t pmask = 0;  // per-slot parity of param_ready (advances once per use)
@@ -804,7 +865,9 @@ __global__ void __launch_bounds__(GE::THREADS, GE::CPS) k_engine(LossArgs a) {
               }
               continue;
             }
-            if (MODE == M_FUSED) {
+            if (MODE == M_FUSED && a.wave_ng > 0) {
+              more = wave_next(a, Wv, totalF, nzero, fwd, tk) > 0;
+            } else if (MODE == M_FUSED) {
               const int r = fused_next(a, totalF, nzero, D, ahead == 0, fwd, tk);
               if (r < 0) break;  // stream the rows already held, then retry
               more = r > 0;
@@ -1316,6 +1379,7 @@ static void base_args(LossArgs& a, const void* logits, int64_t B, int64_t T, int
   a.seq_logp = nullptr; a.z_out = nullptr; a.stats = nullptr; a.status = status;
   a.tok_out = nullptr; a.lse_out = nullptr; a.seqsum = 0;
   a.w = w; a.lag = 1; a.max_lead = 1; a.look = kLook; a.esize = es;
+  a.wave_ng = 0; a.wave_gs = 0; a.wave_gap = 0;
   a.row_scale = nullptr;
   a.row_gap = 0;
   a.pg_kind = -1;
@@ -1348,6 +1412,38 @@ odpo_status odpo_seq_logprobs(const void* logits, odpo_dtype dt, int64_t B, int6
   k_prep<<<1, kPrepThreads, 0, s>>>(nullptr, B, 0, w, nullptr);
   if ((e = launched()) != ODPO_OK) return e;
   return launch_engine(dt == ODPO_F32 ? 0 : 1, M_SEQ, kPolyDefault, a, 0, s, -1);
+}
+
+// Wave schedule geometry: groups of 2T CTAs (one row per CTA per pair), as many groups as the
+// resident grid holds and as keep every group's in-flight pair within half of L2; 0 when the
+// wave does not apply (2T above the grid, a pair larger than the L2 budget, clusters).
+#ifndef ODPO_WAVE_BUDGET_PCT
+#define ODPO_WAVE_BUDGET_PCT 90
+#endif
+constexpr int kWaveGap = 1;
+static int wave_groups(int64_t T, int64_t P, int64_t row_bytes, int cps, int geo, int dti,
+                       bool busy_half, int gap) {
+  if (kCS != 1) return 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const DevInfo& di = dev_info(dev);
+  const int g = geo >= 0 ? geo : 0;
+  if (g > 1) return 0;
+  int occ = di.occ[g][dti][M_FUSED];
+  if (occ < 1) occ = 1;
+  if (cps <= 0 || cps > occ) cps = occ;
+  const int64_t grid = (int64_t)di.sms * cps;
+  const int64_t R = 2 * T;
+  const int64_t pair_bytes = R * row_bytes;
+  if (R > grid) return 0;
+  int64_t ng = grid / R;
+  // logits of (1 + gap) pairs per group are held between their forward and backward rows
+  const int64_t budget = (int64_t)di.l2 * ODPO_WAVE_BUDGET_PCT / 100;
+  if (ng * (1 + gap) * pair_bytes > budget) ng = budget / ((1 + gap) * pair_bytes);
+  if (ng > P) ng = P;
+  if (ng < 1) return 0;
+  if (busy_half && ng * R * 2 < grid) return 0;  // AUTO: at least half the CTAs busy
+  return (int)ng;
 }
 
 // Shared argument checks of the two loss entry points (dl = dlogits or G).
@@ -1389,10 +1485,21 @@ odpo_status odpo_online_dpo_loss_fwd_bwd_ex(const void* policy_logits, odpo_dtyp
                              dstride_b, dstride_t, seq_logp, stats, workspace, workspace_bytes);
   if (e != ODPO_OK) return e;
   const int64_t es = dt == ODPO_F32 ? 4 : 2;
-  const int sched = opts ? opts->schedule : ODPO_SCHED_AUTO;
-  if (sched < ODPO_SCHED_AUTO || sched > ODPO_SCHED_TWO_PASS) return ODPO_ERR_UNSUPPORTED;
+  int sched = opts ? opts->schedule : ODPO_SCHED_AUTO;
+  if (sched < ODPO_SCHED_AUTO || sched > ODPO_SCHED_WAVE) return ODPO_ERR_UNSUPPORTED;
   const int pv = (opts && opts->exp2_split >= 0) ? opts->exp2_split : kPolyDefault;
   if (pv >= kNumPoly) return ODPO_ERR_UNSUPPORTED;
+  int wave_ng = 0;
+  const int wave_gap = (opts && opts->row_gap >= 0) ? (opts->row_gap > 0 ? 1 : 0) : kWaveGap;
+  // AUTO = FUSED: the wave keeps every pair in L2 (1R+1W at HBM) but its per-pair waits cost
+  // more than the re-read saves on B200
+  if (sched == ODPO_SCHED_AUTO) sched = ODPO_SCHED_FUSED;
+  if (sched == ODPO_SCHED_WAVE) {
+    wave_ng = wave_groups(T, P, V * es, opts ? opts->ctas_per_sm : 0, opts ? opts->engine : -1,
+                          dt == ODPO_F32 ? 0 : 1, false, wave_gap);
+    if (wave_ng == 0) return ODPO_ERR_UNSUPPORTED;
+    sched = ODPO_SCHED_FUSED;
+  }
 
   Workspace w;
   ws_layout(B, T, P, (char*)workspace, &w);
@@ -1434,6 +1541,9 @@ odpo_status odpo_online_dpo_loss_fwd_bwd_ex(const void* policy_logits, odpo_dtyp
     int64_t lead = (opts && opts->lag_pairs > 0) ? (int64_t)opts->lag_pairs * R : (int64_t)INT32_MAX;
     if (lead < 2 * R) lead = 2 * R;
     a.max_lead = lead;
+    a.wave_ng = wave_ng;
+    a.wave_gs = (int)(2 * T);
+    a.wave_gap = wave_gap;
     const int cps = opts ? opts->ctas_per_sm : 0;
     if ((e = launch_engine(dti, M_FUSED, pv, a, cps, s, geo)) != ODPO_OK) return e;
     launches += 1;

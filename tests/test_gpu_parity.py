@@ -18,7 +18,7 @@ from gpu_helpers import (NCPU, Batch, alloc_rows, check_dlogits, check_seq, coef
 pytestmark = [pytest.mark.gpu,
               pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a CUDA device")]
 
-SCHEDS = ["fused", "two_pass"]
+SCHEDS = ["fused", "two_pass", "wave"]
 
 
 @pytest.fixture(scope="module")
@@ -274,6 +274,12 @@ def test_full_size_sampled_parity(odpo, name, mask_kind, nsample):
     assert torch.equal(out.seq_logp, two.seq_logp)
     assert torch.equal(out.z, two.z)
     assert torch.equal(out.stats[:10], two.stats[:10])
+    del two
+    # the wave schedule (pairs pinned to CTA groups) gives the same bits, dlogits included
+    auto = run_loss(odpo, b, ref, w.beta, "wave" if 2 * w.T <= 148 * 4 else "auto")
+    assert torch.equal(auto.seq_logp, out.seq_logp) and torch.equal(auto.stats[:10], out.stats[:10])
+    assert torch.equal(auto.dlogits, out.dlogits)
+    del auto
     pairs = synth.permutation(1, w.P)[:nsample]
     seqs = np.stack([2 * pairs, 2 * pairs + 1], 1).reshape(-1)
     h_x = b.host_rows(seqs)
@@ -300,7 +306,7 @@ def test_full_size_sampled_parity(odpo, name, mask_kind, nsample):
     assert st[0] == w.P and st[2] == np.count_nonzero(z_all > 0)
     assert st[8] + st[9] == b.mask.sum()
     assert int(out.status.item()) == 0
-    del b, out, two
+    del b, out
     torch.cuda.empty_cache()
 
 
