@@ -38,7 +38,8 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="pythia", choices=["tiny", "pythia", "rho", "llama", "strong"])
+    ap.add_argument("--config", default="pythia",
+                    choices=["tiny", "pythia", "rho", "llama", "strong", "rho_k4"])
     ap.add_argument("--chunk-pairs", type=int, default=64)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--schedule", default="auto", choices=["auto", "fused", "two_pass", "wave"])
@@ -130,20 +131,28 @@ def oracle_sample(w, seed, npairs, mask_kind, n_threads, p0=0):
     """Time the CPU oracle (as it stands) on npairs pairs of the same workload."""
     import oracle
     import synth
-    seqs = np.arange(2 * npairs) + 2 * p0
+    K = w.K
+    seqs = np.arange(K * npairs) + K * p0
     rows = (seqs[:, None] * w.T + np.arange(w.T)[None, :]).reshape(-1)
-    tok = synth.tokens_rows(seed, rows, w.V).reshape(-1, w.T)
-    mask = synth.mask_for(seed, seqs, w.T, mask_kind, w.lbar)
-    x = synth.logits_rows(seed, rows, w.V, tokens=tok.reshape(-1), peak=14.0).astype(np.float32)
-    x = x.reshape(len(seqs), w.T, w.V)
+    tok_all = synth.tokens_rows(seed, rows, w.V).reshape(-1, w.T)
+    mask_all = synth.mask_for(seed, seqs, w.T, mask_kind, w.lbar)
+    rewards = synth.rewards_for(seed, npairs, K, p0=p0, kind=w.reward_kind)
+    eos = synth.has_eos_for(seed, npairs, K, p0=p0) if w.eos_penalty is not None else None
+    pen = w.eos_penalty if w.eos_penalty is not None else 0.0
+    # K > 2: logits exist for the selected pair only (PAPER.md:617)
+    sel_rows = oracle.pair_select(rewards, eos, pen)["pair_rows"].reshape(-1) if K > 2 \
+        else np.arange(2 * npairs)
+    tok, mask = tok_all[sel_rows], mask_all[sel_rows]
+    grow = (seqs[sel_rows][:, None] * w.T + np.arange(w.T)[None, :]).reshape(-1)
+    x = synth.logits_rows(seed, grow, w.V, tokens=tok.reshape(-1), peak=14.0).astype(np.float32)
+    x = x.reshape(len(sel_rows), w.T, w.V)
     if w.dtype == "bf16":
         x = oracle.to_bf16_bits(x)
-    rewards = synth.rewards_for(seed, npairs, 2, p0=p0, kind=w.reward_kind)
-    eos = synth.has_eos_for(seed, npairs, 2, p0=p0) if w.eos_penalty is not None else None
-    ref = np.full(len(seqs), -0.08 * w.T, np.float32)
+    ref = np.full(len(sel_rows), -0.08 * w.T, np.float32)
     t0 = time.perf_counter()
-    sel = oracle.pair_select(rewards, eos, w.eos_penalty if w.eos_penalty is not None else 0.0)
-    o = oracle.online_dpo_loss_fwd_bwd(x, ref, tok, mask, w.beta, pair_rows=sel["pair_rows"],
+    sel = oracle.pair_select(rewards, eos, pen)
+    o = oracle.online_dpo_loss_fwd_bwd(x, ref, tok, mask, w.beta,
+                                       pair_rows=sel["pair_rows"] if K == 2 else None,
                                        want_dlogits=True, n_threads=n_threads)
     dt = time.perf_counter() - t0
     return dt, o
@@ -197,18 +206,30 @@ def run_ours(args, rank, world, local_rank):
     Pg = P * world
     tdt = torch.bfloat16 if w.dtype == "bf16" else torch.float32
     s_in = 2 if w.dtype == "bf16" else 4
-    seqs = np.arange(B) + 2 * p0
+    Kc = w.K                            # completions per prompt
+    n_src = Kc * P                      # completions of this rank
+    if Kc > 2 and args.loss != "dpo":
+        raise SystemExit("App B losses are benchmarked with K = 2 configs")
+    seqs = np.arange(n_src) + Kc * p0
     rows = (seqs[:, None] * T + np.arange(T)[None, :]).reshape(-1)
 
     # ---------------- inputs (untimed): rewards, tokens, mask on device; logits via device twin
-    rewards = torch.from_numpy(synth.rewards_for(args.seed, P, 2, p0=p0, kind=w.reward_kind)).to(dev)
-    eos = (torch.from_numpy(synth.has_eos_for(args.seed, P, 2, p0=p0)).to(dev)
+    rewards = torch.from_numpy(synth.rewards_for(args.seed, P, Kc, p0=p0, kind=w.reward_kind)).to(dev)
+    eos = (torch.from_numpy(synth.has_eos_for(args.seed, P, Kc, p0=p0)).to(dev)
            if w.eos_penalty is not None else None)
     pen = w.eos_penalty if w.eos_penalty is not None else 0.0
-    tokens = torch.from_numpy(synth.tokens_rows(args.seed, rows, V).reshape(B, T)).to(dev)
-    mask_np = synth.mask_for(args.seed, seqs, T, args.mask, w.lbar)
-    mask = torch.from_numpy(mask_np).to(dev)
-    rho = float(mask_np.mean())
+    tokens_all = torch.from_numpy(synth.tokens_rows(args.seed, rows, V).reshape(n_src, T)).to(dev)
+    mask_all = torch.from_numpy(synth.mask_for(args.seed, seqs, T, args.mask, w.lbar)).to(dev)
+    if Kc > 2:
+        # K completions per prompt, only the selected pair is trained on: the
+        # policy logits exist for the 2P selected completions, compacted by odpo_gather_pairs
+        sel0 = odpo.pair_select(rewards, eos, pen)
+        tokens, mask, _ = odpo.gather_pairs(sel0.pair_rows, tokens_all, mask_all)
+    else:
+        sel0 = None
+        tokens, mask = tokens_all, mask_all
+    torch.cuda.synchronize()
+    rho = float(mask.float().mean().item())
     logits = torch.empty((B, T, V), dtype=tdt, device=dev)
     dlogits = torch.empty_like(logits)
 
@@ -225,6 +246,12 @@ def run_ours(args, rank, world, local_rank):
         torch.cuda.synchronize()
         ref_ms.append(e0.elapsed_time(e1))
     synth.fill_logits_device(logits, args.seed, row0=int(rows[0]), tokens=tokens, peak=14.0)
+    if Kc > 2:
+        # per-completion reference log-probs (the selected ones from the pass above)
+        ref_all = torch.full((n_src,), -0.08 * T, dtype=torch.float32, device=dev)
+        ref_all[sel0.pair_rows.reshape(-1).long()] = ref_logp
+    else:
+        ref_all = ref_logp
     torch.cuda.synchronize()
 
     stats = torch.zeros(16, dtype=torch.float64, device=dev)
@@ -257,6 +284,17 @@ def run_ours(args, rank, world, local_rank):
 
     def step(timed_loss=None, gradient=args.gradient):
         sel = odpo.pair_select(rewards, eos, pen, status=status, sel_stats=stats[10:13])
+        if Kc > 2:
+            tok_g, msk_g, ref_g = odpo.gather_pairs(sel.pair_rows, tokens_all, mask_all, ref_all,
+                                                    status=status)
+            if timed_loss is not None:
+                timed_loss[0].record()
+            out = loss_call(gradient, None, ref_g, tok_g, msk_g)
+            if timed_loss is not None:
+                timed_loss[1].record()
+            odpo.allreduce_stats(stats)
+            launches[0] = 2 + out.launches
+            return out
         if timed_loss is not None:
             timed_loss[0].record()
         out = loss_call(gradient, sel.pair_rows, ref_logp, tokens, mask)
@@ -334,13 +372,13 @@ def run_ours(args, rank, world, local_rank):
         h_logits.copy_(logits)
         h_rew = rewards.cpu().pin_memory()
         h_eos = eos.cpu().pin_memory() if eos is not None else None
-        h_tok = tokens.cpu().pin_memory()
-        h_mask = mask.cpu().pin_memory()
-        h_ref = ref_logp.cpu().pin_memory()
+        h_tok = tokens_all.cpu().pin_memory()
+        h_mask = mask_all.cpu().pin_memory()
+        h_ref = ref_all.cpu().pin_memory()
         h_stats = torch.empty(16, dtype=torch.float64, pin_memory=True)
         h_z = torch.empty(P, dtype=torch.float32, pin_memory=True)
-        d_rew, d_tok, d_mask, d_ref = (torch.empty_like(rewards), torch.empty_like(tokens),
-                                       torch.empty_like(mask), torch.empty_like(ref_logp))
+        d_rew, d_tok, d_mask, d_ref = (torch.empty_like(rewards), torch.empty_like(tokens_all),
+                                       torch.empty_like(mask_all), torch.empty_like(ref_all))
         d_eos = torch.empty_like(eos) if eos is not None else None
         h2d = (h_logits.numel() * s_in + h_rew.numel() * 4 + (h_eos.numel() if h_eos is not None else 0)
                + h_tok.numel() * 4 + h_mask.numel() + h_ref.numel() * 4)
@@ -355,7 +393,11 @@ def run_ours(args, rank, world, local_rank):
             d_mask.copy_(h_mask, non_blocking=True)
             d_ref.copy_(h_ref, non_blocking=True)
             sel = odpo.pair_select(d_rew, d_eos, pen, status=status, sel_stats=stats[10:13])
-            out = loss_call(args.gradient, sel.pair_rows, d_ref, d_tok, d_mask)
+            if Kc > 2:
+                tg, mg, rg = odpo.gather_pairs(sel.pair_rows, d_tok, d_mask, d_ref, status=status)
+                out = loss_call(args.gradient, None, rg, tg, mg)
+            else:
+                out = loss_call(args.gradient, sel.pair_rows, d_ref, d_tok, d_mask)
             odpo.allreduce_stats(stats)
             h_stats.copy_(stats, non_blocking=True)
             h_z.copy_(out.z, non_blocking=True)
@@ -405,7 +447,7 @@ def run_ours(args, rank, world, local_rank):
             "warmup": args.warmup, "ms_per_step": tot_ms / K, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": w.dtype, "data": "synthetic",
             "config": {"workload": args.config, "pairs_per_rank": P, "global_pairs": P * world,
-                       "K": 2, "T": T, "V": V, "beta": w.beta, "mask": args.mask,
+                       "K": Kc, "T": T, "V": V, "beta": w.beta, "mask": args.mask,
                        "ref_logp": "seq_logprobs over independent reference logits (setup)",
                        "schedule": args.schedule, "exp2_split": args.exp2_split,
                        "loss": args.loss, "gradient": args.gradient, "engine": args.engine,

@@ -148,6 +148,24 @@ odpo_status odpo_pair_select(const float* rewards, const uint8_t* has_eos, float
                              uint32_t* status, void* stream);
 
 /*
+ * odpo_gather_pairs -- compact the selected completions into pair order for the loss call
+ * (App A.3: of K completions per prompt only the best and worst are trained on,
+ * "we throw out 2 samples").  For d in [0, 2P): destination row d <- source row pair_rows[d]
+ * (pair_select's output), so the loss call then takes pair_rows = NULL (rows 2p, 2p+1).
+ *
+ *   pair_rows   [P][2] i32 device (indices into n_src source rows).
+ *   tokens_in / tokens_out   [rows][T] i32 device, mask_in / mask_out [rows][T] u8 device,
+ *   ref_in / ref_out         [rows] f32 device; each output (with its input) may be NULL.
+ *   status      u32 device or NULL: PAIR_RANGE for an index outside [0, n_src) (that row
+ *               is written as zeros).
+ * One launch; bit-exact (index work).
+ */
+odpo_status odpo_gather_pairs(const int32_t* pair_rows, int64_t P, int64_t n_src, int64_t T,
+                              const int32_t* tokens_in, const uint8_t* mask_in,
+                              const float* ref_in, int32_t* tokens_out, uint8_t* mask_out,
+                              float* ref_out, uint32_t* status, void* stream);
+
+/*
  * odpo_seq_logprobs -- log pi(y|x) = sum_t mask[b,t] * log_softmax(invT * logits[b,t,:])[tokens[b,t]]
  * (reading R1: token-wise, pre-shifted, not length-normalised).
  *

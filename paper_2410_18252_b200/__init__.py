@@ -73,6 +73,8 @@ def _L():
         L.odpo_online_dpo_loss_fwd_bwd_unscaled.argtypes = [
             P, C.c_int, i64, i64, i64, i64, i64, P, P, P, P, i64, i64, f32, f32, P, i64, i64, P, P,
             P, P, P, P, sz, C.POINTER(_Opts), P]
+        L.odpo_gather_pairs.argtypes = [P, i64, i64, i64, P, P, P, P, P, P, P, P]
+        L.odpo_gather_pairs.restype = C.c_int
         L.odpo_pg_loss_fwd_bwd.argtypes = [
             P, C.c_int, i64, i64, i64, i64, i64, P, P, P, i64, i64, i32, P, P, f32, f32, P, i64,
             i64, P, P, P, P, sz, C.POINTER(_Opts), P]
@@ -157,6 +159,28 @@ def pair_select(rewards: torch.Tensor, has_eos: torch.Tensor | None = None, eos_
                                  _p(rejected), _p(pair_rows), _p(margin), _p(sel_stats), _p(status),
                                  _stream()), "odpo_pair_select")
     return SelectOutput(chosen, rejected, pair_rows, margin, sel_stats, status)
+
+
+def gather_pairs(pair_rows: torch.Tensor, tokens: torch.Tensor, mask: torch.Tensor,
+                 ref_logp: torch.Tensor | None = None, status: torch.Tensor | None = None):
+    """Selected completions in pair order: returns (tokens[2P, T],
+    mask[2P, T], ref_logp[2P] or None) for a loss call with pair_rows=None."""
+    pair_rows = _dev(pair_rows, "pair_rows", torch.int32).contiguous()
+    tokens = _dev(tokens, "tokens", torch.int32).contiguous()
+    mask = _dev(mask, "mask", torch.uint8).contiguous()
+    P = pair_rows.shape[0]
+    n_src, T = tokens.shape
+    dev = tokens.device
+    tok_o = torch.empty((2 * P, T), dtype=torch.int32, device=dev)
+    mask_o = torch.empty((2 * P, T), dtype=torch.uint8, device=dev)
+    ref_o = None
+    if ref_logp is not None:
+        ref_logp = _dev(ref_logp, "ref_logp", torch.float32).contiguous()
+        ref_o = torch.empty(2 * P, dtype=torch.float32, device=dev)
+    _check(_L().odpo_gather_pairs(_p(pair_rows), P, n_src, T, _p(tokens), _p(mask), _p(ref_logp),
+                                  _p(tok_o), _p(mask_o), _p(ref_o), _p(status), _stream()),
+           "odpo_gather_pairs")
+    return tok_o, mask_o, ref_o
 
 
 def _logits_meta(x: torch.Tensor, name="logits"):

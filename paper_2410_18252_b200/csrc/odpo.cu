@@ -209,6 +209,26 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep(const int32_t* __restrict
   if (tid == kPrepThreads - 1) w.counters[C_NUNREF] = (unsigned)scan[tid];
 }
 
+// ------------------------------------------------------------------ K1b compact the selected pairs
+// dst row 2p+k <- src row pair_rows[2p+k] for tokens / mask [rows][T] and ref_logp [rows]
+// (of K completions only the chosen and rejected are trained on).  One CTA per
+// destination row, 16-byte copies where the row strides allow.
+__global__ void k_gather_pairs(const int32_t* __restrict__ pair_rows, int64_t n_src, int64_t T,
+                               const int32_t* __restrict__ tok_in, const uint8_t* __restrict__ mask_in,
+                               const float* __restrict__ ref_in, int32_t* __restrict__ tok_out,
+                               uint8_t* __restrict__ mask_out, float* __restrict__ ref_out,
+                               uint32_t* status) {
+  const int64_t d = blockIdx.x;
+  const int64_t src = pair_rows[d];
+  const bool ok = src >= 0 && src < n_src;
+  if (!ok && threadIdx.x == 0) flag(status, ODPO_FLAG_PAIR_RANGE);
+  if (threadIdx.x == 0 && ref_out) ref_out[d] = ok ? ref_in[src] : 0.f;
+  for (int64_t t = threadIdx.x; t < T; t += blockDim.x) {
+    if (tok_out) tok_out[d * T + t] = ok ? tok_in[src * T + t] : 0;
+    if (mask_out) mask_out[d * T + t] = ok ? mask_in[src * T + t] : (uint8_t)0;
+  }
+}
+
 // ------------------------------------------------------------------ shared arguments
 struct LossArgs {
   const void* logits;
@@ -1677,6 +1697,21 @@ odpo_status odpo_pg_loss_fwd_bwd(const void* policy_logits, odpo_dtype dt, int64
   }
   if (opts) opts->launches = launches;
   return ODPO_OK;
+}
+
+odpo_status odpo_gather_pairs(const int32_t* pair_rows, int64_t P, int64_t n_src, int64_t T,
+                              const int32_t* tokens_in, const uint8_t* mask_in,
+                              const float* ref_in, int32_t* tokens_out, uint8_t* mask_out,
+                              float* ref_out, uint32_t* status, void* stream) {
+  if (P < 0 || n_src < 0 || T <= 0) return ODPO_ERR_INVALID_ARG;
+  if (P == 0) return ODPO_OK;
+  if (!pair_rows) return ODPO_ERR_INVALID_ARG;
+  if ((tokens_out && !tokens_in) || (mask_out && !mask_in) || (ref_out && !ref_in))
+    return ODPO_ERR_INVALID_ARG;
+  if (2 * P > (int64_t)INT32_MAX) return ODPO_ERR_UNSUPPORTED;
+  k_gather_pairs<<<(unsigned)(2 * P), 128, 0, (cudaStream_t)stream>>>(
+      pair_rows, n_src, T, tokens_in, mask_in, ref_in, tokens_out, mask_out, ref_out, status);
+  return launched();
 }
 
 }  // extern "C"

@@ -43,6 +43,9 @@ CONFIGS = {
     "pythia": Workload("pythia", 256, 2, 53, 50304, "bf16", 0.1, -1.0, "rm", 26),
     "rho": Workload("rho", 128, 2, 512, 32000, "bf16", 0.05, None, "verifier", 256),
     "llama": Workload("llama", 64, 2, 1024, 128256, "bf16", 0.03, -10.0, "rm", 290),
+    # GSM8k as the paper ran it (App A.3): 63 prompts x 4 completions
+    # (batch 252), the best and worst of each prompt trained on (NEXT-1)
+    "rho_k4": Workload("rho_k4", 63, 4, 512, 32000, "bf16", 0.05, None, "verifier", 256),
     # strong-scaling sweep: 2048 pairs in LLaMA-shaped 64-pair chunks
     "strong": Workload("strong", 2048, 2, 1024, 128256, "bf16", 0.03, -10.0, "rm", 290),
 }
@@ -52,5 +55,6 @@ CONFIG_TEXT = {
     "pythia": "Pythia-2.8B TLDR shape: 256 prompts×2, response len 53, V=50304, bf16 logits, staleness N=1 reference log-probs",
     "rho": "Rho-1B GSM8k shape: 128 prompts×2 samples, response len 512, V=32000, bf16 logits",
     "llama": "LLaMA-3.1-8B No Robots shape: 64 prompts×2, response len 1024, V=128256, bf16 logits",
+    "rho_k4": "Rho-1B GSM8k as run in App A.3: 63 prompts x 4 completions (batch 252), best/worst pair, T 512, V 32000, bf16",
     "strong": "strong-scaling sweep: 2048 pairs, response len 1024, V=128256, bf16, batch-sharded over 1/2/4/8 B200",
 }

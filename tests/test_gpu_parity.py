@@ -430,3 +430,31 @@ def test_seq_logprobs_per_token(odpo):
     lg = lse.cpu().numpy().astype(np.float64)
     assert np.all(np.abs(lg - o["row_lse"]) <= 1e-6 * np.maximum(np.abs(o["row_lse"]), 1.0))
     assert np.all(tg[b.mask == 0] == 0)
+
+
+# ------------------------------------------------------------------------ NEXT-1 gather
+def test_gather_pairs_bit_exact(odpo):
+    """K = 4: the selected completions compacted into pair order equal numpy fancy indexing
+    of pair_select's rows; an out-of-range row is flagged and zeroed."""
+    P, K, T = 63, 4, 37
+    rewards = synth.rewards_for(3, P, K, kind="verifier")
+    sel = odpo.pair_select(torch.from_numpy(rewards).cuda())
+    pr = oracle.pair_select(rewards)["pair_rows"]
+    tok = synth.tokens_rows(3, np.arange(P * K * T), 32000).reshape(P * K, T)
+    mask = synth.mask_for(3, np.arange(P * K), T, "prefix", 11)
+    ref = synth.rewards_for(4, P * K, 1).reshape(-1).astype(np.float32)
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    t, m, r = odpo.gather_pairs(sel.pair_rows, torch.from_numpy(tok).cuda(),
+                                torch.from_numpy(mask).cuda(), torch.from_numpy(ref).cuda(),
+                                status=status)
+    rows = pr.reshape(-1)
+    assert np.array_equal(t.cpu().numpy(), tok[rows])
+    assert np.array_equal(m.cpu().numpy(), mask[rows])
+    assert np.array_equal(r.cpu().numpy(), ref[rows])
+    assert int(status.item()) == 0
+    bad = sel.pair_rows.clone()
+    bad[5, 1] = P * K + 3
+    t2, m2, _ = odpo.gather_pairs(bad, torch.from_numpy(tok).cuda(), torch.from_numpy(mask).cuda(),
+                                  status=status)
+    assert int(status.item()) & odpo.FLAGS["PAIR_RANGE"]
+    assert torch.count_nonzero(t2[11]).item() == 0 and torch.count_nonzero(m2[11]).item() == 0
