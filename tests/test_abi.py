@@ -126,6 +126,26 @@ def test_unscaled_argument_errors_are_synchronous(lib):
     assert _unscaled(lib, dl=FAKE, logits=FAKE, dsb=256, dst=64) == 1
 
 
+def test_pg_and_gather_argument_errors_are_synchronous(lib):
+    import paper_2410_18252_b200 as odpo
+
+    def pg(kind=0, rewards=FAKE, old=None, eps=0.2, sched=0, dl=FAKE):
+        opts = odpo._Opts(sched, 0, 0, 0, -1, -1, -1, -1)
+        return lib.odpo_pg_loss_fwd_bwd(FAKE, 1, 4, 3, 64, 192, 64, FAKE, FAKE, None, 2, 2, kind,
+                                        rewards, old, eps, 1.0, dl, 192, 64, FAKE, FAKE, None,
+                                        FAKE, 1 << 20, C.byref(opts), None)
+    assert pg(kind=7) == 1
+    assert pg(rewards=None) == 1
+    assert pg(kind=1, old=None) == 1          # CoPG needs log pi_old
+    assert pg(kind=2, old=FAKE, eps=1.5) == 1  # clip range
+    assert pg(dl=FAKE_MIS) == 2
+    assert pg(sched=9) == 4
+    assert lib.odpo_gather_pairs(None, 2, 8, 5, FAKE, FAKE, None, FAKE, FAKE, None, None, None) == 1
+    assert lib.odpo_gather_pairs(FAKE, 2, 8, 0, FAKE, FAKE, None, FAKE, FAKE, None, None, None) == 1
+    assert lib.odpo_gather_pairs(FAKE, 2, 8, 5, None, FAKE, None, FAKE, FAKE, None, None, None) == 1
+    assert lib.odpo_gather_pairs(FAKE, 0, 8, 5, None, None, None, None, None, None, None, None) == 0
+
+
 def test_product_has_no_oracle_or_cpu_fallback():
     """The product package never imports the oracle and refuses CPU tensors."""
     pkg = os.path.join(ROOT, "paper_2410_18252_b200")

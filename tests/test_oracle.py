@@ -566,3 +566,24 @@ def test_rloo_uniform_rows_closed_form(orc):
     A = [1.5, -1.75]
     want = (-0.5 * (A[0] * (S[0] - S[1]) + A[1] * (S[2] - S[3]))) / 2
     assert abs(out["stats"][1] - want) < 1e-12
+
+
+@pytest.mark.parametrize("kind", ["rloo", "sft"])
+def test_pg_shard_decomposition(orc, kind):
+    """App B losses shard like DPO: with a static P_global, per-shard loss stats sum to the
+    unsharded ones and shard gradients equal the unsharded rows (weak-scaling invariance)."""
+    rng = np.random.default_rng(31)
+    P, T, V, W = 6, 3, 9, 3
+    x = rng.normal(0, 1.2, size=(2 * P, T, V))
+    tok = rng.integers(0, V, size=(2 * P, T)).astype(np.int32)
+    mask = np.ones((2 * P, T), np.uint8)
+    rew = rng.normal(0, 1, size=2 * P).astype(np.float32)
+    full = orc.pg_loss_fwd_bwd(x, tok, mask, kind, rew, None, 0.2, None, P, 1.0, want_dlogits=True)
+    acc = np.zeros(10)
+    for r in range(W):
+        sl = slice(2 * P * r // W, 2 * P * (r + 1) // W)
+        o = orc.pg_loss_fwd_bwd(x[sl], tok[sl], mask[sl], kind, rew[sl], None, 0.2, None, P, 1.0,
+                                want_dlogits=True)
+        acc += o["stats"]
+        assert np.array_equal(o["dlogits"], full["dlogits"][sl])
+    assert np.allclose(acc, full["stats"], rtol=1e-12, atol=1e-12)
