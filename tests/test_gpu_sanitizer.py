@@ -1,0 +1,31 @@
+"""compute-sanitizer memcheck / synccheck / initcheck over every entry
+point on small shapes (profiles/sanitize_run.py); racecheck is recorded in
+profiles/r01_sanitizer.md (it does not model mbarrier phase waits)."""
+import os
+import shutil
+import subprocess
+import sys
+
+import pytest
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a CUDA device")]
+
+
+def _sanitizer():
+    for c in (shutil.which("compute-sanitizer"), "/usr/local/cuda/bin/compute-sanitizer"):
+        if c and os.path.exists(c):
+            return c
+    pytest.skip("compute-sanitizer not found")
+
+
+@pytest.mark.parametrize("tool", ["memcheck", "synccheck", "initcheck"])
+def test_compute_sanitizer(tool):
+    cmd = [_sanitizer(), "--tool", tool, "--print-limit", "10", sys.executable,
+           os.path.join(ROOT, "profiles", "sanitize_run.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    out = r.stdout + r.stderr
+    assert "sanitize run ok" in out, out[-2000:]
+    assert "ERROR SUMMARY: 0 errors" in out, out[-2000:]
