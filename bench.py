@@ -600,8 +600,16 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
+        # ODPO_DIST_BACKEND=gloo + ODPO_SHARE_GPU=1: several ranks on one GPU (tests the
+        # multi-rank path on a 1-GPU box; NCCL refuses duplicate devices)
+        if os.environ.get("ODPO_SHARE_GPU") == "1":
+            local_rank = local_rank % max(1, torch.cuda.device_count())
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        backend = os.environ.get("ODPO_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group(backend)
     try:
         if args.config == "strong":
             run_strong(args, rank, world, local_rank)
