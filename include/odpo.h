@@ -295,6 +295,43 @@ odpo_status odpo_pg_loss_fwd_bwd(const void* policy_logits, odpo_dtype dt, int64
                                  double* stats, uint32_t* status, void* workspace,
                                  size_t workspace_bytes, odpo_launch_opts* opts, void* stream);
 
+/*
+ * Vocabulary-parallel loss: the LM head's vocabulary is
+ * sharded over W ranks, rank w holding logits[:, :, v0_w : v0_w + V_shard_w] (v0 increasing
+ * with w).  Two calls per rank with an all-gather of 16-byte row partials between them (the
+ * caller's collective, e.g. NCCL all_gather over NVLink):
+ *
+ * odpo_vp_row_partials -- one read of this rank's shard: for every row with mask = 1,
+ *   parts[row] = (m, log1p r, x_tok, owns) with 1 + r = sum over the shard of
+ *   exp(invT (x - m)), m the shard maximum, x_tok the sampled token's logit if
+ *   v0 <= tok < v0 + V_shard (owns = 1) else 0 (owns = 0); masked rows get (-inf, 0, 0, 0).
+ *   parts: [B*T][4] f32 device, 16-byte aligned.  TOKEN_RANGE if tok is outside [0, V_total).
+ *
+ * odpo_vp_loss_fwd_bwd -- merges parts_all ([W][B*T][4], rank order) into the full-vocabulary
+ *   row statistics (lse = invT m* + log1p R, R = r_w* + sum_{w != w*} e^{invT (m_w - m*)}(1+r_w),
+ *   w* the first rank holding the maximum), then the same pair reduction and statistics as
+ *   odpo_online_dpo_loss_fwd_bwd (identical on every rank: the stats are already global over
+ *   the vocabulary group, do not sum them over it), and writes this rank's dlogits shard
+ *   coef_b (softmax - onehot) with the global normaliser.  One read of the shard again (2R+1W
+ *   per shard).  Other arguments and errors as odpo_online_dpo_loss_fwd_bwd.
+ */
+odpo_status odpo_vp_row_partials(const void* logits_shard, odpo_dtype dt, int64_t B, int64_t T,
+                                 int64_t V_shard, int64_t stride_b, int64_t stride_t,
+                                 int64_t v0, int64_t V_total, const int32_t* tokens,
+                                 const uint8_t* mask, float inv_temperature, float* parts,
+                                 uint32_t* status, void* workspace, size_t workspace_bytes,
+                                 void* stream);
+odpo_status odpo_vp_loss_fwd_bwd(const float* parts_all, int32_t W, const void* logits_shard,
+                                 odpo_dtype dt, int64_t B, int64_t T, int64_t V_shard,
+                                 int64_t stride_b, int64_t stride_t, int64_t v0, int64_t V_total,
+                                 const float* ref_logp, const int32_t* tokens,
+                                 const uint8_t* mask, const int32_t* pair_rows, int64_t P,
+                                 int64_t P_global, float beta, float inv_temperature,
+                                 void* dlogits_shard, int64_t dstride_b, int64_t dstride_t,
+                                 float* seq_logp, float* pair_logit, double* stats,
+                                 uint32_t* status, void* workspace, size_t workspace_bytes,
+                                 void* stream);
+
 /* Host-only: device scratch bytes needed by the calls above for B sequences of T tokens
    and P pairs (about 13 bytes per row + 80 bytes per pair + small). */
 size_t odpo_workspace_bytes(int64_t B, int64_t T, int64_t P);

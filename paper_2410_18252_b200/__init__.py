@@ -73,6 +73,13 @@ def _L():
         L.odpo_online_dpo_loss_fwd_bwd_unscaled.argtypes = [
             P, C.c_int, i64, i64, i64, i64, i64, P, P, P, P, i64, i64, f32, f32, P, i64, i64, P, P,
             P, P, P, P, sz, C.POINTER(_Opts), P]
+        L.odpo_vp_row_partials.argtypes = [P, C.c_int, i64, i64, i64, i64, i64, i64, i64, P, P,
+                                           f32, P, P, P, sz, P]
+        L.odpo_vp_loss_fwd_bwd.argtypes = [P, i32, P, C.c_int, i64, i64, i64, i64, i64, i64, i64,
+                                           P, P, P, P, i64, i64, f32, f32, P, i64, i64, P, P, P,
+                                           P, P, sz, P]
+        L.odpo_vp_row_partials.restype = C.c_int
+        L.odpo_vp_loss_fwd_bwd.restype = C.c_int
         L.odpo_gather_pairs.argtypes = [P, i64, i64, i64, P, P, P, P, P, P, P, P]
         L.odpo_gather_pairs.restype = C.c_int
         L.odpo_pg_loss_fwd_bwd.argtypes = [
@@ -384,6 +391,80 @@ def pg_loss_fwd_bwd(policy_logits: torch.Tensor, tokens: torch.Tensor, mask: tor
         _p(dl), dl.stride(0), dl.stride(1), _p(seq), _p(stats), _p(status), _p(ws), ws.numel(),
         C.byref(opts), _stream()), "odpo_pg_loss_fwd_bwd")
     return LossOutput(stats, dl, seq, seq[:0], status, int(opts.launches))
+
+
+def vp_row_partials(logits_shard: torch.Tensor, v0: int, V_total: int, tokens: torch.Tensor,
+                    mask: torch.Tensor, inv_temperature: float = 1.0,
+                    status: torch.Tensor | None = None) -> torch.Tensor:
+    """Vocabulary-parallel forward of one shard (columns [v0, v0 + V_shard) of V_total):
+    returns the [B*T, 4] f32 row partials (m, log1p r, x_tok, owns)."""
+    dt, B, T, V, sb, st = _logits_meta(logits_shard, "logits_shard")
+    tokens = _dev(tokens, "tokens", torch.int32).contiguous()
+    mask = _dev(mask, "mask", torch.uint8).contiguous()
+    parts = torch.empty((B * T, 4), dtype=torch.float32, device=logits_shard.device)
+    ws = _workspace(logits_shard.device, workspace_bytes(B, T, B // 2 + 1))
+    _check(_L().odpo_vp_row_partials(_p(logits_shard), dt, B, T, V, sb, st, int(v0), int(V_total),
+                                     _p(tokens), _p(mask), float(inv_temperature), _p(parts),
+                                     _p(status), _p(ws), ws.numel(), _stream()),
+           "odpo_vp_row_partials")
+    return parts
+
+
+def vp_loss_fwd_bwd(parts_all: torch.Tensor, logits_shard: torch.Tensor, v0: int, V_total: int,
+                    ref_logp: torch.Tensor, tokens: torch.Tensor, mask: torch.Tensor, beta: float,
+                    pair_rows: torch.Tensor | None = None, p_global: int | None = None,
+                    inv_temperature: float = 1.0, dlogits: torch.Tensor | None = None,
+                    stats: torch.Tensor | None = None,
+                    status: torch.Tensor | None = None) -> LossOutput:
+    """Vocabulary-parallel loss of one shard from the all-gathered partials [W, B*T, 4]:
+    global log-probs, loss and stats (identical on every rank of the vocabulary group) and
+    this shard's dlogits."""
+    dt, B, T, V, sb, st = _logits_meta(logits_shard, "logits_shard")
+    parts_all = _dev(parts_all, "parts_all", torch.float32).contiguous()
+    W = parts_all.shape[0]
+    ref_logp = _dev(ref_logp, "ref_logp", torch.float32).contiguous()
+    tokens = _dev(tokens, "tokens", torch.int32).contiguous()
+    mask = _dev(mask, "mask", torch.uint8).contiguous()
+    dev = logits_shard.device
+    if pair_rows is not None:
+        pair_rows = _dev(pair_rows, "pair_rows", torch.int32).contiguous()
+        P = pair_rows.shape[0]
+    else:
+        P = B // 2
+    Pg = P if p_global is None else int(p_global)
+    dl = torch.empty_like(logits_shard) if dlogits is None else _dev(dlogits, "dlogits", logits_shard.dtype)
+    seq = torch.empty(B, dtype=torch.float32, device=dev)
+    z = torch.empty(max(P, 1), dtype=torch.float32, device=dev)
+    if stats is None:
+        stats = torch.zeros(STATS_BUF, dtype=torch.float64, device=dev)
+    if status is None:
+        status = torch.zeros(1, dtype=torch.int32, device=dev)
+    ws = _workspace(dev, workspace_bytes(B, T, max(P, 1)))
+    _check(_L().odpo_vp_loss_fwd_bwd(
+        _p(parts_all), W, _p(logits_shard), dt, B, T, V, sb, st, int(v0), int(V_total),
+        _p(ref_logp), _p(tokens), _p(mask), _p(pair_rows), P, Pg, float(beta),
+        float(inv_temperature), _p(dl), dl.stride(0), dl.stride(1), _p(seq), _p(z), _p(stats),
+        _p(status), _p(ws), ws.numel(), _stream()), "odpo_vp_loss_fwd_bwd")
+    return LossOutput(stats, dl, seq, z[:P], status, 4)
+
+
+def vp_loss_step(logits_shard: torch.Tensor, v0: int, V_total: int, ref_logp: torch.Tensor,
+                 tokens: torch.Tensor, mask: torch.Tensor, beta: float, group=None,
+                 **kw) -> LossOutput:
+    """One vocabulary-parallel learner step on this rank: partials, all-gather over the
+    vocabulary group (NCCL over NVLink with the nccl backend), loss and dlogits shard."""
+    import torch.distributed as dist
+    parts = vp_row_partials(logits_shard, v0, V_total, tokens, mask,
+                            kw.get("inv_temperature", 1.0), kw.get("status"))
+    W = dist.get_world_size(group)
+    if dist.get_backend(group) == "nccl":
+        parts_all = torch.empty((W,) + tuple(parts.shape), dtype=parts.dtype, device=parts.device)
+        dist.all_gather_into_tensor(parts_all, parts, group=group)
+    else:
+        chunks = [torch.empty_like(parts) for _ in range(W)]
+        dist.all_gather(chunks, parts, group=group)
+        parts_all = torch.stack(chunks)
+    return vp_loss_fwd_bwd(parts_all, logits_shard, v0, V_total, ref_logp, tokens, mask, beta, **kw)
 
 
 def allreduce_stats(stats: torch.Tensor, group=None) -> torch.Tensor:

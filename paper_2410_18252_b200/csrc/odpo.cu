@@ -265,6 +265,12 @@ struct LossArgs {
   const float* rewards;  // [B] per-sequence rewards (advantages A1 = R1 - R2)
   const float* old_logp; // [B] log pi_old (CoPG, Proximal RLOO)
   float clip_eps;
+  // vocabulary-parallel forward (NEXT-4): this call sees columns [tok_off, tok_off + V) of a
+  // V_total vocabulary and writes per-row partials (m, log1p r, x_tok, owns tok) instead of
+  // log-probs
+  float4* vp_parts;
+  int64_t tok_off;
+  int64_t V_total;
 };
 
 __device__ __forceinline__ const char* row_ptr(const LossArgs& a, int64_t b, int64_t t) {
@@ -422,6 +428,48 @@ __device__ __noinline__ void pair_reduce_warp(const LossArgs& a, int64_t p) {
 // ------------------------------------------------------------------ K3b pair reduce (grid = P)
 __global__ void __launch_bounds__(32) k_pair_reduce(LossArgs a) { pair_reduce_warp(a, blockIdx.x); }
 
+// ------------------------------------------------------------------ NEXT-4 vocabulary-parallel merge
+// Row statistics of the full vocabulary from W shard partials (m_w, log1p r_w, x_tok, owner),
+// merged in rank order with the log1p form: w* = first argmax m_w,
+//   R = r_w* + sum_{w != w*} exp(invT (m_w - m*)) (1 + r_w),  lse = invT m* + log1p(R).
+// One thread per row.  The token's logit comes from the shard that owns it.
+__global__ void k_vp_combine(LossArgs a, const float4* __restrict__ parts, int W) {
+  const int64_t rows = a.B * a.T;
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= rows || !a.mask[g]) return;
+  int ws = 0;
+  float ms = -INFINITY;
+  for (int w = 0; w < W; ++w) {
+    const float mw = __ldg(&parts[(int64_t)w * rows + g].x);
+    if (mw > ms) { ms = mw; ws = w; }
+  }
+  uint32_t fl = 0;
+  float R = 0.f, xt = 0.f;
+  int owners = 0;
+  for (int w = 0; w < W; ++w) {
+    const float4 pw = parts[(int64_t)w * rows + g];
+    if (pw.w != 0.f) { xt = pw.z; ++owners; }
+    if (w == ws) {
+      R += expm1f(pw.y);
+    } else if (pw.x != -INFINITY) {
+      R += ex2((pw.x - ms) * (a.invT * kLog2e)) * (1.f + expm1f(pw.y));
+    }
+  }
+  const float l1p = log1pf(R);
+  float logp = 0.f;
+  if (owners != 1) {
+    fl |= ODPO_FLAG_TOKEN_RANGE;
+  } else {
+    logp = __fsub_rn(__fmul_rn(__fsub_rn(xt, ms), a.invT), l1p);
+    if (!isfinite(logp)) fl |= ODPO_FLAG_NONFINITE_LOGIT;
+  }
+  if (!isfinite(ms)) fl |= ODPO_FLAG_NONFINITE_LOGIT;
+  a.w.row_m[g] = ms;
+  a.w.row_l1p[g] = l1p;
+  a.w.row_logp[g] = logp;
+  flag(a.status, fl);
+}
+
 // ------------------------------------------------------------------ App B known coefficients
 // RLOO / CoPG: coef_b = A_b invT / (2 P_global); Best-of-2 SFT: invT / P_global on the chosen
 // completion, 0 on the other.  One thread per pair.
@@ -453,7 +501,9 @@ __global__ void __launch_bounds__(kRowThreads, 2) k_row_bwd(LossArgs a) {
     return;
   }
   const float coef = a.w.seq_coef[b];
-  row_backward<DT, LD_STREAM, NPB>(row_ptr(a, b, t), drow, (int)a.V, a.tokens[g], a.invT, a.w.row_m[g],
+  const int64_t tl = (int64_t)a.tokens[g] - a.tok_off;   // shard-local (vocabulary-parallel)
+  const int tok = (tl >= 0 && tl < a.V) ? (int)tl : -1;
+  row_backward<DT, LD_STREAM, NPB>(row_ptr(a, b, t), drow, (int)a.V, tok, a.invT, a.w.row_m[g],
                               a.w.row_l1p[g], a.w.row_logp[g], coef, 0);
 }
 
@@ -632,7 +682,7 @@ __device__ __forceinline__ bool decode_row(const LossArgs& a, int64_t tk, bool f
     if (a.mask[S.g]) {
       S.kind = K_F;
       S.row = row_ptr(a, S.s, tk % T);
-      S.tok = a.tokens[S.g];
+      S.tok = (int32_t)(a.tokens[S.g] - a.tok_off);  // shard-local (vocabulary-parallel)
       return true;
     }
     S.kind = K_FSKIP;
@@ -1004,7 +1054,18 @@ __global__ void __launch_bounds__(GE::THREADS, GE::CPS) k_engine(LossArgs a) {
           v.m = lane < NPART ? S.pm[lane] : -INFINITY;
           v.r = lane < NPART ? S.pr[lane] : 0.f;
           v = warp_merge(v, k2);
-          if (lane == 0) {
+          if (MODE == M_SEQ && a.vp_parts) {
+            // vocabulary-parallel partial of this shard; k_vp_combine merges the shards
+            if (lane == 0) {
+              uint32_t fl = 0;
+              const int64_t gt = (int64_t)S.tok + a.tok_off;
+              if (gt < 0 || gt >= a.V_total) fl |= ODPO_FLAG_TOKEN_RANGE;
+              if (isnan(v.m) || v.m == INFINITY || !isfinite(v.r)) fl |= ODPO_FLAG_NONFINITE_LOGIT;
+              const bool own = S.tok >= 0 && S.tok < V;
+              a.vp_parts[S.g] = make_float4(v.m, log1pf(v.r), own ? S.xtok : 0.f, own ? 1.f : 0.f);
+              flag(a.status, fl);
+            }
+          } else if (lane == 0) {
             uint32_t fl = 0;
             const float l1p = log1pf(v.r);
             float logp = 0.f;
@@ -1039,6 +1100,7 @@ __global__ void __launch_bounds__(GE::THREADS, GE::CPS) k_engine(LossArgs a) {
           if (lane == 0 && MODE == M_SEQ) {
             if (a.tok_out) a.tok_out[S.g] = 0.f;
             if (a.lse_out) a.lse_out[S.g] = 0.f;
+            if (a.vp_parts) a.vp_parts[S.g] = make_float4(-INFINITY, 0.f, 0.f, 0.f);
           }
           if (count_row<MODE>(a, S, lane)) complete_unit<MODE>(a, S, lane);
         } else if (MODE == M_UNSC && kind == K_ZERO) {
@@ -1407,6 +1469,9 @@ static void base_args(LossArgs& a, const void* logits, int64_t B, int64_t T, int
   a.rewards = nullptr;
   a.old_logp = nullptr;
   a.clip_eps = 0.f;
+  a.vp_parts = nullptr;
+  a.tok_off = 0;
+  a.V_total = V;
 }
 
 odpo_status odpo_seq_logprobs(const void* logits, odpo_dtype dt, int64_t B, int64_t T, int64_t V,
@@ -1711,6 +1776,76 @@ odpo_status odpo_gather_pairs(const int32_t* pair_rows, int64_t P, int64_t n_src
   if (2 * P > (int64_t)INT32_MAX) return ODPO_ERR_UNSUPPORTED;
   k_gather_pairs<<<(unsigned)(2 * P), 128, 0, (cudaStream_t)stream>>>(
       pair_rows, n_src, T, tokens_in, mask_in, ref_in, tokens_out, mask_out, ref_out, status);
+  return launched();
+}
+
+odpo_status odpo_vp_row_partials(const void* logits_shard, odpo_dtype dt, int64_t B, int64_t T,
+                                 int64_t V_shard, int64_t stride_b, int64_t stride_t,
+                                 int64_t v0, int64_t V_total, const int32_t* tokens,
+                                 const uint8_t* mask, float inv_temperature, float* parts,
+                                 uint32_t* status, void* workspace, size_t workspace_bytes,
+                                 void* stream) {
+  odpo_status e = check_logits(logits_shard, dt, B, T, V_shard, stride_b, stride_t);
+  if (e != ODPO_OK) return e;
+  if (!tokens || !mask || !parts || !finite_pos(inv_temperature)) return ODPO_ERR_INVALID_ARG;
+  if (v0 < 0 || V_total < v0 + V_shard) return ODPO_ERR_INVALID_ARG;
+  if (((uintptr_t)parts & 15u) != 0) return ODPO_ERR_ALIGNMENT;
+  const int64_t P = B / 2 + 1;
+  if (!workspace || workspace_bytes < ws_layout(B, T, P, nullptr, nullptr)) return ODPO_ERR_WORKSPACE;
+  Workspace w;
+  ws_layout(B, T, P, (char*)workspace, &w);
+  cudaStream_t s = (cudaStream_t)stream;
+  LossArgs a;
+  base_args(a, logits_shard, B, T, V_shard, stride_b, stride_t, tokens, mask, inv_temperature,
+            status, w, dt == ODPO_F32 ? 4 : 2);
+  a.vp_parts = reinterpret_cast<float4*>(parts);
+  a.tok_off = v0;
+  a.V_total = V_total;
+  a.seqsum = 0;
+  k_prep<<<1, kPrepThreads, 0, s>>>(nullptr, B, 0, w, nullptr);
+  if ((e = launched()) != ODPO_OK) return e;
+  return launch_engine(dt == ODPO_F32 ? 0 : 1, M_SEQ, kPolyDefault, a, 0, s, -1);
+}
+
+odpo_status odpo_vp_loss_fwd_bwd(const float* parts_all, int32_t W, const void* logits_shard,
+                                 odpo_dtype dt, int64_t B, int64_t T, int64_t V_shard,
+                                 int64_t stride_b, int64_t stride_t, int64_t v0, int64_t V_total,
+                                 const float* ref_logp, const int32_t* tokens,
+                                 const uint8_t* mask, const int32_t* pair_rows, int64_t P,
+                                 int64_t P_global, float beta, float inv_temperature,
+                                 void* dlogits_shard, int64_t dstride_b, int64_t dstride_t,
+                                 float* seq_logp, float* pair_logit, double* stats,
+                                 uint32_t* status, void* workspace, size_t workspace_bytes,
+                                 void* stream) {
+  if (!parts_all || W < 1) return ODPO_ERR_INVALID_ARG;
+  if (v0 < 0 || V_total < v0 + V_shard) return ODPO_ERR_INVALID_ARG;
+  odpo_status e = check_loss(logits_shard, dt, B, T, V_shard, stride_b, stride_t, ref_logp, tokens,
+                             mask, pair_rows, P, P_global, beta, inv_temperature, dlogits_shard,
+                             dstride_b, dstride_t, seq_logp, stats, workspace, workspace_bytes);
+  if (e != ODPO_OK) return e;
+  if (((uintptr_t)parts_all & 15u) != 0) return ODPO_ERR_ALIGNMENT;
+  Workspace w;
+  ws_layout(B, T, P, (char*)workspace, &w);
+  cudaStream_t s = (cudaStream_t)stream;
+  LossArgs a;
+  base_args(a, logits_shard, B, T, V_shard, stride_b, stride_t, tokens, mask, inv_temperature,
+            status, w, dt == ODPO_F32 ? 4 : 2);
+  a.ref = ref_logp; a.pair_rows = pair_rows;
+  a.P = P; a.Pg = (double)P_global; a.beta = beta;
+  a.dl = dlogits_shard; a.dsb = dstride_b; a.dst = dstride_t;
+  a.seq_logp = seq_logp; a.z_out = pair_logit; a.stats = stats;
+  a.tok_off = v0;
+  a.V_total = V_total;
+  k_prep<<<1, kPrepThreads, 0, s>>>(pair_rows, B, P, w, status);
+  if ((e = launched()) != ODPO_OK) return e;
+  const int64_t rows = B * T;
+  k_vp_combine<<<(unsigned)((rows + 255) / 256), 256, 0, s>>>(
+      a, reinterpret_cast<const float4*>(parts_all), W);
+  if ((e = launched()) != ODPO_OK) return e;
+  k_pair_reduce<<<(unsigned)P, 32, 0, s>>>(a);
+  if ((e = launched()) != ODPO_OK) return e;
+  if (dt == ODPO_F32) k_row_bwd<0, 0><<<(unsigned)rows, kRowThreads, 0, s>>>(a);
+  else k_row_bwd<1, 0><<<(unsigned)rows, kRowThreads, 0, s>>>(a);
   return launched();
 }
 
