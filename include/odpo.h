@@ -99,12 +99,20 @@ enum {
                               adaptively (a backward row is taken as soon as its pair's
                               forward pass has completed), per-pair completion counters  */
   ODPO_SCHED_TWO_PASS = 2, /* forward kernel, pair-reduce kernel, backward kernel (2R+1W) */
-  ODPO_SCHED_WAVE = 3      /* one persistent kernel, pairs statically assigned to groups
+  ODPO_SCHED_WAVE = 3,     /* one persistent kernel, pairs statically assigned to groups
                               of 2T CTAs (one row per CTA per pair, forward then
                               backward), few enough groups that every in-flight pair
                               stays in L2 (1R+1W at HBM); needs 2T <= resident CTAs and
                               all CTAs co-resident (UNSUPPORTED otherwise).  Measured
                               slower than FUSED on B200          */
+  ODPO_SCHED_RESIDENT = 4  /* one persistent CTA per SM; each row stays ON CHIP between its
+                              forward and its backward pass (shared-memory row buffers and
+                              tensor-memory row slots), so the call moves exactly one read
+                              and one write of the logits (1R+1W).  Applies when two rows
+                              fit in shared memory (row <= 110 KB: V*elt <= 113 152 bytes),
+                              a row spans <= 8 16-KB chunks, and SMs * (buffers + TMEM
+                              slots) >= 4T; UNSUPPORTED otherwise.  Needs all CTAs
+                              co-resident (the GPU not shared with other work)          */
 };
 
 typedef struct {

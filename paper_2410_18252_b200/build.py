@@ -9,7 +9,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libodpo.so")
 SOURCES = [os.path.join(CSRC, "odpo.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, "odpo_device.cuh"), os.path.join(CSRC, "odpo_engine.cuh"),
+DEPS = SOURCES + [os.path.join(CSRC, "odpo_device.cuh"), os.path.join(CSRC, "odpo_engine.cuh"), os.path.join(CSRC, "odpo_resident.cuh"),
                   os.path.join(ROOT, "include", "odpo.h")]
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",

@@ -40,6 +40,7 @@ struct Workspace {
   unsigned* pair_ready;
   unsigned* pair_bcnt; // backward rows dispensed per pair (FUSED dispatch)
   double* pair_vals;   // [P][ODPO_NSTATS]
+  unsigned long long* seq_cf;  // [B] ready bit (bit 32) | fp32 bits of the sequence's coef
   unsigned long long* dbg_t;  // debug builds: [P][4] timestamps
   unsigned* counters;  // [0] ticket, [1] pairs done, [2] n_unref
 };
@@ -48,6 +49,7 @@ enum { C_TICKET = 0, C_PAIRS_DONE = 1, C_NUNREF = 2, C_BPAIR = 3, C_ZTICKET = 4,
        C_DBG_N = 6, C_DBG_MAX = 7, C_DBG_DONE = 8, C_COUNT = 16 };
 
 static inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+constexpr unsigned long long kCfReady = 1ull << 32;
 
 static size_t ws_layout(int64_t B, int64_t T, int64_t P, char* base, Workspace* w) {
   size_t off = 0;
@@ -68,6 +70,7 @@ static size_t ws_layout(int64_t B, int64_t T, int64_t P, char* base, Workspace* 
   char* p_pr = take((size_t)P * 4);
   char* p_pb = take((size_t)P * 4);
   char* p_pv = take((size_t)P * ODPO_NSTATS * 8);
+  char* p_cf = take((size_t)B * 8);
   char* p_ct = take(C_COUNT * 4);
 #ifdef ODPO_DEBUG_LEAD
   char* p_dt = take((size_t)P * 4 * 8);
@@ -87,6 +90,7 @@ static size_t ws_layout(int64_t B, int64_t T, int64_t P, char* base, Workspace* 
     w->pair_ready = (unsigned*)p_pr;
     w->pair_bcnt = (unsigned*)p_pb;
     w->pair_vals = (double*)p_pv;
+    w->seq_cf = (unsigned long long*)p_cf;
     w->counters = (unsigned*)p_ct;
   }
   return off;
@@ -172,6 +176,7 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep(const int32_t* __restrict
   for (int64_t b = tid; b < B; b += kPrepThreads) {
     w.seq_pair[b] = -1;
     w.seq_cnt[b] = 0;
+    w.seq_cf[b] = 0ull;
   }
   for (int64_t p = tid; p < P; p += kPrepThreads) {
     w.pair_cnt[p] = 0;
@@ -287,6 +292,18 @@ __device__ __forceinline__ void pair_seqs(const LossArgs& a, int64_t p, int64_t&
   if (r < 0 || r >= a.B) r = -1;
 }
 
+// A pair with an out-of-range member (flagged ODPO_FLAG_PAIR_RANGE by k_prep): its in-range
+// sequence gets coefficient 0 (zero dlogits) and a published ready word, so no schedule waits
+// on it or reads a stale coefficient.
+__device__ __forceinline__ void invalid_pair_coefs(const LossArgs& a, int64_t c, int64_t r) {
+  const int64_t y[2] = {c, r};
+  for (int k = 0; k < 2; ++k) {
+    if (y[k] < 0) continue;
+    a.w.seq_coef[y[k]] = 0.f;
+    st_release_u64(&a.w.seq_cf[y[k]], kCfReady);
+  }
+}
+
 // Pair reduction (K3b) by ONE warp: fixed-order sums of both sequences, then lane 0 forms z,
 // loss, sigma(-z), coef, publishes them (release) and the pair's statistics; the warp that
 // completes the LAST pair reduces all pairs' statistics in fixed order.
@@ -296,14 +313,16 @@ __device__ __noinline__ void pair_reduce_warp(const LossArgs& a, int64_t p) {
   pair_seqs(a, p, c, r);
   double Sc = 0.0, Sr = 0.0;
   int nc = 0, nr = 0;
-  if (c >= 0) seq_sum_warp(a.w.row_logp + c * a.T, a.mask + c * a.T, a.T, Sc, nc);
-  if (r >= 0) seq_sum_warp(a.w.row_logp + r * a.T, a.mask + r * a.T, a.T, Sr, nr);
+  seq_sum2_warp(c >= 0 ? a.w.row_logp + c * a.T : nullptr, c >= 0 ? a.mask + c * a.T : nullptr,
+                r >= 0 ? a.w.row_logp + r * a.T : nullptr, r >= 0 ? a.mask + r * a.T : nullptr,
+                a.T, Sc, nc, Sr, nr);
   unsigned last = 0;
   if (lane == 0 && a.pg_kind >= 0) {
     uint32_t fl = 0;
     double* pv = a.w.pair_vals + p * ODPO_NSTATS;
     if (c < 0 || r < 0) {
       for (int k = 0; k < ODPO_NSTATS; ++k) pv[k] = 0.0;
+      invalid_pair_coefs(a, c, r);
     } else {
       if (nc == 0 || nr == 0) fl |= ODPO_FLAG_EMPTY_SEQ;
       const float fS[2] = {nc ? (float)Sc : 0.f, nr ? (float)Sr : 0.f};
@@ -330,6 +349,7 @@ __device__ __noinline__ void pair_reduce_warp(const LossArgs& a, int64_t p) {
           cf = u <= v ? rt * A[k] * scale : 0.0;
           rsum += rt;
           a.w.seq_coef[y[k]] = (float)cf;   // the only kind whose coefficient needs S
+          st_release_u64(&a.w.seq_cf[y[k]], kCfReady | __float_as_uint((float)cf));
         } else if (k == 0) {               // Best-of-2 SFT on the chosen completion
           loss += -S;
           cf = 2.0 * scale;
@@ -358,6 +378,7 @@ __device__ __noinline__ void pair_reduce_warp(const LossArgs& a, int64_t p) {
     if (c < 0 || r < 0) {
       for (int k = 0; k < ODPO_NSTATS; ++k) pv[k] = 0.0;
       if (a.z_out) a.z_out[p] = 0.f;
+      invalid_pair_coefs(a, c, r);
     } else {
       if (nc == 0 || nr == 0) fl |= ODPO_FLAG_EMPTY_SEQ;
       const float fSc = nc ? (float)Sc : 0.f;
@@ -371,6 +392,9 @@ __device__ __noinline__ void pair_reduce_warp(const LossArgs& a, int64_t p) {
       const float coef = (float)((double)a.beta * sig_neg * (double)a.invT / a.Pg);
       a.w.seq_coef[c] = coef;
       a.w.seq_coef[r] = -coef;
+      // the RESIDENT schedule's parameter warps poll these (ready bit + coefficient, one load)
+      st_release_u64(&a.w.seq_cf[c], kCfReady | __float_as_uint(coef));
+      st_release_u64(&a.w.seq_cf[r], kCfReady | __float_as_uint(-coef));
       a.seq_logp[c] = fSc;
       a.seq_logp[r] = fSr;
       if (a.z_out) a.z_out[p] = z;
@@ -1263,6 +1287,10 @@ __global__ void __launch_bounds__(GE::THREADS, GE::CPS) k_engine(LossArgs a) {
   if (CS > 1) cluster_sync_all();
 }
 
+}  // namespace odpo
+#include "odpo_resident.cuh"
+namespace odpo {
+
 // ------------------------------------------------------------------ host side
 struct DevInfo {
   int sms = 0;
@@ -1333,11 +1361,35 @@ static const DevInfo& dev_info(int dev) {
     setup_geo<Geo0>(d, 0);
     setup_geo<Geo1>(d, 1);
     setup_pv<1>();
+    cudaFuncSetAttribute(k_resident<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kResSmemMax);
+    cudaFuncSetAttribute(k_resident<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kResSmemMax);
   });
   return g_dev[dev];
 }
 
 static bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+
+// RESIDENT schedule geometry (odpo_resident.cuh): shared row buffers and TMEM row slots per
+// SM.  Applicable when at least two whole rows fit in shared memory, a row spans at most 8
+// chunks, and the GPU-wide on-chip stash holds two pairs' rows (deadlock freedom needs one).
+static ResGeo res_geo(int64_t V, int64_t T, int es, int sms) {
+  ResGeo g{0, 0, 0, 0};
+  const int64_t nvec = V * es / 16;   // whole 16-byte vectors per row
+  if (nvec < 1) return g;
+  const int64_t nch = (nvec + kCV - 1) / kCV;
+  if (nch > kResMaxCh) return g;
+  const int64_t rb = (nvec * 16 + 127) / 128 * 128;
+  int64_t nb = (kResSmemMax) / rb;
+  if (nb > kResMaxNB) nb = kResMaxNB;
+  if (nb < 2) return g;
+  int64_t nsl = (kResTmemCols / kResCols) / nch;
+  if (nsl > kResMaxSL) nsl = kResMaxSL;
+  int64_t stash = nb + nsl;
+  if (stash > kResNIt) stash = kResNIt;
+  if ((int64_t)sms * stash < 2 * (2 * T)) return g;
+  g.nb = (int)nb; g.nsl = (int)nsl; g.nch = (int)nch; g.rb = (int)rb;
+  return g;
+}
 static bool finite_pos(float x) { return isfinite(x) && x > 0.f; }
 
 static odpo_status check_logits(const void* logits, odpo_dtype dt, int64_t B, int64_t T, int64_t V,
@@ -1419,6 +1471,14 @@ using namespace odpo;
 extern "C" {
 
 const char* odpo_version(void) { return ODPO_VERSION_STR; }
+
+#ifdef ODPO_RES_DEBUG
+// debug builds only (not declared in odpo.h): copy the RESIDENT per-ticket timestamps
+int odpo_res_debug_dump(unsigned long long* host, int64_t n_rows) {
+  if (n_rows > kResDbgRows) n_rows = kResDbgRows;
+  return (int)cudaMemcpyFromSymbol(host, g_res_dbg, (size_t)n_rows * 8 * sizeof(unsigned long long));
+}
+#endif
 
 const char* odpo_status_string(odpo_status s) {
   switch (s) {
@@ -1571,14 +1631,21 @@ odpo_status odpo_online_dpo_loss_fwd_bwd_ex(const void* policy_logits, odpo_dtyp
   if (e != ODPO_OK) return e;
   const int64_t es = dt == ODPO_F32 ? 4 : 2;
   int sched = opts ? opts->schedule : ODPO_SCHED_AUTO;
-  if (sched < ODPO_SCHED_AUTO || sched > ODPO_SCHED_WAVE) return ODPO_ERR_UNSUPPORTED;
+  if (sched < ODPO_SCHED_AUTO || sched > ODPO_SCHED_RESIDENT) return ODPO_ERR_UNSUPPORTED;
   const int pv = (opts && opts->exp2_split >= 0) ? opts->exp2_split : kPolyDefault;
   if (pv >= kNumPoly) return ODPO_ERR_UNSUPPORTED;
   int wave_ng = 0;
   const int wave_gap = (opts && opts->row_gap >= 0) ? (opts->row_gap > 0 ? 1 : 0) : kWaveGap;
-  // AUTO = FUSED: the wave keeps every pair in L2 (1R+1W at HBM) but its per-pair waits cost
-  // more than the re-read saves on B200
-  if (sched == ODPO_SCHED_AUTO) sched = ODPO_SCHED_FUSED;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const DevInfo& di = dev_info(dev);
+  // AUTO = RESIDENT where the rows fit on chip (1R+1W), else FUSED.  The wave keeps every pair
+  // in L2 too but its per-pair waits cost more than the re-read saves on B200 (DESIGN.md
+  // section 4)
+  const ResGeo rg = res_geo(V, T, (int)es, di.sms);
+  const bool res_ok = rg.nb > 0 && pv == 0 && (!opts || (opts->ctas_per_sm <= 0 && opts->engine < 0));
+  if (sched == ODPO_SCHED_AUTO) sched = (res_ok && kResAuto) ? ODPO_SCHED_RESIDENT : ODPO_SCHED_FUSED;
+  if (sched == ODPO_SCHED_RESIDENT && !res_ok) return ODPO_ERR_UNSUPPORTED;
   if (sched == ODPO_SCHED_WAVE) {
     wave_ng = wave_groups(T, P, V * es, opts ? opts->ctas_per_sm : 0, opts ? opts->engine : -1,
                           dt == ODPO_F32 ? 0 : 1, false, wave_gap);
@@ -1589,9 +1656,6 @@ odpo_status odpo_online_dpo_loss_fwd_bwd_ex(const void* policy_logits, odpo_dtyp
   Workspace w;
   ws_layout(B, T, P, (char*)workspace, &w);
   cudaStream_t s = (cudaStream_t)stream;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  const DevInfo& di = dev_info(dev);
 
   LossArgs a;
   base_args(a, policy_logits, B, T, V, stride_b, stride_t, tokens, mask, inv_temperature, status,
@@ -1607,7 +1671,13 @@ odpo_status odpo_online_dpo_loss_fwd_bwd_ex(const void* policy_logits, odpo_dtyp
   const int dti = dt == ODPO_F32 ? 0 : 1;
   const int geo = opts ? opts->engine : -1;
 
-  if (sched == ODPO_SCHED_TWO_PASS) {
+  if (sched == ODPO_SCHED_RESIDENT) {
+    const int smem = rg.nb * rg.rb > kResSmemMin ? rg.nb * rg.rb : kResSmemMin;
+    if (dti == 0) k_resident<0><<<di.sms, kResThreads, smem, s>>>(a, rg);
+    else k_resident<1><<<di.sms, kResThreads, smem, s>>>(a, rg);
+    if ((e = launched()) != ODPO_OK) return e;
+    launches += 1;
+  } else if (sched == ODPO_SCHED_TWO_PASS) {
     a.seqsum = 0;   // forward rows only; k_pair_reduce sums the sequences
     if ((e = launch_engine(dti, M_SEQ, pv, a, opts ? opts->ctas_per_sm : 0, s, geo)) != ODPO_OK)
       return e;

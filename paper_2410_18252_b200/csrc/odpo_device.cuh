@@ -133,6 +133,14 @@ __device__ __forceinline__ unsigned atom_add_acq_rel(unsigned* p, unsigned v) {
 __device__ __forceinline__ void fence_acq_rel_gpu() {
   asm volatile("fence.acq_rel.gpu;" ::: "memory");
 }
+__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -463,6 +471,34 @@ __device__ __forceinline__ void seq_sum_warp(const float* row_logp, const uint8_
   }
   S = s;
   n = c;
+}
+
+// Both sequences of a pair at once (the pair reduction): per sequence exactly seq_sum_warp's
+// order (lane l sums t = l, l+32, ... in order, then the same shfl_down tree), with the two
+// sequences' loads interleaved so their latencies overlap.  c < 0 / r < 0: that sum is 0.
+__device__ __forceinline__ void seq_sum2_warp(const float* lp_c, const uint8_t* mk_c,
+                                              const float* lp_r, const uint8_t* mk_r, int64_t T,
+                                              double& Sc, int& nc, double& Sr, int& nr) {
+  const int lane = threadIdx.x & 31;
+  double sc = 0.0, sr = 0.0;
+  int cc = 0, cr = 0;
+#pragma unroll 2
+  for (int64_t t = lane; t < T; t += 32) {
+    const uint8_t mc = lp_c ? __ldcg(mk_c + t) : (uint8_t)0;
+    const uint8_t mr = lp_r ? __ldcg(mk_r + t) : (uint8_t)0;
+    const float vc = lp_c ? __ldcg(lp_c + t) : 0.f;
+    const float vr = lp_r ? __ldcg(lp_r + t) : 0.f;
+    if (mc) { sc += (double)vc; ++cc; }
+    if (mr) { sr += (double)vr; ++cr; }
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    sc += __shfl_down_sync(kFull, sc, off);
+    cc += __shfl_down_sync(kFull, cc, off);
+    sr += __shfl_down_sync(kFull, sr, off);
+    cr += __shfl_down_sync(kFull, cr, off);
+  }
+  Sc = sc; nc = cc; Sr = sr; nr = cr;
 }
 
 }  // namespace odpo

@@ -60,7 +60,16 @@ struct Geo {
   static_assert(kCV % NCT == 0, "chunk must split evenly over consumers");
 };
 using Geo0 = Geo<ODPO_NCW, ODPO_STAGES, ODPO_CTAS_PER_SM>;
-using Geo1 = Geo<8, 6, 2>;
+#ifndef ODPO_G1_NCW
+#define ODPO_G1_NCW 8
+#endif
+#ifndef ODPO_G1_STAGES
+#define ODPO_G1_STAGES 6
+#endif
+#ifndef ODPO_G1_CPS
+#define ODPO_G1_CPS 2
+#endif
+using Geo1 = Geo<ODPO_G1_NCW, ODPO_G1_STAGES, ODPO_G1_CPS>;
 
 // ------------------------------------------------------------------ mbarrier / TMA PTX
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {

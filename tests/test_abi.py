@@ -56,7 +56,7 @@ def test_status_strings_and_version(lib):
 def test_workspace_bytes(lib):
     n = lib.odpo_workspace_bytes(512, 53, 256)
     rows = 512 * 53
-    assert 12 * rows <= n <= 12 * rows + 512 * 12 + 256 * 100 + 16 * 256
+    assert 12 * rows <= n <= 12 * rows + 512 * 20 + 256 * 100 + 16 * 256
     assert lib.odpo_workspace_bytes(0, 5, 1) == 0
 
 

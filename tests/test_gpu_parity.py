@@ -18,7 +18,7 @@ from gpu_helpers import (NCPU, Batch, alloc_rows, check_dlogits, check_seq, coef
 pytestmark = [pytest.mark.gpu,
               pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a CUDA device")]
 
-SCHEDS = ["fused", "two_pass", "wave"]
+SCHEDS = ["fused", "two_pass", "wave", "resident"]
 
 
 @pytest.fixture(scope="module")
@@ -31,9 +31,16 @@ def odpo():
 def run_loss(odpo, b: Batch, ref, beta, sched="fused", Pg=None, **kw):
     if not kw.get("inplace"):
         kw.setdefault("dlogits", b.new_out())
-    out = odpo.online_dpo_loss_fwd_bwd(b.d_logits, ref, b.d_tokens, b.d_mask, beta,
-                                       pair_rows=b.d_pair_rows, p_global=Pg,
-                                       inv_temperature=b.invT, schedule=sched, **kw)
+    try:
+        out = odpo.online_dpo_loss_fwd_bwd(b.d_logits, ref, b.d_tokens, b.d_mask, beta,
+                                           pair_rows=b.d_pair_rows, p_global=Pg,
+                                           inv_temperature=b.invT, schedule=sched, **kw)
+    except odpo.OdpoError as e:
+        # the RESIDENT schedule applies only where two rows fit in shared memory and the
+        # on-chip stash holds two pairs (odpo.h); elsewhere the library refuses it
+        if sched == "resident" and "unsupported" in str(e):
+            pytest.skip(f"resident schedule does not apply: {e}")
+        raise
     torch.cuda.synchronize()
     return out
 
@@ -116,10 +123,16 @@ def test_identity_rows_bit_exact(odpo, dtype, permute, sched, shape):
     d_x.copy_(torch.from_numpy(x.astype(np.float32)).cuda().to(tdt))
     h_x = x.astype(np.float32) if dtype == "f32" else oracle.to_bf16_bits(x)
     beta = 0.125
-    out = odpo.online_dpo_loss_fwd_bwd(
-        d_x, torch.from_numpy(ref).cuda(), torch.from_numpy(tok).cuda(), torch.from_numpy(mask).cuda(),
-        beta, pair_rows=None if pr is None else torch.from_numpy(pr).cuda(), schedule=sched,
-        dlogits=alloc_rows(B, T, V, dtype))
+    try:
+        out = odpo.online_dpo_loss_fwd_bwd(
+            d_x, torch.from_numpy(ref).cuda(), torch.from_numpy(tok).cuda(),
+            torch.from_numpy(mask).cuda(), beta,
+            pair_rows=None if pr is None else torch.from_numpy(pr).cuda(), schedule=sched,
+            dlogits=alloc_rows(B, T, V, dtype))
+    except odpo.OdpoError as e:
+        if sched == "resident" and "unsupported" in str(e):
+            pytest.skip(f"resident schedule does not apply: {e}")
+        raise
     torch.cuda.synchronize()
     o = oracle.online_dpo_loss_fwd_bwd(h_x, ref, tok, mask, beta, pair_rows=pr, n_threads=NCPU)
     # per-sequence log-probs and z are exact (1/8-grid arithmetic)
@@ -280,6 +293,16 @@ def test_full_size_sampled_parity(odpo, name, mask_kind, nsample):
     assert torch.equal(auto.seq_logp, out.seq_logp) and torch.equal(auto.stats[:10], out.stats[:10])
     assert torch.equal(auto.dlogits, out.dlogits)
     del auto
+    # the RESIDENT schedule (rows kept on chip; AUTO for the Pythia shape): same parity bar
+    outs = {"fused": out}
+    try:
+        outs["resident"] = odpo.online_dpo_loss_fwd_bwd(
+            b.d_logits, ref, b.d_tokens, b.d_mask, w.beta, pair_rows=b.d_pair_rows,
+            schedule="resident", dlogits=b.new_out())
+        torch.cuda.synchronize()
+        assert int(outs["resident"].status.item()) == int(out.status.item())
+    except odpo.OdpoError as e:
+        assert "unsupported" in str(e) and name != "pythia"
     pairs = synth.permutation(1, w.P)[:nsample]
     seqs = np.stack([2 * pairs, 2 * pairs + 1], 1).reshape(-1)
     h_x = b.host_rows(seqs)
@@ -291,13 +314,15 @@ def test_full_size_sampled_parity(odpo, name, mask_kind, nsample):
     take = rows.reshape(len(seqs), w.T)[:, :3].reshape(-1)
     o = oracle.online_dpo_loss_fwd_bwd(h_x, h_ref, sub_tok, sub_mask, w.beta, p_global=w.P,
                                        dl_rows=take, n_threads=NCPU)
-    check_seq(out.seq_logp.cpu().numpy()[seqs], o["seq_logp"], w.dtype)
-    zg = out.z.cpu().numpy()[pairs].astype(np.float64)
-    assert np.all(np.abs(zg - o["z"]) <= 2e-3 * np.maximum(np.abs(o["z"]), 1.0))
-    gi = torch.from_numpy(seqs).cuda()
-    g = to_f64(out.dlogits[gi][:, :3].reshape(-1, w.V))
-    coef = np.repeat(coef_from_oracle(o, nsample, w.P, w.beta, 1.0, None, len(seqs)), 3)
-    check_dlogits(g, o["dlogits"], coef[:, None], w.dtype)
+    for out in outs.values():
+        check_seq(out.seq_logp.cpu().numpy()[seqs], o["seq_logp"], w.dtype)
+        zg = out.z.cpu().numpy()[pairs].astype(np.float64)
+        assert np.all(np.abs(zg - o["z"]) <= 2e-3 * np.maximum(np.abs(o["z"]), 1.0))
+        gi = torch.from_numpy(seqs).cuda()
+        g = to_f64(out.dlogits[gi][:, :3].reshape(-1, w.V))
+        coef = np.repeat(coef_from_oracle(o, nsample, w.P, w.beta, 1.0, None, len(seqs)), 3)
+        check_dlogits(g, o["dlogits"], coef[:, None], w.dtype)
+    del outs
     # global stats: properties of the GPU's own per-pair outputs (any size)
     z_all = out.z.cpu().double().numpy()
     st = out.stats.cpu().numpy()
