@@ -1353,6 +1353,23 @@ static void setup_geo(DevInfo& d, int g) {
   setup_one<1, M_UNSC, 0, GE>(&d.occ[g][1][M_UNSC]);
 }
 
+template <int PV>
+static void setup_res() {
+  cudaFuncSetAttribute(k_resident<1, PV>, cudaFuncAttributeMaxDynamicSharedMemorySize, kResSmemMax);
+  if constexpr (PV == 0)
+    cudaFuncSetAttribute(k_resident<0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kResSmemMax);
+  if constexpr (PV + 1 < kNumPoly) setup_res<PV + 1>();
+}
+template <int PV>
+static void launch_res_bf16(int pv, int grid, int smem, const LossArgs& a, const ResGeo& g,
+                            cudaStream_t s) {
+  if (pv == PV) {
+    k_resident<1, PV><<<grid, kResThreads, smem, s>>>(a, g);
+    return;
+  }
+  if constexpr (PV + 1 < kNumPoly) launch_res_bf16<PV + 1>(pv, grid, smem, a, g, s);
+}
+
 static const DevInfo& dev_info(int dev) {
   std::call_once(g_once[dev], [dev]() {
     DevInfo& d = g_dev[dev];
@@ -1361,35 +1378,32 @@ static const DevInfo& dev_info(int dev) {
     setup_geo<Geo0>(d, 0);
     setup_geo<Geo1>(d, 1);
     setup_pv<1>();
-    cudaFuncSetAttribute(k_resident<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kResSmemMax);
-    cudaFuncSetAttribute(k_resident<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kResSmemMax);
+    setup_res<0>();
   });
   return g_dev[dev];
 }
 
 static bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
 
-// RESIDENT schedule geometry (odpo_resident.cuh): shared row buffers and TMEM row slots per
-// SM.  Applicable when at least two whole rows fit in shared memory, a row spans at most 8
-// chunks, and the GPU-wide on-chip stash holds two pairs' rows (deadlock freedom needs one).
-static ResGeo res_geo(int64_t V, int64_t T, int es, int sms) {
-  ResGeo g{0, 0, 0, 0};
+// RESIDENT schedule geometry (odpo_resident.cuh): TMEM row slots per SM, forward/backward TMA
+// rings, and the L2-backed rows each SM may hold beyond its TMEM stash (cap).  Applicable
+// when a row spans at most 8 16-KB chunks (two TMEM slots) and the rows in flight GPU-wide,
+// SMs * (slots + cap), cover two pairs (one is the deadlock-freedom bound).
+static ResGeo res_geo(int64_t V, int64_t T, int es, int sms, int cap) {
+  ResGeo g{0, 0, 0, 0, 0};
   const int64_t nvec = V * es / 16;   // whole 16-byte vectors per row
   if (nvec < 1) return g;
   const int64_t nch = (nvec + kCV - 1) / kCV;
   if (nch > kResMaxCh) return g;
-  const int64_t rb = (nvec * 16 + 127) / 128 * 128;
-  int64_t nb = (kResSmemMax) / rb;
-  if (nb > kResMaxNB) nb = kResMaxNB;
-  if (nb < 2) return g;
   int64_t nsl = (kResTmemCols / kResCols) / nch;
   if (nsl > kResMaxSL) nsl = kResMaxSL;
-  int64_t stash = nb + nsl;
-  if (stash > kResNIt) stash = kResNIt;
-  if ((int64_t)sms * stash < 2 * (2 * T)) return g;
-  g.nb = (int)nb; g.nsl = (int)nsl; g.nch = (int)nch; g.rb = (int)rb;
+  if (cap < 0) cap = kResCapDefault;
+  if (nsl + cap > kResNIt) cap = kResNIt - (int)nsl;
+  if ((int64_t)sms * (nsl + cap) < 2 * (2 * T)) return g;
+  g.nsl = (int)nsl; g.nch = (int)nch; g.rf = kResRF; g.rbs = kResRB; g.cap = cap;
   return g;
 }
+
 static bool finite_pos(float x) { return isfinite(x) && x > 0.f; }
 
 static odpo_status check_logits(const void* logits, odpo_dtype dt, int64_t B, int64_t T, int64_t V,
@@ -1642,8 +1656,8 @@ odpo_status odpo_online_dpo_loss_fwd_bwd_ex(const void* policy_logits, odpo_dtyp
   // AUTO = RESIDENT where the rows fit on chip (1R+1W), else FUSED.  The wave keeps every pair
   // in L2 too but its per-pair waits cost more than the re-read saves on B200 (DESIGN.md
   // section 4)
-  const ResGeo rg = res_geo(V, T, (int)es, di.sms);
-  const bool res_ok = rg.nb > 0 && pv == 0 && (!opts || (opts->ctas_per_sm <= 0 && opts->engine < 0));
+  const ResGeo rg = res_geo(V, T, (int)es, di.sms, opts ? opts->lookahead : -1);
+  const bool res_ok = rg.nsl > 0 && (!opts || (opts->ctas_per_sm <= 0 && opts->engine < 0));
   if (sched == ODPO_SCHED_AUTO) sched = (res_ok && kResAuto) ? ODPO_SCHED_RESIDENT : ODPO_SCHED_FUSED;
   if (sched == ODPO_SCHED_RESIDENT && !res_ok) return ODPO_ERR_UNSUPPORTED;
   if (sched == ODPO_SCHED_WAVE) {
@@ -1672,9 +1686,10 @@ odpo_status odpo_online_dpo_loss_fwd_bwd_ex(const void* policy_logits, odpo_dtyp
   const int geo = opts ? opts->engine : -1;
 
   if (sched == ODPO_SCHED_RESIDENT) {
-    const int smem = rg.nb * rg.rb > kResSmemMin ? rg.nb * rg.rb : kResSmemMin;
-    if (dti == 0) k_resident<0><<<di.sms, kResThreads, smem, s>>>(a, rg);
-    else k_resident<1><<<di.sms, kResThreads, smem, s>>>(a, rg);
+    const int ring_bytes = (rg.rf + rg.rbs) * kChunk;
+    const int smem = ring_bytes > kResSmemMin ? ring_bytes : kResSmemMin;
+    if (dti == 0) k_resident<0, 0><<<di.sms, kResThreads, smem, s>>>(a, rg);
+    else launch_res_bf16<0>(pv, di.sms, smem, a, rg, s);
     if ((e = launched()) != ODPO_OK) return e;
     launches += 1;
   } else if (sched == ODPO_SCHED_TWO_PASS) {

@@ -46,10 +46,30 @@ constexpr int kResFT = kResFW * 32;            // forward threads (128)
 constexpr int kResUB = kCV / kResFT;           // vectors per forward thread per chunk (8)
 constexpr int kResCols = 32;                   // TMEM columns per lane per chunk (8 vectors)
 constexpr int kResFG = kResFW / 4;             // forward warps per TMEM lane quadrant
-constexpr int kResMaxNB = 4;                   // shared row buffers (max)
+constexpr int kResMaxRing = 13;                // forward / backward ring stages (max each)
+// ring split of the 13 16-KB stages that fit: the forward ring sets the bytes in flight per SM
+// (HBM latency x bandwidth share), the backward ring re-streams L2-backed rows
+#ifndef ODPO_RES_RF
+#define ODPO_RES_RF 10
+#endif
+#ifndef ODPO_RES_RB
+#define ODPO_RES_RB 3
+#endif
+constexpr int kResRF = ODPO_RES_RF, kResRB = ODPO_RES_RB;
+static_assert(kResRF + kResRB <= 13 && kResRB >= 1 && kResRF >= 1, "13 x 16 KB stages fit");
 constexpr int kResMaxSL = 4;                   // TMEM row slots (max)
 constexpr int kResMaxCh = 8;                   // 16 KB chunks per row (max: 128 KB rows)
 constexpr int kResNIt = 8;                     // item (row descriptor) ring
+#ifndef ODPO_RES_CAP
+#define ODPO_RES_CAP 2
+#endif
+constexpr int kResCapDefault = ODPO_RES_CAP;   // L2-backed rows in flight per CTA (default)
+// live rows claimed but not yet through the forward warps (bounds the per-SM forward queue,
+// whose tail latency decides when a pair completes)
+#ifndef ODPO_RES_FQ
+#define ODPO_RES_FQ 8
+#endif
+constexpr int kResFQ = ODPO_RES_FQ;
 constexpr int kResTmemCols = 512;
 // dynamic shared memory: row buffers (at most this much); every launch asks for at least
 // kResSmemMin so that exactly one CTA (one 512-column TMEM allocation) fits per SM
@@ -69,9 +89,7 @@ enum { R_END = 0, R_LIVE = 1, R_MASK = 2, R_NONE = 3, R_ZERO = 4 };
 struct ResItem {
   int32_t kind;
   int32_t tok;
-  int32_t buf;    // shared buffer (R_LIVE)
-  int32_t tslot;  // TMEM slot, -1 = stays in the shared buffer
-  uint32_t bph;   // parity of this use of the buffer's chunk barriers
+  int32_t tslot;  // TMEM slot, -1 = L2-backed row (the backward re-streams it)
   int32_t pad_;
   int64_t p, s, g, tk;
   const char* row;
@@ -82,8 +100,9 @@ struct ResItem {
 };
 
 struct ResGeo {
-  int nb, nsl, nch;  // shared buffers, TMEM slots, chunks per row
-  int rb;            // bytes per shared buffer (row vectors, 128-aligned)
+  int nsl, nch;  // TMEM row slots, 16 KB chunks per row
+  int rf, rbs;   // forward / backward TMA ring stages (16 KB each)
+  int cap;       // L2-backed rows in flight per CTA (rows beyond the TMEM stash)
 };
 
 #ifdef ODPO_RES_DEBUG
@@ -172,12 +191,16 @@ __device__ __forceinline__ void tm_ld16(uint32_t taddr, uint4 (&v)[4]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-template <int DT>
+template <int DT, int PV>
 __global__ void __launch_bounds__(kResThreads, 1) k_resident(LossArgs a, ResGeo G) {
   constexpr int N = Traits<DT>::N;
-  extern __shared__ __align__(128) uint8_t rbuf[];
-  __shared__ __align__(8) uint64_t full[kResMaxNB][kResMaxCh];
-  __shared__ __align__(8) uint64_t buf_free[kResMaxNB];
+  constexpr int NPF = DT == 1 ? kPoly[PV].npf : 0;  // exp2 split
+  constexpr int NPB = DT == 1 ? kPoly[PV].npb : 0;
+  extern __shared__ __align__(128) uint8_t rbuf[];  // [rf] forward stages, [rbs] backward stages
+  __shared__ __align__(8) uint64_t f_full[kResMaxRing];
+  __shared__ __align__(8) uint64_t f_empty[kResMaxRing];
+  __shared__ __align__(8) uint64_t b_full[kResMaxRing];
+  __shared__ __align__(8) uint64_t b_empty[kResMaxRing];
   __shared__ __align__(8) uint64_t tm_free[kResMaxSL];
   __shared__ __align__(8) uint64_t it_full[kResNIt];
   __shared__ __align__(8) uint64_t it_empty[kResNIt];
@@ -185,11 +208,15 @@ __global__ void __launch_bounds__(kResThreads, 1) k_resident(LossArgs a, ResGeo 
   __shared__ __align__(8) uint64_t param_ready[kResNIt];
   __shared__ __align__(16) ResItem items[kResNIt];
   __shared__ uint32_t tm_base_sh;
+  __shared__ int l2_out;  // L2-backed rows claimed and not yet through their backward
+  __shared__ int f_q;     // live rows claimed and not yet through the forward warps
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
-    for (int b = 0; b < kResMaxNB; ++b) {
-      for (int c = 0; c < kResMaxCh; ++c) mbar_init(&full[b][c], 1);
-      mbar_init(&buf_free[b], 1);  // one arrival: forward thread 0 (TMEM row) or backward thread 0
+    for (int q = 0; q < kResMaxRing; ++q) {
+      mbar_init(&f_full[q], 1);
+      mbar_init(&f_empty[q], kResFW);
+      mbar_init(&b_full[q], 1);
+      mbar_init(&b_empty[q], kResBW);
     }
     for (int j = 0; j < kResMaxSL; ++j) mbar_init(&tm_free[j], 1);
     for (int i = 0; i < kResNIt; ++i) {
@@ -198,6 +225,8 @@ __global__ void __launch_bounds__(kResThreads, 1) k_resident(LossArgs a, ResGeo 
       mbar_init(&part_ready[i], kResFW);
       mbar_init(&param_ready[i], 1);
     }
+    l2_out = 0;
+    f_q = 0;
     mbar_fence_init();
   }
   if (warp == kResProd) {
@@ -212,8 +241,11 @@ __global__ void __launch_bounds__(kResThreads, 1) k_resident(LossArgs a, ResGeo 
   tm_fence_after();
   const uint32_t tm_base = tm_base_sh;
 
-  const uint32_t rbuf_s = smem_u32(rbuf);
-  const uint32_t full_s = smem_u32(full), bfree_s = smem_u32(buf_free), tfree_s = smem_u32(tm_free);
+  const uint32_t fring_s = smem_u32(rbuf);
+  const uint32_t bring_s = fring_s + (uint32_t)(G.rf * kChunk);
+  const uint32_t ffull_s = smem_u32(f_full), fempty_s = smem_u32(f_empty);
+  const uint32_t bfull_s = smem_u32(b_full), bempty_s = smem_u32(b_empty);
+  const uint32_t tfree_s = smem_u32(tm_free);
   const uint32_t itf_s = smem_u32(it_full), ite_s = smem_u32(it_empty);
   const uint32_t pready_s = smem_u32(part_ready), mready_s = smem_u32(param_ready);
   const int64_t T = a.T;
@@ -226,31 +258,34 @@ __global__ void __launch_bounds__(kResThreads, 1) k_resident(LossArgs a, ResGeo 
 
   if (warp == kResProd) {
     if (lane == 0) {
-      // ================= producer: a free shared buffer first, then a ticket (pair order) ->
-      // item; TMA of a live row into the buffer; a TMEM slot if one is free right now
-      const uint64_t pol = policy_evict_first();
+      // ================= producer: a row store first (a free TMEM slot, else an L2 allowance),
+      // then a ticket (pair order) -> item; the live row's chunks into the forward ring
+      const uint64_t pol_drop = policy_evict_first();  // TMEM rows: read once
+      const uint64_t pol_keep = policy_evict_last();   // L2 rows: read again by the backward
       const int64_t totalF = a.P * 2 * T;
       const int64_t total = totalF + (int64_t)__ldcg(&a.w.counters[C_NUNREF]) * T;
-      uint32_t busy_b = 0, busy_t = 0, ub = 0, ut = 0;  // busy masks; per-resource use parities
+      uint32_t busy_t = 0, ut = 0;  // TMEM slot busy mask, per-slot use parities
+      int fst = 0;
+      uint32_t fph = 0;
       for (int64_t k = 0;; ++k) {
         const int it = (int)(k % kResNIt);
         mbar_wait(ite_s + 8 * it, (uint32_t)((k / kResNIt) & 1) ^ 1u);
-        int buf = -1;
+        int ts = -1;
         for (;;) {
-          for (int b = 0; b < G.nb; ++b) {
-            if (((busy_b >> b) & 1u) && mbar_test(bfree_s + 8 * b, (ub >> b) & 1u)) {
-              busy_b &= ~(1u << b);
-              ub ^= 1u << b;
+          for (int j = 0; j < G.nsl; ++j) {
+            if (((busy_t >> j) & 1u) && mbar_test(tfree_s + 8 * j, (ut >> j) & 1u)) {
+              busy_t &= ~(1u << j);
+              ut ^= 1u << j;
             }
-            if (buf < 0 && !((busy_b >> b) & 1u)) buf = b;
+            if (ts < 0 && !((busy_t >> j) & 1u)) ts = j;
           }
-          if (buf >= 0) break;
+          if ((ts >= 0 || *((volatile int*)&l2_out) < G.cap) && *((volatile int*)&f_q) < kResFQ)
+            break;
           __nanosleep(32);
         }
         const int64_t tk = (int64_t)atomicAdd(&a.w.counters[C_TICKET], 1u);
         ResItem& I = items[it];
         I.tslot = -1;
-        I.buf = -1;
         I.tok = 0;
         I.p = 0;
         I.s = -1;
@@ -292,35 +327,37 @@ __global__ void __launch_bounds__(kResThreads, 1) k_resident(LossArgs a, ResGeo 
           I.drow = drow_ptr(a, s, t);
         }
         if (I.kind == R_LIVE) {
-          I.buf = buf;
-          I.bph = (ub >> buf) & 1u;
-          busy_b |= 1u << buf;
-          for (int j = 0; j < G.nsl; ++j) {
-            if (((busy_t >> j) & 1u) && mbar_test(tfree_s + 8 * j, (ut >> j) & 1u)) {
-              busy_t &= ~(1u << j);
-              ut ^= 1u << j;
-            }
-            if (I.tslot < 0 && !((busy_t >> j) & 1u)) I.tslot = j;
+          if (ts >= 0) {
+            I.tslot = ts;
+            busy_t |= 1u << ts;
+          } else {
+            atomicAdd(&l2_out, 1);
           }
-          if (I.tslot >= 0) busy_t |= 1u << I.tslot;
-          const char* src = I.row;
-          for (int c = 0; c < nch; ++c) {
-            const int nv = min(kCV, nvec - c * kCV);
-            const uint32_t bytes = (uint32_t)nv * 16u;
-            const uint32_t bar = full_s + 8 * (buf * kResMaxCh + c);
-            mbar_arrive_tx(bar, bytes);
-            tma_load_1d(rbuf_s + (uint32_t)(buf * G.rb + c * kChunk), src + (size_t)c * kChunk,
-                        bytes, bar, pol);
-          }
+          atomicAdd(&f_q, 1);
         }
         mbar_arrive(itf_s + 8 * it);
+        if (I.kind == R_LIVE) {
+          const char* src = I.row;
+          const uint64_t pol = ts >= 0 ? pol_drop : pol_keep;
+          for (int c = 0; c < nch; ++c) {
+            mbar_wait(fempty_s + 8 * fst, fph ^ 1u);
+            const int nv = min(kCV, nvec - c * kCV);
+            const uint32_t bytes = (uint32_t)nv * 16u;
+            mbar_arrive_tx(ffull_s + 8 * fst, bytes);
+            tma_load_1d(fring_s + (uint32_t)(fst * kChunk), src + (size_t)c * kChunk, bytes,
+                        ffull_s + 8 * fst, pol);
+            if (++fst == G.rf) { fst = 0; fph ^= 1u; }
+          }
+        }
       }
     }
   } else if (warp < kResFW) {
-    // ================= forward warps: (m, r) over the row out of the shared buffer, exactly
+    // ================= forward warps: (m, r) over the row out of the forward ring, exactly
     // the engine's geometry-0 consumer arithmetic; the same registers go to the TMEM slot
     const uint32_t lane_base = (uint32_t)(32 * (warp & 3)) << 16;
     const uint32_t gcol = (uint32_t)((warp >> 2) * kResUB * 4);  // this warp's column group
+    int fst = 0;
+    uint32_t fph = 0;
     for (int64_t k = 0;; ++k) {
       const int it = (int)(k % kResNIt);
       const uint32_t ph = (uint32_t)((k / kResNIt) & 1);
@@ -329,43 +366,45 @@ __global__ void __launch_bounds__(kResThreads, 1) k_resident(LossArgs a, ResGeo 
       const int kind = I.kind;
       if (kind == R_END) break;
       if (kind == R_LIVE) {
-        const int buf = I.buf, ts = I.tslot, tok = I.tok;
-        const uint32_t bph = I.bph;
+        const int ts = I.tslot, tok = I.tok;
         const int tvec = (tok >= 0 && tok < nvec * N) ? tok / N : -1;
-        const uint4* sb = reinterpret_cast<const uint4*>(rbuf + (size_t)buf * G.rb);
         const uint32_t tcol = tm_base + lane_base + (uint32_t)(ts * scols) + gcol;
         if (ts >= 0) tm_fence_after();
         MR s{-INFINITY, 0.f};
         for (int c = 0; c < nch; ++c) {
-          mbar_wait(full_s + 8 * (buf * kResMaxCh + c), bph);
+          mbar_wait(ffull_s + 8 * fst, fph);
           if (tid == 0 && c == 0) RES_DBG(I.tk, 1);
           if (tid == 0 && c == nch - 1) RES_DBG(I.tk, 2);
+          const uint4* sb = reinterpret_cast<const uint4*>(rbuf + (size_t)fst * kChunk);
           const int c0 = c * kCV;
           const int cnv = min(kCV, nvec - c0);
           uint4 v[kResUB];
           if (cnv == kCV) {
 #pragma unroll
-            for (int u = 0; u < kResUB; ++u) v[u] = sb[c0 + tid + u * kResFT];
+            for (int u = 0; u < kResUB; ++u) v[u] = sb[tid + u * kResFT];
             if (ts >= 0) tm_st<kResUB>(tcol + (uint32_t)(c * kResCols), v);
-            mr_batch<DT, kResUB, 0>(v, k2, s.m, s.r);
+            mr_batch<DT, kResUB, NPF>(v, k2, s.m, s.r);
           } else {
             const uint32_t NI = Traits<DT>::kNegInfWord;
 #pragma unroll
             for (int u = 0; u < kResUB; ++u) {
               const int i = tid + u * kResFT;
-              v[u] = i < cnv ? sb[c0 + i] : make_uint4(NI, NI, NI, NI);
+              v[u] = i < cnv ? sb[i] : make_uint4(NI, NI, NI, NI);
             }
             if (ts >= 0) tm_st<kResUB>(tcol + (uint32_t)(c * kResCols), v);
-            if (tid < cnv) mr_batch<DT, kResUB, 0>(v, k2, s.m, s.r);
+            if (tid < cnv) mr_batch<DT, kResUB, NPF>(v, k2, s.m, s.r);
           }
           if (tvec >= c0 && tvec < c0 + cnv && ((tvec - c0) % kResFT) == tid) {
             float f[N];
-            Traits<DT>::unpack(sb[tvec], f);
+            Traits<DT>::unpack(sb[tvec - c0], f);
             float x = f[0];
 #pragma unroll
             for (int j = 1; j < N; ++j) x = (tok % N == j) ? f[j] : x;
             I.xtok = x;
           }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(fempty_s + 8 * fst);
+          if (++fst == G.rf) { fst = 0; fph ^= 1u; }
         }
         if (tid < tail) {
           const int64_t vv = (int64_t)nvec * N + tid;
@@ -383,12 +422,7 @@ __global__ void __launch_bounds__(kResThreads, 1) k_resident(LossArgs a, ResGeo 
           I.pm[warp] = wv.m;
           I.pr[warp] = wv.r;
           mbar_arrive(pready_s + 8 * it);
-        }
-        // the row is in TMEM: its shared buffer goes back to the producer once all four
-        // forward warps are past it (named barrier 2 over the forward warps)
-        if (ts >= 0) {
-          asm volatile("bar.sync 2, %0;" ::"n"(kResFT) : "memory");
-          if (tid == 0) mbar_arrive(bfree_s + 8 * buf);
+          if (warp == 0) atomicSub(&f_q, 1);
         }
       } else {
         __syncwarp();
@@ -396,15 +430,19 @@ __global__ void __launch_bounds__(kResThreads, 1) k_resident(LossArgs a, ResGeo 
       }
     }
   } else if (warp < kResProd) {
-    // ================= backward warps: dlogits = coef (softmax - onehot) from TMEM or the
-    // shared buffer; warp 4 + j (8 + j) handles vectors u = 0..3 (4..7) of forward warp j's
-    // threads -- the columns that forward warp wrote into lane quadrant j
+    // ================= backward warps: dlogits = coef (softmax - onehot) from TMEM, or, for an
+    // L2-backed row, re-streamed through the backward ring (TMA issued by backward thread 0);
+    // warp 4 + j (8 + j) handles vectors u = 0..3 (4..7) of forward warp j's threads -- the
+    // columns that forward warp wrote into lane quadrant j
     const int j = (warp - kResFW) & 3, half = (warp - kResFW) >> 2;
     // the forward thread whose TMEM lane / columns this thread reads, and its first vector
     const int ftid = kResFW == 4 ? j * 32 + lane : (warp - kResFW) * 32 + lane;
     const int u0 = kResFW == 4 ? 4 * half : 0;
     const uint32_t lane_base = (uint32_t)(32 * j) << 16;
-    const int btid = tid - kResFT;  // 0..255 (zero rows, tail)
+    const int btid = tid - kResFT;  // 0..255 (zero rows, tail, TMA issue)
+    const uint64_t pol_drop = policy_evict_first();
+    int bst = 0, ist = 0;  // backward ring: next stage to consume / to fill
+    uint32_t bph = 0, iph = 0;
     for (int64_t k = 0;; ++k) {
       const int it = (int)(k % kResNIt);
       const uint32_t ph = (uint32_t)((k / kResNIt) & 1);
@@ -414,14 +452,25 @@ __global__ void __launch_bounds__(kResThreads, 1) k_resident(LossArgs a, ResGeo 
       if (kind == R_END) break;
       uint4* vout = reinterpret_cast<uint4*>(I.drow);
       if (kind == R_LIVE) {
+        const int ts = I.tslot, tok = I.tok;
+        // an L2 row: start re-streaming it before waiting for the coefficient
+        auto issue = [&](int c) {
+          mbar_wait(bempty_s + 8 * ist, iph ^ 1u);
+          const int nv = min(kCV, nvec - c * kCV);
+          const uint32_t bytes = (uint32_t)nv * 16u;
+          mbar_arrive_tx(bfull_s + 8 * ist, bytes);
+          tma_load_1d(bring_s + (uint32_t)(ist * kChunk), I.row + (size_t)c * kChunk, bytes,
+                      bfull_s + 8 * ist, pol_drop);
+          if (++ist == G.rbs) { ist = 0; iph ^= 1u; }
+        };
+        const int ahead = ts < 0 ? min(nch, G.rbs) : 0;
+        if (btid == 0)
+          for (int c = 0; c < ahead; ++c) issue(c);
         mbar_wait(mready_s + 8 * it, ph);
         if (btid == 0) RES_DBG(I.tk, 5);
-        const int buf = I.buf, ts = I.tslot, tok = I.tok;
-        const uint32_t bph = I.bph;
         const float bc = I.c, coef = I.coef, gtok = I.gtok;
         const bool neg = coef < 0.f;
         const int tvec = (tok >= 0 && tok < nvec * N) ? tok / N : -1;
-        const uint4* sb = reinterpret_cast<const uint4*>(rbuf + (size_t)buf * G.rb);
         const uint32_t tcol = tm_base + lane_base + (uint32_t)(ts * scols + half * (kResCols / 2));
         static_assert(kResBW == 8, "8 backward warps: two 16-column halves per lane quadrant");
         if (ts >= 0) tm_fence_after();
@@ -441,19 +490,24 @@ __global__ void __launch_bounds__(kResThreads, 1) k_resident(LossArgs a, ResGeo 
             const int c0 = cc * kCV;
             const int cnv = min(kCV, nvec - c0);
             if (ts < 0) {
-              mbar_wait(full_s + 8 * (buf * kResMaxCh + cc), bph);  // visibility of the TMA bytes
+              mbar_wait(bfull_s + 8 * bst, bph);
+              const uint4* sb = reinterpret_cast<const uint4*>(rbuf + (size_t)(G.rf + bst) * kChunk);
 #pragma unroll
               for (int u = 0; u < 4; ++u) {
                 const int i = ftid + (u0 + u) * kResFT;
-                v[q][u] = i < cnv ? sb[c0 + i] : make_uint4(0, 0, 0, 0);
+                v[q][u] = i < cnv ? sb[i] : make_uint4(0, 0, 0, 0);
               }
+              __syncwarp();
+              if (lane == 0) mbar_arrive(bempty_s + 8 * bst);
+              if (++bst == G.rbs) { bst = 0; bph ^= 1u; }
+              if (btid == 0 && cc + G.rbs < nch) issue(cc + G.rbs);
             }
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
               const int i = ftid + (u0 + u) * kResFT;
               if (i < cnv)
-                st16_stream(vout + c0 + i, neg ? bwd_vec<DT, 0, true>(v[q][u], k2, bc)
-                                               : bwd_vec<DT, 0, false>(v[q][u], k2, bc));
+                st16_stream(vout + c0 + i, neg ? bwd_vec<DT, NPB, true>(v[q][u], k2, bc)
+                                               : bwd_vec<DT, NPB, false>(v[q][u], k2, bc));
             }
             // onehot entry: the thread that stored tok's vector overwrites it (program order)
             if (tvec >= c0 && tvec < c0 + cnv && ((tvec - c0) % kResFT) == ftid &&
@@ -467,10 +521,11 @@ __global__ void __launch_bounds__(kResThreads, 1) k_resident(LossArgs a, ResGeo 
           Traits<DT>::store1(I.drow, vv, vv == tok ? gtok : copysignf(ex2(fmaf(x, k2, -bc)), coef));
         }
         if (ts >= 0) tm_fence_before();
-        // all eight backward warps are past the row: release its TMEM slot / shared buffer
+        // all eight backward warps are past the row: release its TMEM slot / L2 allowance
         asm volatile("bar.sync 3, %0;" ::"n"(kResBW * 32) : "memory");
         if (btid == 0) {
-          mbar_arrive(ts >= 0 ? tfree_s + 8 * ts : bfree_s + 8 * buf);
+          if (ts >= 0) mbar_arrive(tfree_s + 8 * ts);
+          else atomicSub(&l2_out, 1);
           RES_DBG(I.tk, 6);
         }
       } else if (kind == R_MASK || kind == R_ZERO) {

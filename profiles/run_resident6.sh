@@ -1,0 +1,11 @@
+# RESIDENT: forward/backward ring split x L2 cap
+mkdir -p gpurun_out; : > gpurun_out/res_ring.log
+line() { python -c "
+import json,sys
+l=sys.stdin.read()
+try:
+  d=json.loads(l.strip().splitlines()[-1]); print('$1', '| loss_ms %.3f | frac %.3f | status %s' % (d['roofline']['loss_ms_mean'], d['roofline']['frac'], d['status']))
+except Exception as e: print('$1 FAILED', l[-300:])
+" >> gpurun_out/res_ring.log; }
+for cap in 1 2 3 4; do timeout 120 python bench.py --steps 10 --warmup 3 --no-cpu --no-e2e --no-aux --schedule resident --lookahead $cap 2>&1 | line "ring10_3 cap$cap"; done
+for v in 12_1 11_2 9_4 7_6; do for cap in 1 2 3 4; do ODPO_LIB=build_variants/libodpo_ring$v.so timeout 120 python bench.py --steps 10 --warmup 3 --no-cpu --no-e2e --no-aux --schedule resident --lookahead $cap 2>&1 | line "ring$v cap$cap"; done; done
