@@ -105,14 +105,16 @@ enum {
                               stays in L2 (1R+1W at HBM); needs 2T <= resident CTAs and
                               all CTAs co-resident (UNSUPPORTED otherwise).  Measured
                               slower than FUSED on B200          */
-  ODPO_SCHED_RESIDENT = 4  /* one persistent CTA per SM; each row stays ON CHIP between its
-                              forward and its backward pass (shared-memory row buffers and
-                              tensor-memory row slots), so the call moves exactly one read
-                              and one write of the logits (1R+1W).  Applies when two rows
-                              fit in shared memory (row <= 110 KB: V*elt <= 113 152 bytes),
-                              a row spans <= 8 16-KB chunks, and SMs * (buffers + TMEM
-                              slots) >= 4T; UNSUPPORTED otherwise.  Needs all CTAs
-                              co-resident (the GPU not shared with other work)          */
+  ODPO_SCHED_RESIDENT = 4  /* one persistent CTA per SM; a row's forward pass writes it into a
+                              tensor-memory row slot (tcgen05.st) and its backward reads it
+                              back (tcgen05.ld), so TMEM-held rows are read from HBM once;
+                              rows beyond the TMEM slots are L2-backed (re-streamed for the
+                              backward), at most opts->lookahead of them per SM (-1 = 2).
+                              Bit-identical to FUSED.  Applies when a row spans <= 8 16-KB
+                              chunks (V*elt <= 131072 bytes) and SMs * (TMEM slots + cap)
+                              >= 4T; UNSUPPORTED otherwise.  Needs all CTAs co-resident (the
+                              GPU not shared with other work).  Measured slower than FUSED
+                              on B200                           */
 };
 
 typedef struct {
@@ -123,7 +125,8 @@ typedef struct {
   int32_t launches;     /* OUT: number of kernels this call launched               */
   int32_t exp2_split;   /* bf16 only: index of the MUFU/FMA-polynomial exp2 split
                            (-1 = library default)        */
-  int32_t lookahead;    /* FUSED: rows a CTA decodes ahead of the row it streams (-1 = default) */
+  int32_t lookahead;    /* FUSED: rows a CTA decodes ahead of the row it streams (-1 = default);
+                           RESIDENT: L2-backed rows in flight per SM (-1 = default 2)   */
   int32_t row_gap;      /* UNSCALED: forward rows a CTA streams between a row's forward and its
                            backward, 0 or 1 (-1 = default 0); WAVE: pair-steps between a
                            pair's forward and backward rows, 0 or 1 (-1 = default 1)  */
