@@ -353,6 +353,36 @@ const char* odpo_status_string(odpo_status s);
 /* Host-only: library version string. */
 const char* odpo_version(void);
 
+/*
+ * odpo_lmhead_seq_logprobs -- NEXT-2, forward part: sequence log-probs
+ * straight from the LM head (Sec 2.1, with the policy's output layer written
+ * out), the [B, T, V] logits never written to memory.
+ *
+ *   logits[b, t, v] = invT * sum_i hidden[b, t, i] * weight[v, i]
+ *   tok_logp[b, t]  = logits[b, t, tokens[b, t]] - logsumexp_v logits[b, t, v]   (mask = 1)
+ *   seq_logp[b]     = sum_t mask[b, t] tok_logp[b, t]
+ *
+ *   hidden     bf16 [B, T, d], contiguous (row b*T + t at hidden + (b*T + t)*d), 16-byte
+ *              aligned; d a multiple of 64.
+ *   weight     bf16 [V, d], contiguous, 16-byte aligned (the LM head / unembedding).
+ *   tokens, mask  int32 / uint8 [B, T].
+ *   tok_logp, row_lse  fp32 [B, T] outputs (may be NULL); 0 where mask = 0.
+ *   seq_logp   fp32 [B] output.
+ *   status     device uint32, OR-ed ODPO_FLAG_* (TOKEN_RANGE, NONFINITE_LOGIT, EMPTY_SEQ).
+ *   workspace  >= odpo_lmhead_workspace_bytes(B, T, V) bytes of device scratch.
+ * Implementation: tcgen05.mma (bf16 in, fp32 accumulators in TMEM, 128 x 256 tiles) fed by
+ * 2-D TMA; the epilogue folds each 256-wide logit tile into the row's online logsumexp.
+ * Errors: INVALID_ARG (NULL pointers, non-positive sizes, invT not finite > 0), UNSUPPORTED
+ * (d % 64 != 0, B*T or V > 2^31 - 1), ALIGNMENT, WORKSPACE, CUDA (launch or tensor-map
+ * encoding failed).
+ */
+size_t odpo_lmhead_workspace_bytes(int64_t B, int64_t T, int64_t V);
+odpo_status odpo_lmhead_seq_logprobs(const void* hidden, const void* weight, int64_t B, int64_t T,
+                                     int64_t d, int64_t V, const int32_t* tokens,
+                                     const uint8_t* mask, float inv_temperature, float* tok_logp,
+                                     float* row_lse, float* seq_logp, uint32_t* status,
+                                     void* workspace, size_t workspace_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

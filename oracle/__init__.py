@@ -207,6 +207,21 @@ def pg_loss_fwd_bwd(logits, tokens, mask, kind, rewards, old_logp=None, clip_eps
     return dict(seq_logp=S, stats=stats, status=int(status[0]), dlogits=dl)
 
 
+def lmhead_seq_logprobs(hidden, weight, tokens, mask, inv_temperature=1.0, n_threads=1):
+    """NEXT-2: sequence log-probs from the LM head.  The logits are the LM
+    head's definition, logits[b, t, v] = sum_i hidden[b, t, i] * weight[v, i], formed in fp64
+    by a library matmul (hidden and weight hold bf16-exact values, so the fp64 products and
+    sums are exact up to fp64 rounding); the log-softmax, gather and masked sum are
+    seq_logprobs' (PAPER.md:83, Sec 2.1).  Returns seq_logprobs' dict."""
+    h = np.asarray(hidden, dtype=np.float64)
+    w = np.asarray(weight, dtype=np.float64)
+    if h.ndim != 3 or w.ndim != 2 or h.shape[2] != w.shape[1]:
+        raise ValueError("hidden must be [B, T, d] and weight [V, d]")
+    B, T, d = h.shape
+    logits = (h.reshape(B * T, d) @ w.T).reshape(B, T, w.shape[0])
+    return seq_logprobs(np.ascontiguousarray(logits), tokens, mask, inv_temperature, n_threads)
+
+
 def to_bf16_bits(x) -> np.ndarray:
     """Round float values to bf16 (round-to-nearest-even) and return the uint16 bits.
 

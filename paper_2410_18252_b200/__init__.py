@@ -89,6 +89,11 @@ def _L():
                   L.odpo_online_dpo_loss_fwd_bwd_ex, L.odpo_online_dpo_loss_fwd_bwd_unscaled,
                   L.odpo_pg_loss_fwd_bwd):
             f.restype = C.c_int
+        L.odpo_lmhead_seq_logprobs.argtypes = [P, P, i64, i64, i64, i64, P, P, f32, P, P, P, P,
+                                               P, sz, P]
+        L.odpo_lmhead_seq_logprobs.restype = C.c_int
+        L.odpo_lmhead_workspace_bytes.argtypes = [i64, i64, i64]
+        L.odpo_lmhead_workspace_bytes.restype = sz
         L.odpo_workspace_bytes.argtypes = [i64, i64, i64]
         L.odpo_workspace_bytes.restype = sz
         L.odpo_status_string.argtypes = [C.c_int]
@@ -223,6 +228,38 @@ def seq_logprobs(logits: torch.Tensor, tokens: torch.Tensor, mask: torch.Tensor,
     if per_token:
         return seq, tok, lse, status
     return seq
+
+
+def lmhead_seq_logprobs(hidden: torch.Tensor, weight: torch.Tensor, tokens: torch.Tensor,
+                        mask: torch.Tensor, inv_temperature: float = 1.0,
+                        status: torch.Tensor | None = None):
+    """log pi(y|x) per sequence straight from the LM head (forward):
+    hidden [B, T, d] bf16, weight [V, d] bf16 (both contiguous, d % 64 == 0); the logits
+    hidden @ weight.T * invT are formed tile by tile in tensor memory (tcgen05) and never
+    written.  Returns (seq_logp [B], tok_logp [B, T], row_lse [B, T], status)."""
+    hidden = _dev(hidden, "hidden", torch.bfloat16)
+    weight = _dev(weight, "weight", torch.bfloat16)
+    if hidden.dim() != 3 or weight.dim() != 2 or hidden.shape[2] != weight.shape[1]:
+        raise ValueError("hidden must be [B, T, d] and weight [V, d]")
+    if not (hidden.is_contiguous() and weight.is_contiguous()):
+        raise ValueError("hidden and weight must be contiguous")
+    B, T, d = hidden.shape
+    V = weight.shape[0]
+    tokens = _dev(tokens, "tokens", torch.int32).contiguous()
+    mask = _dev(mask, "mask", torch.uint8).contiguous()
+    dev = hidden.device
+    seq = torch.empty(B, dtype=torch.float32, device=dev)
+    tok = torch.empty((B, T), dtype=torch.float32, device=dev)
+    lse = torch.empty((B, T), dtype=torch.float32, device=dev)
+    if status is None:
+        status = torch.zeros(1, dtype=torch.int32, device=dev)
+    nb = _L().odpo_lmhead_workspace_bytes(B, T, V)
+    ws = _workspace(dev, nb)
+    _check(_L().odpo_lmhead_seq_logprobs(_p(hidden), _p(weight), B, T, d, V, _p(tokens), _p(mask),
+                                         float(inv_temperature), _p(tok), _p(lse), _p(seq),
+                                         _p(status), _p(ws), ws.numel(), _stream()),
+           "odpo_lmhead_seq_logprobs")
+    return seq, tok, lse, status
 
 
 @dataclass

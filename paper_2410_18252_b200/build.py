@@ -8,7 +8,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libodpo.so")
-SOURCES = [os.path.join(CSRC, "odpo.cu")]
+SOURCES = [os.path.join(CSRC, "odpo.cu"), os.path.join(CSRC, "odpo_lmhead.cu")]
 DEPS = SOURCES + [os.path.join(CSRC, "odpo_device.cuh"), os.path.join(CSRC, "odpo_engine.cuh"), os.path.join(CSRC, "odpo_resident.cuh"),
                   os.path.join(ROOT, "include", "odpo.h")]
 

@@ -1,0 +1,409 @@
+// odpo_lmhead.cu -- NEXT-2, forward part: sequence log-probs straight from the
+// LM head, logits never written to HBM (sm_100a, tcgen05 / TMEM / TMA).
+//
+//   logits[row, v] = invT * <hidden[row, :], W[v, :]>           (the LM head, bf16 x bf16 -> fp32)
+//   logp[row]      = logits[row, tok] - logsumexp_v logits[row, v]      (Sec 2.1)
+//   S_b            = sum_t mask[b, t] logp[b*T + t]                     (reading R2)
+//
+// K6a k_lmhead_fwd: persistent, one CTA per SM, warp-specialised.  Work unit = (block of 128
+// rows, vocabulary segment).  Warp 0 (one lane) streams 128x64 hidden tiles and 256x64 weight
+// tiles (bf16, 128-byte swizzle) into a 4-stage shared-memory ring with 2-D TMA; warp 1 (one
+// lane) issues tcgen05.mma.cta_group::1.kind::f16 (M=128, N=256, K=16) into one of two TMEM
+// accumulators (2 x 256 fp32 columns) and commits stage/accumulator barriers; warps 2..5 drain
+// the finished accumulator with tcgen05.ld.32x32b.x32 (TMEM lane = row, so each thread owns one
+// row) and fold the 256 logits into the row's online (m, r) state -- the same fp32 log1p-form
+// update as the logits path (mr_batch<fp32>) -- while the tensor cores fill the other buffer.
+// K6b k_lmhead_merge: per row, the segments' (m, r, x_tok) in fixed order -> logp, lse; per
+// sequence, the fixed-order masked sum.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "odpo.h"
+#include "odpo_device.cuh"
+#include "odpo_engine.cuh"
+
+namespace odpo {
+namespace lmh {
+
+constexpr int BM = 128;            // rows per tile (UMMA M)
+constexpr int BN = 256;            // vocabulary per tile (UMMA N)
+constexpr int BK = 64;             // hidden elements per stage (128 B = one swizzle row)
+constexpr int UK = 16;             // UMMA K for kind::f16
+constexpr int STAGES = 4;
+constexpr int A_BYTES = BM * BK * 2;   // 16 KB
+constexpr int B_BYTES = BN * BK * 2;   // 32 KB
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int SMEM = STAGES * STAGE_BYTES + 1024;  // + alignment slack (SW128 atoms: 1024 B)
+constexpr int THREADS = 192;       // producer, MMA, 4 epilogue warps
+constexpr int TMEM_COLS = 2 * BN;  // two fp32 accumulators
+
+// instruction descriptor: D fp32 (bits 4-5 = 1), A/B bf16 (bits 7-9, 10-12 = 1), both K-major,
+// N >> 3 at bits 17-22, M >> 4 at bits 24-28
+constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                            ((uint32_t)(BM >> 4) << 24);
+
+// shared-memory matrix descriptor, K-major, 128-byte swizzle: start address >> 4, LBO = 1
+// (unused for swizzled K-major), SBO = 1024 B between 8-row atoms, version 1, layout 2
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFFu) | (1ull << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         (1ull << 46) | (2ull << 61);
+}
+
+__device__ __forceinline__ void tma_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1,
+                                       uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(map), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(kIdesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void tm_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr)
+      : "memory");
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+struct Args {
+  int64_t R, d, V;     // rows, hidden size, vocabulary
+  int nseg;            // vocabulary segments per row block
+  int64_t seg_len;     // vocabulary per segment (multiple of BN)
+  int64_t nrb;         // row blocks
+  float invT;
+  const int32_t* tokens;  // [R]
+  const uint8_t* mask;    // [R]
+  float4* parts;          // [R][nseg] (m, r, x_tok, owns tok)
+};
+
+// ---------------------------------------------------------------- K6a: GEMM + online LSE
+__global__ void __launch_bounds__(THREADS, 1)
+    k_lmhead_fwd(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+                 Args a) {
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES], tfull[2], tempty[2];
+  __shared__ uint32_t tmem_sh;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;  // SW128 atoms need 1024 B
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], 4);
+    }
+    mbar_fence_init();
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&mapA) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&mapB) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&tmem_sh)),
+                 "n"(TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = tmem_sh;
+  const uint32_t full_s = smem_u32(full), empty_s = smem_u32(empty);
+  const uint32_t tfull_s = smem_u32(tfull), tempty_s = smem_u32(tempty);
+  const int64_t nunits = a.nrb * a.nseg;
+  const int nkb = (int)(a.d / BK);
+  auto seg_tiles = [&](int64_t sg) {
+    const int64_t v0 = sg * a.seg_len;
+    const int64_t v1 = min(a.V, v0 + a.seg_len);
+    return (int)((v1 - v0 + BN - 1) / BN);
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ================= TMA producer
+      int st = 0;
+      uint32_t ph = 0;
+      for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x) {
+        const int64_t rb = u / a.nseg, sg = u % a.nseg;
+        const int nt = seg_tiles(sg);
+        for (int n = 0; n < nt; ++n) {
+          const int vrow = (int)(sg * a.seg_len + (int64_t)n * BN);
+          for (int kb = 0; kb < nkb; ++kb) {
+            mbar_wait(empty_s + 8 * st, ph ^ 1u);
+            const uint32_t sa = base + (uint32_t)(st * STAGE_BYTES);
+            mbar_arrive_tx(full_s + 8 * st, STAGE_BYTES);
+            tma_2d(sa, &mapA, kb * BK, (int)(rb * BM), full_s + 8 * st);
+            tma_2d(sa + A_BYTES, &mapB, kb * BK, vrow, full_s + 8 * st);
+            if (++st == STAGES) { st = 0; ph ^= 1u; }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ================= MMA issuer (one thread)
+      int st = 0;
+      uint32_t ph = 0;
+      int acc = 0;
+      uint32_t aph = 0;
+      for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x) {
+        const int nt = seg_tiles(u % a.nseg);
+        for (int n = 0; n < nt; ++n) {
+          mbar_wait(tempty_s + 8 * acc, aph ^ 1u);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t td = tmem + (uint32_t)(acc * BN);
+          for (int kb = 0; kb < nkb; ++kb) {
+            mbar_wait(full_s + 8 * st, ph);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t sa = base + (uint32_t)(st * STAGE_BYTES);
+            const uint64_t da = sdesc(sa), db = sdesc(sa + A_BYTES);
+#pragma unroll
+            for (int k = 0; k < BK / UK; ++k)  // +32 bytes along K inside the swizzle atom
+              mma_bf16(td, da + (uint64_t)(2 * k), db + (uint64_t)(2 * k), (kb | k) != 0);
+            mma_commit(empty_s + 8 * st);  // frees the stage once these MMAs have read it
+            if (++st == STAGES) { st = 0; ph ^= 1u; }
+          }
+          mma_commit(tfull_s + 8 * acc);   // accumulator complete
+          if (++acc == 2) { acc = 0; aph ^= 1u; }
+        }
+      }
+    }
+  } else {
+    // ================= epilogue warps 2..5: TMEM lane quadrant = warp % 4, one row per thread
+    const int q = warp & 3;
+    const uint32_t lane_base = (uint32_t)(32 * q) << 16;
+    const float k2 = a.invT * kLog2e;
+    int acc = 0;
+    uint32_t aph = 0;
+    for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x) {
+      const int64_t rb = u / a.nseg, sg = u % a.nseg;
+      const int64_t row = rb * BM + 32 * q + lane;
+      const bool live = row < a.R;
+      const int tok = live ? a.tokens[row] : -1;
+      const int64_t v0 = sg * a.seg_len;
+      const int64_t v1 = min(a.V, v0 + a.seg_len);
+      const int nt = (int)((v1 - v0 + BN - 1) / BN);
+      MR s{-INFINITY, 0.f};
+      float xtok = 0.f;
+      bool own = false;
+      for (int n = 0; n < nt; ++n) {
+        mbar_wait(tfull_s + 8 * acc, aph);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const int64_t c0 = v0 + (int64_t)n * BN;
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          uint32_t r[32];
+          tm_ld32(tmem + lane_base + (uint32_t)(acc * BN + c * 32), r);
+          const int64_t cb = c0 + 32 * c;  // first vocabulary index of these 32 columns
+          if (cb >= v1) break;
+          if (cb + 32 > v1) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (cb + j >= v1) r[j] = Traits<0>::kNegInfWord;
+          }
+          if (tok >= cb && tok < cb + 32) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (tok == cb + j) xtok = __uint_as_float(r[j]);
+            own = true;
+          }
+          uint4 v[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) v[j] = make_uint4(r[4 * j], r[4 * j + 1], r[4 * j + 2], r[4 * j + 3]);
+          mr_batch<0, 8, 0>(v, k2, s.m, s.r);
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(tempty_s + 8 * acc);
+        if (++acc == 2) { acc = 0; aph ^= 1u; }
+      }
+      if (live) a.parts[row * a.nseg + sg] = make_float4(s.m, s.r, own ? xtok : 0.f, own ? 1.f : 0.f);
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS)
+                 : "memory");
+  }
+}
+
+// ---------------------------------------------------------------- K6b: merge + sequence sums
+// One warp per sequence: lane l handles t = l, l+32, ... : the segments of its row merged in
+// fixed order, logp and lse written; then the fixed-order masked sum (seq_sum_warp's order).
+__global__ void __launch_bounds__(32) k_lmhead_merge(Args a, int64_t T, float* tok_logp,
+                                                      float* row_lse, float* seq_logp,
+                                                      uint32_t* status) {
+  const int64_t b = blockIdx.x;
+  const int lane = threadIdx.x;
+  const float k2 = a.invT * kLog2e;
+  double S = 0.0;
+  int cnt = 0;
+  uint32_t fl = 0;
+  for (int64_t t = lane; t < T; t += 32) {
+    const int64_t row = b * T + t;
+    MR v{-INFINITY, 0.f};
+    float xt = 0.f;
+    bool own = false;
+    for (int sg = 0; sg < a.nseg; ++sg) {
+      const float4 p = a.parts[row * a.nseg + sg];
+      v = mr_merge(v, MR{p.x, p.y}, k2);
+      if (p.w != 0.f) { xt = p.z; own = true; }
+    }
+    const float l1p = log1pf(v.r);
+    float logp = 0.f;
+    if (a.mask[row]) {
+      const int tok = a.tokens[row];
+      if (tok < 0 || tok >= a.V || !own) {
+        fl |= ODPO_FLAG_TOKEN_RANGE;
+      } else {
+        logp = __fsub_rn(__fmul_rn(__fsub_rn(xt, v.m), a.invT), l1p);
+        if (!isfinite(logp)) fl |= ODPO_FLAG_NONFINITE_LOGIT;
+      }
+      if (!isfinite(v.m) || !isfinite(v.r)) fl |= ODPO_FLAG_NONFINITE_LOGIT;
+      S += (double)logp;
+      ++cnt;
+    }
+    if (tok_logp) tok_logp[row] = a.mask[row] ? logp : 0.f;
+    if (row_lse) row_lse[row] = a.mask[row] ? __fadd_rn(__fmul_rn(v.m, a.invT), l1p) : 0.f;
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    S += __shfl_down_sync(kFull, S, off);
+    cnt += __shfl_down_sync(kFull, cnt, off);
+  }
+  fl = __reduce_or_sync(kFull, fl);
+  if (lane == 0) {
+    seq_logp[b] = cnt ? (float)S : 0.f;
+    if (!cnt) fl |= ODPO_FLAG_EMPTY_SEQ;
+    if (fl && status) atomicOr(status, fl);
+  }
+}
+
+// ---------------------------------------------------------------- host
+typedef CUresult (*EncodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiled encode_fn() {
+  static EncodeTiled fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeTiled)p;
+  }
+  return fn;
+}
+static bool make_map(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int64_t ld,
+                     int box_rows) {
+  EncodeTiled enc = encode_fn();
+  if (!enc) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
+  const cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+  const cuuint32_t es[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+static int sm_count() {
+  int dev = 0, n = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n;
+}
+
+// vocabulary segments per 128-row block: enough work units to fill the SMs (>= 4 per SM when
+// possible), each segment a whole number of 256-wide tiles
+static int pick_nseg(int64_t nrb, int64_t V, int sms) {
+  const int64_t tiles = (V + BN - 1) / BN;
+  int64_t nseg = (4 * (int64_t)sms + nrb - 1) / nrb;
+  if (nseg < 1) nseg = 1;
+  if (nseg > tiles) nseg = tiles;
+  if (nseg > 64) nseg = 64;
+  return (int)nseg;
+}
+
+}  // namespace lmh
+}  // namespace odpo
+
+using namespace odpo;
+using namespace odpo::lmh;
+
+extern "C" {
+
+size_t odpo_lmhead_workspace_bytes(int64_t B, int64_t T, int64_t V) {
+  if (B <= 0 || T <= 0 || V <= 0) return 0;
+  const int64_t R = B * T;
+  const int64_t nrb = (R + BM - 1) / BM;
+  return (size_t)R * 64 * sizeof(float4) + 0 * nrb;  // up to 64 segments per row
+}
+
+odpo_status odpo_lmhead_seq_logprobs(const void* hidden, const void* weight, int64_t B, int64_t T,
+                                     int64_t d, int64_t V, const int32_t* tokens,
+                                     const uint8_t* mask, float inv_temperature, float* tok_logp,
+                                     float* row_lse, float* seq_logp, uint32_t* status,
+                                     void* workspace, size_t workspace_bytes, void* stream) {
+  if (!hidden || !weight || !tokens || !mask || !seq_logp) return ODPO_ERR_INVALID_ARG;
+  if (B <= 0 || T <= 0 || V <= 0 || d <= 0) return ODPO_ERR_INVALID_ARG;
+  if (!(isfinite(inv_temperature) && inv_temperature > 0.f)) return ODPO_ERR_INVALID_ARG;
+  if (d % BK) return ODPO_ERR_UNSUPPORTED;
+  if (((uintptr_t)hidden & 15u) || ((uintptr_t)weight & 15u)) return ODPO_ERR_ALIGNMENT;
+  const int64_t R = B * T;
+  if (R > (int64_t)INT32_MAX || V > (int64_t)INT32_MAX || d > (1 << 20)) return ODPO_ERR_UNSUPPORTED;
+  if (!workspace || workspace_bytes < odpo_lmhead_workspace_bytes(B, T, V)) return ODPO_ERR_WORKSPACE;
+  CUtensorMap mA, mB;
+  if (!make_map(&mA, hidden, R, d, d, BM) || !make_map(&mB, weight, V, d, d, BN))
+    return ODPO_ERR_CUDA;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_lmhead_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    attr = true;
+  }
+  const int sms = sm_count();
+  Args a;
+  a.R = R; a.d = d; a.V = V;
+  a.nrb = (R + BM - 1) / BM;
+  a.nseg = pick_nseg(a.nrb, V, sms);
+  const int64_t tiles = (V + BN - 1) / BN;
+  a.seg_len = ((tiles + a.nseg - 1) / a.nseg) * BN;
+  a.nseg = (int)((V + a.seg_len - 1) / a.seg_len);  // no empty segments
+  a.invT = inv_temperature;
+  a.tokens = tokens; a.mask = mask;
+  a.parts = reinterpret_cast<float4*>(workspace);
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t nunits = a.nrb * a.nseg;
+  const int grid = (int)(nunits < sms ? nunits : sms);
+  k_lmhead_fwd<<<grid, THREADS, SMEM, s>>>(mA, mB, a);
+  if (cudaGetLastError() != cudaSuccess) return ODPO_ERR_CUDA;
+  k_lmhead_merge<<<(unsigned)B, 32, 0, s>>>(a, T, tok_logp, row_lse, seq_logp, status);
+  return cudaGetLastError() == cudaSuccess ? ODPO_OK : ODPO_ERR_CUDA;
+}
+
+}  // extern "C"

@@ -20,6 +20,10 @@ Recipe (SURVEY.md §8(d) "Synthetic inputs"):
 * rewards     RM-like grid ((h % 4096) - 2048) / 256 in [-8, 8)
               or verifier rewards h & 1 in {0, 1}
 * has_eos     (h(seed, S_EOS, p*K + k) % 32) != 0  (~3% truncated completions)
+* LM head     (NEXT-2) hidden[g, i] = ((h(seed, S_HIDDEN, g*d + i) % 64) - 32) / 32 and
+              W[v, i] = ((h(seed, S_WEIGHT, v*d + i) % 64) - 32) / 256: dyadic grids exact in
+              bf16, so hidden @ W.T is exact in fp64; logits have std ~ 0.04 sqrt(d)
+              (2.1 at the Pythia-2.8B width d = 2560)
 """
 from __future__ import annotations
 
@@ -34,6 +38,8 @@ S_EOS = 6
 S_DELTA = 7
 S_PERM = 8
 S_SPLIT = 9
+S_HIDDEN = 10
+S_WEIGHT = 11
 
 _G = np.uint64(0x9E3779B97F4A7C15)
 _M1 = np.uint64(0xBF58476D1CE4E5B9)
@@ -183,3 +189,17 @@ def fill_logits_device(x, seed: int, row0: int = 0, tokens=None, peak: float | N
         1 if tk is not None else 0, torch.cuda.current_stream().cuda_stream)
     if rc:
         raise RuntimeError(f"synth_fill_logits failed ({rc})")
+
+
+def lmhead_inputs(seed: int, rows_global, d: int, V: int, v_rows=None):
+    """NEXT-2 inputs: hidden [len(rows_global), d] and W [V, d] (or the rows v_rows of W) as
+    float64 arrays whose values are exact in bf16 (see the recipe above)."""
+    rows_global = np.asarray(rows_global, dtype=np.uint64)
+    i = np.arange(d, dtype=np.uint64)
+    h = hash_u64(seed, S_HIDDEN, rows_global[:, None] * np.uint64(d) + i[None, :])
+    hidden = ((h % np.uint64(64)).astype(np.int64) - 32).astype(np.float64) / 32.0
+    vr = np.arange(V, dtype=np.uint64) if v_rows is None else np.asarray(v_rows, dtype=np.uint64)
+    w = hash_u64(seed, S_WEIGHT, vr[:, None] * np.uint64(d) + i[None, :])
+    weight = ((w % np.uint64(64)).astype(np.int64) - 32).astype(np.float64) / 256.0
+    return hidden, weight
+

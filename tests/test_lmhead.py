@@ -1,0 +1,103 @@
+"""NEXT-2, forward part: sequence log-probs from the LM head without
+materialising the logits.  CPU tests pin the oracle (closed form, brute force); GPU tests
+compare the tcgen05 kernel (odpo_lmhead_seq_logprobs) with it element by element."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+
+# ------------------------------------------------------------------ oracle pins (CPU)
+def test_oracle_zero_head_is_uniform():
+    """W = 0: every logit is 0, so log p = -log V and lse = log V exactly."""
+    B, T, d, V = 2, 3, 64, 50
+    h, _ = synth.lmhead_inputs(1, np.arange(B * T), d, V)
+    w = np.zeros((V, d))
+    tok = synth.tokens_rows(1, np.arange(B * T), V).reshape(B, T)
+    mask = np.ones((B, T), np.uint8)
+    o = oracle.lmhead_seq_logprobs(h.reshape(B, T, d), w, tok, mask)
+    assert np.allclose(o["tok_logp"], -math.log(V), rtol=0, atol=1e-15)
+    assert np.allclose(o["row_lse"], math.log(V), rtol=0, atol=1e-15)
+    assert np.allclose(o["seq_logp"], -T * math.log(V), rtol=1e-15)
+
+
+@pytest.mark.parametrize("invT", [1.0, 1 / 0.7])
+def test_oracle_brute_force(invT):
+    """Tiny shapes, pure-Python loops: logits[r, v] = sum_i h[r, i] w[v, i] (PAPER.md:83 with
+    the LM head written out), log p = invT x_tok - log sum_v exp(invT x_v)."""
+    B, T, d, V = 2, 3, 5, 7
+    rows = np.arange(B * T)
+    h, w = synth.lmhead_inputs(3, rows, d, V)
+    tok = synth.tokens_rows(3, rows, V).reshape(B, T)
+    mask = synth.mask_for(3, np.arange(B), T, "prefix", 2)
+    o = oracle.lmhead_seq_logprobs(h.reshape(B, T, d), w, tok, mask, inv_temperature=invT)
+    it = float(np.float32(invT))
+    for b in range(B):
+        S = 0.0
+        for t in range(T):
+            r = b * T + t
+            x = [math.fsum(h[r, i] * w[v, i] for i in range(d)) for v in range(V)]
+            mx = max(x)
+            lse = it * mx + math.log(math.fsum(math.exp(it * (xv - mx)) for xv in x))
+            lp = it * x[tok[b, t]] - lse
+            if mask[b, t]:
+                assert abs(o["tok_logp"][b, t] - lp) <= 1e-12
+                S += lp
+        assert abs(o["seq_logp"][b] - S) <= 1e-11
+
+
+# ------------------------------------------------------------------ GPU parity
+
+CASES = [
+    # (B, T, d, V, mask): ragged vocabulary tile, ragged row block, several row blocks / segments
+    (2, 5, 128, 1000, "dense"),
+    (3, 50, 256, 4133, "prefix"),
+    (4, 53, 2560, 50304, "dense"),   # the Pythia-2.8B LM head (d = 2560, V = 50304)
+]
+
+
+@pytest.mark.parametrize("case", CASES, ids=lambda c: f"B{c[0]}T{c[1]}d{c[2]}V{c[3]}{c[4]}")
+@pytest.mark.gpu
+@pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a CUDA device")
+def test_lmhead_parity(case):
+    import paper_2410_18252_b200 as odpo
+    B, T, d, V, mk = case
+    rows = np.arange(B * T)
+    h, w = synth.lmhead_inputs(7, rows, d, V)
+    tok = synth.tokens_rows(7, rows, V).reshape(B, T).astype(np.int32)
+    mask = synth.mask_for(7, np.arange(B), T, mk, max(1, T // 2))
+    hd = torch.from_numpy(h.reshape(B, T, d)).to(torch.bfloat16).cuda()   # exact (bf16 grid)
+    wd = torch.from_numpy(w).to(torch.bfloat16).cuda()
+    seq, tlp, lse, st = odpo.lmhead_seq_logprobs(hd, wd, torch.from_numpy(tok).cuda(),
+                                                 torch.from_numpy(mask).cuda())
+    torch.cuda.synchronize()
+    o = oracle.lmhead_seq_logprobs(h.reshape(B, T, d), w, tok, mask, n_threads=8)
+    assert int(st.item()) == 0
+    # fp32 tensor-core accumulation of exact bf16 products: per-token error << the bf16
+    # contract (2e-3 relative on sequence log-probs)
+    g = tlp.cpu().numpy().astype(np.float64)
+    assert np.all(np.abs(g - o["tok_logp"]) <= 1e-4 * np.maximum(1.0, np.abs(o["tok_logp"])))
+    gl = lse.cpu().numpy().astype(np.float64)
+    m = mask == 1
+    assert np.all(np.abs(gl[m] - o["row_lse"][m]) <= 1e-4 * np.maximum(1.0, np.abs(o["row_lse"][m])))
+    S = seq.cpu().numpy().astype(np.float64)
+    assert np.all(np.abs(S - o["seq_logp"]) <= 2e-3 * np.maximum(1.0, np.abs(o["seq_logp"])))
+    assert np.all(np.abs(S - o["seq_logp"]) <= 1e-4 * np.maximum(1.0, np.abs(o["seq_logp"])))
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a CUDA device")
+def test_lmhead_token_range_flag():
+    import paper_2410_18252_b200 as odpo
+    B, T, d, V = 1, 4, 64, 300
+    h, w = synth.lmhead_inputs(2, np.arange(B * T), d, V)
+    tok = np.array([[0, 5, V, 7]], np.int32)
+    mask = np.ones((B, T), np.uint8)
+    _, _, _, st = odpo.lmhead_seq_logprobs(torch.from_numpy(h.reshape(B, T, d)).to(torch.bfloat16).cuda(),
+                                           torch.from_numpy(w).to(torch.bfloat16).cuda(),
+                                           torch.from_numpy(tok).cuda(), torch.from_numpy(mask).cuda())
+    assert int(st.item()) & odpo.FLAGS["TOKEN_RANGE"]
