@@ -5,20 +5,21 @@
 //   logp[row]      = logits[row, tok] - logsumexp_v logits[row, v]      (Sec 2.1)
 //   S_b            = sum_t mask[b, t] logp[b*T + t]                     (reading R2)
 //
-// K6a k_lmhead_fwd: persistent, one CTA per SM, warp-specialised.  Work unit = (block of 128
-// rows, vocabulary segment).  Warp 0 (one lane) streams 128x64 hidden tiles and 256x64 weight
+// K6a k_lmhead_fwd: persistent, one CTA per SM, warp-specialised; CTA c owns an equal contiguous
+// range of the (128-row block, 256-wide vocabulary tile) grid (see Args).  Warp 0 (one lane) streams 128x64 hidden tiles and 256x64 weight
 // tiles (bf16, 128-byte swizzle) into a 4-stage shared-memory ring with 2-D TMA; warp 1 (one
 // lane) issues tcgen05.mma.cta_group::1.kind::f16 (M=128, N=256, K=16) into one of two TMEM
 // accumulators (2 x 256 fp32 columns) and commits stage/accumulator barriers; warps 2..5 drain
 // the finished accumulator with tcgen05.ld.32x32b.x32 (TMEM lane = row, so each thread owns one
 // row) and fold the 256 logits into the row's online (m, r) state -- the same fp32 log1p-form
 // update as the logits path (mr_batch<fp32>) -- while the tensor cores fill the other buffer.
-// K6b k_lmhead_merge: per row, the segments' (m, r, x_tok) in fixed order -> logp, lse; per
+// K6b k_lmhead_merge: per row, the pieces' (m, r, x_tok) in fixed (CTA) order -> logp, lse; per
 // sequence, the fixed-order masked sum.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "odpo.h"
 #include "odpo_device.cuh"
@@ -86,16 +87,32 @@ __device__ __forceinline__ void tm_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// Work split: the nrb x NT grid of (128-row block, 256-wide vocabulary tile) tiles, ordered in
+// groups of G row blocks, vocabulary-major inside a group, and dealt round-robin to the
+// persistent CTAs (tile i*grid + c to CTA c).  The ~grid tiles in flight at any moment span G
+// row blocks x grid/G vocabulary tiles, so their hidden blocks and weight tiles are shared
+// through L2.  Every tile writes its rows' partial (m, r) -- the merge order (vocabulary tile
+// order) does not depend on the CTA mapping.
 struct Args {
   int64_t R, d, V;     // rows, hidden size, vocabulary
-  int nseg;            // vocabulary segments per row block
-  int64_t seg_len;     // vocabulary per segment (multiple of BN)
-  int64_t nrb;         // row blocks
+  int64_t nrb, NT;     // row blocks, vocabulary tiles per row block
+  int64_t Ttot;        // nrb * NT
+  int G;               // row blocks per raster group
   float invT;
   const int32_t* tokens;  // [R]
   const uint8_t* mask;    // [R]
-  float4* parts;          // [R][nseg] (m, r, x_tok, owns tok)
+  float2* parts;          // [R][NT] (m, r) of each vocabulary tile
+  float* xtok;            // [R] the sampled token's logit (written by the tile holding it)
 };
+
+__device__ __forceinline__ void tile_coords(const Args& a, int64_t t, int64_t& rb, int64_t& n) {
+  const int64_t grp = t / ((int64_t)a.G * a.NT);
+  const int64_t r0 = grp * a.G;
+  const int64_t gg = min((int64_t)a.G, a.nrb - r0);
+  const int64_t idx = t - grp * (int64_t)a.G * a.NT;
+  n = idx / gg;
+  rb = r0 + idx % gg;
+}
 
 // ---------------------------------------------------------------- K6a: GEMM + online LSE
 __global__ void __launch_bounds__(THREADS, 1)
@@ -132,24 +149,18 @@ __global__ void __launch_bounds__(THREADS, 1)
   const uint32_t tmem = tmem_sh;
   const uint32_t full_s = smem_u32(full), empty_s = smem_u32(empty);
   const uint32_t tfull_s = smem_u32(tfull), tempty_s = smem_u32(tempty);
-  const int64_t nunits = a.nrb * a.nseg;
   const int nkb = (int)(a.d / BK);
-  auto seg_tiles = [&](int64_t sg) {
-    const int64_t v0 = sg * a.seg_len;
-    const int64_t v1 = min(a.V, v0 + a.seg_len);
-    return (int)((v1 - v0 + BN - 1) / BN);
-  };
 
   if (warp == 0) {
     if (lane == 0) {
       // ================= TMA producer
       int st = 0;
       uint32_t ph = 0;
-      for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x) {
-        const int64_t rb = u / a.nseg, sg = u % a.nseg;
-        const int nt = seg_tiles(sg);
-        for (int n = 0; n < nt; ++n) {
-          const int vrow = (int)(sg * a.seg_len + (int64_t)n * BN);
+      for (int64_t t = blockIdx.x; t < a.Ttot; t += gridDim.x) {
+        int64_t rb, nt;
+        tile_coords(a, t, rb, nt);
+        const int vrow = (int)(nt * BN);
+        {
           for (int kb = 0; kb < nkb; ++kb) {
             mbar_wait(empty_s + 8 * st, ph ^ 1u);
             const uint32_t sa = base + (uint32_t)(st * STAGE_BYTES);
@@ -168,9 +179,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       uint32_t ph = 0;
       int acc = 0;
       uint32_t aph = 0;
-      for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x) {
-        const int nt = seg_tiles(u % a.nseg);
-        for (int n = 0; n < nt; ++n) {
+      for (int64_t t = blockIdx.x; t < a.Ttot; t += gridDim.x) {
+        {
           mbar_wait(tempty_s + 8 * acc, aph ^ 1u);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint32_t td = tmem + (uint32_t)(acc * BN);
@@ -197,49 +207,44 @@ __global__ void __launch_bounds__(THREADS, 1)
     const float k2 = a.invT * kLog2e;
     int acc = 0;
     uint32_t aph = 0;
-    for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x) {
-      const int64_t rb = u / a.nseg, sg = u % a.nseg;
+    for (int64_t t = blockIdx.x; t < a.Ttot; t += gridDim.x) {
+      int64_t rb, n;
+      tile_coords(a, t, rb, n);
       const int64_t row = rb * BM + 32 * q + lane;
       const bool live = row < a.R;
       const int tok = live ? a.tokens[row] : -1;
-      const int64_t v0 = sg * a.seg_len;
-      const int64_t v1 = min(a.V, v0 + a.seg_len);
-      const int nt = (int)((v1 - v0 + BN - 1) / BN);
       MR s{-INFINITY, 0.f};
-      float xtok = 0.f;
-      bool own = false;
-      for (int n = 0; n < nt; ++n) {
-        mbar_wait(tfull_s + 8 * acc, aph);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const int64_t c0 = v0 + (int64_t)n * BN;
+      mbar_wait(tfull_s + 8 * acc, aph);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int64_t c0 = n * BN;
 #pragma unroll 1
-        for (int c = 0; c < BN / 32; ++c) {
-          uint32_t r[32];
-          tm_ld32(tmem + lane_base + (uint32_t)(acc * BN + c * 32), r);
-          const int64_t cb = c0 + 32 * c;  // first vocabulary index of these 32 columns
-          if (cb >= v1) break;
-          if (cb + 32 > v1) {
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t r[32];
+        tm_ld32(tmem + lane_base + (uint32_t)(acc * BN + c * 32), r);
+        const int64_t cb = c0 + 32 * c;  // first vocabulary index of these 32 columns
+        if (cb >= a.V) break;
+        if (cb + 32 > a.V) {
 #pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if (cb + j >= v1) r[j] = Traits<0>::kNegInfWord;
-          }
-          if (tok >= cb && tok < cb + 32) {
-#pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if (tok == cb + j) xtok = __uint_as_float(r[j]);
-            own = true;
-          }
-          uint4 v[8];
-#pragma unroll
-          for (int j = 0; j < 8; ++j) v[j] = make_uint4(r[4 * j], r[4 * j + 1], r[4 * j + 2], r[4 * j + 3]);
-          mr_batch<0, 8, 0>(v, k2, s.m, s.r);
+          for (int j = 0; j < 32; ++j)
+            if (cb + j >= a.V) r[j] = Traits<0>::kNegInfWord;
         }
-        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-        __syncwarp();
-        if (lane == 0) mbar_arrive(tempty_s + 8 * acc);
-        if (++acc == 2) { acc = 0; aph ^= 1u; }
+        if (live && tok >= cb && tok < cb + 32) {
+          float x = 0.f;
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (tok == cb + j) x = __uint_as_float(r[j]);
+          a.xtok[row] = x;
+        }
+        uint4 v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = make_uint4(r[4 * j], r[4 * j + 1], r[4 * j + 2], r[4 * j + 3]);
+        mr_batch<0, 8, 0>(v, k2, s.m, s.r);
       }
-      if (live) a.parts[row * a.nseg + sg] = make_float4(s.m, s.r, own ? xtok : 0.f, own ? 1.f : 0.f);
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty_s + 8 * acc);
+      if (++acc == 2) { acc = 0; aph ^= 1u; }
+      if (live) a.parts[row * a.NT + n] = make_float2(s.m, s.r);
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -251,55 +256,51 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
 }
 
-// ---------------------------------------------------------------- K6b: merge + sequence sums
-// One warp per sequence: lane l handles t = l, l+32, ... : the segments of its row merged in
-// fixed order, logp and lse written; then the fixed-order masked sum (seq_sum_warp's order).
-__global__ void __launch_bounds__(32) k_lmhead_merge(Args a, int64_t T, float* tok_logp,
-                                                      float* row_lse, float* seq_logp,
-                                                      uint32_t* status) {
-  const int64_t b = blockIdx.x;
-  const int lane = threadIdx.x;
+// ---------------------------------------------------------------- K6b: merge, K6c: sequence sums
+// K6b: one warp per row: lane l merges vocabulary tiles l, l+32, ... in order, then the fixed
+// shfl_down tree; lane 0 forms logp and lse (the logits path's arithmetic).
+__global__ void __launch_bounds__(256) k_lmhead_merge(Args a, float* tok_logp, float* row_lse,
+                                                       uint32_t* status) {
+  const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= a.R) return;
   const float k2 = a.invT * kLog2e;
-  double S = 0.0;
-  int cnt = 0;
+  MR v{-INFINITY, 0.f};
+  for (int64_t n = lane; n < a.NT; n += 32) {
+    const float2 p = a.parts[row * a.NT + n];
+    v = mr_merge(v, MR{p.x, p.y}, k2);
+  }
+  v = warp_merge(v, k2);
+  if (lane != 0) return;
   uint32_t fl = 0;
-  for (int64_t t = lane; t < T; t += 32) {
-    const int64_t row = b * T + t;
-    MR v{-INFINITY, 0.f};
-    float xt = 0.f;
-    bool own = false;
-    for (int sg = 0; sg < a.nseg; ++sg) {
-      const float4 p = a.parts[row * a.nseg + sg];
-      v = mr_merge(v, MR{p.x, p.y}, k2);
-      if (p.w != 0.f) { xt = p.z; own = true; }
-    }
+  float logp = 0.f, lse = 0.f;
+  if (a.mask[row]) {
     const float l1p = log1pf(v.r);
-    float logp = 0.f;
-    if (a.mask[row]) {
-      const int tok = a.tokens[row];
-      if (tok < 0 || tok >= a.V || !own) {
-        fl |= ODPO_FLAG_TOKEN_RANGE;
-      } else {
-        logp = __fsub_rn(__fmul_rn(__fsub_rn(xt, v.m), a.invT), l1p);
-        if (!isfinite(logp)) fl |= ODPO_FLAG_NONFINITE_LOGIT;
-      }
-      if (!isfinite(v.m) || !isfinite(v.r)) fl |= ODPO_FLAG_NONFINITE_LOGIT;
-      S += (double)logp;
-      ++cnt;
+    const int tok = a.tokens[row];
+    if (tok < 0 || tok >= a.V) {
+      fl |= ODPO_FLAG_TOKEN_RANGE;
+    } else {
+      logp = __fsub_rn(__fmul_rn(__fsub_rn(a.xtok[row], v.m), a.invT), l1p);
+      if (!isfinite(logp)) fl |= ODPO_FLAG_NONFINITE_LOGIT;
     }
-    if (tok_logp) tok_logp[row] = a.mask[row] ? logp : 0.f;
-    if (row_lse) row_lse[row] = a.mask[row] ? __fadd_rn(__fmul_rn(v.m, a.invT), l1p) : 0.f;
+    if (!isfinite(v.m) || !isfinite(v.r)) fl |= ODPO_FLAG_NONFINITE_LOGIT;
+    lse = __fadd_rn(__fmul_rn(v.m, a.invT), l1p);
   }
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
-    S += __shfl_down_sync(kFull, S, off);
-    cnt += __shfl_down_sync(kFull, cnt, off);
-  }
-  fl = __reduce_or_sync(kFull, fl);
-  if (lane == 0) {
-    seq_logp[b] = cnt ? (float)S : 0.f;
-    if (!cnt) fl |= ODPO_FLAG_EMPTY_SEQ;
-    if (fl && status) atomicOr(status, fl);
+  tok_logp[row] = logp;
+  if (row_lse) row_lse[row] = lse;
+  if (fl && status) atomicOr(status, fl);
+}
+
+// K6c: one warp per sequence, seq_sum_warp's fixed order.
+__global__ void __launch_bounds__(32) k_lmhead_seqsum(const float* tok_logp, const uint8_t* mask,
+                                                       int64_t T, float* seq_logp, uint32_t* status) {
+  const int64_t b = blockIdx.x;
+  double S;
+  int n;
+  seq_sum_warp(tok_logp + b * T, mask + b * T, T, S, n);
+  if (threadIdx.x == 0) {
+    seq_logp[b] = n ? (float)S : 0.f;
+    if (!n && status) atomicOr(status, ODPO_FLAG_EMPTY_SEQ);
   }
 }
 
@@ -339,16 +340,7 @@ static int sm_count() {
   return n;
 }
 
-// vocabulary segments per 128-row block: enough work units to fill the SMs (>= 4 per SM when
-// possible), each segment a whole number of 256-wide tiles
-static int pick_nseg(int64_t nrb, int64_t V, int sms) {
-  const int64_t tiles = (V + BN - 1) / BN;
-  int64_t nseg = (4 * (int64_t)sms + nrb - 1) / nrb;
-  if (nseg < 1) nseg = 1;
-  if (nseg > tiles) nseg = tiles;
-  if (nseg > 64) nseg = 64;
-  return (int)nseg;
-}
+constexpr int kRasterG = 64;  // row blocks per raster group (tuned: 8/16/32/64 -> 1636/1723/1751/1802 TF/s)
 
 }  // namespace lmh
 }  // namespace odpo
@@ -361,8 +353,9 @@ extern "C" {
 size_t odpo_lmhead_workspace_bytes(int64_t B, int64_t T, int64_t V) {
   if (B <= 0 || T <= 0 || V <= 0) return 0;
   const int64_t R = B * T;
-  const int64_t nrb = (R + BM - 1) / BM;
-  return (size_t)R * 64 * sizeof(float4) + 0 * nrb;  // up to 64 segments per row
+  const int64_t NT = (V + BN - 1) / BN;
+  // per row: NT (m, r) partials, the sampled logit, and an fp32 log-prob scratch
+  return (size_t)R * (size_t)NT * sizeof(float2) + (size_t)R * 8 + 256;
 }
 
 odpo_status odpo_lmhead_seq_logprobs(const void* hidden, const void* weight, int64_t B, int64_t T,
@@ -390,19 +383,22 @@ odpo_status odpo_lmhead_seq_logprobs(const void* hidden, const void* weight, int
   Args a;
   a.R = R; a.d = d; a.V = V;
   a.nrb = (R + BM - 1) / BM;
-  a.nseg = pick_nseg(a.nrb, V, sms);
-  const int64_t tiles = (V + BN - 1) / BN;
-  a.seg_len = ((tiles + a.nseg - 1) / a.nseg) * BN;
-  a.nseg = (int)((V + a.seg_len - 1) / a.seg_len);  // no empty segments
+  a.NT = (V + BN - 1) / BN;
+  a.Ttot = a.nrb * a.NT;
+  a.G = kRasterG;
+  if (const char* g = getenv("ODPO_LMH_G")) a.G = atoi(g) > 0 ? atoi(g) : kRasterG;  // tuning
   a.invT = inv_temperature;
   a.tokens = tokens; a.mask = mask;
-  a.parts = reinterpret_cast<float4*>(workspace);
+  a.parts = reinterpret_cast<float2*>(workspace);
+  a.xtok = reinterpret_cast<float*>(reinterpret_cast<char*>(workspace) + (size_t)R * a.NT * sizeof(float2));
+  float* tlp = tok_logp ? tok_logp : a.xtok + R;  // log-prob scratch when not requested
   cudaStream_t s = (cudaStream_t)stream;
-  const int64_t nunits = a.nrb * a.nseg;
-  const int grid = (int)(nunits < sms ? nunits : sms);
+  const int grid = (int)(a.Ttot < sms ? a.Ttot : sms);
   k_lmhead_fwd<<<grid, THREADS, SMEM, s>>>(mA, mB, a);
   if (cudaGetLastError() != cudaSuccess) return ODPO_ERR_CUDA;
-  k_lmhead_merge<<<(unsigned)B, 32, 0, s>>>(a, T, tok_logp, row_lse, seq_logp, status);
+  k_lmhead_merge<<<(unsigned)((R + 7) / 8), 256, 0, s>>>(a, tlp, row_lse, status);
+  if (cudaGetLastError() != cudaSuccess) return ODPO_ERR_CUDA;
+  k_lmhead_seqsum<<<(unsigned)B, 32, 0, s>>>(tlp, mask, T, seq_logp, status);
   return cudaGetLastError() == cudaSuccess ? ODPO_OK : ODPO_ERR_CUDA;
 }
 
