@@ -484,10 +484,12 @@ __device__ __forceinline__ void seq_sum2_warp(const float* lp_c, const uint8_t* 
   int cc = 0, cr = 0;
 #pragma unroll 2
   for (int64_t t = lane; t < T; t += 32) {
+    // both masks, then both (written) log-probs: two overlapped round trips, and masked rows'
+    // log-probs (never written) are never read
     const uint8_t mc = lp_c ? __ldcg(mk_c + t) : (uint8_t)0;
     const uint8_t mr = lp_r ? __ldcg(mk_r + t) : (uint8_t)0;
-    const float vc = lp_c ? __ldcg(lp_c + t) : 0.f;
-    const float vr = lp_r ? __ldcg(lp_r + t) : 0.f;
+    const float vc = mc ? __ldcg(lp_c + t) : 0.f;
+    const float vr = mr ? __ldcg(lp_r + t) : 0.f;
     if (mc) { sc += (double)vc; ++cc; }
     if (mr) { sr += (double)vr; ++cr; }
   }
