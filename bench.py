@@ -72,6 +72,62 @@ def peaks():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def bf16_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        if "bf16_tflops" in d:
+            return float(d["bf16_tflops"]), "measured (MEASURED_PEAKS.json bf16_tflops, cuBLAS)"
+    return 1590.0, "fallback (B200_PROFILING.md)"
+
+
+# LM-head shapes of the paper's models (hidden width d, vocabulary V) for the NEXT-2 aux line
+HEADS = {"pythia": (2560, 50304), "rho": (2048, 32000)}
+
+
+def aux_lmhead(config, B, T, reps=5):
+    """NEXT-2 forward (odpo_lmhead_seq_logprobs: tcgen05 GEMM + online log-softmax, logits never
+    stored) on the config's model head, beside cuBLAS's bf16 GEMM + odpo_seq_logprobs."""
+    import torch
+
+    import paper_2410_18252_b200 as odpo
+    if config not in HEADS:
+        return None
+    d, V = HEADS[config]
+    g = torch.Generator(device="cuda").manual_seed(0)
+    hid = (torch.randint(-32, 32, (B, T, d), device="cuda", generator=g).float() / 32).to(torch.bfloat16)
+    Wh = (torch.randint(-32, 32, (V, d), device="cuda", generator=g).float() / 256).to(torch.bfloat16)
+    tok = torch.randint(0, V, (B, T), device="cuda", generator=g, dtype=torch.int32)
+    msk = torch.ones((B, T), dtype=torch.uint8, device="cuda")
+
+    def t(fn):
+        for _ in range(2):
+            fn()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(reps)]
+        torch.cuda.synchronize()
+        for a, b in ev:
+            a.record()
+            fn()
+            b.record()
+        torch.cuda.synchronize()
+        return float(np.median([a.elapsed_time(b) for a, b in ev]))
+
+    fused = t(lambda: odpo.lmhead_seq_logprobs(hid, Wh, tok, msk))
+    gemm = t(lambda: torch.matmul(hid.view(B * T, d), Wh.t()))
+    lg = torch.matmul(hid.view(B * T, d), Wh.t()).view(B, T, V)
+    seqp = t(lambda: odpo.seq_logprobs(lg, tok, msk))
+    del lg, hid, Wh
+    torch.cuda.empty_cache()
+    flops = 2.0 * B * T * d * V
+    pk, src = bf16_peak()
+    return {"kernel": "odpo_lmhead_seq_logprobs (k_lmhead_fwd + merge)", "rows": B * T, "d": d,
+            "V": V, "bound": "tensor", "ms": fused, "achieved": flops / fused / 1e9,
+            "unit": "TFLOP/s", "peak": pk, "peak_source": src, "frac": flops / fused / 1e9 / pk,
+            "cublas_gemm_ms": gemm, "cublas_tflops": flops / gemm / 1e9,
+            "unfused_ms": gemm + seqp, "speedup_vs_unfused": (gemm + seqp) / fused}
+
+
 class ClockSampler:
     """NVML SM-clock / throttle-reason sampler running during the timed region."""
 
@@ -356,6 +412,7 @@ def run_ours(args, rank, world, local_rank):
         aux = {"gradient": other, "loss_ms_mean": float(ams.mean()), "achieved": aach,
                "frac": aach / peak, "pairs_per_s_loss_only": world * P / (ams.mean() / 1e3),
                "status": int(status.item())}
+    lmh = aux_lmhead(args.config, B, T) if not args.no_aux and args.loss == "dpo" else None
     traffic = None
     sfx = ("" if args.gradient == "scaled" else "_unscaled") if args.loss == "dpo" else "_" + args.loss
     tp = os.path.join(ROOT, "profiles", f"ncu_traffic_{args.config}{sfx}.json")
@@ -466,6 +523,7 @@ def run_ours(args, rank, world, local_rank):
             "e2e": e2e,
             "gpu_launches": int(n_launch * K),
             "aux_gradient_form": aux,
+            "aux_lmhead_fwd": lmh,
             "clocks": clk.summary(),
             "tokens_vocab_per_s": world * B * T * V * K / (tot_ms / 1e3),
             "eff_gbs_step": world * alg_bytes * K / (tot_ms / 1e3) / 1e9,

@@ -53,19 +53,20 @@ def test_oracle_brute_force(invT):
 # ------------------------------------------------------------------ GPU parity
 
 CASES = [
-    # (B, T, d, V, mask): ragged vocabulary tile, ragged row block, several row blocks / segments
-    (2, 5, 128, 1000, "dense"),
-    (3, 50, 256, 4133, "prefix"),
-    (4, 53, 2560, 50304, "dense"),   # the Pythia-2.8B LM head (d = 2560, V = 50304)
+    # (B, T, d, V, mask, invT): ragged vocabulary tile, ragged row block, several raster groups
+    (2, 5, 128, 1000, "dense", 1.0),
+    (3, 50, 256, 4133, "prefix", 1 / 0.7),
+    (4, 53, 2560, 50304, "dense", 1.0),   # the Pythia-2.8B LM head (d = 2560, V = 50304)
+    (70, 64, 64, 300, "prefix", 1.0),     # 4480 rows = 35 row blocks: > 1 raster group of rows
 ]
 
 
-@pytest.mark.parametrize("case", CASES, ids=lambda c: f"B{c[0]}T{c[1]}d{c[2]}V{c[3]}{c[4]}")
+@pytest.mark.parametrize("case", CASES, ids=lambda c: f"B{c[0]}T{c[1]}d{c[2]}V{c[3]}{c[4]}t{c[5]:.2f}")
 @pytest.mark.gpu
 @pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a CUDA device")
 def test_lmhead_parity(case):
     import paper_2410_18252_b200 as odpo
-    B, T, d, V, mk = case
+    B, T, d, V, mk, invT = case
     rows = np.arange(B * T)
     h, w = synth.lmhead_inputs(7, rows, d, V)
     tok = synth.tokens_rows(7, rows, V).reshape(B, T).astype(np.int32)
@@ -73,9 +74,10 @@ def test_lmhead_parity(case):
     hd = torch.from_numpy(h.reshape(B, T, d)).to(torch.bfloat16).cuda()   # exact (bf16 grid)
     wd = torch.from_numpy(w).to(torch.bfloat16).cuda()
     seq, tlp, lse, st = odpo.lmhead_seq_logprobs(hd, wd, torch.from_numpy(tok).cuda(),
-                                                 torch.from_numpy(mask).cuda())
+                                                 torch.from_numpy(mask).cuda(), inv_temperature=invT)
     torch.cuda.synchronize()
-    o = oracle.lmhead_seq_logprobs(h.reshape(B, T, d), w, tok, mask, n_threads=8)
+    o = oracle.lmhead_seq_logprobs(h.reshape(B, T, d), w, tok, mask, inv_temperature=invT,
+                                   n_threads=8)
     assert int(st.item()) == 0
     # fp32 tensor-core accumulation of exact bf16 products: per-token error << the bf16
     # contract (2e-3 relative on sequence log-probs)
