@@ -103,6 +103,7 @@ struct Args {
   const uint8_t* mask;    // [R]
   float2* parts;          // [R][NT] (m, r) of each vocabulary tile
   float* xtok;            // [R] the sampled token's logit (written by the tile holding it)
+  int64_t nrb2;           // 2-CTA kernel: 256-row blocks (one per CTA pair)
 };
 
 __device__ __forceinline__ void tile_coords(const Args& a, int64_t t, int64_t& rb, int64_t& n) {
@@ -256,6 +257,200 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
 }
 
+// ---------------------------------------------------------------- K6a2: the same, on CTA pairs
+// Thread-block clusters of 2 CTAs on the two SMs of a TPC run tcgen05.mma.cta_group::2 with
+// M = 256, N = 256: each CTA stages its own 128 hidden rows and HALF of the 256 weight rows of
+// the tile, so a CTA's tensor core reads 128 + 128 operand rows per K step instead of 128 + 256
+// (the 1-CTA kernel is bound by those shared-memory operand reads: ncu sm__mem_tensor 94%).
+// The leader (rank 0) issues the MMAs and commits with a 2-CTA multicast to both CTAs' stage /
+// accumulator barriers; both CTAs' TMA loads complete on the leader's stage barrier
+// (.cta_group::2 TMA, peer bit cleared), which expects both CTAs' bytes; the epilogue warps of
+// both CTAs release the leader's accumulator barrier (remote arrive).  Accumulator rows 0-127 sit
+// in the leader's TMEM, 128-255 in the peer's, so each CTA's epilogue drains its own rows.
+constexpr int STAGES2 = 6;
+constexpr int HALF_B = (BN / 2) * BK * 2;          // 16 KB: this CTA's half of the weight tile
+constexpr int STAGE2_BYTES = A_BYTES + HALF_B;     // 32 KB per CTA per stage
+constexpr int SMEM2 = STAGES2 * STAGE2_BYTES + 1024;
+constexpr uint32_t kIdesc2 = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                             ((uint32_t)(256 >> 4) << 24);
+constexpr uint32_t kPeerMask = 0xFEFFFFFFu;  // shared::cluster address -> the leader CTA's copy
+
+__device__ __forceinline__ void tma_2d_pair(uint32_t dst, const CUtensorMap* map, int c0, int c1,
+                                            uint32_t bar_leader) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(map), "r"(c0), "r"(c1), "r"(bar_leader)
+      : "memory");
+}
+__device__ __forceinline__ void mma_bf16_pair(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(kIdesc2), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit_pair(uint32_t bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
+      "h"((uint16_t)3)
+      : "memory");
+}
+
+__device__ __forceinline__ void tile_coords2(const Args& a, int64_t t, int64_t& rb2, int64_t& n) {
+  const int64_t grp = t / ((int64_t)a.G * a.NT);
+  const int64_t r0 = grp * a.G;
+  const int64_t gg = min((int64_t)a.G, a.nrb2 - r0);
+  const int64_t idx = t - grp * (int64_t)a.G * a.NT;
+  n = idx / gg;
+  rb2 = r0 + idx % gg;
+}
+
+__global__ void __launch_bounds__(THREADS, 1)
+    k_lmhead_fwd2(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+                  Args a) {
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t full[STAGES2], empty[STAGES2], tfull[2], tempty[2];
+  __shared__ uint32_t tmem_sh;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES2; ++s) {
+      mbar_init(&full[s], 1);    // the leader's producer (expect_tx of both CTAs' bytes)
+      mbar_init(&empty[s], 1);   // the leader's multicast MMA commit
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull[s], 1);   // multicast commit
+      mbar_init(&tempty[s], 8);  // 4 epilogue warps x 2 CTAs (leader's copy is the one used)
+    }
+    mbar_fence_init();
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&mapA) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&mapB) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&tmem_sh)),
+                 "n"(TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cluster_sync_all();  // both CTAs' barriers initialised and TMEM allocated
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = tmem_sh;
+  const uint32_t full_s = smem_u32(full), empty_s = smem_u32(empty);
+  const uint32_t tfull_s = smem_u32(tfull), tempty_s = smem_u32(tempty);
+  const int nkb = (int)(a.d / BK);
+  const int64_t cl = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  const int64_t Tt = a.nrb2 * a.NT;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ================= TMA producer (both CTAs): own hidden rows + own half of the weights
+      int st = 0;
+      uint32_t ph = 0;
+      for (int64_t t = cl; t < Tt; t += ncl) {
+        int64_t rb2, nt;
+        tile_coords2(a, t, rb2, nt);
+        const int arow = (int)(rb2 * 256 + rank * 128);
+        const int vrow = (int)(nt * BN + rank * (BN / 2));
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(empty_s + 8 * st, ph ^ 1u);
+          const uint32_t sa = base + (uint32_t)(st * STAGE2_BYTES);
+          const uint32_t fb = (full_s + 8 * st) & kPeerMask;
+          if (leader) mbar_arrive_tx(full_s + 8 * st, 2 * STAGE2_BYTES);
+          tma_2d_pair(sa, &mapA, kb * BK, arow, fb);
+          tma_2d_pair(sa + A_BYTES, &mapB, kb * BK, vrow, fb);
+          if (++st == STAGES2) { st = 0; ph ^= 1u; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && leader) {
+      // ================= MMA issuer (leader CTA, one thread): M = 256 across the pair
+      int st = 0;
+      uint32_t ph = 0;
+      int acc = 0;
+      uint32_t aph = 0;
+      for (int64_t t = cl; t < Tt; t += ncl) {
+        mbar_wait(tempty_s + 8 * acc, aph ^ 1u);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t td = tmem + (uint32_t)(acc * BN);
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(full_s + 8 * st, ph);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t sa = base + (uint32_t)(st * STAGE2_BYTES);
+          const uint64_t da = sdesc(sa), db = sdesc(sa + A_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / UK; ++k)
+            mma_bf16_pair(td, da + (uint64_t)(2 * k), db + (uint64_t)(2 * k), (kb | k) != 0);
+          mma_commit_pair(empty_s + 8 * st);  // frees this stage in both CTAs
+          if (++st == STAGES2) { st = 0; ph ^= 1u; }
+        }
+        mma_commit_pair(tfull_s + 8 * acc);   // accumulator complete in both CTAs
+        if (++acc == 2) { acc = 0; aph ^= 1u; }
+      }
+    }
+  } else {
+    // ================= epilogue warps 2..5 (both CTAs): this CTA's 128 accumulator rows
+    const int q = warp & 3;
+    const uint32_t lane_base = (uint32_t)(32 * q) << 16;
+    const uint32_t tempty_leader = mapa(tempty_s, 0);
+    const float k2 = a.invT * kLog2e;
+    int acc = 0;
+    uint32_t aph = 0;
+    for (int64_t t = cl; t < Tt; t += ncl) {
+      int64_t rb2, n;
+      tile_coords2(a, t, rb2, n);
+      const int64_t row = rb2 * 256 + rank * 128 + 32 * q + lane;
+      const bool live = row < a.R;
+      const int tok = live ? a.tokens[row] : -1;
+      MR s{-INFINITY, 0.f};
+      mbar_wait(tfull_s + 8 * acc, aph);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int64_t c0 = n * BN;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t r[32];
+        tm_ld32(tmem + lane_base + (uint32_t)(acc * BN + c * 32), r);
+        const int64_t cb = c0 + 32 * c;
+        if (cb >= a.V) break;
+        if (cb + 32 > a.V) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (cb + j >= a.V) r[j] = Traits<0>::kNegInfWord;
+        }
+        if (live && tok >= cb && tok < cb + 32) {
+          float x = 0.f;
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (tok == cb + j) x = __uint_as_float(r[j]);
+          a.xtok[row] = x;
+        }
+        uint4 v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = make_uint4(r[4 * j], r[4 * j + 1], r[4 * j + 2], r[4 * j + 3]);
+        mr_batch<0, 8, 0>(v, k2, s.m, s.r);
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cl(tempty_leader + 8 * acc);
+      if (++acc == 2) { acc = 0; aph ^= 1u; }
+      if (live) a.parts[row * a.NT + n] = make_float2(s.m, s.r);
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cluster_sync_all();  // no CTA frees TMEM (or exits) while its peer can still touch it
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS)
+                 : "memory");
+  }
+}
+
 // ---------------------------------------------------------------- K6b: merge, K6c: sequence sums
 // K6b: one warp per row: lane l merges vocabulary tiles l, l+32, ... in order, then the fixed
 // shfl_down tree; lane 0 forms logp and lse (the logits path's arithmetic).
@@ -371,12 +566,15 @@ odpo_status odpo_lmhead_seq_logprobs(const void* hidden, const void* weight, int
   const int64_t R = B * T;
   if (R > (int64_t)INT32_MAX || V > (int64_t)INT32_MAX || d > (1 << 20)) return ODPO_ERR_UNSUPPORTED;
   if (!workspace || workspace_bytes < odpo_lmhead_workspace_bytes(B, T, V)) return ODPO_ERR_WORKSPACE;
+  const char* one = getenv("ODPO_LMH_1CTA");  // tuning / comparison: the single-CTA kernel
+  const bool pair = !(one && atoi(one) != 0);
   CUtensorMap mA, mB;
-  if (!make_map(&mA, hidden, R, d, d, BM) || !make_map(&mB, weight, V, d, d, BN))
+  if (!make_map(&mA, hidden, R, d, d, BM) || !make_map(&mB, weight, V, d, d, pair ? BN / 2 : BN))
     return ODPO_ERR_CUDA;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_lmhead_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    cudaFuncSetAttribute(k_lmhead_fwd2, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2);
     attr = true;
   }
   const int sms = sm_count();
@@ -393,8 +591,30 @@ odpo_status odpo_lmhead_seq_logprobs(const void* hidden, const void* weight, int
   a.xtok = reinterpret_cast<float*>(reinterpret_cast<char*>(workspace) + (size_t)R * a.NT * sizeof(float2));
   float* tlp = tok_logp ? tok_logp : a.xtok + R;  // log-prob scratch when not requested
   cudaStream_t s = (cudaStream_t)stream;
-  const int grid = (int)(a.Ttot < sms ? a.Ttot : sms);
-  k_lmhead_fwd<<<grid, THREADS, SMEM, s>>>(mA, mB, a);
+  if (pair) {
+    a.nrb2 = (R + 255) / 256;
+    a.G = kRasterG / 2;
+    if (const char* g = getenv("ODPO_LMH_G")) a.G = atoi(g) > 0 ? atoi(g) : a.G;  // tuning
+    const int64_t t2 = a.nrb2 * a.NT;
+    int clusters = sms / 2;
+    if (clusters > t2) clusters = (int)t2;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(2 * clusters));
+    cfg.blockDim = dim3(THREADS);
+    cfg.dynamicSmemBytes = SMEM2;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k_lmhead_fwd2, mA, mB, a);
+  } else {
+    const int grid = (int)(a.Ttot < sms ? a.Ttot : sms);
+    k_lmhead_fwd<<<grid, THREADS, SMEM, s>>>(mA, mB, a);
+  }
   if (cudaGetLastError() != cudaSuccess) return ODPO_ERR_CUDA;
   k_lmhead_merge<<<(unsigned)((R + 7) / 8), 256, 0, s>>>(a, tlp, row_lse, status);
   if (cudaGetLastError() != cudaSuccess) return ODPO_ERR_CUDA;
