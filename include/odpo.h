@@ -377,6 +377,25 @@ const char* odpo_version(void);
  * encoding failed).
  */
 size_t odpo_lmhead_workspace_bytes(int64_t B, int64_t T, int64_t V);
+
+/*
+ * odpo_online_dpo_loss_from_token_logp -- the Online-DPO loss (Sec 2.1; S3/S4 of
+ * SURVEY.md §8(a)) from per-token policy log-probs, e.g. those odpo_lmhead_seq_logprobs
+ * produced without logits.  Same pair reduction (fixed-order sequence sums, z, -log sigma,
+ * statistics, coefficients) as odpo_online_dpo_loss_fwd_bwd.
+ *   tok_logp   fp32 [B, T] per-token log pi (read where mask = 1 only).
+ *   ref_logp, mask, pair_rows, P, P_global, beta, inv_temperature, seq_logp, pair_logit,
+ *   stats, status, workspace: as odpo_online_dpo_loss_fwd_bwd (workspace >=
+ *   odpo_workspace_bytes(B, T, P)).
+ *   row_scale  fp32 [B, T] output (may be NULL): coef_b * mask[b, t], the per-row factor of the
+ *              gradient with respect to the logits (d loss / d logits = row_scale * G).
+ * Errors: INVALID_ARG, UNSUPPORTED, WORKSPACE, CUDA.
+ */
+odpo_status odpo_online_dpo_loss_from_token_logp(
+    const float* tok_logp, int64_t B, int64_t T, const float* ref_logp, const uint8_t* mask,
+    const int32_t* pair_rows, int64_t P, int64_t P_global, float beta, float inv_temperature,
+    float* seq_logp, float* pair_logit, double* stats, float* row_scale, uint32_t* status,
+    void* workspace, size_t workspace_bytes, void* stream);
 odpo_status odpo_lmhead_seq_logprobs(const void* hidden, const void* weight, int64_t B, int64_t T,
                                      int64_t d, int64_t V, const int32_t* tokens,
                                      const uint8_t* mask, float inv_temperature, float* tok_logp,

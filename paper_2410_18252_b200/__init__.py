@@ -94,6 +94,9 @@ def _L():
         L.odpo_lmhead_seq_logprobs.restype = C.c_int
         L.odpo_lmhead_workspace_bytes.argtypes = [i64, i64, i64]
         L.odpo_lmhead_workspace_bytes.restype = sz
+        L.odpo_online_dpo_loss_from_token_logp.argtypes = [P, i64, i64, P, P, P, i64, i64, f32,
+                                                           f32, P, P, P, P, P, P, sz, P]
+        L.odpo_online_dpo_loss_from_token_logp.restype = C.c_int
         L.odpo_workspace_bytes.argtypes = [i64, i64, i64]
         L.odpo_workspace_bytes.restype = sz
         L.odpo_status_string.argtypes = [C.c_int]
@@ -260,6 +263,37 @@ def lmhead_seq_logprobs(hidden: torch.Tensor, weight: torch.Tensor, tokens: torc
                                          _p(status), _p(ws), ws.numel(), _stream()),
            "odpo_lmhead_seq_logprobs")
     return seq, tok, lse, status
+
+
+def lmhead_online_dpo_loss_fwd(hidden: torch.Tensor, weight: torch.Tensor,
+                               ref_logp: torch.Tensor, tokens: torch.Tensor, mask: torch.Tensor,
+                               beta: float, pair_rows: torch.Tensor | None = None,
+                               p_global: int | None = None, inv_temperature: float = 1.0):
+    """NEXT-2 forward: the Online-DPO loss, statistics and per-row gradient scale straight from
+    the policy's LM head (hidden [B, T, d] bf16, weight [V, d] bf16), logits never stored.
+    Returns LossOutput with dlogits = None and row_scale [B, T] = coef_b * mask."""
+    _, tok_logp, _, status = lmhead_seq_logprobs(hidden, weight, tokens, mask, inv_temperature)
+    B, T = tok_logp.shape
+    dev = hidden.device
+    ref_logp = _dev(ref_logp, "ref_logp", torch.float32).contiguous()
+    mask = _dev(mask, "mask", torch.uint8).contiguous()
+    if pair_rows is not None:
+        pair_rows = _dev(pair_rows, "pair_rows", torch.int32).contiguous()
+        P = pair_rows.shape[0]
+    else:
+        P = B // 2
+    Pg = P if p_global is None else int(p_global)
+    seq = torch.empty(B, dtype=torch.float32, device=dev)
+    z = torch.empty(max(P, 1), dtype=torch.float32, device=dev)
+    stats = torch.zeros(STATS_BUF, dtype=torch.float64, device=dev)
+    row_scale = torch.empty((B, T), dtype=torch.float32, device=dev)
+    ws = _workspace(dev, workspace_bytes(B, T, P))
+    _check(_L().odpo_online_dpo_loss_from_token_logp(
+        _p(tok_logp), B, T, _p(ref_logp), _p(mask), _p(pair_rows), P, Pg, float(beta),
+        float(inv_temperature), _p(seq), _p(z), _p(stats), _p(row_scale), _p(status), _p(ws),
+        ws.numel(), _stream()), "odpo_online_dpo_loss_from_token_logp")
+    return LossOutput(stats=stats, dlogits=None, seq_logp=seq, z=z, status=status, launches=5,
+                      row_scale=row_scale)
 
 
 @dataclass

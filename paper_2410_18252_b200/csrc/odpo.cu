@@ -1738,6 +1738,37 @@ odpo_status odpo_online_dpo_loss_fwd_bwd(const void* policy_logits, odpo_dtype d
                                          nullptr, stream);
 }
 
+odpo_status odpo_online_dpo_loss_from_token_logp(
+    const float* tok_logp, int64_t B, int64_t T, const float* ref_logp, const uint8_t* mask,
+    const int32_t* pair_rows, int64_t P, int64_t P_global, float beta, float inv_temperature,
+    float* seq_logp, float* pair_logit, double* stats, float* row_scale, uint32_t* status,
+    void* workspace, size_t workspace_bytes, void* stream) {
+  if (!tok_logp || !ref_logp || !mask || !seq_logp || !stats) return ODPO_ERR_INVALID_ARG;
+  if (B <= 0 || T <= 0 || P <= 0 || P_global < P) return ODPO_ERR_INVALID_ARG;
+  if (!finite_pos(beta) || !finite_pos(inv_temperature)) return ODPO_ERR_INVALID_ARG;
+  if (!pair_rows && B != 2 * P) return ODPO_ERR_INVALID_ARG;
+  if (B * T > (int64_t)INT32_MAX || P > (int64_t)INT32_MAX / 2) return ODPO_ERR_UNSUPPORTED;
+  if (!workspace || workspace_bytes < ws_layout(B, T, P, nullptr, nullptr)) return ODPO_ERR_WORKSPACE;
+  Workspace w;
+  ws_layout(B, T, P, (char*)workspace, &w);
+  w.row_logp = const_cast<float*>(tok_logp);  // the pair reduction reads (never writes) these
+  cudaStream_t s = (cudaStream_t)stream;
+  LossArgs a;
+  base_args(a, nullptr, B, T, 1, T, 1, nullptr, mask, inv_temperature, status, w, 2);
+  a.ref = ref_logp; a.pair_rows = pair_rows;
+  a.P = P; a.Pg = (double)P_global; a.beta = beta;
+  a.seq_logp = seq_logp; a.z_out = pair_logit; a.stats = stats;
+  a.row_scale = row_scale;
+  // rows of unreferenced sequences get row_scale 0; the pair reduction writes the others
+  if (row_scale && cudaMemsetAsync(row_scale, 0, (size_t)(B * T) * sizeof(float), s) != cudaSuccess)
+    return ODPO_ERR_CUDA;
+  k_prep<<<1, kPrepThreads, 0, s>>>(pair_rows, B, P, w, status);
+  odpo_status e;
+  if ((e = launched()) != ODPO_OK) return e;
+  k_pair_reduce<<<(unsigned)P, 32, 0, s>>>(a);
+  return launched();
+}
+
 odpo_status odpo_online_dpo_loss_fwd_bwd_unscaled(
     const void* policy_logits, odpo_dtype dt, int64_t B, int64_t T, int64_t V, int64_t stride_b,
     int64_t stride_t, const float* ref_logp, const int32_t* tokens, const uint8_t* mask,

@@ -103,3 +103,42 @@ def test_lmhead_token_range_flag():
                                            torch.from_numpy(w).to(torch.bfloat16).cuda(),
                                            torch.from_numpy(tok).cuda(), torch.from_numpy(mask).cuda())
     assert int(st.item()) & odpo.FLAGS["TOKEN_RANGE"]
+
+
+@pytest.mark.parametrize("permute", [False, True])
+@pytest.mark.gpu
+@pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a CUDA device")
+def test_lmhead_dpo_loss_parity(permute):
+    """The Online-DPO loss forward from the LM head (odpo_lmhead_seq_logprobs ->
+    odpo_online_dpo_loss_from_token_logp) against the oracle's loss on the head's fp64 logits:
+    sequence log-probs, z, loss and the statistics, and row_scale = coef_b * mask."""
+    import paper_2410_18252_b200 as odpo
+    P, T, d, V, extra = 5, 9, 128, 1000, (2 if permute else 0)
+    B = 2 * P + extra
+    rows = np.arange(B * T)
+    h, w = synth.lmhead_inputs(11, rows, d, V)
+    tok = synth.tokens_rows(11, rows, V).reshape(B, T).astype(np.int32)
+    mask = synth.mask_for(11, np.arange(B), T, "prefix", 5)
+    pr = synth.permutation(11, B)[: 2 * P].reshape(P, 2).astype(np.int32) if permute else None
+    ref = (synth.rewards_for(11, B, 1).reshape(-1) - 40.0).astype(np.float32)
+    beta = 0.1
+    out = odpo.lmhead_online_dpo_loss_fwd(
+        torch.from_numpy(h.reshape(B, T, d)).to(torch.bfloat16).cuda(),
+        torch.from_numpy(w).to(torch.bfloat16).cuda(), torch.from_numpy(ref).cuda(),
+        torch.from_numpy(tok).cuda(), torch.from_numpy(mask).cuda(), beta,
+        pair_rows=None if pr is None else torch.from_numpy(pr).cuda(), p_global=P + 1)
+    torch.cuda.synchronize()
+    logits = (h @ w.T).reshape(B, T, V)
+    o = oracle.online_dpo_loss_fwd_bwd(logits, ref, tok, mask, beta, pair_rows=pr, p_global=P + 1,
+                                       unscaled=True, n_threads=8)
+    live = np.arange(B) if pr is None else pr.reshape(-1)
+    S = out.seq_logp.cpu().numpy().astype(np.float64)
+    assert np.all(np.abs(S[live] - o["seq_logp"][live]) <= 1e-4 * np.maximum(1, np.abs(o["seq_logp"][live])))
+    z = out.z.cpu().numpy().astype(np.float64)
+    assert np.all(np.abs(z - o["z"]) <= 1e-4 * np.maximum(1, np.abs(o["z"])))
+    st = out.stats.cpu().numpy()
+    assert st[0] == o["stats"][0] and st[8] == o["stats"][8] and st[9] == o["stats"][9]
+    assert abs(st[1] - o["stats"][1]) <= 1e-4 * max(1.0, abs(o["stats"][1]))
+    rs = out.row_scale.cpu().numpy().astype(np.float64)
+    assert np.all(np.abs(rs - o["row_scale"]) <= 1e-4 * np.abs(o["row_scale"]) + 1e-12)
+    assert int(out.status.item()) & ~odpo.FLAGS["DEGENERATE_PAIR"] == 0
