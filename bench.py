@@ -330,7 +330,7 @@ def run_ours(args, rank, world, local_rank):
                 logits, ref, tok, msk, w.beta, pair_rows=pair_rows, p_global=Pg, G=dlogits,
                 row_scale=row_scale, ctas_per_sm=args.ctas_per_sm, exp2_split=args.exp2_split,
                 lookahead=args.lookahead, row_gap=args.row_gap, engine=args.engine, stats=stats,
-                status=status)
+                status=status, schedule="resident" if args.schedule == "resident" else "auto")
         return odpo.online_dpo_loss_fwd_bwd(logits, ref, tok, msk, w.beta, pair_rows=pair_rows,
                                             p_global=Pg, dlogits=dlogits, schedule=args.schedule,
                                             lag_pairs=args.lag, ctas_per_sm=args.ctas_per_sm,

@@ -368,10 +368,11 @@ def online_dpo_loss_fwd_bwd_unscaled(policy_logits: torch.Tensor, ref_logp: torc
                                      inplace: bool = False, G: torch.Tensor | None = None,
                                      row_scale: torch.Tensor | None = None, ctas_per_sm: int = 0,
                                      exp2_split: int = -1, lookahead: int = -1, row_gap: int = -1,
-                                     engine: int = -1,
+                                     engine: int = -1, schedule: str = "auto",
                                      stats: torch.Tensor | None = None,
                                      status: torch.Tensor | None = None) -> LossOutput:
-    """The loss call with the gradient factored per row: out.dlogits holds
+    """The loss call with the gradient factored per row (schedule "auto" = the row engine,
+    or "resident": each row's backward read back from tensor memory): out.dlogits holds
     G = mask (softmax - onehot) and out.row_scale [B, T] holds coef_b * mask, so the gradient
     is out.row_scale[..., None] * out.dlogits (one HBM read and one write of the logits)."""
     dt, B, T, V, sb, st = _logits_meta(policy_logits, "policy_logits")
@@ -405,7 +406,7 @@ def online_dpo_loss_fwd_bwd_unscaled(policy_logits: torch.Tensor, ref_logp: torc
     if status is None:
         status = torch.zeros(1, dtype=torch.int32, device=dev)
     ws = _workspace(dev, workspace_bytes(B, T, max(P, 1)))
-    opts = _Opts(SCHEDULES["auto"], 0, int(ctas_per_sm), 0, int(exp2_split), int(lookahead),
+    opts = _Opts(SCHEDULES[schedule], 0, int(ctas_per_sm), 0, int(exp2_split), int(lookahead),
                  int(row_gap), int(engine))
     _check(_L().odpo_online_dpo_loss_fwd_bwd_unscaled(
         _p(policy_logits), dt, B, T, V, sb, st, _p(ref_logp), _p(tokens), _p(mask), _p(pair_rows),

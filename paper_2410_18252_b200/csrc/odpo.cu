@@ -1353,21 +1353,43 @@ static void setup_geo(DevInfo& d, int g) {
   setup_one<1, M_UNSC, 0, GE>(&d.occ[g][1][M_UNSC]);
 }
 
+static ResGeo res_geo(int64_t V, int64_t T, int es, int sms, int cap);
+static odpo_status launched();
+static const struct DevInfo& dev_info(int dev);
+
 template <int PV>
 static void setup_res() {
-  cudaFuncSetAttribute(k_resident<1, PV>, cudaFuncAttributeMaxDynamicSharedMemorySize, kResSmemMax);
-  if constexpr (PV == 0)
-    cudaFuncSetAttribute(k_resident<0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kResSmemMax);
+  cudaFuncSetAttribute(k_resident<1, PV, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kResSmemMax);
+  if constexpr (PV == 0) {
+    cudaFuncSetAttribute(k_resident<0, 0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kResSmemMax);
+    cudaFuncSetAttribute(k_resident<0, 0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kResSmemMax);
+    cudaFuncSetAttribute(k_resident<1, 0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kResSmemMax);
+  }
   if constexpr (PV + 1 < kNumPoly) setup_res<PV + 1>();
 }
 template <int PV>
 static void launch_res_bf16(int pv, int grid, int smem, const LossArgs& a, const ResGeo& g,
                             cudaStream_t s) {
   if (pv == PV) {
-    k_resident<1, PV><<<grid, kResThreads, smem, s>>>(a, g);
+    k_resident<1, PV, 0><<<grid, kResThreads, smem, s>>>(a, g);
     return;
   }
   if constexpr (PV + 1 < kNumPoly) launch_res_bf16<PV + 1>(pv, grid, smem, a, g, s);
+}
+// the factored / known-coefficient RESIDENT mode (MUFU exp2 only); no pair waits, so any
+// shape whose row fits the TMEM slots applies
+static odpo_status launch_res_un(int dti, const LossArgs& a, int64_t V, int64_t es, int cap,
+                                 cudaStream_t s) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const DevInfo& di = dev_info(dev);
+  ResGeo rg = res_geo(V, 1, (int)es, di.sms, cap);
+  if (rg.nsl <= 0) return ODPO_ERR_UNSUPPORTED;
+  const int ring_bytes = (rg.rf + rg.rbs) * kChunk;
+  const int smem = ring_bytes > kResSmemMin ? ring_bytes : kResSmemMin;
+  if (dti == 0) k_resident<0, 0, 1><<<di.sms, kResThreads, smem, s>>>(a, rg);
+  else k_resident<1, 0, 1><<<di.sms, kResThreads, smem, s>>>(a, rg);
+  return launched();
 }
 
 static const DevInfo& dev_info(int dev) {
@@ -1688,7 +1710,7 @@ odpo_status odpo_online_dpo_loss_fwd_bwd_ex(const void* policy_logits, odpo_dtyp
   if (sched == ODPO_SCHED_RESIDENT) {
     const int ring_bytes = (rg.rf + rg.rbs) * kChunk;
     const int smem = ring_bytes > kResSmemMin ? ring_bytes : kResSmemMin;
-    if (dti == 0) k_resident<0, 0><<<di.sms, kResThreads, smem, s>>>(a, rg);
+    if (dti == 0) k_resident<0, 0, 0><<<di.sms, kResThreads, smem, s>>>(a, rg);
     else launch_res_bf16<0>(pv, di.sms, smem, a, rg, s);
     if ((e = launched()) != ODPO_OK) return e;
     launches += 1;
@@ -1781,7 +1803,8 @@ odpo_status odpo_online_dpo_loss_fwd_bwd_unscaled(
                              gstride_t, seq_logp, stats, workspace, workspace_bytes);
   if (e != ODPO_OK) return e;
   if (!row_scale) return ODPO_ERR_INVALID_ARG;
-  if (opts && opts->schedule != ODPO_SCHED_AUTO) return ODPO_ERR_UNSUPPORTED;
+  const bool resident = opts && opts->schedule == ODPO_SCHED_RESIDENT;
+  if (opts && opts->schedule != ODPO_SCHED_AUTO && !resident) return ODPO_ERR_UNSUPPORTED;
   const int pv = (opts && opts->exp2_split >= 0) ? opts->exp2_split : kPolyDefault;
   if (pv >= kNumPoly) return ODPO_ERR_UNSUPPORTED;
   Workspace w;
@@ -1802,6 +1825,14 @@ odpo_status odpo_online_dpo_loss_fwd_bwd_unscaled(
   a.row_gap = (opts && opts->row_gap >= 0) ? opts->row_gap : 0;
   k_prep<<<1, kPrepThreads, 0, s>>>(pair_rows, B, P, w, status);
   if ((e = launched()) != ODPO_OK) return e;
+  if (resident) {
+    if (pv != 0) return ODPO_ERR_UNSUPPORTED;
+    if ((e = launch_res_un(dt == ODPO_F32 ? 0 : 1, a, V, dt == ODPO_F32 ? 4 : 2, opts->lookahead,
+                           s)) != ODPO_OK)
+      return e;
+    opts->launches = 2;
+    return ODPO_OK;
+  }
   const int geo = opts ? opts->engine : -1;
   if ((e = launch_engine(dt == ODPO_F32 ? 0 : 1, M_UNSC, pv, a, opts ? opts->ctas_per_sm : 0, s,
                          geo)) != ODPO_OK)

@@ -191,7 +191,11 @@ __device__ __forceinline__ void tm_ld16(uint32_t taddr, uint4 (&v)[4]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-template <int DT, int PV>
+// UN = 0: the scaled Online-DPO output (the coefficient waits for the pair).  UN = 1: the
+// factored gradient G = softmax - onehot, or coef_b G with a coefficient known before the call
+// (App B losses, a.coef_known) -- no row waits on another row, so a row's backward follows its
+// forward straight out of TMEM (exactly 1R+1W, no pair-completion latency).
+template <int DT, int PV, int UN>
 __global__ void __launch_bounds__(kResThreads, 1) k_resident(LossArgs a, ResGeo G) {
   constexpr int N = Traits<DT>::N;
   constexpr int NPF = DT == 1 ? kPoly[PV].npf : 0;  // exp2 split
@@ -206,6 +210,7 @@ __global__ void __launch_bounds__(kResThreads, 1) k_resident(LossArgs a, ResGeo 
   __shared__ __align__(8) uint64_t it_empty[kResNIt];
   __shared__ __align__(8) uint64_t part_ready[kResNIt];
   __shared__ __align__(8) uint64_t param_ready[kResNIt];
+  __shared__ __align__(8) uint64_t stat_ready[kResNIt];  // epilogue -> parameter warp
   __shared__ __align__(16) ResItem items[kResNIt];
   __shared__ uint32_t tm_base_sh;
   __shared__ int l2_out;  // L2-backed rows claimed and not yet through their backward
@@ -224,6 +229,7 @@ __global__ void __launch_bounds__(kResThreads, 1) k_resident(LossArgs a, ResGeo 
       mbar_init(&it_empty[i], 2 + kResBW);  // epilogue + parameter warp + backward warps
       mbar_init(&part_ready[i], kResFW);
       mbar_init(&param_ready[i], 1);
+      mbar_init(&stat_ready[i], 1);
     }
     l2_out = 0;
     f_q = 0;
@@ -248,6 +254,7 @@ __global__ void __launch_bounds__(kResThreads, 1) k_resident(LossArgs a, ResGeo 
   const uint32_t tfree_s = smem_u32(tm_free);
   const uint32_t itf_s = smem_u32(it_full), ite_s = smem_u32(it_empty);
   const uint32_t pready_s = smem_u32(part_ready), mready_s = smem_u32(param_ready);
+  const uint32_t sready_s = smem_u32(stat_ready);
   const int64_t T = a.T;
   const int V = (int)a.V;
   const int nvec = V / N;
@@ -546,15 +553,20 @@ __global__ void __launch_bounds__(kResThreads, 1) k_resident(LossArgs a, ResGeo 
         ResItem& I = items[it];
         const int kind = I.kind;
         if (kind == R_END) break;
+        mbar_wait(sready_s + 8 * it, ph);  // this row's statistics are in the item
         if (kind == R_LIVE) {
-          unsigned long long w;
-          while (!((w = ld_relaxed_u64(&a.w.seq_cf[I.s])) & kCfReady)) __nanosleep(20);
-          // acquire: the pair reduction followed this row's count, which followed the
-          // epilogue's writes of m, l1p, logp into the item
-          fence_acq_rel_gpu();
-          const float coef = __uint_as_float((uint32_t)w);
+          float coef;
+          if (UN) {
+            // G (coef 1) or the known coefficient (k_pg_coef ran before this kernel)
+            coef = a.coef_known ? __ldcg(a.w.seq_coef + I.s) : 1.f;
+          } else {
+            unsigned long long w;
+            while (!((w = ld_relaxed_u64(&a.w.seq_cf[I.s])) & kCfReady)) __nanosleep(20);
+            fence_acq_rel_gpu();
+            coef = __uint_as_float((uint32_t)w);
+          }
           const float m = I.m, l1p = I.l1p, logp = I.logp;
-          I.c = fmaf(l1p, kLog2e, m * k2) - log2f(fabsf(coef));
+          I.c = coef != 0.f ? fmaf(l1p, kLog2e, m * k2) - log2f(fabsf(coef)) : INFINITY;
           I.coef = coef;
           I.gtok = coef * expm1f(logp);
           RES_DBG(I.tk, 4);
@@ -601,6 +613,9 @@ __global__ void __launch_bounds__(kResThreads, 1) k_resident(LossArgs a, ResGeo 
           flag(a.status, fl);
         }
       }
+      if (UN && kind == R_ZERO && lane == 0 && a.row_scale) a.row_scale[I.g] = 0.f;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(sready_s + 8 * it);
       if (kind == R_LIVE || kind == R_MASK || kind == R_NONE) {
         unsigned last = 0;
         if (lane == 0) last = (atom_add_acq_rel(&a.w.pair_cnt[I.p], 1u) == (unsigned)(2 * T) - 1u);

@@ -49,14 +49,16 @@ CASES = [
 
 
 @pytest.mark.parametrize("case", CASES, ids=lambda c: f"P{c[0]}T{c[1]}V{c[2]}{c[3]}{c[4]}x{c[5]}")
-@pytest.mark.parametrize("engine,row_gap", [(-1, -1), (0, 1), (1, 0)])
-def test_unscaled_parity_small(odpo, case, engine, row_gap):
+@pytest.mark.parametrize("engine,row_gap,sched", [(-1, -1, "auto"), (0, 1, "auto"), (1, 0, "auto"),
+                                                  (-1, -1, "resident")])
+def test_unscaled_parity_small(odpo, case, engine, row_gap, sched):
+    """sched "resident": each row's backward read back from tensor memory (k_resident, UN)."""
     P, T, V, dt, mk, extra, invT = case
     b = Batch(P, T, V, dt, seed=2, mask_kind=mk, lbar=max(1, T // 2), extra_seqs=extra, invT=invT)
     ref = (synth.rewards_for(2, b.B, 1).reshape(-1) - 30.0).astype(np.float32)
     beta, Pg = 0.1, P + 3
     d_ref = torch.from_numpy(ref).cuda()
-    out = run_unscaled(odpo, b, d_ref, beta, Pg=Pg, engine=engine, row_gap=row_gap)
+    out = run_unscaled(odpo, b, d_ref, beta, Pg=Pg, engine=engine, row_gap=row_gap, schedule=sched)
     o = oracle.online_dpo_loss_fwd_bwd(b.h_logits, ref, b.tokens, b.mask, beta,
                                        pair_rows=b.pair_rows, p_global=Pg, inv_temperature=invT,
                                        want_dlogits=True, n_threads=NCPU, unscaled=True)
@@ -113,6 +115,8 @@ def test_best_worst_of_k4_workload(odpo):
     b.d_pair_rows = sel.pair_rows
     ref = np.full(b.B, -0.5 * T, np.float32)
     out = run_unscaled(odpo, b, torch.from_numpy(ref).cuda(), 0.1)
+    res = run_unscaled(odpo, b, torch.from_numpy(ref).cuda(), 0.1, schedule="resident")
+    assert torch.equal(res.dlogits, out.dlogits) and torch.equal(res.row_scale, out.row_scale)
     o = oracle.online_dpo_loss_fwd_bwd(b.h_logits, ref, b.tokens, b.mask, 0.1,
                                        pair_rows=b.pair_rows, want_dlogits=True, n_threads=NCPU,
                                        unscaled=True)
@@ -152,6 +156,12 @@ def test_unscaled_full_size_sampled(odpo, name, mask_kind):
     # every live row of G sums to ~0 (softmax sums to 1): a property at any size
     s = out.dlogits[:, :4].float().sum(dim=2)
     assert float(s.abs().max()) < 0.02
+    if w.V * 2 <= (128 << 10):
+        # the RESIDENT factored gradient (rows read back from TMEM) gives the same bits
+        res = run_unscaled(odpo, b, ref, w.beta, schedule="resident")
+        assert torch.equal(res.dlogits, out.dlogits) and torch.equal(res.row_scale, out.row_scale)
+        assert torch.equal(res.seq_logp, seq) and torch.equal(res.stats[:10], stats)
+        del res
     del out
     # same engine geometry as the unscaled call's automatic choice (the geometry fixes the
     # per-row reduction tree): geometry 1 for rows longer than 128 KB
