@@ -41,6 +41,8 @@ struct Workspace {
   unsigned* pair_bcnt; // backward rows dispensed per pair (FUSED dispatch)
   double* pair_vals;   // [P][ODPO_NSTATS]
   unsigned long long* seq_cf;  // [B] ready bit (bit 32) | fp32 bits of the sequence's coef
+  float4* fparts;      // [B*T][kFS] forward-part partials (m, r, x_tok, owns tok) (kFS > 1)
+  unsigned* fpart_cnt; // [B*T] forward parts done (kFS > 1)
   unsigned long long* dbg_t;  // debug builds: [P][4] timestamps
   unsigned* counters;  // [0] ticket, [1] pairs done, [2] n_unref
 };
@@ -71,6 +73,8 @@ static size_t ws_layout(int64_t B, int64_t T, int64_t P, char* base, Workspace* 
   char* p_pb = take((size_t)P * 4);
   char* p_pv = take((size_t)P * ODPO_NSTATS * 8);
   char* p_cf = take((size_t)B * 8);
+  char* p_fp = kFS > 1 ? take(rows * kFS * 16) : nullptr;
+  char* p_fc = kFS > 1 ? take(rows * 4) : nullptr;
   char* p_ct = take(C_COUNT * 4);
 #ifdef ODPO_DEBUG_LEAD
   char* p_dt = take((size_t)P * 4 * 8);
@@ -91,6 +95,8 @@ static size_t ws_layout(int64_t B, int64_t T, int64_t P, char* base, Workspace* 
     w->pair_bcnt = (unsigned*)p_pb;
     w->pair_vals = (double*)p_pv;
     w->seq_cf = (unsigned long long*)p_cf;
+    w->fparts = (float4*)p_fp;
+    w->fpart_cnt = (unsigned*)p_fc;
     w->counters = (unsigned*)p_ct;
   }
   return off;
@@ -170,9 +176,11 @@ constexpr int kPrepThreads = 1024;
 
 __global__ void __launch_bounds__(kPrepThreads) k_prep(const int32_t* __restrict__ pair_rows,
                                                        int64_t B, int64_t P, Workspace w,
-                                                       uint32_t* status) {
+                                                       uint32_t* status, int64_t rows = 0) {
   __shared__ int scan[kPrepThreads];
   const int tid = threadIdx.x;
+  if (w.fpart_cnt)
+    for (int64_t g = tid; g < rows; g += kPrepThreads) w.fpart_cnt[g] = 0;
   for (int64_t b = tid; b < B; b += kPrepThreads) {
     w.seq_pair[b] = -1;
     w.seq_cnt[b] = 0;
@@ -556,6 +564,7 @@ struct Dispatch {
 // only when may_block is false -- the producer then streams the rows it already holds).
 __device__ __forceinline__ int fused_next(const LossArgs& a, int64_t totalF, int64_t nzero,
                                           Dispatch& D, bool may_block, bool& fwd, int64_t& idx) {
+  const int64_t totalFp = totalF * kFS;  // forward work units (row parts)
   const int64_t R = 2 * a.T;
   unsigned* cnt = a.w.counters;
   for (;;) {
@@ -600,11 +609,11 @@ __device__ __forceinline__ int fused_next(const LossArgs& a, int64_t totalF, int
       bool capped = false;
       if (a.max_lead < (int64_t)INT32_MAX) {
         const int64_t ft = (int64_t)ld_relaxed(&cnt[C_TICKET]);
-        capped = ft - pb * R >= a.max_lead;
+        capped = ft / kFS - pb * R >= a.max_lead;
       }
       if (!capped) {
         const int64_t f = (int64_t)atomicAdd(&cnt[C_TICKET], 1u);
-        if (f < totalF) {
+        if (f < totalFp) {
           fwd = true;
           idx = f;
 #ifdef ODPO_DEBUG_LEAD
@@ -698,7 +707,12 @@ __device__ __forceinline__ bool decode_row(const LossArgs& a, int64_t tk, bool f
   S.g = 0;
   S.row = nullptr;
   S.drow = nullptr;
+  S.part = 0;
   pol = pol_drop;
+  if (MODE == M_FUSED && kFS > 1 && fwd_in) {  // forward work unit = (row, vocabulary part)
+    S.part = (int32_t)(tk % kFS);
+    tk /= kFS;
+  }
   if (MODE == M_SEQ) {
     S.g = tk;
     S.s = tk / T;
@@ -726,7 +740,7 @@ __device__ __forceinline__ bool decode_row(const LossArgs& a, int64_t tk, bool f
     S.g = s >= 0 ? s * T + t : 0;
     const bool live = s >= 0 && a.mask[S.g];
     if (fwd) {
-      if (!live) { S.kind = K_FSKIP; return false; }
+      if (!live) { S.kind = S.part == 0 ? K_FSKIP : K_NONE; return false; }  // counted once
       S.kind = K_F;
       S.row = row_ptr(a, s, t);
       S.tok = a.tokens[S.g];
@@ -806,6 +820,7 @@ __global__ void __launch_bounds__(GE::THREADS, GE::CPS) k_engine(LossArgs a) {
   constexpr int NPART = CS * kNCW;  // partials per row
   static_assert(NPART <= 32, "one warp merges the partials");
   static_assert(MODE != M_UNSC || CS == 1, "the unscaled mode runs on single-CTA clusters");
+  static_assert(kFS == 1 || CS == 1, "forward parts run on single-CTA clusters");
   extern __shared__ __align__(128) uint8_t ring[];
   __shared__ __align__(8) uint64_t full[kStages];
   __shared__ __align__(8) uint64_t empty[kStages];
@@ -978,15 +993,20 @@ __global__ void __launch_bounds__(GE::THREADS, GE::CPS) k_engine(LossArgs a) {
         const RowSlot& S = slots[psl];
         const int kind = S.kind;
         if (kind == K_F || kind == K_B || kind == K_ZERO || kind == K_END) {
-          const bool data = (kind == K_F || kind == K_B) && S.nchunk > 0 && v_hi > v_lo;
-          const int nstage = data ? lch : 1;
+          int s_lo = v_lo, s_hi = v_hi;
+          if (MODE == M_FUSED && kFS > 1 && kind == K_F) {
+            s_lo = (int)((int64_t)nvec * S.part / kFS);
+            s_hi = (int)((int64_t)nvec * (S.part + 1) / kFS);
+          }
+          const bool data = (kind == K_F || kind == K_B) && S.nchunk > 0 && s_hi > s_lo;
+          const int nstage = data ? (s_hi - s_lo + kCV - 1) / kCV : 1;
           const uint64_t pol = (MODE != M_SEQ && kind == K_F) ? pol_keep : pol_drop;
           for (int c = 0; c < nstage; ++c) {
             wait(empty_s + 8 * st, sph ^ 1u);
             stage_slot[st] = kind == K_END ? -1 : psl;
             stage_chunk[st] = c;
-            const int vs = v_lo + c * kCV;
-            const int nv = data ? min(kCV, v_hi - vs) : 0;
+            const int vs = s_lo + c * kCV;
+            const int nv = data ? min(kCV, s_hi - vs) : 0;
             if (nv > 0) {
               const uint32_t bytes = (uint32_t)nv * 16u;
               mbar_arrive_tx(full_s + 8 * st, bytes);
@@ -1078,7 +1098,36 @@ __global__ void __launch_bounds__(GE::THREADS, GE::CPS) k_engine(LossArgs a) {
           v.m = lane < NPART ? S.pm[lane] : -INFINITY;
           v.r = lane < NPART ? S.pr[lane] : 0.f;
           v = warp_merge(v, k2);
-          if (MODE == M_SEQ && a.vp_parts) {
+          float xt = S.xtok;
+          bool whole = true;  // this unit completes its row (always, unless rows are split)
+          if (MODE == M_FUSED && kFS > 1) {
+            // a vocabulary part: publish its partial; the part that finishes last merges all
+            // parts in part order (deterministic) and finalises the row
+            unsigned last = 0;
+            if (lane == 0) {
+              const int lo = (int)((int64_t)nvec * S.part / kFS);
+              const int hi = (int)((int64_t)nvec * (S.part + 1) / kFS);
+              const int tv = S.tok >= 0 ? S.tok / N : -1;
+              const bool own = (tv >= lo && tv < hi && S.tok < nvec * N) ||
+                               (S.part == kFS - 1 && S.tok >= nvec * N && S.tok < V);
+              a.w.fparts[S.g * kFS + S.part] = make_float4(v.m, v.r, own ? S.xtok : 0.f, own ? 1.f : 0.f);
+              last = atom_add_acq_rel(&a.w.fpart_cnt[S.g], 1u) == (unsigned)(kFS - 1);
+              if (last) {
+                fence_acq_rel_gpu();
+                MR u{-INFINITY, 0.f};
+                for (int h = 0; h < kFS; ++h) {
+                  const float4 q = __ldcg(&a.w.fparts[S.g * kFS + h]);
+                  u = mr_merge(u, MR{q.x, q.y}, k2);
+                  if (q.w != 0.f) xt = q.z;
+                }
+                v = u;
+              }
+            }
+            whole = __shfl_sync(kFull, last, 0) != 0;
+          }
+          if (!whole) {
+            // another part of this row is still streaming: nothing to count yet
+          } else if (MODE == M_SEQ && a.vp_parts) {
             // vocabulary-parallel partial of this shard; k_vp_combine merges the shards
             if (lane == 0) {
               uint32_t fl = 0;
@@ -1096,7 +1145,7 @@ __global__ void __launch_bounds__(GE::THREADS, GE::CPS) k_engine(LossArgs a) {
             if (S.tok < 0 || S.tok >= V) {
               fl |= ODPO_FLAG_TOKEN_RANGE;
             } else {
-              logp = __fsub_rn(__fmul_rn(__fsub_rn(S.xtok, v.m), a.invT), l1p);
+              logp = __fsub_rn(__fmul_rn(__fsub_rn(xt, v.m), a.invT), l1p);
               if (!isfinite(logp)) fl |= ODPO_FLAG_NONFINITE_LOGIT;
             }
             if (!isfinite(v.m) || !isfinite(v.r)) fl |= ODPO_FLAG_NONFINITE_LOGIT;
@@ -1119,7 +1168,7 @@ __global__ void __launch_bounds__(GE::THREADS, GE::CPS) k_engine(LossArgs a) {
             }
             flag(a.status, fl);
           }
-          if (count_row<MODE>(a, S, lane)) complete_unit<MODE>(a, S, lane);
+          if (whole && count_row<MODE>(a, S, lane)) complete_unit<MODE>(a, S, lane);
         } else if (kind == K_FSKIP) {
           if (lane == 0 && MODE == M_SEQ) {
             if (a.tok_out) a.tok_out[S.g] = 0.f;
@@ -1147,6 +1196,8 @@ __global__ void __launch_bounds__(GE::THREADS, GE::CPS) k_engine(LossArgs a) {
     MR s{-INFINITY, 0.f};
     float b_c = 0.f, b_coef = 0.f, b_gtok = 0.f;
     int r_kind = K_NONE, r_tok = 0, r_nst = 1, r_tch = -1, r_tvl = -1;
+    int r_lo = v_lo, r_hi = v_hi;
+    bool r_tail = tail_owner;
     const char* r_row = nullptr;
     char* r_drow = nullptr;
     for (;;) {
@@ -1159,20 +1210,29 @@ __global__ void __launch_bounds__(GE::THREADS, GE::CPS) k_engine(LossArgs a) {
       if (ch == 0) {  // a new row: cache its fields (a row's chunks occupy consecutive stages)
         r_kind = S.kind;
         r_tok = S.tok;
-        r_nst = ((r_kind == K_F || r_kind == K_B) && S.nchunk > 0 && v_hi > v_lo) ? lch : 1;
+        r_lo = v_lo;
+        r_hi = v_hi;
+        r_tail = tail_owner;
+        if (MODE == M_FUSED && kFS > 1 && r_kind == K_F) {
+          r_lo = (int)((int64_t)nvec * S.part / kFS);
+          r_hi = (int)((int64_t)nvec * (S.part + 1) / kFS);
+          r_tail = S.part == kFS - 1;
+        }
+        r_nst = ((r_kind == K_F || r_kind == K_B) && S.nchunk > 0 && r_hi > r_lo)
+                    ? (r_hi - r_lo + kCV - 1) / kCV : 1;
         r_row = S.row;
         r_drow = S.drow;
         // the vector holding tok, if it is in this CTA's range: its chunk and chunk-local index
         const int tvec = (r_tok >= 0 && r_tok < nvec * N) ? r_tok / N : -1;
-        const bool mine = tvec >= v_lo && tvec < v_hi;
-        r_tch = mine ? (tvec - v_lo) / kCV : -1;
-        r_tvl = mine ? (tvec - v_lo) - r_tch * kCV : -1;
+        const bool mine = tvec >= r_lo && tvec < r_hi;
+        r_tch = mine ? (tvec - r_lo) / kCV : -1;
+        r_tvl = mine ? (tvec - r_lo) - r_tch * kCV : -1;
       }
       const int kind = r_kind;
       const bool last_chunk = ch == r_nst - 1;
       const uint4* sv = reinterpret_cast<const uint4*>(ring + (size_t)st * kChunk);
-      const int c0 = v_lo + ch * kCV;  // first vector of this chunk within the row
-      const int cnv = v_hi > v_lo ? min(kCV, v_hi - c0) : 0;
+      const int c0 = r_lo + ch * kCV;  // first vector of this chunk within the row
+      const int cnv = r_hi > r_lo ? min(kCV, r_hi - c0) : 0;
       const bool own_tok = ch == r_tch && (r_tvl % kNCT) == tid;
       if (kind == K_F) {
         if (ch == 0) s = MR{-INFINITY, 0.f};
@@ -1202,7 +1262,7 @@ __global__ void __launch_bounds__(GE::THREADS, GE::CPS) k_engine(LossArgs a) {
         __syncwarp();
         if (lane == 0) mbar_arrive(empty_s + 8 * st);
         if (last_chunk) {
-          if (tail_owner && tid < tail) {
+          if (r_tail && tid < tail) {
             const int64_t vv = (int64_t)nvec * N + tid;
             const float x = Traits<DT>::load1(r_row, vv);
             s = mr_push1(s, x, k2);
@@ -1263,7 +1323,7 @@ __global__ void __launch_bounds__(GE::THREADS, GE::CPS) k_engine(LossArgs a) {
         // onehot entry: the thread that stored tok's vector overwrites it (program order)
         if (own_tok) Traits<DT>::store1(r_drow, r_tok, b_gtok);
         if (last_chunk) {
-          if (tail_owner && tid < tail) {
+          if (r_tail && tid < tail) {
             const int64_t vv = (int64_t)nvec * N + tid;
             const float x = Traits<DT>::load1(r_row, vv);
             Traits<DT>::store1(r_drow, vv, vv == r_tok ? b_gtok : copysignf(ex2(fmaf(x, k2, -b_c)), b_coef));
@@ -1590,7 +1650,7 @@ odpo_status odpo_seq_logprobs(const void* logits, odpo_dtype dt, int64_t B, int6
   a.tok_out = tok_logp;
   a.lse_out = row_lse;
   a.seqsum = 1;
-  k_prep<<<1, kPrepThreads, 0, s>>>(nullptr, B, 0, w, nullptr);
+  k_prep<<<1, kPrepThreads, 0, s>>>(nullptr, B, 0, w, nullptr, B * T);
   if ((e = launched()) != ODPO_OK) return e;
   return launch_engine(dt == ODPO_F32 ? 0 : 1, M_SEQ, kPolyDefault, a, 0, s, -1);
 }
@@ -1701,7 +1761,7 @@ odpo_status odpo_online_dpo_loss_fwd_bwd_ex(const void* policy_logits, odpo_dtyp
   a.dl = dlogits; a.dsb = dstride_b; a.dst = dstride_t;
   a.seq_logp = seq_logp; a.z_out = pair_logit; a.stats = stats;
 
-  k_prep<<<1, kPrepThreads, 0, s>>>(pair_rows, B, P, w, status);
+  k_prep<<<1, kPrepThreads, 0, s>>>(pair_rows, B, P, w, status, B * T);
   if ((e = launched()) != ODPO_OK) return e;
   int launches = 1;
   const int dti = dt == ODPO_F32 ? 0 : 1;
@@ -1784,7 +1844,7 @@ odpo_status odpo_online_dpo_loss_from_token_logp(
   // rows of unreferenced sequences get row_scale 0; the pair reduction writes the others
   if (row_scale && cudaMemsetAsync(row_scale, 0, (size_t)(B * T) * sizeof(float), s) != cudaSuccess)
     return ODPO_ERR_CUDA;
-  k_prep<<<1, kPrepThreads, 0, s>>>(pair_rows, B, P, w, status);
+  k_prep<<<1, kPrepThreads, 0, s>>>(pair_rows, B, P, w, status, B * T);
   odpo_status e;
   if ((e = launched()) != ODPO_OK) return e;
   k_pair_reduce<<<(unsigned)P, 32, 0, s>>>(a);
@@ -1823,7 +1883,7 @@ odpo_status odpo_online_dpo_loss_fwd_bwd_unscaled(
   a.look = look < kSlots - 6 ? look : kSlots - 6;
   if (opts && opts->row_gap > 1) return ODPO_ERR_UNSUPPORTED;
   a.row_gap = (opts && opts->row_gap >= 0) ? opts->row_gap : 0;
-  k_prep<<<1, kPrepThreads, 0, s>>>(pair_rows, B, P, w, status);
+  k_prep<<<1, kPrepThreads, 0, s>>>(pair_rows, B, P, w, status, B * T);
   if ((e = launched()) != ODPO_OK) return e;
   if (resident) {
     if (pv != 0) return ODPO_ERR_UNSUPPORTED;
@@ -1876,7 +1936,7 @@ odpo_status odpo_pg_loss_fwd_bwd(const void* policy_logits, odpo_dtype dt, int64
   const int dti = dt == ODPO_F32 ? 0 : 1;
   const int geo = opts ? opts->engine : -1;
   const int cps = opts ? opts->ctas_per_sm : 0;
-  k_prep<<<1, kPrepThreads, 0, s>>>(pair_rows, B, P, w, status);
+  k_prep<<<1, kPrepThreads, 0, s>>>(pair_rows, B, P, w, status, B * T);
   if ((e = launched()) != ODPO_OK) return e;
   int launches = 1;
   if (kind != ODPO_PG_PROX_RLOO) {
@@ -1949,7 +2009,7 @@ odpo_status odpo_vp_row_partials(const void* logits_shard, odpo_dtype dt, int64_
   a.tok_off = v0;
   a.V_total = V_total;
   a.seqsum = 0;
-  k_prep<<<1, kPrepThreads, 0, s>>>(nullptr, B, 0, w, nullptr);
+  k_prep<<<1, kPrepThreads, 0, s>>>(nullptr, B, 0, w, nullptr, B * T);
   if ((e = launched()) != ODPO_OK) return e;
   return launch_engine(dt == ODPO_F32 ? 0 : 1, M_SEQ, kPolyDefault, a, 0, s, -1);
 }
@@ -1983,7 +2043,7 @@ odpo_status odpo_vp_loss_fwd_bwd(const float* parts_all, int32_t W, const void* 
   a.seq_logp = seq_logp; a.z_out = pair_logit; a.stats = stats;
   a.tok_off = v0;
   a.V_total = V_total;
-  k_prep<<<1, kPrepThreads, 0, s>>>(pair_rows, B, P, w, status);
+  k_prep<<<1, kPrepThreads, 0, s>>>(pair_rows, B, P, w, status, B * T);
   if ((e = launched()) != ODPO_OK) return e;
   const int64_t rows = B * T;
   k_vp_combine<<<(unsigned)((rows + 255) / 256), 256, 0, s>>>(

@@ -43,6 +43,13 @@ constexpr int kChunk = ODPO_CHUNK;         // bytes per stage
 constexpr int kCV = kChunk / 16;           // 16-byte vectors per chunk
 constexpr int kSlots = 8;                  // rows in flight per CTA (row-slot ring)
 constexpr int kLook = 1;                   // default rows decoded ahead of the row being pushed
+// Experimental (build flag): FUSED forward rows dispatched as ODPO_FSPLIT vocabulary parts
+// (separate work units, merged in part order by the unit that finishes last) to shorten the
+// pair-completion latency; 1 = whole rows (default).
+#ifndef ODPO_FSPLIT
+#define ODPO_FSPLIT 1
+#endif
+constexpr int kFS = ODPO_FSPLIT;
 static_assert(kSlots % kNEpi == 0, "epilogue warps must tile the slot ring");
 
 template <int NCW_, int STAGES_, int CPS_>
@@ -165,7 +172,7 @@ struct RowSlot {
   int32_t nchunk;
   uint32_t pphase;  // parity of the param_ready phase this (B) row waits for
   int32_t fslot;    // UNSC backward rows: the slot holding the same row's forward pass
-  int32_t pad_;
+  int32_t part;    // FUSED forward rows split in ODPO_FSPLIT vocabulary parts: this part
   int64_t p;       // pair (FUSED) or sequence (SEQ)
   int64_t s;       // sequence
   int64_t g;       // row = s*T + t
