@@ -58,6 +58,8 @@ CASES = [
     (3, 50, 256, 4133, "prefix", 1 / 0.7),
     (4, 53, 2560, 50304, "dense", 1.0),   # the Pythia-2.8B LM head (d = 2560, V = 50304)
     (70, 64, 64, 300, "prefix", 1.0),     # 4480 rows = 35 row blocks: > 1 raster group of rows
+    (2, 64, 4096, 128256, "prefix", 1.0), # the LLaMA-3.1-8B head; 128 rows: the CTA pair's
+                                          # second half-block is all out of range
 ]
 
 
