@@ -159,3 +159,34 @@ def test_product_has_no_oracle_or_cpu_fallback():
     import paper_2410_18252_b200 as odpo
     with pytest.raises(odpo.OdpoError):
         odpo.pair_select(torch.zeros(3, 2))
+
+
+def test_lmhead_and_token_logp_argument_errors(lib):
+    """NEXT-2 calls: argument errors are synchronous return codes, no GPU needed."""
+    import paper_2410_18252_b200 as odpo
+    L = odpo._L()
+    ws = odpo._L().odpo_lmhead_workspace_bytes(2, 3, 1000)
+    assert ws > 0 and L.odpo_lmhead_workspace_bytes(0, 3, 1000) == 0
+
+    def head(**kw):
+        a = dict(h=FAKE, w=FAKE, B=2, T=3, d=128, V=1000, tok=FAKE, mask=FAKE, invT=1.0,
+                 tlp=None, lse=None, seq=FAKE, status=None, ws=FAKE, wsb=ws)
+        a.update(kw)
+        return L.odpo_lmhead_seq_logprobs(a["h"], a["w"], a["B"], a["T"], a["d"], a["V"],
+                                          a["tok"], a["mask"], a["invT"], a["tlp"], a["lse"],
+                                          a["seq"], a["status"], a["ws"], a["wsb"], None)
+    assert head(h=None) == 1 and head(seq=None) == 1 and head(B=0) == 1 and head(invT=0.0) == 1
+    assert head(d=100) == 4                       # d % 64 != 0
+    assert head(h=FAKE_MIS) == 2                  # 16-byte alignment
+    assert head(wsb=16) == 3 and head(ws=None) == 3
+
+    def tl(**kw):
+        a = dict(tlp=FAKE, B=4, T=3, ref=FAKE, mask=FAKE, pr=None, P=2, Pg=2, beta=0.1, invT=1.0,
+                 seq=FAKE, z=None, stats=FAKE, rs=None, status=None, ws=FAKE, wsb=1 << 20)
+        a.update(kw)
+        return L.odpo_online_dpo_loss_from_token_logp(
+            a["tlp"], a["B"], a["T"], a["ref"], a["mask"], a["pr"], a["P"], a["Pg"], a["beta"],
+            a["invT"], a["seq"], a["z"], a["stats"], a["rs"], a["status"], a["ws"], a["wsb"], None)
+    assert tl(tlp=None) == 1 and tl(stats=None) == 1 and tl(P=0) == 1 and tl(Pg=1) == 1
+    assert tl(beta=-1.0) == 1 and tl(B=5) == 1    # B != 2P without pair_rows
+    assert tl(wsb=16) == 3
