@@ -21,6 +21,8 @@
 #include <stdint.h>
 #include <stdlib.h>
 
+#include <mutex>
+
 #include "odpo.h"
 #include "odpo_device.cuh"
 #include "odpo_engine.cuh"
@@ -571,12 +573,15 @@ odpo_status odpo_lmhead_seq_logprobs(const void* hidden, const void* weight, int
   CUtensorMap mA, mB;
   if (!make_map(&mA, hidden, R, d, d, BM) || !make_map(&mB, weight, V, d, d, pair ? BN / 2 : BN))
     return ODPO_ERR_CUDA;
-  static bool attr = false;
-  if (!attr) {
+  // kernel attributes are per device: set them once for each device this process uses
+  static std::once_flag attr_once[128];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 128) return ODPO_ERR_UNSUPPORTED;
+  std::call_once(attr_once[dev], []() {
     cudaFuncSetAttribute(k_lmhead_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
     cudaFuncSetAttribute(k_lmhead_fwd2, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2);
-    attr = true;
-  }
+  });
   const int sms = sm_count();
   Args a;
   a.R = R; a.d = d; a.V = V;
