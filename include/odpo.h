@@ -379,6 +379,31 @@ const char* odpo_version(void);
 size_t odpo_lmhead_workspace_bytes(int64_t B, int64_t T, int64_t V);
 
 /*
+ * odpo_lmhead_grad -- NEXT-2 backward: the LM-head gradients of the loss whose per-row logit
+ * gradient is row_scale * (softmax - onehot) (the factored gradient of
+ * odpo_online_dpo_loss_fwd_bwd_unscaled / odpo_online_dpo_loss_from_token_logp):
+ *
+ *   G[r, v]     = row_scale[r] * (softmax(invT * logits[r, :])[v] - [v == tokens[r]])
+ *   dhidden     = G weight          fp32 [R, d] (overwritten)
+ *   dweight     = G^T hidden        fp32 [V, d] (overwritten)
+ *
+ * The logits are recomputed chunk by chunk (chunk_rows rows at a time, rounded up to 256) by
+ * the NEXT-2 tcgen05 kernel, whose epilogue writes G (bf16) into `scratch` instead of
+ * reducing it; the two GEMMs with G are plain cuBLAS GEMMs (bf16 in, fp32 accumulate), loaded
+ * at run time.  row_lse is odpo_lmhead_seq_logprobs' row_lse (natural log, invT applied).
+ *   hidden bf16 [R, d], weight bf16 [V, d] contiguous, 16-byte aligned, d % 64 == 0.
+ *   scratch >= odpo_lmhead_grad_scratch_bytes(chunk_rows, V) bytes, 16-byte aligned.
+ * Errors: INVALID_ARG, UNSUPPORTED (d % 64, sizes, cuBLAS not loadable), ALIGNMENT,
+ * WORKSPACE, CUDA.
+ */
+size_t odpo_lmhead_grad_scratch_bytes(int64_t chunk_rows, int64_t V);
+odpo_status odpo_lmhead_grad(const void* hidden, const void* weight, int64_t R, int64_t d,
+                             int64_t V, const int32_t* tokens, const float* row_lse,
+                             const float* row_scale, float inv_temperature, float* dhidden,
+                             float* dweight, void* scratch, size_t scratch_bytes,
+                             int64_t chunk_rows, void* stream);
+
+/*
  * odpo_online_dpo_loss_from_token_logp -- the Online-DPO loss (Sec 2.1; S3/S4 of
  * SURVEY.md §8(a)) from per-token policy log-probs, e.g. those odpo_lmhead_seq_logprobs
  * produced without logits.  Same pair reduction (fixed-order sequence sums, z, -log sigma,

@@ -222,6 +222,33 @@ def lmhead_seq_logprobs(hidden, weight, tokens, mask, inv_temperature=1.0, n_thr
     return seq_logprobs(np.ascontiguousarray(logits), tokens, mask, inv_temperature, n_threads)
 
 
+def lmhead_dpo_grad(hidden, weight, ref_logp, tokens, mask, beta, pair_rows=None,
+                    p_global=None, inv_temperature=1.0, n_threads=1):
+    """NEXT-2 backward oracle: gradients of the Online-DPO loss (online_dpo_loss_fwd_bwd on the
+    head's fp64 logits) with respect to the LM head's input and weight, by the chain rule
+    written out: G = row_scale * (softmax(invT * logits) - onehot) (row_scale = coef_b * mask
+    from the unscaled loss oracle), dhidden = G @ weight, dweight = G.T @ hidden.  Returns
+    dict(dhidden [B, T, d], dweight [V, d], row_scale, loss)."""
+    h = np.asarray(hidden, dtype=np.float64)
+    w = np.asarray(weight, dtype=np.float64)
+    B, T, d = h.shape
+    V = w.shape[0]
+    logits = np.ascontiguousarray((h.reshape(B * T, d) @ w.T).reshape(B, T, V))
+    o = online_dpo_loss_fwd_bwd(logits, ref_logp, tokens, mask, beta, pair_rows=pair_rows,
+                                p_global=p_global, inv_temperature=inv_temperature,
+                                n_threads=n_threads, unscaled=True)
+    it = float(np.float32(inv_temperature))
+    x = it * logits.reshape(B * T, V)
+    x = x - x.max(axis=1, keepdims=True)
+    p = np.exp(x)
+    p /= p.sum(axis=1, keepdims=True)
+    tok = np.asarray(tokens, dtype=np.int64).reshape(-1)
+    p[np.arange(B * T), tok] -= 1.0
+    G = o["row_scale"].reshape(B * T, 1) * p
+    return dict(dhidden=(G @ w).reshape(B, T, d), dweight=G.T @ h.reshape(B * T, d),
+                row_scale=o["row_scale"], loss=o["stats"][1])
+
+
 def to_bf16_bits(x) -> np.ndarray:
     """Round float values to bf16 (round-to-nearest-even) and return the uint16 bits.
 

@@ -97,6 +97,10 @@ def _L():
         L.odpo_online_dpo_loss_from_token_logp.argtypes = [P, i64, i64, P, P, P, i64, i64, f32,
                                                            f32, P, P, P, P, P, P, sz, P]
         L.odpo_online_dpo_loss_from_token_logp.restype = C.c_int
+        L.odpo_lmhead_grad_scratch_bytes.argtypes = [i64, i64]
+        L.odpo_lmhead_grad_scratch_bytes.restype = sz
+        L.odpo_lmhead_grad.argtypes = [P, P, i64, i64, i64, P, P, P, f32, P, P, P, sz, i64, P]
+        L.odpo_lmhead_grad.restype = C.c_int
         L.odpo_workspace_bytes.argtypes = [i64, i64, i64]
         L.odpo_workspace_bytes.restype = sz
         L.odpo_status_string.argtypes = [C.c_int]
@@ -294,6 +298,35 @@ def lmhead_online_dpo_loss_fwd(hidden: torch.Tensor, weight: torch.Tensor,
         ws.numel(), _stream()), "odpo_online_dpo_loss_from_token_logp")
     return LossOutput(stats=stats, dlogits=None, seq_logp=seq, z=z, status=status, launches=5,
                       row_scale=row_scale)
+
+
+def lmhead_grad(hidden: torch.Tensor, weight: torch.Tensor, tokens: torch.Tensor,
+                row_lse: torch.Tensor, row_scale: torch.Tensor, inv_temperature: float = 1.0,
+                chunk_rows: int = 16384):
+    """NEXT-2 backward: (dhidden fp32 [B, T, d], dweight fp32 [V, d]) of the loss whose logit
+    gradient is row_scale * (softmax - onehot); logits recomputed chunk by chunk on tcgen05,
+    G written to a bf16 scratch of chunk_rows rows, two cuBLAS GEMMs per chunk."""
+    hidden = _dev(hidden, "hidden", torch.bfloat16)
+    weight = _dev(weight, "weight", torch.bfloat16)
+    if not (hidden.is_contiguous() and weight.is_contiguous()):
+        raise ValueError("hidden and weight must be contiguous")
+    d = hidden.shape[-1]
+    R = hidden.numel() // d
+    V = weight.shape[0]
+    tokens = _dev(tokens, "tokens", torch.int32).contiguous()
+    row_lse = _dev(row_lse, "row_lse", torch.float32).contiguous()
+    row_scale = _dev(row_scale, "row_scale", torch.float32).contiguous()
+    dev = hidden.device
+    dh = torch.empty(hidden.shape, dtype=torch.float32, device=dev)
+    dw = torch.empty((V, d), dtype=torch.float32, device=dev)
+    cr = min(int(chunk_rows), R)
+    cr = -(-cr // 256) * 256
+    nb = _L().odpo_lmhead_grad_scratch_bytes(cr, V)
+    scratch = torch.empty(max(nb, 256), dtype=torch.uint8, device=dev)
+    _check(_L().odpo_lmhead_grad(_p(hidden), _p(weight), R, d, V, _p(tokens), _p(row_lse),
+                                 _p(row_scale), float(inv_temperature), _p(dh), _p(dw),
+                                 _p(scratch), scratch.numel(), cr, _stream()), "odpo_lmhead_grad")
+    return dh, dw
 
 
 @dataclass

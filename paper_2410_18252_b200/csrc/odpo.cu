@@ -875,7 +875,6 @@ __global__ void __launch_bounds__(GE::THREADS, GE::CPS) k_engine(LossArgs a) {
   // this CTA's contiguous vector range of every row
   const int v_lo = (int)((int64_t)nvec * crank / CS);
   const int v_hi = (int)((int64_t)nvec * (crank + 1) / CS);
-  const int lch = v_hi > v_lo ? (v_hi - v_lo + kCV - 1) / kCV : 1;  // chunks per row (>= 1)
   const bool tail_owner = crank == CS - 1;
   const float k2 = a.invT * kLog2e;
 

@@ -16,7 +16,9 @@
 // K6b k_lmhead_merge: per row, the pieces' (m, r, x_tok) in fixed (CTA) order -> logp, lse; per
 // sequence, the fixed-order masked sum.
 #include <cuda.h>
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 #include <math.h>
 #include <stdint.h>
 #include <stdlib.h>
@@ -106,6 +108,11 @@ struct Args {
   float2* parts;          // [R][NT] (m, r) of each vocabulary tile
   float* xtok;            // [R] the sampled token's logit (written by the tile holding it)
   int64_t nrb2;           // 2-CTA kernel: 256-row blocks (one per CTA pair)
+  // GRAD epilogue (backward): G[row, v] = row_scale[row] (softmax - onehot), bf16 [R][ldg]
+  const float* row_lse;   // [R] logsumexp of invT * logits (natural log), from the forward
+  const float* row_scale; // [R] coef_b * mask (d loss / d logits = row_scale * G)
+  __nv_bfloat16* gout;   // [R][ldg]
+  int64_t ldg;
 };
 
 __device__ __forceinline__ void tile_coords(const Args& a, int64_t t, int64_t& rb, int64_t& n) {
@@ -309,6 +316,10 @@ __device__ __forceinline__ void tile_coords2(const Args& a, int64_t t, int64_t& 
   rb2 = r0 + idx % gg;
 }
 
+// GRAD = true: the same GEMM tiles, but the epilogue writes the row's gradient with respect to
+// the logits, G = row_scale (softmax(invT x) - onehot) in bf16, instead of folding an online
+// logsumexp (the backward recomputes the logits a row chunk at a time; see odpo_lmhead_grad).
+template <bool GRAD>
 __global__ void __launch_bounds__(THREADS, 1)
     k_lmhead_fwd2(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                   Args a) {
@@ -411,6 +422,11 @@ __global__ void __launch_bounds__(THREADS, 1)
       const bool live = row < a.R;
       const int tok = live ? a.tokens[row] : -1;
       MR s{-INFINITY, 0.f};
+      float g_rs = 0.f, g_c = 0.f;
+      if (GRAD && live) {
+        g_rs = a.row_scale[row];
+        g_c = a.row_lse[row] * kLog2e;  // p = 2^(acc * invT * log2e - lse * log2e)
+      }
       mbar_wait(tfull_s + 8 * acc, aph);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const int64_t c0 = n * BN;
@@ -420,6 +436,31 @@ __global__ void __launch_bounds__(THREADS, 1)
         tm_ld32(tmem + lane_base + (uint32_t)(acc * BN + c * 32), r);
         const int64_t cb = c0 + 32 * c;
         if (cb >= a.V) break;
+        if (GRAD) {
+          if (!live) continue;
+          // g_j = row_scale * p_j; at the sampled token row_scale * expm1(log p) (no p - 1
+          // cancellation); rows with row_scale 0 (masked, unreferenced) get exact zeros
+          uint32_t w[16];
+#pragma unroll
+          for (int j = 0; j < 32; j += 2) {
+            float g0 = g_rs * ex2(fmaf(__uint_as_float(r[j]), k2, -g_c));
+            float g1 = g_rs * ex2(fmaf(__uint_as_float(r[j + 1]), k2, -g_c));
+            if (tok == cb + j) g0 = g_rs * expm1f(fmaf(__uint_as_float(r[j]), a.invT, -a.row_lse[row]));
+            if (tok == cb + j + 1) g1 = g_rs * expm1f(fmaf(__uint_as_float(r[j + 1]), a.invT, -a.row_lse[row]));
+            w[j / 2] = pack_bf16x2(g0, g1);
+          }
+          __nv_bfloat16* dst = a.gout + row * a.ldg + cb;
+          if (cb + 32 <= a.V) {
+            uint4* d4 = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) d4[k] = make_uint4(w[4 * k], w[4 * k + 1], w[4 * k + 2], w[4 * k + 3]);
+          } else {
+            unsigned short* d2 = reinterpret_cast<unsigned short*>(dst);
+            for (int j = 0; j < 32 && cb + j < a.V; ++j)
+              d2[j] = (unsigned short)((w[j / 2] >> (16 * (j & 1))) & 0xFFFFu);
+          }
+          continue;
+        }
         if (cb + 32 > a.V) {
 #pragma unroll
           for (int j = 0; j < 32; ++j)
@@ -441,7 +482,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive_cl(tempty_leader + 8 * acc);
       if (++acc == 2) { acc = 0; aph ^= 1u; }
-      if (live) a.parts[row * a.NT + n] = make_float2(s.m, s.r);
+      if (!GRAD && live) a.parts[row * a.NT + n] = make_float2(s.m, s.r);
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -539,6 +580,40 @@ static int sm_count() {
 
 constexpr int kRasterG = 64;  // row blocks per raster group (tuned: 8/16/32/64 -> 1636/1723/1751/1802 TF/s)
 
+// ---------------------------------------------------------------- cuBLAS (plain GEMMs), loaded at
+// run time so that libodpo.so has no load-time dependency on it (the process -- e.g. torch --
+// normally has libcublas.so.12 loaded already)
+struct Blas {
+  typedef int (*Create)(void**);
+  typedef int (*SetStream)(void*, cudaStream_t);
+  typedef int (*GemmEx)(void*, int, int, int, int, int, const void*, const void*, int, int,
+                        const void*, int, int, const void*, void*, int, int, int, int);
+  Create create = nullptr;
+  SetStream set_stream = nullptr;
+  GemmEx gemm = nullptr;
+  void* handle[128] = {};
+  std::mutex mu;
+  bool load() {
+    if (gemm) return true;
+    void* h = dlopen("libcublas.so.12", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("/usr/local/cuda/lib64/libcublas.so.12", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return false;
+    create = (Create)dlsym(h, "cublasCreate_v2");
+    set_stream = (SetStream)dlsym(h, "cublasSetStream_v2");
+    gemm = (GemmEx)dlsym(h, "cublasGemmEx");
+    return create && set_stream && gemm;
+  }
+  void* get(int dev) {
+    std::lock_guard<std::mutex> g(mu);
+    if (!load() || dev < 0 || dev >= 128) return nullptr;
+    if (!handle[dev] && create(&handle[dev]) != 0) handle[dev] = nullptr;
+    return handle[dev];
+  }
+};
+static Blas g_blas;
+// cuBLAS enum values (cublas_api.h / library_types.h)
+constexpr int kOpN = 0, kOpT = 1, kR16BF = 14, kR32F = 0, kCompute32F = 68, kGemmDefault = -1;
+
 }  // namespace lmh
 }  // namespace odpo
 
@@ -580,7 +655,8 @@ odpo_status odpo_lmhead_seq_logprobs(const void* hidden, const void* weight, int
   if (dev < 0 || dev >= 128) return ODPO_ERR_UNSUPPORTED;
   std::call_once(attr_once[dev], []() {
     cudaFuncSetAttribute(k_lmhead_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-    cudaFuncSetAttribute(k_lmhead_fwd2, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2);
+    cudaFuncSetAttribute(k_lmhead_fwd2<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2);
+    cudaFuncSetAttribute(k_lmhead_fwd2<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2);
   });
   const int sms = sm_count();
   Args a;
@@ -615,7 +691,7 @@ odpo_status odpo_lmhead_seq_logprobs(const void* hidden, const void* weight, int
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, k_lmhead_fwd2, mA, mB, a);
+    cudaLaunchKernelEx(&cfg, k_lmhead_fwd2<false>, mA, mB, a);
   } else {
     const int grid = (int)(a.Ttot < sms ? a.Ttot : sms);
     k_lmhead_fwd<<<grid, THREADS, SMEM, s>>>(mA, mB, a);
@@ -625,6 +701,94 @@ odpo_status odpo_lmhead_seq_logprobs(const void* hidden, const void* weight, int
   if (cudaGetLastError() != cudaSuccess) return ODPO_ERR_CUDA;
   k_lmhead_seqsum<<<(unsigned)B, 32, 0, s>>>(tlp, mask, T, seq_logp, status);
   return cudaGetLastError() == cudaSuccess ? ODPO_OK : ODPO_ERR_CUDA;
+}
+
+size_t odpo_lmhead_grad_scratch_bytes(int64_t chunk_rows, int64_t V) {
+  if (chunk_rows <= 0 || V <= 0) return 0;
+  const int64_t ldg = (V + 7) / 8 * 8;
+  return (size_t)chunk_rows * (size_t)ldg * 2;
+}
+
+odpo_status odpo_lmhead_grad(const void* hidden, const void* weight, int64_t R, int64_t d,
+                             int64_t V, const int32_t* tokens, const float* row_lse,
+                             const float* row_scale, float inv_temperature, float* dhidden,
+                             float* dweight, void* scratch, size_t scratch_bytes,
+                             int64_t chunk_rows, void* stream) {
+  if (!hidden || !weight || !tokens || !row_lse || !row_scale || !dhidden || !dweight)
+    return ODPO_ERR_INVALID_ARG;
+  if (R <= 0 || d <= 0 || V <= 0 || chunk_rows <= 0) return ODPO_ERR_INVALID_ARG;
+  if (!(isfinite(inv_temperature) && inv_temperature > 0.f)) return ODPO_ERR_INVALID_ARG;
+  if (d % BK) return ODPO_ERR_UNSUPPORTED;
+  if (R > (int64_t)INT32_MAX || V > (int64_t)INT32_MAX || d > (1 << 20)) return ODPO_ERR_UNSUPPORTED;
+  if (((uintptr_t)hidden & 15u) || ((uintptr_t)weight & 15u) || ((uintptr_t)scratch & 15u))
+    return ODPO_ERR_ALIGNMENT;
+  if (chunk_rows > R) chunk_rows = R;
+  chunk_rows = (chunk_rows + 255) / 256 * 256;  // whole CTA-pair row blocks
+  if (!scratch || scratch_bytes < odpo_lmhead_grad_scratch_bytes(chunk_rows, V))
+    return ODPO_ERR_WORKSPACE;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  void* blas = g_blas.get(dev);
+  if (!blas) return ODPO_ERR_UNSUPPORTED;  // cuBLAS not loadable
+  static std::once_flag attr_once[128];
+  if (dev < 0 || dev >= 128) return ODPO_ERR_UNSUPPORTED;
+  std::call_once(attr_once[dev], []() {
+    cudaFuncSetAttribute(k_lmhead_fwd2<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2);
+  });
+  cudaStream_t s = (cudaStream_t)stream;
+  if (g_blas.set_stream(blas, s) != 0) return ODPO_ERR_CUDA;
+  CUtensorMap mB;
+  if (!make_map(&mB, weight, V, d, d, BN / 2)) return ODPO_ERR_CUDA;
+  const int sms = sm_count();
+  const int64_t ldg = (V + 7) / 8 * 8;
+  __nv_bfloat16* G = reinterpret_cast<__nv_bfloat16*>(scratch);
+  const float one = 1.f, zero = 0.f;
+  for (int64_t r0 = 0; r0 < R; r0 += chunk_rows) {
+    const int64_t Rc = min(chunk_rows, R - r0);
+    const char* hc = reinterpret_cast<const char*>(hidden) + r0 * d * 2;
+    CUtensorMap mA;
+    if (!make_map(&mA, hc, Rc, d, d, BM)) return ODPO_ERR_CUDA;
+    Args a{};
+    a.R = Rc; a.d = d; a.V = V;
+    a.nrb = (Rc + BM - 1) / BM;
+    a.NT = (V + BN - 1) / BN;
+    a.Ttot = a.nrb * a.NT;
+    a.nrb2 = (Rc + 255) / 256;
+    a.G = kRasterG / 2;
+    a.invT = inv_temperature;
+    a.tokens = tokens + r0;
+    a.row_lse = row_lse + r0;
+    a.row_scale = row_scale + r0;
+    a.gout = G;
+    a.ldg = ldg;
+    int clusters = sms / 2;
+    if (clusters > a.nrb2 * a.NT) clusters = (int)(a.nrb2 * a.NT);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(2 * clusters));
+    cfg.blockDim = dim3(THREADS);
+    cfg.dynamicSmemBytes = SMEM2;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k_lmhead_fwd2<true>, mA, mB, a);
+    if (cudaGetLastError() != cudaSuccess) return ODPO_ERR_CUDA;
+    // dH[r0:r0+Rc] = G W   (column-major: dH^T[d, Rc] = W^T[d, V] G^T[V, Rc])
+    if (g_blas.gemm(blas, kOpN, kOpN, (int)d, (int)Rc, (int)V, &one, weight, kR16BF, (int)d, G,
+                    kR16BF, (int)ldg, &zero, dhidden + r0 * d, kR32F, (int)d, kCompute32F,
+                    kGemmDefault) != 0)
+      return ODPO_ERR_CUDA;
+    // dW (+)= G^T H         (column-major: dW^T[d, V] (+)= H^T[d, Rc] G[Rc, V])
+    if (g_blas.gemm(blas, kOpN, kOpT, (int)d, (int)V, (int)Rc, &one, hc, kR16BF, (int)d, G,
+                    kR16BF, (int)ldg, r0 == 0 ? &zero : &one, dweight, kR32F, (int)d, kCompute32F,
+                    kGemmDefault) != 0)
+      return ODPO_ERR_CUDA;
+  }
+  return ODPO_OK;
 }
 
 }  // extern "C"

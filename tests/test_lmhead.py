@@ -144,3 +144,73 @@ def test_lmhead_dpo_loss_parity(permute):
     rs = out.row_scale.cpu().numpy().astype(np.float64)
     assert np.all(np.abs(rs - o["row_scale"]) <= 1e-4 * np.abs(o["row_scale"]) + 1e-12)
     assert int(out.status.item()) & ~odpo.FLAGS["DEGENERATE_PAIR"] == 0
+
+
+# ------------------------------------------------------------------ NEXT-2 backward
+def _grad_case(seed=13, P=3, T=4, d=16, V=40, permute=True):
+    B = 2 * P + (1 if permute else 0)
+    rows = np.arange(B * T)
+    h, w = synth.lmhead_inputs(seed, rows, d, V)
+    tok = synth.tokens_rows(seed, rows, V).reshape(B, T).astype(np.int32)
+    mask = synth.mask_for(seed, np.arange(B), T, "prefix", 3)
+    pr = synth.permutation(seed, B)[: 2 * P].reshape(P, 2).astype(np.int32) if permute else None
+    ref = (synth.rewards_for(seed, B, 1).reshape(-1) - 12.0).astype(np.float32)
+    return B, T, d, V, h.reshape(B, T, d), w, tok, mask, pr, ref
+
+
+def test_oracle_grad_central_differences():
+    """dL/dhidden and dL/dweight of the oracle loss (fp64 logits = hidden @ weight.T) by central
+    differences: pins the chain rule (a dropped row_scale, a transposed product or a wrong
+    sign fails it)."""
+    B, T, d, V, h, w, tok, mask, pr, ref = _grad_case()
+    beta, eps = 0.5, 1e-5
+    g = oracle.lmhead_dpo_grad(h, w, ref, tok, mask, beta, pair_rows=pr)
+
+    def loss(hh, ww):
+        lg = np.ascontiguousarray((hh.reshape(B * T, d) @ ww.T).reshape(B, T, V))
+        return oracle.online_dpo_loss_fwd_bwd(lg, ref, tok, mask, beta, pair_rows=pr)["stats"][1]
+
+    rng = np.random.default_rng(0)
+    for _ in range(6):
+        b, t, i = rng.integers(B), rng.integers(T), rng.integers(d)
+        hp, hm = h.copy(), h.copy()
+        hp[b, t, i] += eps
+        hm[b, t, i] -= eps
+        fd = (loss(hp, w) - loss(hm, w)) / (2 * eps)
+        assert abs(fd - g["dhidden"][b, t, i]) <= 1e-6 + 1e-5 * abs(fd), (b, t, i, fd, g["dhidden"][b, t, i])
+        v, j = rng.integers(V), rng.integers(d)
+        wp, wm = w.copy(), w.copy()
+        wp[v, j] += eps
+        wm[v, j] -= eps
+        fd = (loss(h, wp) - loss(h, wm)) / (2 * eps)
+        assert abs(fd - g["dweight"][v, j]) <= 1e-6 + 1e-5 * abs(fd), (v, j, fd, g["dweight"][v, j])
+    assert np.any(g["dhidden"] != 0) and np.any(g["dweight"] != 0)
+
+
+@pytest.mark.parametrize("shape", [(5, 9, 128, 1000, 256), (40, 53, 256, 4133, 1024)],
+                         ids=lambda s: f"P{s[0]}T{s[1]}d{s[2]}V{s[3]}c{s[4]}")
+@pytest.mark.gpu
+@pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a CUDA device")
+def test_lmhead_grad_parity(shape):
+    """odpo_lmhead_grad (logits recomputed on tcgen05 chunk by chunk, G in bf16, cuBLAS GEMMs)
+    against the oracle's chain rule, with row_lse / row_scale from the GPU forward."""
+    import paper_2410_18252_b200 as odpo
+    P, T, d, V, chunk = shape
+    B, _, _, _, h, w, tok, mask, pr, ref = _grad_case(seed=17, P=P, T=T, d=d, V=V)
+    beta = 0.1
+    hd = torch.from_numpy(h).to(torch.bfloat16).cuda()
+    wd = torch.from_numpy(w).to(torch.bfloat16).cuda()
+    td, md = torch.from_numpy(tok).cuda(), torch.from_numpy(mask).cuda()
+    prd = torch.from_numpy(pr).cuda()
+    _, _, lse, _ = odpo.lmhead_seq_logprobs(hd, wd, td, md)
+    out = odpo.lmhead_online_dpo_loss_fwd(hd, wd, torch.from_numpy(ref).cuda(), td, md, beta,
+                                          pair_rows=prd)
+    dh, dw = odpo.lmhead_grad(hd, wd, td, lse, out.row_scale, chunk_rows=chunk)
+    torch.cuda.synchronize()
+    o = oracle.lmhead_dpo_grad(h, w, ref, tok, mask, beta, pair_rows=pr, n_threads=8)
+    for gpu, orc in ((dh.cpu().double().numpy(), o["dhidden"]), (dw.cpu().double().numpy(), o["dweight"])):
+        # G is rounded to bf16 (2^-9 relative) before the fp32-accumulated GEMMs
+        err = np.linalg.norm(gpu - orc) / max(np.linalg.norm(orc), 1e-30)
+        assert err <= 1e-2, err
+        big = np.abs(orc) > 0.1 * np.abs(orc).max()
+        assert np.all(np.abs(gpu[big] - orc[big]) <= 2e-2 * np.abs(orc[big]))
