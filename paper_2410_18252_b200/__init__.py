@@ -276,7 +276,8 @@ def lmhead_online_dpo_loss_fwd(hidden: torch.Tensor, weight: torch.Tensor,
     """NEXT-2 forward: the Online-DPO loss, statistics and per-row gradient scale straight from
     the policy's LM head (hidden [B, T, d] bf16, weight [V, d] bf16), logits never stored.
     Returns LossOutput with dlogits = None and row_scale [B, T] = coef_b * mask."""
-    _, tok_logp, _, status = lmhead_seq_logprobs(hidden, weight, tokens, mask, inv_temperature)
+    _, tok_logp, row_lse, status = lmhead_seq_logprobs(hidden, weight, tokens, mask,
+                                                       inv_temperature)
     B, T = tok_logp.shape
     dev = hidden.device
     ref_logp = _dev(ref_logp, "ref_logp", torch.float32).contiguous()
@@ -297,7 +298,7 @@ def lmhead_online_dpo_loss_fwd(hidden: torch.Tensor, weight: torch.Tensor,
         float(inv_temperature), _p(seq), _p(z), _p(stats), _p(row_scale), _p(status), _p(ws),
         ws.numel(), _stream()), "odpo_online_dpo_loss_from_token_logp")
     return LossOutput(stats=stats, dlogits=None, seq_logp=seq, z=z, status=status, launches=5,
-                      row_scale=row_scale)
+                      row_scale=row_scale, row_lse=row_lse)
 
 
 def lmhead_grad(hidden: torch.Tensor, weight: torch.Tensor, tokens: torch.Tensor,
@@ -338,6 +339,7 @@ class LossOutput:
     status: torch.Tensor
     launches: int
     row_scale: torch.Tensor | None = None  # unscaled call: dlogits holds G, grad = row_scale * G
+    row_lse: torch.Tensor | None = None    # LM-head loss forward: logsumexp per row (backward)
 
     def named(self) -> dict:
         s = self.stats.tolist()

@@ -202,10 +202,9 @@ def test_lmhead_grad_parity(shape):
     wd = torch.from_numpy(w).to(torch.bfloat16).cuda()
     td, md = torch.from_numpy(tok).cuda(), torch.from_numpy(mask).cuda()
     prd = torch.from_numpy(pr).cuda()
-    _, _, lse, _ = odpo.lmhead_seq_logprobs(hd, wd, td, md)
     out = odpo.lmhead_online_dpo_loss_fwd(hd, wd, torch.from_numpy(ref).cuda(), td, md, beta,
                                           pair_rows=prd)
-    dh, dw = odpo.lmhead_grad(hd, wd, td, lse, out.row_scale, chunk_rows=chunk)
+    dh, dw = odpo.lmhead_grad(hd, wd, td, out.row_lse, out.row_scale, chunk_rows=chunk)
     torch.cuda.synchronize()
     o = oracle.lmhead_dpo_grad(h, w, ref, tok, mask, beta, pair_rows=pr, n_threads=8)
     for gpu, orc in ((dh.cpu().double().numpy(), o["dhidden"]), (dw.cpu().double().numpy(), o["dweight"])):
