@@ -190,3 +190,21 @@ def test_lmhead_and_token_logp_argument_errors(lib):
     assert tl(tlp=None) == 1 and tl(stats=None) == 1 and tl(P=0) == 1 and tl(Pg=1) == 1
     assert tl(beta=-1.0) == 1 and tl(B=5) == 1    # B != 2P without pair_rows
     assert tl(wsb=16) == 3
+
+
+def test_lmhead_grad_argument_errors(lib):
+    import paper_2410_18252_b200 as odpo
+    L = odpo._L()
+    sb = L.odpo_lmhead_grad_scratch_bytes(256, 1000)
+    assert sb == 256 * 1000 * 2 and L.odpo_lmhead_grad_scratch_bytes(0, 10) == 0
+
+    def grad(**kw):
+        a = dict(h=FAKE, w=FAKE, R=100, d=128, V=1000, tok=FAKE, lse=FAKE, rs=FAKE, invT=1.0,
+                 dh=FAKE, dw=FAKE, sc=FAKE, scb=sb, chunk=256)
+        a.update(kw)
+        return L.odpo_lmhead_grad(a["h"], a["w"], a["R"], a["d"], a["V"], a["tok"], a["lse"],
+                                  a["rs"], a["invT"], a["dh"], a["dw"], a["sc"], a["scb"],
+                                  a["chunk"], None)
+    assert grad(h=None) == 1 and grad(rs=None) == 1 and grad(R=0) == 1 and grad(chunk=0) == 1
+    assert grad(invT=float("nan")) == 1 and grad(d=96) == 4 and grad(w=FAKE_MIS) == 2
+    assert grad(scb=16) == 3 and grad(sc=None) == 3
