@@ -117,15 +117,35 @@ def aux_lmhead(config, B, T, reps=5):
     gemm = t(lambda: torch.matmul(hid.view(B * T, d), Wh.t()))
     lg = torch.matmul(hid.view(B * T, d), Wh.t()).view(B, T, V)
     seqp = t(lambda: odpo.seq_logprobs(lg, tok, msk))
-    del lg, hid, Wh
+    del lg
+    # the full head learner step: fused (logits never stored; backward recomputes them in
+    # 8192-row chunks) vs unfused (cuBLAS logits, the loss call in place, two cuBLAS GEMMs)
+    ref_h = torch.full((B,), -4.0 * T, device="cuda")
+
+    def fused_step():
+        o = odpo.lmhead_online_dpo_loss_fwd(hid, Wh, ref_h, tok, msk, 0.1)
+        return odpo.lmhead_grad(hid, Wh, tok, o.row_lse, o.row_scale, chunk_rows=8192)
+
+    def unfused_step():
+        lg2 = torch.matmul(hid.view(B * T, d), Wh.t()).view(B, T, V)
+        o = odpo.online_dpo_loss_fwd_bwd(lg2, ref_h, tok, msk, 0.1, inplace=True)
+        dl = o.dlogits.view(B * T, V)
+        return torch.matmul(dl, Wh), torch.matmul(dl.t(), hid.view(B * T, d))
+
+    step_f = t(fused_step)
+    step_u = t(unfused_step)
+    del hid, Wh
     torch.cuda.empty_cache()
     flops = 2.0 * B * T * d * V
     pk, src = bf16_peak()
-    return {"kernel": "odpo_lmhead_seq_logprobs (k_lmhead_fwd + merge)", "rows": B * T, "d": d,
+    return {"kernel": "odpo_lmhead_seq_logprobs (k_lmhead_fwd2 + merge)", "rows": B * T, "d": d,
             "V": V, "bound": "tensor", "ms": fused, "achieved": flops / fused / 1e9,
             "unit": "TFLOP/s", "peak": pk, "peak_source": src, "frac": flops / fused / 1e9 / pk,
             "cublas_gemm_ms": gemm, "cublas_tflops": flops / gemm / 1e9,
-            "unfused_ms": gemm + seqp, "speedup_vs_unfused": (gemm + seqp) / fused}
+            "unfused_ms": gemm + seqp, "speedup_vs_unfused": (gemm + seqp) / fused,
+            "step_fused_ms": step_f, "step_unfused_ms": step_u,
+            "step_note": "fwd + DPO loss + dhidden/dweight; fused keeps no logits (backward "
+                         "recomputes them in 8192-row chunks), unfused materialises them"}
 
 
 class ClockSampler:
