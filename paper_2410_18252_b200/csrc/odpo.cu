@@ -882,7 +882,11 @@ __global__ void __launch_bounds__(GE::THREADS, GE::CPS) k_engine(LossArgs a) {
     if (lane == 0) {
       // ================= producer: (leader) tickets -> row slots, broadcast; every CTA streams
       // its own vocabulary range of each row into its TMA ring
+#ifdef ODPO_KEEP_FRAC
+      const uint64_t pol_keep = MODE == M_FUSED ? policy_evict_last_frac(ODPO_KEEP_FRAC) : policy_evict_last();
+#else
       const uint64_t pol_keep = policy_evict_last();
+#endif
       const uint64_t pol_drop = policy_evict_first();
       const int64_t totalF = a.P * 2 * T;
       const int64_t nzero = (int64_t)__ldcg(&a.w.counters[C_NUNREF]) * T;
