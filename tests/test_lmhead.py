@@ -187,15 +187,16 @@ def test_oracle_grad_central_differences():
     assert np.any(g["dhidden"] != 0) and np.any(g["dweight"] != 0)
 
 
-@pytest.mark.parametrize("shape", [(5, 9, 128, 1000, 256), (40, 53, 256, 4133, 1024)],
-                         ids=lambda s: f"P{s[0]}T{s[1]}d{s[2]}V{s[3]}c{s[4]}")
+@pytest.mark.parametrize("shape", [(5, 9, 128, 1000, 256, 1.0), (40, 53, 256, 4133, 1024, 1.0),
+                                   (6, 11, 192, 3001, 256, 1 / 0.7)],
+                         ids=lambda s: f"P{s[0]}T{s[1]}d{s[2]}V{s[3]}c{s[4]}t{s[5]:.2f}")
 @pytest.mark.gpu
 @pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a CUDA device")
 def test_lmhead_grad_parity(shape):
     """odpo_lmhead_grad (logits recomputed on tcgen05 chunk by chunk, G in bf16, cuBLAS GEMMs)
     against the oracle's chain rule, with row_lse / row_scale from the GPU forward."""
     import paper_2410_18252_b200 as odpo
-    P, T, d, V, chunk = shape
+    P, T, d, V, chunk, invT = shape
     B, _, _, _, h, w, tok, mask, pr, ref = _grad_case(seed=17, P=P, T=T, d=d, V=V)
     beta = 0.1
     hd = torch.from_numpy(h).to(torch.bfloat16).cuda()
@@ -203,10 +204,12 @@ def test_lmhead_grad_parity(shape):
     td, md = torch.from_numpy(tok).cuda(), torch.from_numpy(mask).cuda()
     prd = torch.from_numpy(pr).cuda()
     out = odpo.lmhead_online_dpo_loss_fwd(hd, wd, torch.from_numpy(ref).cuda(), td, md, beta,
-                                          pair_rows=prd)
-    dh, dw = odpo.lmhead_grad(hd, wd, td, out.row_lse, out.row_scale, chunk_rows=chunk)
+                                          pair_rows=prd, inv_temperature=invT)
+    dh, dw = odpo.lmhead_grad(hd, wd, td, out.row_lse, out.row_scale, inv_temperature=invT,
+                              chunk_rows=chunk)
     torch.cuda.synchronize()
-    o = oracle.lmhead_dpo_grad(h, w, ref, tok, mask, beta, pair_rows=pr, n_threads=8)
+    o = oracle.lmhead_dpo_grad(h, w, ref, tok, mask, beta, pair_rows=pr, inv_temperature=invT,
+                               n_threads=8)
     for gpu, orc in ((dh.cpu().double().numpy(), o["dhidden"]), (dw.cpu().double().numpy(), o["dweight"])):
         # G is rounded to bf16 (2^-9 relative) before the fp32-accumulated GEMMs
         err = np.linalg.norm(gpu - orc) / max(np.linalg.norm(orc), 1e-30)
