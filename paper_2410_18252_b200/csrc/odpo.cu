@@ -523,6 +523,127 @@ __global__ void k_pg_coef(LossArgs a) {
 }
 
 // ------------------------------------------------------------------ K4 row backward (grid = rows)
+// Short rows (vocabulary shards of NEXT-4): one WARP per row, 8 rows per CTA, each lane with 8
+// 16-byte vectors in flight -- one 512-thread CTA per 12-32 KB row spends its time being
+// scheduled.  Same per-element arithmetic as row_backward (bit-identical output).
+constexpr int kWarpRowsPerCta = 8;
+template <int DT>
+__global__ void __launch_bounds__(32 * kWarpRowsPerCta) k_row_bwd_warp(LossArgs a) {
+  constexpr int N = Traits<DT>::N;
+  constexpr int U = 8;
+  const int lane = threadIdx.x & 31;
+  const int64_t g = (int64_t)blockIdx.x * kWarpRowsPerCta + (threadIdx.x >> 5);
+  if (g >= a.B * a.T) return;
+  const int64_t b = g / a.T, t = g % a.T;
+  const int V = (int)a.V;
+  const int nvec = V / N, tail = V - nvec * N;
+  uint4* vout = reinterpret_cast<uint4*>(drow_ptr(a, b, t));
+  if (a.w.seq_pair[b] < 0 || !a.mask[g]) {
+    for (int i = lane; i < nvec; i += 32) st16_stream(vout + i, make_uint4(0, 0, 0, 0));
+    if (lane < tail) Traits<DT>::store1(vout, (int64_t)nvec * N + lane, 0.f);
+    return;
+  }
+  const float coef = a.w.seq_coef[b];
+  const int64_t tl = (int64_t)a.tokens[g] - a.tok_off;
+  const int tok = (tl >= 0 && tl < V) ? (int)tl : -1;
+  const float k2 = a.invT * kLog2e;
+  const float c = fmaf(a.w.row_l1p[g], kLog2e, a.w.row_m[g] * k2) - log2f(fabsf(coef));
+  const float gtok = coef * expm1f(a.w.row_logp[g]);
+  const bool neg = coef < 0.f;
+  const uint4* vrow = reinterpret_cast<const uint4*>(row_ptr(a, b, t));
+  for (int base = lane; base < nvec; base += 32 * U) {
+    uint4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = base + 32 * u;
+      if (i < nvec) v[u] = ld16<LD_STREAM>(vrow + i, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = base + 32 * u;
+      if (i < nvec)
+        st16_stream(vout + i, neg ? bwd_vec<DT, 0, true>(v[u], k2, c) : bwd_vec<DT, 0, false>(v[u], k2, c));
+    }
+  }
+  if (lane < tail) {
+    const int64_t vv = (int64_t)nvec * N + lane;
+    const float x = Traits<DT>::load1(vrow, vv);
+    Traits<DT>::store1(vout, vv, vv == tok ? gtok : copysignf(ex2(fmaf(x, k2, -c)), coef));
+  }
+  // onehot entry: the lane that stored tok's vector overwrites it (program order)
+  if (tok >= 0 && tok < nvec * N && (tok / N) % 32 == lane) Traits<DT>::store1(vout, tok, gtok);
+}
+
+// Short-row forward partials (NEXT-4 vocabulary shards): one warp per row, each lane with
+// 8 16-byte vectors per batch, the online (m, r) update of the engine (mr_batch), the
+// fixed-order warp merge; writes the shard partial (m, log1p r, x_tok, owns tok) as the
+// engine's vocabulary-parallel epilogue does.
+template <int DT>
+__global__ void __launch_bounds__(32 * kWarpRowsPerCta) k_vp_partials_warp(LossArgs a) {
+  constexpr int N = Traits<DT>::N;
+  constexpr int U = 8;
+  const int lane = threadIdx.x & 31;
+  const int64_t g = (int64_t)blockIdx.x * kWarpRowsPerCta + (threadIdx.x >> 5);
+  if (g >= a.B * a.T) return;
+  if (!a.mask[g]) {
+    if (lane == 0) a.vp_parts[g] = make_float4(-INFINITY, 0.f, 0.f, 0.f);
+    return;
+  }
+  const int64_t b = g / a.T, t = g % a.T;
+  const int V = (int)a.V;
+  const int nvec = V / N, tail = V - nvec * N;
+  const float k2 = a.invT * kLog2e;
+  const int64_t tl = (int64_t)a.tokens[g] - a.tok_off;
+  const int tok = (tl >= 0 && tl < V) ? (int)tl : -1;
+  const uint4* vrow = reinterpret_cast<const uint4*>(row_ptr(a, b, t));
+  const uint32_t NI = Traits<DT>::kNegInfWord;
+  MR s{-INFINITY, 0.f};
+  float xt = 0.f;
+  for (int base = lane; base < nvec; base += 32 * U) {
+    uint4 v[U];
+    bool any = false;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = base + 32 * u;
+      any |= i < nvec;
+      v[u] = i < nvec ? ld16<LD_STREAM>(vrow + i, 0) : make_uint4(NI, NI, NI, NI);
+    }
+    if (any) mr_batch<DT, U, 0>(v, k2, s.m, s.r);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = base + 32 * u;
+      if (tok >= 0 && i < nvec && i == tok / N) {
+        float f[N];
+        Traits<DT>::unpack(v[u], f);
+        float x = f[0];
+#pragma unroll
+        for (int j = 1; j < N; ++j) x = (tok % N == j) ? f[j] : x;
+        xt = x;
+      }
+    }
+  }
+  if (lane < tail) {
+    const int64_t vv = (int64_t)nvec * N + lane;
+    const float x = Traits<DT>::load1(vrow, vv);
+    s = mr_push1(s, x, k2);
+    if (vv == tok) xt = x;
+  }
+  const MR v = warp_merge(s, k2);
+  // the sampled logit from the lane that read it
+  int src = 0;
+  if (tok >= 0) src = tok < nvec * N ? (tok / N) % 32 : tok - nvec * N;
+  xt = __shfl_sync(kFull, xt, src);
+  if (lane == 0) {
+    uint32_t fl = 0;
+    const int64_t gt = tl + a.tok_off;
+    if (gt < 0 || gt >= a.V_total) fl |= ODPO_FLAG_TOKEN_RANGE;
+    if (isnan(v.m) || v.m == INFINITY || !isfinite(v.r)) fl |= ODPO_FLAG_NONFINITE_LOGIT;
+    const bool own = tok >= 0;
+    a.vp_parts[g] = make_float4(v.m, log1pf(v.r), own ? xt : 0.f, own ? 1.f : 0.f);
+    flag(a.status, fl);
+  }
+}
+
 template <int DT, int NPB>
 __global__ void __launch_bounds__(kRowThreads, 2) k_row_bwd(LossArgs a) {
   const int64_t g = blockIdx.x;
@@ -2012,6 +2133,13 @@ odpo_status odpo_vp_row_partials(const void* logits_shard, odpo_dtype dt, int64_
   a.tok_off = v0;
   a.V_total = V_total;
   a.seqsum = 0;
+  if (V_shard * (dt == ODPO_F32 ? 4 : 2) <= (32 << 10)) {  // short shard rows: a warp per row
+    const int64_t rows = B * T;
+    const unsigned grid = (unsigned)((rows + kWarpRowsPerCta - 1) / kWarpRowsPerCta);
+    if (dt == ODPO_F32) k_vp_partials_warp<0><<<grid, 32 * kWarpRowsPerCta, 0, s>>>(a);
+    else k_vp_partials_warp<1><<<grid, 32 * kWarpRowsPerCta, 0, s>>>(a);
+    return launched();
+  }
   k_prep<<<1, kPrepThreads, 0, s>>>(nullptr, B, 0, w, nullptr, B * T);
   if ((e = launched()) != ODPO_OK) return e;
   return launch_engine(dt == ODPO_F32 ? 0 : 1, M_SEQ, kPolyDefault, a, 0, s, -1);
@@ -2054,8 +2182,15 @@ odpo_status odpo_vp_loss_fwd_bwd(const float* parts_all, int32_t W, const void* 
   if ((e = launched()) != ODPO_OK) return e;
   k_pair_reduce<<<(unsigned)P, 32, 0, s>>>(a);
   if ((e = launched()) != ODPO_OK) return e;
-  if (dt == ODPO_F32) k_row_bwd<0, 0><<<(unsigned)rows, kRowThreads, 0, s>>>(a);
-  else k_row_bwd<1, 0><<<(unsigned)rows, kRowThreads, 0, s>>>(a);
+  if (V_shard * (dt == ODPO_F32 ? 4 : 2) <= (32 << 10)) {  // short shard rows: a warp per row
+    const unsigned grid = (unsigned)((rows + kWarpRowsPerCta - 1) / kWarpRowsPerCta);
+    if (dt == ODPO_F32) k_row_bwd_warp<0><<<grid, 32 * kWarpRowsPerCta, 0, s>>>(a);
+    else k_row_bwd_warp<1><<<grid, 32 * kWarpRowsPerCta, 0, s>>>(a);
+  } else if (dt == ODPO_F32) {
+    k_row_bwd<0, 0><<<(unsigned)rows, kRowThreads, 0, s>>>(a);
+  } else {
+    k_row_bwd<1, 0><<<(unsigned)rows, kRowThreads, 0, s>>>(a);
+  }
   return launched();
 }
 
