@@ -6,29 +6,30 @@
 // The scaled output dlogits = coef_b (softmax - onehot) needs the pair's coefficient, known
 // only after BOTH sequences' forward passes (Eq. 3 / SURVEY.md §8(a) S3-S5).  The
 // FUSED engine re-reads a row for its backward; on B200 that re-read misses L2 (DESIGN.md
-// section 4) and the call moves 2R+1W.  This schedule keeps every row ON CHIP between its
-// forward and its backward pass, so the call moves exactly 1R+1W:
+// section 4) and the call moves 2R+1W.  This schedule keeps rows ON CHIP between their
+// forward and backward passes instead (an explicit option: measured slower than FUSED, see
+// DESIGN.md section 4 for the numbers and the Little's-law reason):
 //
 //   * one persistent CTA per SM (grid = #SMs, all co-resident);
-//   * NB whole-row shared-memory buffers, filled by 1-D TMA bulk copies (one mbarrier per
-//     16 KB chunk, so the forward pass starts on the first chunk);
-//   * NSL row slots in TENSOR MEMORY (512 columns x 128 lanes x 32 bit = 256 KB per SM): the
-//     forward warps load a chunk from shared memory into registers for the (m, r) pass and,
-//     when the row owns a TMEM slot, write the same registers to TMEM (tcgen05.st) -- the
-//     shared buffer is released as soon as the forward pass is done; the backward warps read
-//     the row back with tcgen05.ld.  A row without a free TMEM slot stays in its shared
-//     buffer until its backward.  On-chip stash per SM: NB + NSL rows (Pythia bf16: 2 + 2);
-//   * warps: 4 forward warps (geometry 0's per-row reduction tree: 128 threads x 8 vectors
-//     per 16 KB chunk, then the same fixed-order merge -- so row statistics, sequence sums,
-//     loss and dlogits are bit-identical to the FUSED/TWO_PASS schedules and seq_logprobs),
-//     8 backward warps (warps 4+j and 8+j read the two column halves forward warp j wrote:
-//     same TMEM lane quadrant j, same vectors), a producer warp (claims rows in pair order,
-//     owns the TMEM allocation), a parameter warp (polls the sequence's ready+coefficient
-//     word) and an epilogue warp (row statistics, pair counting, pair reduction);
-//   * deadlock freedom: the producer claims a row only while holding a free shared buffer, so
-//     a claimed row's forward pass waits on nothing but its own TMA; a pair therefore
-//     completes once all its 2T rows are claimed, which needs SMs * min(NB + NSL, 8) >= 2T
-//     (the host requires twice that so the next pairs stream while one completes).
+//   * a forward TMA ring (ODPO_RES_RF x 16 KB stages, 1-D bulk copies) feeds 4 forward warps,
+//     which run the online (m, r) pass from registers and, when the row owns a TMEM slot, write
+//     the same registers to TENSOR MEMORY (tcgen05.st; 512 columns x 128 lanes x 32 bit = 256 KB
+//     per SM = NSL row slots, two Pythia rows);
+//   * 8 backward warps read a TMEM row back (tcgen05.ld; warps 4+j and 8+j read the two column
+//     halves forward warp j wrote: same lane quadrant j, same vectors).  Rows beyond the TMEM
+//     slots are "L2-backed" (forward loads evict_last): a backward thread re-streams them
+//     through a second TMA ring (ODPO_RES_RB stages); at most `cap` of them per SM;
+//   * the forward warps reproduce geometry 0's per-row reduction tree (128 threads x 8 vectors
+//     per chunk, then the same fixed-order merge), so row statistics, sequence sums, loss and
+//     dlogits are bit-identical to FUSED / TWO_PASS and seq_logprobs;
+//   * a producer warp (claims rows in pair order, owns the TMEM allocation), a parameter warp
+//     (UN = 0: polls the sequence's packed ready+coefficient word from the pair reduction;
+//     UN = 1: the factored gradient or a known coefficient, no wait) and an epilogue warp (row
+//     statistics, pair counting, pair reduction);
+//   * deadlock freedom (UN = 0): the producer claims a row only while holding a TMEM slot or an
+//     L2 allowance, so a claimed row's forward pass waits on nothing but its own TMA; a pair
+//     completes once all its 2T rows are claimed, which needs SMs * min(NSL + cap, 8) >= 2T
+//     (the host requires twice that).
 #pragma once
 
 namespace odpo {
