@@ -325,6 +325,8 @@ __global__ void __launch_bounds__(THREADS, 1)
                   Args a) {
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full[STAGES2], empty[STAGES2], tfull[2], tempty[2];
+  // GRAD epilogue: per epilogue warp a 32-row x 64-byte staging tile (rows padded to 80 B)
+  __shared__ __align__(16) uint4 gstage[4][GRAD ? 32 * 5 : 1];
   __shared__ uint32_t tmem_sh;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
@@ -437,7 +439,6 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int64_t cb = c0 + 32 * c;
         if (cb >= a.V) break;
         if (GRAD) {
-          if (!live) continue;
           // g_j = row_scale * p_j; at the sampled token row_scale * expm1(log p) (no p - 1
           // cancellation); rows with row_scale 0 (masked, unreferenced) get exact zeros
           uint32_t w[16];
@@ -449,13 +450,26 @@ __global__ void __launch_bounds__(THREADS, 1)
             if (tok == cb + j + 1) g1 = g_rs * expm1f(fmaf(__uint_as_float(r[j + 1]), a.invT, -a.row_lse[row]));
             w[j / 2] = pack_bf16x2(g0, g1);
           }
-          __nv_bfloat16* dst = a.gout + row * a.ldg + cb;
           if (cb + 32 <= a.V) {
-            uint4* d4 = reinterpret_cast<uint4*>(dst);
+            // stage the warp's 32 rows x 64 B, then store row-contiguous: each store
+            // instruction writes 64 B to each of 8 rows instead of 16 B to each of 32
+            uint4* st_w = gstage[q];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) d4[k] = make_uint4(w[4 * k], w[4 * k + 1], w[4 * k + 2], w[4 * k + 3]);
-          } else {
-            unsigned short* d2 = reinterpret_cast<unsigned short*>(dst);
+            for (int k = 0; k < 4; ++k)
+              st_w[lane * 5 + k] = make_uint4(w[4 * k], w[4 * k + 1], w[4 * k + 2], w[4 * k + 3]);
+            __syncwarp();
+            const int64_t row0 = rb2 * 256 + rank * 128 + 32 * q;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const int rr = 8 * k + (lane >> 2), sg = lane & 3;
+              if (row0 + rr < a.R) {
+                uint4* d4 = reinterpret_cast<uint4*>(a.gout + (row0 + rr) * a.ldg + cb) + sg;
+                *d4 = st_w[rr * 5 + sg];
+              }
+            }
+            __syncwarp();
+          } else if (live) {
+            unsigned short* d2 = reinterpret_cast<unsigned short*>(a.gout + row * a.ldg + cb);
             for (int j = 0; j < 32 && cb + j < a.V; ++j)
               d2[j] = (unsigned short)((w[j / 2] >> (16 * (j & 1))) & 0xFFFFu);
           }
