@@ -37,9 +37,16 @@ namespace odpo {
 #ifndef ODPO_RES_FW
 #define ODPO_RES_FW 4
 #endif
-constexpr int kResFW = ODPO_RES_FW;            // forward warps (4: geometry 0's tree; or 8)
-constexpr int kResBW = 8;                      // backward warps (4..11)
-constexpr int kResProd = kResFW + kResBW;      // producer warp (12), TMEM owner
+constexpr int kResFW = ODPO_RES_FW;            // forward warps per group (4: geometry 0's tree; or 8)
+// forward warp groups (experiment): each group of kResFW warps streams every kResFGr-th live
+// row, so kResFGr rows are in their forward pass at once per SM
+#ifndef ODPO_RES_FGROUPS
+#define ODPO_RES_FGROUPS 1
+#endif
+constexpr int kResFGr = ODPO_RES_FGROUPS;
+constexpr int kResFWt = kResFW * kResFGr;      // all forward warps
+constexpr int kResBW = 8;                      // backward warps
+constexpr int kResProd = kResFWt + kResBW;     // producer warp, TMEM owner
 constexpr int kResPar = kResProd + 1;          // parameter warp (13)
 constexpr int kResEpi = kResProd + 2;          // epilogue warp (14)
 constexpr int kResThreads = (kResEpi + 1) * 32;
@@ -77,6 +84,7 @@ constexpr int kResTmemCols = 512;
 constexpr int kResSmemMax = 227 * 1024 - 6 * 1024;
 constexpr int kResSmemMin = 120 * 1024;
 static_assert(kResFW == 4 || kResFW == 8, "4 or 8 forward warps");
+static_assert(kResFGr == 1 || kResFW == 4, "forward groups of 4 warps");
 static_assert(kResUB * 4 * kResFG == kResCols, "a chunk fills 32 columns of every lane");
 
 // AUTO picks RESIDENT only when this is set (measured slower than FUSED so far: DESIGN.md)
@@ -359,13 +367,15 @@ __global__ void __launch_bounds__(kResThreads, 1) k_resident(LossArgs a, ResGeo 
         }
       }
     }
-  } else if (warp < kResFW) {
+  } else if (warp < kResFWt) {
     // ================= forward warps: (m, r) over the row out of the forward ring, exactly
     // the engine's geometry-0 consumer arithmetic; the same registers go to the TMEM slot
-    const uint32_t lane_base = (uint32_t)(32 * (warp & 3)) << 16;
-    const uint32_t gcol = (uint32_t)((warp >> 2) * kResUB * 4);  // this warp's column group
-    int fst = 0;
-    uint32_t fph = 0;
+    const int grp = warp / kResFW;           // forward group (rows live_idx % kResFGr)
+    const int gw = warp % kResFW;            // warp within the group
+    const int gtid = gw * 32 + lane;         // thread within the group (the reduction tree)
+    const uint32_t lane_base = (uint32_t)(32 * (gw & 3)) << 16;
+    const uint32_t gcol = (uint32_t)((gw >> 2) * kResUB * 4);  // this warp's column group
+    int64_t live_idx = 0;                    // live rows seen so far (ring stage bookkeeping)
     for (int64_t k = 0;; ++k) {
       const int it = (int)(k % kResNIt);
       const uint32_t ph = (uint32_t)((k / kResNIt) & 1);
@@ -373,6 +383,10 @@ __global__ void __launch_bounds__(kResThreads, 1) k_resident(LossArgs a, ResGeo 
       ResItem& I = items[it];
       const int kind = I.kind;
       if (kind == R_END) break;
+      const bool mine = kind == R_LIVE ? (live_idx % kResFGr) == grp : grp == 0;
+      const int64_t li = live_idx;
+      if (kind == R_LIVE) ++live_idx;
+      if (!mine) continue;
       if (kind == R_LIVE) {
         const int ts = I.tslot, tok = I.tok;
         const int tvec = (tok >= 0 && tok < nvec * N) ? tok / N : -1;
@@ -380,29 +394,32 @@ __global__ void __launch_bounds__(kResThreads, 1) k_resident(LossArgs a, ResGeo 
         if (ts >= 0) tm_fence_after();
         MR s{-INFINITY, 0.f};
         for (int c = 0; c < nch; ++c) {
+          const int64_t qst = li * nch + c;  // this chunk's position in the forward ring
+          const int fst = (int)(qst % G.rf);
+          const uint32_t fph = (uint32_t)((qst / G.rf) & 1);
           mbar_wait(ffull_s + 8 * fst, fph);
-          if (tid == 0 && c == 0) RES_DBG(I.tk, 1);
-          if (tid == 0 && c == nch - 1) RES_DBG(I.tk, 2);
+          if (gtid == 0 && c == 0) RES_DBG(I.tk, 1);
+          if (gtid == 0 && c == nch - 1) RES_DBG(I.tk, 2);
           const uint4* sb = reinterpret_cast<const uint4*>(rbuf + (size_t)fst * kChunk);
           const int c0 = c * kCV;
           const int cnv = min(kCV, nvec - c0);
           uint4 v[kResUB];
           if (cnv == kCV) {
 #pragma unroll
-            for (int u = 0; u < kResUB; ++u) v[u] = sb[tid + u * kResFT];
+            for (int u = 0; u < kResUB; ++u) v[u] = sb[gtid + u * kResFT];
             if (ts >= 0) tm_st<kResUB>(tcol + (uint32_t)(c * kResCols), v);
             mr_batch<DT, kResUB, NPF>(v, k2, s.m, s.r);
           } else {
             const uint32_t NI = Traits<DT>::kNegInfWord;
 #pragma unroll
             for (int u = 0; u < kResUB; ++u) {
-              const int i = tid + u * kResFT;
+              const int i = gtid + u * kResFT;
               v[u] = i < cnv ? sb[i] : make_uint4(NI, NI, NI, NI);
             }
             if (ts >= 0) tm_st<kResUB>(tcol + (uint32_t)(c * kResCols), v);
-            if (tid < cnv) mr_batch<DT, kResUB, NPF>(v, k2, s.m, s.r);
+            if (gtid < cnv) mr_batch<DT, kResUB, NPF>(v, k2, s.m, s.r);
           }
-          if (tvec >= c0 && tvec < c0 + cnv && ((tvec - c0) % kResFT) == tid) {
+          if (tvec >= c0 && tvec < c0 + cnv && ((tvec - c0) % kResFT) == gtid) {
             float f[N];
             Traits<DT>::unpack(sb[tvec - c0], f);
             float x = f[0];
@@ -412,10 +429,9 @@ __global__ void __launch_bounds__(kResThreads, 1) k_resident(LossArgs a, ResGeo 
           }
           __syncwarp();
           if (lane == 0) mbar_arrive(fempty_s + 8 * fst);
-          if (++fst == G.rf) { fst = 0; fph ^= 1u; }
         }
-        if (tid < tail) {
-          const int64_t vv = (int64_t)nvec * N + tid;
+        if (gtid < tail) {
+          const int64_t vv = (int64_t)nvec * N + gtid;
           const float x = Traits<DT>::load1(I.row, vv);
           s = mr_push1(s, x, k2);
           if (vv == tok) I.xtok = x;
@@ -427,10 +443,10 @@ __global__ void __launch_bounds__(kResThreads, 1) k_resident(LossArgs a, ResGeo 
         }
         __syncwarp();
         if (lane == 0) {
-          I.pm[warp] = wv.m;
-          I.pr[warp] = wv.r;
+          I.pm[gw] = wv.m;
+          I.pr[gw] = wv.r;
           mbar_arrive(pready_s + 8 * it);
-          if (warp == 0) atomicSub(&f_q, 1);
+          if (gw == 0) atomicSub(&f_q, 1);
         }
       } else {
         __syncwarp();
@@ -442,12 +458,12 @@ __global__ void __launch_bounds__(kResThreads, 1) k_resident(LossArgs a, ResGeo 
     // L2-backed row, re-streamed through the backward ring (TMA issued by backward thread 0);
     // warp 4 + j (8 + j) handles vectors u = 0..3 (4..7) of forward warp j's threads -- the
     // columns that forward warp wrote into lane quadrant j
-    const int j = (warp - kResFW) & 3, half = (warp - kResFW) >> 2;
+    const int j = (warp - kResFWt) & 3, half = (warp - kResFWt) >> 2;
     // the forward thread whose TMEM lane / columns this thread reads, and its first vector
-    const int ftid = kResFW == 4 ? j * 32 + lane : (warp - kResFW) * 32 + lane;
+    const int ftid = kResFW == 4 ? j * 32 + lane : (warp - kResFWt) * 32 + lane;
     const int u0 = kResFW == 4 ? 4 * half : 0;
     const uint32_t lane_base = (uint32_t)(32 * j) << 16;
-    const int btid = tid - kResFT;  // 0..255 (zero rows, tail, TMA issue)
+    const int btid = tid - kResFWt * 32;  // 0..255 (zero rows, tail, TMA issue)
     const uint64_t pol_drop = policy_evict_first();
     int bst = 0, ist = 0;  // backward ring: next stage to consume / to fill
     uint32_t bph = 0, iph = 0;
