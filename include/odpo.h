@@ -377,7 +377,7 @@ const char* odpo_version(void);
  * (d % 64 != 0, B*T or V > 2^31 - 1), ALIGNMENT, WORKSPACE, CUDA (launch or tensor-map
  * encoding failed).
  * Tuning only (environment, read per call): ODPO_LMH_1CTA=1 selects the single-CTA kernel,
- * ODPO_LMH_G=<n> the raster group size; results do not depend on either.
+ * ODPO_LMH_G=<n> the raster group size (the raster order does not change results).
  */
 size_t odpo_lmhead_workspace_bytes(int64_t B, int64_t T, int64_t V);
 
