@@ -56,8 +56,10 @@ def lib():
             P, P, C.c_int]
         L.orc_pg_loss_fwd_bwd.argtypes = [P, C.c_int, i64, i64, i64, i64, i64, P, P, P, i64, i64,
                                           C.c_int, P, P, f32, f32, P, P, i64, P, P, P, C.c_int]
+        L.orc_seq_ppl.argtypes = [P, C.c_int, i64, i64, i64, i64, i64, P, P, f32, P, P, P, P,
+                                  C.c_int]
         for f in (L.orc_pair_select, L.orc_seq_logprobs, L.orc_online_dpo_loss_fwd_bwd,
-                  L.orc_online_dpo_loss_fwd_bwd_unscaled, L.orc_pg_loss_fwd_bwd):
+                  L.orc_online_dpo_loss_fwd_bwd_unscaled, L.orc_pg_loss_fwd_bwd, L.orc_seq_ppl):
             f.restype = C.c_int
         _lib = L
     return _lib
@@ -120,6 +122,26 @@ def seq_logprobs(logits, tokens, mask, inv_temperature=1.0, n_threads=1):
     if rc:
         raise ValueError("orc_seq_logprobs: invalid argument")
     return dict(seq_logp=S, tok_logp=tlp, row_lse=lse, status=int(status[0]))
+
+
+def seq_ppl(logits, tokens, mask, inv_temperature=1.0, n_threads=1):
+    """KL proxy: per-completion perplexity exp(-S_b / n_b) of the model
+    whose logits are given.  Returns dict(seq_logp[B], ppl[B], ppl_stats[4] = (#nonempty,
+    sum ppl, sum S, sum n), status)."""
+    a, dt, sb, st = _logits_args(logits)
+    B, T, V = a.shape
+    tok = np.ascontiguousarray(tokens, dtype=np.int32).reshape(B, T)
+    msk = np.ascontiguousarray(mask, dtype=np.uint8).reshape(B, T)
+    S = np.zeros(B, np.float64)
+    ppl = np.zeros(B, np.float64)
+    ps = np.zeros(4, np.float64)
+    status = np.zeros(1, np.uint32)
+    rc = lib().orc_seq_ppl(_ptr(a), dt, B, T, V, sb, st, _ptr(tok), _ptr(msk),
+                           float(np.float32(inv_temperature)), _ptr(S), _ptr(ppl), _ptr(ps),
+                           _ptr(status), int(n_threads))
+    if rc:
+        raise ValueError("orc_seq_ppl: invalid argument")
+    return dict(seq_logp=S, ppl=ppl, ppl_stats=ps, status=int(status[0]))
 
 
 def online_dpo_loss_fwd_bwd(logits, ref_logp, tokens, mask, beta, pair_rows=None, p_global=None,

@@ -29,6 +29,8 @@
  *                     token log-probs: RLOO with k = 2, CoPG
  *                     (PAPER.md:716-719), Proximal RLOO and the Best-of-2
  *                     SFT baseline; see that function's comment.
+ *   orc_seq_ppl       the KL proxy of PAPER.md:121 (Sec 3) / PAPER.md:333 (Sec 5.2): the
+ *                     reference model's per-completion perplexity exp(-S_b / n_b).
  *   orc_online_dpo_loss_fwd_bwd_unscaled
  *                     the same, with the gradient returned factored per row:
  *                     G = softmax - onehot and row_scale = coef_b (dL/dx = row_scale * G).
@@ -239,6 +241,45 @@ int orc_seq_logprobs(const void* logits, int dtype, int64_t B, int64_t T, int64_
   if (!logits || !tokens || !mask || !seq_logp || B <= 0 || T <= 0 || V <= 0) return 1;
   rows_in in = {logits, dtype, B, T, V, stride_b, stride_t, tokens, mask, (double)inv_temperature};
   uint32_t st = run_seqs(&in, seq_logp, NULL, tok_logp, row_lse, n_threads);
+  if (status) *status |= st;
+  return 0;
+}
+
+/* ------------------------------------------------------------------ KL proxy (PPL)
+ * PAPER.md:121 (Sec 3, Evaluation: "we measure the SFT model's perplexity on the RLHF
+ * policy's summaries") and PAPER.md:333 (Sec 5.2, "Final KL is measured using the perplexity
+ * of the base model on the generated completions"), read per completion (R20):
+ *   ppl_b = exp(-S_b / n_b),  S_b = orc_seq_logprobs' log pi_ref(y_b|x),  n_b = #mask tokens.
+ * An empty completion (n_b = 0, flagged EMPTY_SEQ) gets ppl_b = 1 and is left out of
+ * ppl_stats = {#completions with n_b > 0, sum_b ppl_b, sum_b S_b, sum_b n_b}
+ * (the corpus perplexity is exp(-ppl_stats[2] / ppl_stats[3])). */
+int orc_seq_ppl(const void* logits, int dtype, int64_t B, int64_t T, int64_t V, int64_t stride_b,
+                int64_t stride_t, const int32_t* tokens, const uint8_t* mask,
+                float inv_temperature, double* seq_logp, double* ppl, double* ppl_stats,
+                uint32_t* status, int n_threads) {
+  if (!logits || !tokens || !mask || !seq_logp || !ppl || B <= 0 || T <= 0 || V <= 0) return 1;
+  rows_in in = {logits, dtype, B, T, V, stride_b, stride_t, tokens, mask, (double)inv_temperature};
+  double* ntok = (double*)calloc((size_t)B, sizeof(double));
+  uint32_t st = run_seqs(&in, seq_logp, ntok, NULL, NULL, n_threads);
+  double nseq = 0.0, sp = 0.0, sS = 0.0, sn = 0.0;
+  for (int64_t b = 0; b < B; ++b) {
+    if (ntok[b] > 0.0) {
+      ppl[b] = exp(-seq_logp[b] / ntok[b]);
+      nseq += 1.0;
+      sp += ppl[b];
+      sS += seq_logp[b];
+      sn += ntok[b];
+    } else {
+      ppl[b] = 1.0;
+    }
+  }
+  if (ppl_stats) {
+    ppl_stats[0] = nseq;
+    ppl_stats[1] = sp;
+    ppl_stats[2] = sS;
+    ppl_stats[3] = sn;
+  }
+  free(ntok);
   if (status) *status |= st;
   return 0;
 }

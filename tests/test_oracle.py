@@ -226,6 +226,95 @@ def test_w1_golden(orc):
             assert abs(out["stats"][1] - float(loss)) < 1e-8
 
 
+def test_w1_golden_statistics(orc):
+    """All ten loss statistics of the W1 worked example and of its swap, against the closed
+    form (tests/golden/w1_stats.txt): the implicit-reward margin sum z, the chosen / rejected
+    implicit rewards beta (S - ref), the sequence log-prob sums and the token counts."""
+    ln3 = math.log(3.0)
+    x = np.array([[[ln3, 0.0]], [[0.0, ln3]]])
+    tok = np.zeros((2, 1), np.int32)
+    mask = np.ones((2, 1), np.uint8)
+    ref = np.full(2, np.float32(math.log(0.5)), np.float32)
+    for case, beta, *vals in golden_rows("w1_stats.txt"):
+        beta = float(beta)
+        pr = np.array([[0, 1]] if case == "w1" else [[1, 0]], np.int32)
+        out = orc.online_dpo_loss_fwd_bwd(x, ref, tok, mask, beta, pair_rows=pr)
+        st = out["stats"]
+        exp = [float(v) for v in vals]
+        scale = float(np.float32(beta)) / beta  # beta enters as fp32
+        assert st[0] == exp[0] and st[2] == exp[2] and st[8] == exp[8] and st[9] == exp[9]
+        sgn = 1.0 if case == "w1" else -1.0
+        assert abs(st[1] - math.log1p(3.0 ** (-sgn * float(np.float32(beta))))) < 1e-14
+        assert abs(st[1] - exp[1]) < 1e-8 * max(1.0, abs(scale - 1) * 1e8)
+        for i in (3, 4, 5):      # beta-linear columns
+            assert abs(st[i] - exp[i] * scale) < 3e-9, (case, beta, i, st[i], exp[i])
+        for i in (6, 7):
+            assert abs(st[i] - exp[i]) < 1e-14, (case, beta, i)
+
+
+def test_statistics_identities_and_swap(orc):
+    """Identities the mathematics fixes for the margin statistics on a random batch:
+    z_sum = r_chosen - r_rejected, r_chosen = beta (S_c_sum - ref_c_sum), S sums equal the
+    per-sequence log-probs summed over chosen / rejected members, and swapping y+/y- of every
+    pair exchanges the chosen and rejected columns and negates z_sum."""
+    P = 300
+    x, tok, mask, rng = _random_batch(21, P=P, T=4, V=7)
+    ref = rng.normal(-5, 2, size=2 * P).astype(np.float32)
+    pr = synth_perm_pairs(P, seed=4)
+    beta = 0.25
+    a = orc.online_dpo_loss_fwd_bwd(x, ref, tok, mask, beta, pair_rows=pr)
+    b_ = orc.online_dpo_loss_fwd_bwd(x, ref, tok, mask, beta, pair_rows=pr[:, ::-1].copy())
+    S = a["seq_logp"]
+    c, r = pr[:, 0], pr[:, 1]
+    sa = a["stats"]
+    assert abs(sa[6] - S[c].sum()) < 1e-10 and abs(sa[7] - S[r].sum()) < 1e-10
+    assert abs(sa[4] - beta * (S[c] - ref[c].astype(np.float64)).sum()) < 1e-10
+    assert abs(sa[5] - beta * (S[r] - ref[r].astype(np.float64)).sum()) < 1e-10
+    assert abs(sa[3] - (sa[4] - sa[5])) < 1e-10
+    assert sa[8] == mask[c].sum() and sa[9] == mask[r].sum()
+    sb = b_["stats"]
+    assert sb[3] == -sa[3] or abs(sb[3] + sa[3]) < 1e-12
+    for i, j in ((4, 5), (6, 7), (8, 9)):
+        assert abs(sb[i] - sa[j]) < 1e-12 and abs(sb[j] - sa[i]) < 1e-12
+    assert sa[2] + sb[2] == np.count_nonzero(a["z"])
+
+
+def synth_perm_pairs(P, seed):
+    """A random pairing of 2P rows (every row in exactly one pair)."""
+    perm = np.random.default_rng(seed).permutation(2 * P).astype(np.int32)
+    return perm.reshape(P, 2)
+
+
+# ------------------------------------------------------------------ KL proxy (PPL)
+@pytest.mark.parametrize("V", [1, 2, 7, 50304])
+def test_ppl_uniform_rows_is_V(orc, V):
+    """PAPER.md:121/333 KL proxy: on uniform rows every token has probability 1/V, so the
+    perplexity of every completion is exactly V (closed form), whatever its length."""
+    B, T = 3, 5
+    x = np.full((B, T, V), 0.375, np.float32)
+    tok = (np.arange(B * T).reshape(B, T) % V).astype(np.int32)
+    mask = np.ones((B, T), np.uint8)
+    mask[1, 2:] = 0
+    mask[2, :] = 0
+    o = orc.seq_ppl(x, tok, mask)
+    assert abs(o["ppl"][0] - V) <= 1e-12 * V and abs(o["ppl"][1] - V) <= 1e-12 * V
+    assert o["ppl"][2] == 1.0 and o["status"] & orc.FLAG_EMPTY_SEQ
+    ps = o["ppl_stats"]
+    assert ps[0] == 2 and abs(ps[1] - 2 * V) <= 1e-12 * V and ps[3] == T + 2
+    assert abs(math.exp(-ps[2] / ps[3]) - V) <= 1e-12 * V
+
+
+def test_ppl_two_token_closed_form(orc):
+    """V = 2 rows x = (ln 3, 0) with token 0: p = 3/4 per token, so PPL = 4/3 for any length;
+    mixing one p = 1/4 token into a length-2 completion gives PPL = (3/4 * 1/4)^(-1/2)."""
+    ln3 = math.log(3.0)
+    x = np.array([[[ln3, 0.0], [ln3, 0.0]], [[ln3, 0.0], [0.0, ln3]]])
+    tok = np.zeros((2, 2), np.int32)
+    o = orc.seq_ppl(x, tok, np.ones((2, 2), np.uint8))
+    assert abs(o["ppl"][0] - 4.0 / 3.0) < 1e-14
+    assert abs(o["ppl"][1] - (3.0 / 16.0) ** -0.5) < 1e-14
+
+
 # ---------------------------------------------------------------------- O-6 ln 2 / O-7 swap
 def _random_batch(seed, P=40, T=6, V=17, dtype=np.float64):
     rng = np.random.default_rng(seed)
