@@ -1,7 +1,11 @@
 #!/usr/bin/env python
 """bench.py -- Online-DPO learner hot path on B200: pairs/s and achieved HBM GB/s.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config pythia] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config llama] [--impl ours|reference]
+
+The default workload is BASELINE.json configs[3], LLaMA-3.1-8B No Robots (64 pairs x 2,
+T 1024, V 128256, bf16): the largest configuration that fits one GPU (configs[4], the
+strong-scaling sweep, is 2048 pairs of that shape; --config strong).
 
 One STEP = one pass of the whole hot path over one batch of synthetic input
 (SURVEY.md §8(a) rows S1-S6): pair_select over the rewards, the Online-DPO loss
@@ -38,7 +42,7 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="pythia",
+    ap.add_argument("--config", default="llama",
                     choices=["tiny", "pythia", "rho", "llama", "strong", "rho_k4"])
     ap.add_argument("--chunk-pairs", type=int, default=64)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -79,6 +83,74 @@ def bf16_peak():
         if "bf16_tflops" in d:
             return float(d["bf16_tflops"]), "measured (MEASURED_PEAKS.json bf16_tflops, cuBLAS)"
     return 1590.0, "fallback (B200_PROFILING.md)"
+
+
+def src_sha() -> str:
+    """Hash of the product kernel sources (csrc + the C header): an ncu capture is used as this
+    run's traffic evidence only if it was taken on the same sources."""
+    import glob
+    import hashlib
+    h = hashlib.sha256()
+    files = sorted(glob.glob(os.path.join(ROOT, "paper_2410_18252_b200", "csrc", "*.cu*")))
+    for f in files + [os.path.join(ROOT, "include", "odpo.h")]:
+        h.update(open(f, "rb").read())
+    return h.hexdigest()[:16]
+
+
+def ncu_evidence(config, form):
+    """ncu --set full record of this config's dominant kernel (profiles/r02/ncu/), or None when
+    there is none for the current sources."""
+    p = os.path.join(ROOT, "profiles", "r02", "ncu", f"traffic_{config}_{form}.json")
+    if not os.path.exists(p):
+        return None
+    d = json.load(open(p))
+    if d.get("src_sha") != src_sha():
+        return None
+    d["file"] = os.path.relpath(p, ROOT)
+    return d
+
+
+def measure_ceilings(dev):
+    """Copy and read-only HBM ceilings measured in this run: b.copy_(a) over
+    1 Gi bf16 (read + write bytes, MEASURED_PEAKS.json's method) and a bf16 -> fp32 sum over
+    4 GiB (read bytes), best of 5 with CUDA events."""
+    import torch
+    out = {}
+    a = torch.empty(1 << 30, dtype=torch.bfloat16, device=dev)
+    b = torch.empty_like(a)
+    a.fill_(1.0)
+
+    def best(fn, nbytes):
+        fn()
+        ts = []
+        for _ in range(5):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn()
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        return nbytes / (min(ts) / 1e3) / 1e9
+
+    out["copy_gbs"] = best(lambda: b.copy_(a), 2 * a.numel() * 2)
+    del a, b
+    x = torch.empty(2 << 30, dtype=torch.bfloat16, device=dev)
+    x.fill_(0.5)
+    out["read_gbs"] = best(lambda: x.sum(dtype=torch.float32), x.numel() * 2)
+    del x
+    torch.cuda.empty_cache()
+    out["how"] = "copy: b.copy_(a) 1 Gi bf16, read+write bytes; read: x.sum over 4 GiB bf16; best of 5"
+    return out
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 # LM-head shapes of the paper's models (hidden width d, vocabulary V) for the NEXT-2 aux line
@@ -203,8 +275,14 @@ def workload(name):
 
 
 # ----------------------------------------------------------------------------- oracle timing
-def oracle_sample(w, seed, npairs, mask_kind, n_threads, p0=0):
-    """Time the CPU oracle (as it stands) on npairs pairs of the same workload."""
+_SAMPLES: dict = {}
+
+
+def oracle_inputs(w, seed, npairs, mask_kind, p0=0):
+    """Host inputs of npairs pairs of the workload (synth, untimed; cached)."""
+    key = (w.name, seed, npairs, mask_kind, p0)
+    if key in _SAMPLES:
+        return _SAMPLES[key]
     import oracle
     import synth
     K = w.K
@@ -225,13 +303,30 @@ def oracle_sample(w, seed, npairs, mask_kind, n_threads, p0=0):
     if w.dtype == "bf16":
         x = oracle.to_bf16_bits(x)
     ref = np.full(len(sel_rows), -0.08 * w.T, np.float32)
+    _SAMPLES.clear()
+    _SAMPLES[key] = (x, tok, mask, rewards, eos, pen, ref)
+    return _SAMPLES[key]
+
+
+def oracle_sample(w, seed, npairs, mask_kind, n_threads, p0=0):
+    """Time the CPU oracle (as it stands) on npairs pairs of the same workload: pair_select,
+    the fp64 loss and the full dlogits."""
+    import oracle
+    x, tok, mask, rewards, eos, pen, ref = oracle_inputs(w, seed, npairs, mask_kind, p0)
     t0 = time.perf_counter()
     sel = oracle.pair_select(rewards, eos, pen)
     o = oracle.online_dpo_loss_fwd_bwd(x, ref, tok, mask, w.beta,
-                                       pair_rows=sel["pair_rows"] if K == 2 else None,
+                                       pair_rows=sel["pair_rows"] if w.K == 2 else None,
                                        want_dlogits=True, n_threads=n_threads)
     dt = time.perf_counter() - t0
     return dt, o
+
+
+def oracle_pairs_per_sample(w, cores):
+    """A bounded sample: whole pairs, about 2e7 logits per sample at most (one LLaMA pair is
+    2.6e8 and is the unit there)."""
+    per_pair = 2 * w.T * w.V
+    return int(max(1, min(w.P, cores, 2e7 // per_pair)))
 
 
 def run_reference(args, rank, world):
@@ -240,8 +335,8 @@ def run_reference(args, rank, world):
         return
     w = workload(args.config)
     cores = os.cpu_count() or 1
-    npairs = max(1, min(w.P, cores // 2)) if w.T * w.V < 1e7 else 1
-    threads = min(cores, 2 * npairs)
+    npairs = oracle_pairs_per_sample(w, cores)
+    threads = cores
     for _ in range(max(0, min(args.warmup, 1))):
         oracle_sample(w, args.seed, npairs, args.mask, threads)
     times = []
@@ -258,6 +353,7 @@ def run_reference(args, rank, world):
         "config": {"workload": args.config, "pairs_per_step": npairs, "T": w.T, "V": w.V,
                    "logits_dtype": w.dtype, "mask": args.mask},
         "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": threads, "kind": "oracle",
+                         "cpu_model": cpu_model(),
                          "sample": f"{npairs} pairs of {args.config} per step (pair_select + "
                                    f"loss + full dlogits, fp64, {threads} threads)"},
         "e2e": {"value": value, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -275,6 +371,7 @@ def run_ours(args, rank, world, local_rank):
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
+    ceil = measure_ceilings(dev)
     w = workload(args.config)
     P, T, V = w.P, w.T, w.V
     B = 2 * P
@@ -414,7 +511,9 @@ def run_ours(args, rank, world, local_rank):
     achieved = alg_bytes / (loss_ms.mean() / 1e3) / 1e9
     peak, peak_src = peaks()
 
-    # auxiliary: the other gradient form on the same inputs (same bytes, not the headline)
+    # the other gradient form on the same inputs, timed the same way and reported beside the
+    # headline (scaled dlogits = the north_star output; factored = G + row_scale)
+    form = ("scaled" if args.gradient == "scaled" else "unscaled") if args.loss == "dpo" else args.loss
     aux = None
     if not args.no_aux and args.loss == "dpo":
         other = "unscaled" if args.gradient == "scaled" else "scaled"
@@ -429,18 +528,21 @@ def run_ours(args, rank, world, local_rank):
         torch.cuda.synchronize()
         ams = np.array([a.elapsed_time(b) for a, b in aev])
         aach = alg_bytes / (ams.mean() / 1e3) / 1e9
-        aux = {"gradient": other, "loss_ms_mean": float(ams.mean()), "achieved": aach,
-               "frac": aach / peak, "pairs_per_s_loss_only": world * P / (ams.mean() / 1e3),
-               "status": int(status.item())}
-    lmh = aux_lmhead(args.config, B, T) if not args.no_aux and args.loss == "dpo" else None
-    traffic = None
-    sfx = ("" if args.gradient == "scaled" else "_unscaled") if args.loss == "dpo" else "_" + args.loss
-    tp = os.path.join(ROOT, "profiles", f"ncu_traffic_{args.config}{sfx}.json")
-    if os.path.exists(tp):
-        try:
-            traffic = json.load(open(tp)).get("dram_bytes_per_launch")
-        except Exception:
-            traffic = None
+        nv = ncu_evidence(args.config, other)
+        aux = {"gradient": other, "bound": "hbm", "achieved": aach, "peak": peak, "unit": "GB/s",
+               "frac": aach / peak, "frac_of_copy_ceiling": aach / ceil["copy_gbs"],
+               "traffic": nv["dram_bytes_per_launch"] if nv else None,
+               "ncu": nv, "loss_ms_mean": float(ams.mean()),
+               "pairs_per_s_loss_only": world * P / (ams.mean() / 1e3),
+               "alg_bytes_per_launch": alg_bytes, "status": int(status.item()),
+               "kernel": ("odpo_online_dpo_loss_fwd_bwd_unscaled (prep + fwd/bwd)" if other == "unscaled"
+                          else "odpo_online_dpo_loss_fwd_bwd (prep + fused fwd/bwd)")}
+    # NEXT-2 aux: the Pythia-2.8B LM head (the head whose fused step VERDICT r1 asks to beat)
+    lmh = aux_lmhead("pythia", 512, 53) if not args.no_aux and args.loss == "dpo" else None
+    nv_main = ncu_evidence(args.config, form)
+    traffic = nv_main["dram_bytes_per_launch"] if nv_main else None
+    # 2R+1W: the scaled output's traffic floor where a pair does not fit in L2
+    floor_bytes = 2 * rho * B * T * V * s_in + B * T * V * s_in
 
     # ---------------- e2e through host buffers (pinned H2D inputs, D2H stats + z each step)
     e2e = None
@@ -502,21 +604,26 @@ def run_ours(args, rank, world, local_rank):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        # the oracle as it stands, on successive blocks of this workload's pairs until about
-        # args.cpu_seconds of CPU work have been timed (a bounded sample)
+        # the oracle as it stands, on one block of this workload's pairs repeated until about
+        # args.cpu_seconds of CPU work have been timed (a bounded sample), on every host core;
+        # then the same block once on ONE core
+        del dlogits, logits
+        torch.cuda.empty_cache()
         cores = os.cpu_count() or 1
-        npairs = max(1, min(P, cores // 2)) if w.T * w.V < 1e7 else 1
-        threads = min(cores, 2 * npairs)
-        done, spent, p0c = 0, 0.0, 0
+        npairs = oracle_pairs_per_sample(w, cores)
+        done, spent = 0, 0.0
         while spent < args.cpu_seconds and done < 64 * P:
-            dt, _ = oracle_sample(w, args.seed, npairs, args.mask, threads, p0=p0c % P)
+            dt, _ = oracle_sample(w, args.seed, npairs, args.mask, cores)
             spent += dt
             done += npairs
-            p0c += npairs
-        cpu = {"value": done / spent, "unit": "pairs/s", "cores": threads, "kind": "oracle",
+        dt1, _ = oracle_sample(w, args.seed, npairs, args.mask, 1)
+        cpu = {"value": done / spent, "unit": "pairs/s", "cores": cores, "kind": "oracle",
+               "cpu_model": cpu_model(),
                "sample": f"{done} pairs of the {args.config} workload in blocks of {npairs} "
-                         f"(pair_select + fp64 loss + full dlogits), {spent:.1f} s on {threads} "
-                         f"host threads"}
+                         f"(pair_select + fp64 loss + full dlogits), {spent:.1f} s on {cores} "
+                         f"host threads",
+               "single_thread": {"value": npairs / dt1, "unit": "pairs/s", "cores": 1,
+                                 "sample": f"{npairs} pairs, {dt1:.1f} s on one thread"}}
 
     if rank == 0:
         line = {
@@ -533,6 +640,14 @@ def run_ours(args, rank, world, local_rank):
                              % (B * T * V * s_in / 1e9)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                         "frac_of_copy_ceiling": achieved / ceil["copy_gbs"],
+                         "floor_bytes_per_launch": floor_bytes if form == "scaled" else None,
+                         "floor_frac": (floor_bytes / (loss_ms.mean() / 1e3) / 1e9 / peak
+                                        if form == "scaled" else None),
+                         "floor_note": ("2R+1W: the backward of a pair re-reads its rows, which "
+                                        "do not stay in L2 between the pair's forward pass and "
+                                        "its coefficient (DESIGN.md 4)" if form == "scaled" else None),
+                         "ncu": nv_main,
                          "kernel": ("odpo_pg_loss_fwd_bwd (%s)" % args.loss if args.loss != "dpo"
                                     else "odpo_online_dpo_loss_fwd_bwd (prep + fused fwd/bwd)"
                                     if args.gradient == "scaled" else
@@ -542,8 +657,9 @@ def run_ours(args, rank, world, local_rank):
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(n_launch * K),
-            "aux_gradient_form": aux,
-            "aux_lmhead_fwd": lmh,
+            "roofline_factored" if form == "scaled" else "roofline_other_form": aux,
+            "ceilings": ceil,
+            "aux_lmhead_pythia": lmh,
             "clocks": clk.summary(),
             "tokens_vocab_per_s": world * B * T * V * K / (tot_ms / 1e3),
             "eff_gbs_step": world * alg_bytes * K / (tot_ms / 1e3) / 1e9,

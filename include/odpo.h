@@ -11,6 +11,7 @@
  * Three calls follow the paper's statement of the problem:
  *   odpo_pair_select              rewards -> (chosen, rejected) pairs
  *   odpo_seq_logprobs             logits, tokens, mask -> log pi(y|x)
+ *   odpo_seq_ppl                  the same -> per-completion perplexity (KL proxy)
  *   odpo_online_dpo_loss_fwd_bwd  policy logits, ref log-probs, beta ->
  *                                 -log sigma loss, statistics, dlogits
  *
@@ -194,6 +195,27 @@ odpo_status odpo_seq_logprobs(const void* logits, odpo_dtype dt, int64_t B, int6
                               const uint8_t* mask, float inv_temperature, float* seq_logp,
                               float* tok_logp, float* row_lse, uint32_t* status, void* workspace,
                               size_t workspace_bytes, void* stream);
+
+/*
+ * odpo_seq_ppl -- the KL proxy of PAPER.md:121 (Sec 3, "the SFT model's perplexity on the RLHF
+ * policy's summaries") and PAPER.md:333 (Sec 5.2, "the perplexity of the base model on the
+ * generated completions"), read per completion (R20): with the REFERENCE model's
+ * logits, ppl_b = exp(-S_b / n_b), S_b = log pi_ref(y_b|x) (odpo_seq_logprobs), n_b = the
+ * number of mask = 1 tokens.
+ *
+ *   logits .. workspace  as odpo_seq_logprobs (same single-read pass; seq_logp bit-identical).
+ *   ppl[B]          f32 device out; an empty completion (n_b = 0, flagged EMPTY_SEQ) gets 1.
+ *   ppl_stats[4]    f64 device out: {#completions with n_b > 0, sum_b ppl_b, sum_b S_b,
+ *                   sum_b n_b} over the non-empty completions, summed in a fixed order
+ *                   (the corpus perplexity is exp(-ppl_stats[2] / ppl_stats[3]); a SUM
+ *                   all-reduce of these four doubles gives the global values).
+ * Errors: as odpo_seq_logprobs; ppl or ppl_stats NULL -> ODPO_ERR_INVALID_ARG.
+ */
+odpo_status odpo_seq_ppl(const void* logits, odpo_dtype dt, int64_t B, int64_t T, int64_t V,
+                         int64_t stride_b, int64_t stride_t, const int32_t* tokens,
+                         const uint8_t* mask, float inv_temperature, float* seq_logp, float* ppl,
+                         double* ppl_stats, uint32_t* status, void* workspace,
+                         size_t workspace_bytes, void* stream);
 
 /*
  * odpo_online_dpo_loss_fwd_bwd -- Online DPO loss, statistics and dlogits.

@@ -21,12 +21,12 @@ from dataclasses import dataclass
 
 import torch
 
-__all__ = ["pair_select", "seq_logprobs", "online_dpo_loss_fwd_bwd", "allreduce_stats",
+__all__ = ["pair_select", "seq_logprobs", "seq_ppl", "online_dpo_loss_fwd_bwd", "allreduce_stats",
            "workspace_bytes", "LossOutput", "SelectOutput", "OdpoError", "lib_path",
            "STAT_NAMES", "SEL_NAMES", "FLAGS"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.environ.get("ODPO_LIB") or os.path.join(_HERE, "libodpo.so")  # override: tuning builds
+LIB_PATH = os.path.join(_HERE, "libodpo.so")
 
 STAT_NAMES = ["npairs", "loss", "ncorrect", "z_sum", "rchosen_sum", "rrej_sum",
               "schosen_sum", "srej_sum", "ntok_chosen", "ntok_rej"]
@@ -65,6 +65,9 @@ def _L():
         L.odpo_pair_select.argtypes = [P, P, f32, i64, i32, P, P, P, P, P, P, P]
         L.odpo_seq_logprobs.argtypes = [P, C.c_int, i64, i64, i64, i64, i64, P, P, f32, P, P, P, P,
                                         P, sz, P]
+        L.odpo_seq_ppl.argtypes = [P, C.c_int, i64, i64, i64, i64, i64, P, P, f32, P, P, P, P, P,
+                                   sz, P]
+        L.odpo_seq_ppl.restype = C.c_int
         L.odpo_online_dpo_loss_fwd_bwd.argtypes = [P, C.c_int, i64, i64, i64, i64, i64, P, P, P, P,
                                                    i64, i64, f32, f32, P, i64, i64, P, P, P, P, P,
                                                    sz, P]
@@ -139,12 +142,70 @@ _ws_cache: dict = {}
 
 
 def _workspace(device, nbytes: int):
-    key = (device.index if device.index is not None else torch.cuda.current_device())
+    """Scratch for one call, cached per (device, stream): calls on one stream are ordered,
+    so they may share a buffer; calls on different streams never do (each stream's buffer
+    comes from the caching allocator's pool of that stream, so a replaced buffer is reused
+    only after the work queued on its stream)."""
+    dev = device.index if device.index is not None else torch.cuda.current_device()
+    key = (dev, torch.cuda.current_stream(dev).cuda_stream)
     buf = _ws_cache.get(key)
     if buf is None or buf.numel() < nbytes:
         buf = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
         _ws_cache[key] = buf
     return buf
+
+
+def _tokmask(tokens, mask, B, T):
+    tokens = _dev(tokens, "tokens", torch.int32).contiguous()
+    mask = _dev(mask, "mask", torch.uint8).contiguous()
+    if tokens.numel() != B * T or mask.numel() != B * T:
+        raise OdpoError(f"tokens and mask must be [B, T] = [{B}, {T}]")
+    return tokens, mask
+
+
+def _status(status, dev):
+    if status is None:
+        return torch.zeros(1, dtype=torch.int32, device=dev)
+    _dev(status, "status", torch.int32)
+    if status.numel() < 1:
+        raise OdpoError("status must hold one int32")
+    return status
+
+
+def _stats(stats, dev, n=16):
+    if stats is None:
+        return torch.zeros(n, dtype=torch.float64, device=dev)
+    _dev(stats, "stats", torch.float64)
+    if not stats.is_contiguous() or stats.numel() < NSTATS:
+        raise OdpoError(f"stats must be a contiguous float64 buffer of >= {NSTATS} doubles")
+    return stats
+
+
+def _per_seq(x, name, B):
+    x = _dev(x, name, torch.float32).contiguous()
+    if x.numel() != B:
+        raise OdpoError(f"{name} must hold one float per sequence ({B})")
+    return x
+
+
+def _pairs(pair_rows, B):
+    if pair_rows is None:
+        if B % 2:
+            raise OdpoError("pair_rows=None needs an even number of sequences (rows 2p, 2p+1)")
+        return None, B // 2
+    pair_rows = _dev(pair_rows, "pair_rows", torch.int32).contiguous()
+    if pair_rows.dim() != 2 or pair_rows.shape[1] != 2:
+        raise OdpoError("pair_rows must be [P, 2]")
+    return pair_rows, pair_rows.shape[0]
+
+
+def _out_rows(out, like, name):
+    """A caller-supplied [B, T, V] output: same shape and dtype as the logits, contiguous V."""
+    _dev(out, name, like.dtype)
+    if tuple(out.shape) != tuple(like.shape) or out.stride(2) != 1:
+        raise OdpoError(f"{name} must be [B, T, V] = {tuple(like.shape)} with a contiguous last "
+                        f"dimension")
+    return out
 
 
 @dataclass
@@ -172,8 +233,7 @@ def pair_select(rewards: torch.Tensor, has_eos: torch.Tensor | None = None, eos_
     margin = torch.empty(P, dtype=torch.float32, device=dev)
     if sel_stats is None:
         sel_stats = torch.zeros(NSEL, dtype=torch.float64, device=dev)
-    if status is None:
-        status = torch.zeros(1, dtype=torch.int32, device=dev)
+    status = _status(status, dev)
     _check(_L().odpo_pair_select(_p(rewards), _p(has_eos), float(eos_penalty), P, K, _p(chosen),
                                  _p(rejected), _p(pair_rows), _p(margin), _p(sel_stats), _p(status),
                                  _stream()), "odpo_pair_select")
@@ -211,22 +271,29 @@ def _logits_meta(x: torch.Tensor, name="logits"):
     return _DT[x.dtype], x.shape[0], x.shape[1], x.shape[2], x.stride(0), x.stride(1)
 
 
+def _rows_like(x: torch.Tensor) -> torch.Tensor:
+    """An output [B, T, V] with x's dtype whose row stride is padded to 16 bytes (the C ABI's
+    alignment contract), so a default output is valid for every valid input."""
+    B, T, V = x.shape
+    es = x.element_size()
+    vp = -(-V * es // 16) * 16 // es
+    return torch.empty((B, T, vp), dtype=x.dtype, device=x.device)[:, :, :V]
+
+
 def seq_logprobs(logits: torch.Tensor, tokens: torch.Tensor, mask: torch.Tensor,
                  inv_temperature: float = 1.0, per_token: bool = False,
                  status: torch.Tensor | None = None):
     """log pi(y|x) per sequence.  Returns seq_logp[B] (and tok_logp, row_lse
     [B, T] when per_token=True)."""
     dt, B, T, V, sb, st = _logits_meta(logits)
-    tokens = _dev(tokens, "tokens", torch.int32).contiguous()
-    mask = _dev(mask, "mask", torch.uint8).contiguous()
+    tokens, mask = _tokmask(tokens, mask, B, T)
     dev = logits.device
     seq = torch.empty(B, dtype=torch.float32, device=dev)
     tok = lse = None
     if per_token:
         tok = torch.empty((B, T), dtype=torch.float32, device=dev)
         lse = torch.empty((B, T), dtype=torch.float32, device=dev)
-    if status is None:
-        status = torch.zeros(1, dtype=torch.int32, device=dev)
+    status = _status(status, dev)
     nb = workspace_bytes(B, T, B // 2 + 1)
     ws = _workspace(dev, nb)
     _check(_L().odpo_seq_logprobs(_p(logits), dt, B, T, V, sb, st, _p(tokens), _p(mask),
@@ -235,6 +302,25 @@ def seq_logprobs(logits: torch.Tensor, tokens: torch.Tensor, mask: torch.Tensor,
     if per_token:
         return seq, tok, lse, status
     return seq
+
+
+def seq_ppl(logits: torch.Tensor, tokens: torch.Tensor, mask: torch.Tensor,
+            inv_temperature: float = 1.0, status: torch.Tensor | None = None):
+    """KL proxy: with the reference model's logits, the per-completion
+    perplexity exp(-S_b / n_b).  Returns (ppl [B] f32, ppl_stats [4] f64 = (#non-empty,
+    sum ppl, sum S, sum n), seq_logp [B], status)."""
+    dt, B, T, V, sb, st = _logits_meta(logits)
+    tokens, mask = _tokmask(tokens, mask, B, T)
+    dev = logits.device
+    seq = torch.empty(B, dtype=torch.float32, device=dev)
+    ppl = torch.empty(B, dtype=torch.float32, device=dev)
+    ps = torch.zeros(4, dtype=torch.float64, device=dev)
+    status = _status(status, dev)
+    ws = _workspace(dev, workspace_bytes(B, T, B // 2 + 1))
+    _check(_L().odpo_seq_ppl(_p(logits), dt, B, T, V, sb, st, _p(tokens), _p(mask),
+                             float(inv_temperature), _p(seq), _p(ppl), _p(ps), _p(status),
+                             _p(ws), ws.numel(), _stream()), "odpo_seq_ppl")
+    return ppl, ps, seq, status
 
 
 def lmhead_seq_logprobs(hidden: torch.Tensor, weight: torch.Tensor, tokens: torch.Tensor,
@@ -252,14 +338,12 @@ def lmhead_seq_logprobs(hidden: torch.Tensor, weight: torch.Tensor, tokens: torc
         raise ValueError("hidden and weight must be contiguous")
     B, T, d = hidden.shape
     V = weight.shape[0]
-    tokens = _dev(tokens, "tokens", torch.int32).contiguous()
-    mask = _dev(mask, "mask", torch.uint8).contiguous()
+    tokens, mask = _tokmask(tokens, mask, B, T)
     dev = hidden.device
     seq = torch.empty(B, dtype=torch.float32, device=dev)
     tok = torch.empty((B, T), dtype=torch.float32, device=dev)
     lse = torch.empty((B, T), dtype=torch.float32, device=dev)
-    if status is None:
-        status = torch.zeros(1, dtype=torch.int32, device=dev)
+    status = _status(status, dev)
     nb = _L().odpo_lmhead_workspace_bytes(B, T, V)
     ws = _workspace(dev, nb)
     _check(_L().odpo_lmhead_seq_logprobs(_p(hidden), _p(weight), B, T, d, V, _p(tokens), _p(mask),
@@ -280,13 +364,9 @@ def lmhead_online_dpo_loss_fwd(hidden: torch.Tensor, weight: torch.Tensor,
                                                        inv_temperature)
     B, T = tok_logp.shape
     dev = hidden.device
-    ref_logp = _dev(ref_logp, "ref_logp", torch.float32).contiguous()
+    ref_logp = _per_seq(ref_logp, "ref_logp", B)
     mask = _dev(mask, "mask", torch.uint8).contiguous()
-    if pair_rows is not None:
-        pair_rows = _dev(pair_rows, "pair_rows", torch.int32).contiguous()
-        P = pair_rows.shape[0]
-    else:
-        P = B // 2
+    pair_rows, P = _pairs(pair_rows, B)
     Pg = P if p_global is None else int(p_global)
     seq = torch.empty(B, dtype=torch.float32, device=dev)
     z = torch.empty(max(P, 1), dtype=torch.float32, device=dev)
@@ -317,6 +397,8 @@ def lmhead_grad(hidden: torch.Tensor, weight: torch.Tensor, tokens: torch.Tensor
     tokens = _dev(tokens, "tokens", torch.int32).contiguous()
     row_lse = _dev(row_lse, "row_lse", torch.float32).contiguous()
     row_scale = _dev(row_scale, "row_scale", torch.float32).contiguous()
+    if tokens.numel() != R or row_lse.numel() != R or row_scale.numel() != R:
+        raise OdpoError(f"tokens, row_lse and row_scale must hold one value per row ({R})")
     dev = hidden.device
     dh = torch.empty(hidden.shape, dtype=torch.float32, device=dev)
     dw = torch.empty((V, d), dtype=torch.float32, device=dev)
@@ -360,30 +442,23 @@ def online_dpo_loss_fwd_bwd(policy_logits: torch.Tensor, ref_logp: torch.Tensor,
     stats: optional fp64 buffer of >= 10 doubles (the recommended 16-double buffer whose
     [10,13) holds pair_select's sel_stats); loss stats are written to stats[0:10]."""
     dt, B, T, V, sb, st = _logits_meta(policy_logits, "policy_logits")
-    ref_logp = _dev(ref_logp, "ref_logp", torch.float32).contiguous()
-    tokens = _dev(tokens, "tokens", torch.int32).contiguous()
-    mask = _dev(mask, "mask", torch.uint8).contiguous()
+    ref_logp = _per_seq(ref_logp, "ref_logp", B)
+    tokens, mask = _tokmask(tokens, mask, B, T)
     dev = policy_logits.device
-    if pair_rows is not None:
-        pair_rows = _dev(pair_rows, "pair_rows", torch.int32).contiguous()
-        P = pair_rows.shape[0]
-    else:
-        P = B // 2
+    pair_rows, P = _pairs(pair_rows, B)
     Pg = P if p_global is None else int(p_global)
     if inplace:
         dl = policy_logits
     elif dlogits is not None:
-        dl = _dev(dlogits, "dlogits", policy_logits.dtype)
+        dl = _out_rows(dlogits, policy_logits, "dlogits")
     else:
-        dl = torch.empty_like(policy_logits)
+        dl = _rows_like(policy_logits)
     if dl.dim() != 3 or dl.stride(2) != 1:
         raise OdpoError("dlogits must be [B, T, V] with a contiguous last dimension")
     seq = torch.empty(B, dtype=torch.float32, device=dev)
     z = torch.empty(max(P, 1), dtype=torch.float32, device=dev)
-    if stats is None:
-        stats = torch.zeros(STATS_BUF, dtype=torch.float64, device=dev)
-    if status is None:
-        status = torch.zeros(1, dtype=torch.int32, device=dev)
+    stats = _stats(stats, dev)
+    status = _status(status, dev)
     nb = workspace_bytes(B, T, max(P, 1))
     ws = _workspace(dev, nb)
     opts = _Opts(SCHEDULES[schedule], int(lag_pairs), int(ctas_per_sm), 0, int(exp2_split),
@@ -411,22 +486,17 @@ def online_dpo_loss_fwd_bwd_unscaled(policy_logits: torch.Tensor, ref_logp: torc
     G = mask (softmax - onehot) and out.row_scale [B, T] holds coef_b * mask, so the gradient
     is out.row_scale[..., None] * out.dlogits (one HBM read and one write of the logits)."""
     dt, B, T, V, sb, st = _logits_meta(policy_logits, "policy_logits")
-    ref_logp = _dev(ref_logp, "ref_logp", torch.float32).contiguous()
-    tokens = _dev(tokens, "tokens", torch.int32).contiguous()
-    mask = _dev(mask, "mask", torch.uint8).contiguous()
+    ref_logp = _per_seq(ref_logp, "ref_logp", B)
+    tokens, mask = _tokmask(tokens, mask, B, T)
     dev = policy_logits.device
-    if pair_rows is not None:
-        pair_rows = _dev(pair_rows, "pair_rows", torch.int32).contiguous()
-        P = pair_rows.shape[0]
-    else:
-        P = B // 2
+    pair_rows, P = _pairs(pair_rows, B)
     Pg = P if p_global is None else int(p_global)
     if inplace:
         g = policy_logits
     elif G is not None:
-        g = _dev(G, "G", policy_logits.dtype)
+        g = _out_rows(G, policy_logits, "G")
     else:
-        g = torch.empty_like(policy_logits)
+        g = _rows_like(policy_logits)
     if g.dim() != 3 or g.stride(2) != 1:
         raise OdpoError("G must be [B, T, V] with a contiguous last dimension")
     if row_scale is None:
@@ -436,10 +506,8 @@ def online_dpo_loss_fwd_bwd_unscaled(policy_logits: torch.Tensor, ref_logp: torc
         raise OdpoError("row_scale must be a contiguous [B, T] f32 tensor")
     seq = torch.empty(B, dtype=torch.float32, device=dev)
     z = torch.empty(max(P, 1), dtype=torch.float32, device=dev)
-    if stats is None:
-        stats = torch.zeros(STATS_BUF, dtype=torch.float64, device=dev)
-    if status is None:
-        status = torch.zeros(1, dtype=torch.int32, device=dev)
+    stats = _stats(stats, dev)
+    status = _status(status, dev)
     ws = _workspace(dev, workspace_bytes(B, T, max(P, 1)))
     opts = _Opts(SCHEDULES[schedule], 0, int(ctas_per_sm), 0, int(exp2_split), int(lookahead),
                  int(row_gap), int(engine))
@@ -465,31 +533,24 @@ def pg_loss_fwd_bwd(policy_logits: torch.Tensor, tokens: torch.Tensor, mask: tor
     """App B losses on the same path: kind in rloo / copg / prox_rloo /
     sft; rewards[B] and old_logp[B] per sequence.  out.z is empty (no DPO logit)."""
     dt, B, T, V, sb, st = _logits_meta(policy_logits, "policy_logits")
-    tokens = _dev(tokens, "tokens", torch.int32).contiguous()
-    mask = _dev(mask, "mask", torch.uint8).contiguous()
-    rewards = _dev(rewards, "rewards", torch.float32).contiguous()
+    tokens, mask = _tokmask(tokens, mask, B, T)
+    rewards = _per_seq(rewards, "rewards", B)
     if old_logp is not None:
-        old_logp = _dev(old_logp, "old_logp", torch.float32).contiguous()
+        old_logp = _per_seq(old_logp, "old_logp", B)
     dev = policy_logits.device
-    if pair_rows is not None:
-        pair_rows = _dev(pair_rows, "pair_rows", torch.int32).contiguous()
-        P = pair_rows.shape[0]
-    else:
-        P = B // 2
+    pair_rows, P = _pairs(pair_rows, B)
     Pg = P if p_global is None else int(p_global)
     if inplace:
         dl = policy_logits
     elif dlogits is not None:
-        dl = _dev(dlogits, "dlogits", policy_logits.dtype)
+        dl = _out_rows(dlogits, policy_logits, "dlogits")
     else:
-        dl = torch.empty_like(policy_logits)
+        dl = _rows_like(policy_logits)
     if dl.dim() != 3 or dl.stride(2) != 1:
         raise OdpoError("dlogits must be [B, T, V] with a contiguous last dimension")
     seq = torch.empty(B, dtype=torch.float32, device=dev)
-    if stats is None:
-        stats = torch.zeros(STATS_BUF, dtype=torch.float64, device=dev)
-    if status is None:
-        status = torch.zeros(1, dtype=torch.int32, device=dev)
+    stats = _stats(stats, dev)
+    status = _status(status, dev)
     ws = _workspace(dev, workspace_bytes(B, T, max(P, 1)))
     opts = _Opts(SCHEDULES[schedule], 0, int(ctas_per_sm), 0, -1, -1, -1, int(engine))
     _check(_L().odpo_pg_loss_fwd_bwd(
@@ -506,9 +567,9 @@ def vp_row_partials(logits_shard: torch.Tensor, v0: int, V_total: int, tokens: t
     """Vocabulary-parallel forward of one shard (columns [v0, v0 + V_shard) of V_total):
     returns the [B*T, 4] f32 row partials (m, log1p r, x_tok, owns)."""
     dt, B, T, V, sb, st = _logits_meta(logits_shard, "logits_shard")
-    tokens = _dev(tokens, "tokens", torch.int32).contiguous()
-    mask = _dev(mask, "mask", torch.uint8).contiguous()
+    tokens, mask = _tokmask(tokens, mask, B, T)
     parts = torch.empty((B * T, 4), dtype=torch.float32, device=logits_shard.device)
+    status = _status(status, logits_shard.device)
     ws = _workspace(logits_shard.device, workspace_bytes(B, T, B // 2 + 1))
     _check(_L().odpo_vp_row_partials(_p(logits_shard), dt, B, T, V, sb, st, int(v0), int(V_total),
                                      _p(tokens), _p(mask), float(inv_temperature), _p(parts),
@@ -529,23 +590,18 @@ def vp_loss_fwd_bwd(parts_all: torch.Tensor, logits_shard: torch.Tensor, v0: int
     dt, B, T, V, sb, st = _logits_meta(logits_shard, "logits_shard")
     parts_all = _dev(parts_all, "parts_all", torch.float32).contiguous()
     W = parts_all.shape[0]
-    ref_logp = _dev(ref_logp, "ref_logp", torch.float32).contiguous()
-    tokens = _dev(tokens, "tokens", torch.int32).contiguous()
-    mask = _dev(mask, "mask", torch.uint8).contiguous()
+    if parts_all.dim() != 3 or tuple(parts_all.shape[1:]) != (B * T, 4):
+        raise OdpoError(f"parts_all must be [W, B*T, 4] = [W, {B * T}, 4]")
+    ref_logp = _per_seq(ref_logp, "ref_logp", B)
+    tokens, mask = _tokmask(tokens, mask, B, T)
     dev = logits_shard.device
-    if pair_rows is not None:
-        pair_rows = _dev(pair_rows, "pair_rows", torch.int32).contiguous()
-        P = pair_rows.shape[0]
-    else:
-        P = B // 2
+    pair_rows, P = _pairs(pair_rows, B)
     Pg = P if p_global is None else int(p_global)
-    dl = torch.empty_like(logits_shard) if dlogits is None else _dev(dlogits, "dlogits", logits_shard.dtype)
+    dl = _rows_like(logits_shard) if dlogits is None else _out_rows(dlogits, logits_shard, "dlogits")
     seq = torch.empty(B, dtype=torch.float32, device=dev)
     z = torch.empty(max(P, 1), dtype=torch.float32, device=dev)
-    if stats is None:
-        stats = torch.zeros(STATS_BUF, dtype=torch.float64, device=dev)
-    if status is None:
-        status = torch.zeros(1, dtype=torch.int32, device=dev)
+    stats = _stats(stats, dev)
+    status = _status(status, dev)
     ws = _workspace(dev, workspace_bytes(B, T, max(P, 1)))
     _check(_L().odpo_vp_loss_fwd_bwd(
         _p(parts_all), W, _p(logits_shard), dt, B, T, V, sb, st, int(v0), int(V_total),

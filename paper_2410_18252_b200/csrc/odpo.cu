@@ -503,6 +503,42 @@ __global__ void k_vp_combine(LossArgs a, const float4* __restrict__ parts, int W
 }
 
 // ------------------------------------------------------------------ App B known coefficients
+// KL proxy (R20): ppl_b = exp(-S_b / n_b) from the row log-probs
+// the SEQ engine left in the workspace.  One CTA of 32 warps; warp w sums sequences
+// b = w, w + 32, ... (seq_sum_warp's order, so S_b is the engine's own double sum) and keeps
+// its partial statistics in b order; the 32 partials are merged in warp order.
+constexpr int kPplWarps = 32;
+__global__ void __launch_bounds__(32 * kPplWarps) k_seq_ppl(LossArgs a, float* ppl, double* ppl_stats) {
+  __shared__ double part[kPplWarps][4];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int64_t b = warp; b < a.B; b += kPplWarps) {
+    double S;
+    int n;
+    seq_sum_warp(a.w.row_logp + b * a.T, a.mask + b * a.T, a.T, S, n);
+    if (lane == 0) {
+      if (n > 0) {
+        const double p = exp(-S / (double)n);
+        ppl[b] = (float)p;
+        acc[0] += 1.0;
+        acc[1] += p;
+        acc[2] += S;
+        acc[3] += (double)n;
+      } else {
+        ppl[b] = 1.f;
+      }
+    }
+  }
+  if (lane == 0)
+    for (int k = 0; k < 4; ++k) part[warp][k] = acc[k];
+  __syncthreads();
+  if (threadIdx.x < 4) {
+    double s = 0.0;
+    for (int w = 0; w < kPplWarps; ++w) s += part[w][threadIdx.x];
+    ppl_stats[threadIdx.x] = s;
+  }
+}
+
 // RLOO / CoPG: coef_b = A_b invT / (2 P_global); Best-of-2 SFT: invT / P_global on the chosen
 // completion, 0 on the other.  One thread per pair.
 __global__ void k_pg_coef(LossArgs a) {
@@ -547,7 +583,8 @@ __global__ void __launch_bounds__(32 * kWarpRowsPerCta) k_row_bwd_warp(LossArgs 
   const int64_t tl = (int64_t)a.tokens[g] - a.tok_off;
   const int tok = (tl >= 0 && tl < V) ? (int)tl : -1;
   const float k2 = a.invT * kLog2e;
-  const float c = fmaf(a.w.row_l1p[g], kLog2e, a.w.row_m[g] * k2) - log2f(fabsf(coef));
+  const float rm = a.w.row_m[g];
+  const float c = bwd_const<DT>(rm, a.w.row_l1p[g], k2, coef);
   const float gtok = coef * expm1f(a.w.row_logp[g]);
   const bool neg = coef < 0.f;
   const uint4* vrow = reinterpret_cast<const uint4*>(row_ptr(a, b, t));
@@ -562,13 +599,13 @@ __global__ void __launch_bounds__(32 * kWarpRowsPerCta) k_row_bwd_warp(LossArgs 
     for (int u = 0; u < U; ++u) {
       const int i = base + 32 * u;
       if (i < nvec)
-        st16_stream(vout + i, neg ? bwd_vec<DT, 0, true>(v[u], k2, c) : bwd_vec<DT, 0, false>(v[u], k2, c));
+        st16_stream(vout + i, neg ? bwd_vec<DT, 0, true>(v[u], k2, c, rm) : bwd_vec<DT, 0, false>(v[u], k2, c, rm));
     }
   }
   if (lane < tail) {
     const int64_t vv = (int64_t)nvec * N + lane;
     const float x = Traits<DT>::load1(vrow, vv);
-    Traits<DT>::store1(vout, vv, vv == tok ? gtok : copysignf(ex2(fmaf(x, k2, -c)), coef));
+    Traits<DT>::store1(vout, vv, vv == tok ? gtok : copysignf(ex2(bwd_arg<DT>(x, k2, c, rm)), coef));
   }
   // onehot entry: the lane that stored tok's vector overwrites it (program order)
   if (tok >= 0 && tok < nvec * N && (tok / N) % 32 == lane) Traits<DT>::store1(vout, tok, gtok);
@@ -1183,17 +1220,19 @@ __global__ void __launch_bounds__(GE::THREADS, GE::CPS) k_engine(LossArgs a) {
           const float logp = __ldcg(a.w.row_logp + S.g);
           const float coef = __ldcg(a.w.seq_coef + S.s);
           // coef folded into the exponent: coef * 2^e = sign * 2^(e + log2|coef|)
-          const float c = fmaf(l1p, kLog2e, m * k2) - log2f(fabsf(coef));
+          const float c = bwd_const<DT>(m, l1p, k2, coef);
           const float gtok = coef * expm1f(logp);
           S.c = c;
           S.coef = coef;
           S.gtok = gtok;
+          S.xm = m;
           const uint32_t off_c = (uint32_t)offsetof(RowSlot, c);
           for (int r = 1; r < CS; ++r) {
             const uint32_t dst = mapa(slots_s + sl * (uint32_t)sizeof(RowSlot) + off_c, r);
             st_cl_u32(dst, __float_as_uint(c));
             st_cl_u32(dst + 4, __float_as_uint(coef));
             st_cl_u32(dst + 8, __float_as_uint(gtok));
+            st_cl_u32(dst + 16, __float_as_uint(m));
             mbar_arrive_cl(mapa(mready_s + 8 * sl, r));
           }
           mbar_arrive(mready_s + 8 * sl);
@@ -1285,7 +1324,8 @@ __global__ void __launch_bounds__(GE::THREADS, GE::CPS) k_engine(LossArgs a) {
               RowSlot& W = slots[sl];
               // known coefficient (App B losses): coef folded into the exponent as in FUSED
               const float cf = a.coef_known ? __ldcg(a.w.seq_coef + S.s) : 1.f;
-              W.c = cf != 0.f ? fmaf(l1p, kLog2e, v.m * k2) - log2f(fabsf(cf)) : INFINITY;
+              W.c = cf != 0.f ? bwd_const<DT>(v.m, l1p, k2, cf) : INFINITY;
+              W.xm = v.m;
               W.coef = cf;
               W.gtok = cf * expm1f(logp);
               mbar_arrive(mready_s + 8 * sl);
@@ -1318,7 +1358,7 @@ __global__ void __launch_bounds__(GE::THREADS, GE::CPS) k_engine(LossArgs a) {
     int st = 0;
     uint32_t sph = 0;
     MR s{-INFINITY, 0.f};
-    float b_c = 0.f, b_coef = 0.f, b_gtok = 0.f;
+    float b_c = 0.f, b_coef = 0.f, b_gtok = 0.f, b_m = 0.f;
     int r_kind = K_NONE, r_tok = 0, r_nst = 1, r_tch = -1, r_tvl = -1;
     int r_lo = v_lo, r_hi = v_hi;
     bool r_tail = tail_owner;
@@ -1417,6 +1457,7 @@ __global__ void __launch_bounds__(GE::THREADS, GE::CPS) k_engine(LossArgs a) {
           b_c = slots[fs].c;
           b_coef = slots[fs].coef;
           b_gtok = slots[fs].gtok;
+          b_m = slots[fs].xm;
           if (MODE == M_UNSC) {
             __syncwarp();
             if (lane == 0) mbar_arrive(sempty_s + 8 * fs);
@@ -1427,19 +1468,19 @@ __global__ void __launch_bounds__(GE::THREADS, GE::CPS) k_engine(LossArgs a) {
           if (b_coef < 0.f) {
 #pragma unroll
             for (int u = 0; u < kUB; ++u)
-              st16_stream(vout + tid + u * kNCT, bwd_vec<DT, NPB, true>(sv[tid + u * kNCT], k2, b_c));
+              st16_stream(vout + tid + u * kNCT, bwd_vec<DT, NPB, true>(sv[tid + u * kNCT], k2, b_c, b_m));
           } else {
 #pragma unroll
             for (int u = 0; u < kUB; ++u)
-              st16_stream(vout + tid + u * kNCT, bwd_vec<DT, NPB, false>(sv[tid + u * kNCT], k2, b_c));
+              st16_stream(vout + tid + u * kNCT, bwd_vec<DT, NPB, false>(sv[tid + u * kNCT], k2, b_c, b_m));
           }
         } else {
 #pragma unroll
           for (int u = 0; u < kUB; ++u) {
             const int i = tid + u * kNCT;
             if (i < cnv)
-              st16_stream(vout + i, b_coef < 0.f ? bwd_vec<DT, NPB, true>(sv[i], k2, b_c)
-                                                 : bwd_vec<DT, NPB, false>(sv[i], k2, b_c));
+              st16_stream(vout + i, b_coef < 0.f ? bwd_vec<DT, NPB, true>(sv[i], k2, b_c, b_m)
+                                                 : bwd_vec<DT, NPB, false>(sv[i], k2, b_c, b_m));
           }
         }
         __syncwarp();
@@ -1450,7 +1491,7 @@ __global__ void __launch_bounds__(GE::THREADS, GE::CPS) k_engine(LossArgs a) {
           if (r_tail && tid < tail) {
             const int64_t vv = (int64_t)nvec * N + tid;
             const float x = Traits<DT>::load1(r_row, vv);
-            Traits<DT>::store1(r_drow, vv, vv == r_tok ? b_gtok : copysignf(ex2(fmaf(x, k2, -b_c)), b_coef));
+            Traits<DT>::store1(r_drow, vv, vv == r_tok ? b_gtok : copysignf(ex2(bwd_arg<DT>(x, k2, b_c, b_m)), b_coef));
           }
           __syncwarp();
           if (lane == 0) arrive_leader(L_sempty + 8 * sl, 1u);
@@ -1502,7 +1543,7 @@ template <int DT, int MODE, int PV, class GE>
 static void launch_k(int grid, cudaStream_t s, const LossArgs& a) {
   constexpr int CS = mode_cs<MODE>();
   auto kern = k_engine<DT, MODE, PV, CS, GE>;
-  if (CS == 1) {
+  if (CS == 1 && a.wave_ng == 0) {
     kern<<<grid, GE::THREADS, GE::SMEM, s>>>(a);
     return;
   }
@@ -1512,10 +1553,18 @@ static void launch_k(int grid, cudaStream_t s, const LossArgs& a) {
   cfg.dynamicSmemBytes = GE::SMEM;
   cfg.stream = s;
   cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = (unsigned)CS;
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = 1;
+  if (a.wave_ng > 0) {
+    // the wave schedule's CTAs wait on their peers (a backward row on its group's forward
+    // rows): launched cooperatively, so the runtime guarantees every CTA is co-resident (or
+    // fails the launch -> ODPO_ERR_CUDA) whatever else shares the GPU
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+  } else {
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)CS;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+  }
   cfg.attrs = at;
   cfg.numAttrs = 1;
   cudaLaunchKernelEx(&cfg, kern, a);
@@ -1779,6 +1828,25 @@ odpo_status odpo_seq_logprobs(const void* logits, odpo_dtype dt, int64_t B, int6
   return launch_engine(dt == ODPO_F32 ? 0 : 1, M_SEQ, kPolyDefault, a, 0, s, -1);
 }
 
+odpo_status odpo_seq_ppl(const void* logits, odpo_dtype dt, int64_t B, int64_t T, int64_t V,
+                         int64_t stride_b, int64_t stride_t, const int32_t* tokens,
+                         const uint8_t* mask, float inv_temperature, float* seq_logp, float* ppl,
+                         double* ppl_stats, uint32_t* status, void* workspace,
+                         size_t workspace_bytes, void* stream) {
+  if (!ppl || !ppl_stats) return ODPO_ERR_INVALID_ARG;
+  odpo_status e = odpo_seq_logprobs(logits, dt, B, T, V, stride_b, stride_t, tokens, mask,
+                                    inv_temperature, seq_logp, nullptr, nullptr, status,
+                                    workspace, workspace_bytes, stream);
+  if (e != ODPO_OK) return e;
+  Workspace w;
+  ws_layout(B, T, B / 2 + 1, (char*)workspace, &w);
+  LossArgs a;
+  base_args(a, logits, B, T, V, stride_b, stride_t, tokens, mask, inv_temperature, status, w,
+            dt == ODPO_F32 ? 4 : 2);
+  k_seq_ppl<<<1, 32 * kPplWarps, 0, (cudaStream_t)stream>>>(a, ppl, ppl_stats);
+  return launched();
+}
+
 // Wave schedule geometry: groups of 2T CTAs (one row per CTA per pair), as many groups as the
 // resident grid holds and as keep every group's in-flight pair within half of L2; 0 when the
 // wave does not apply (2T above the grid, a pair larger than the L2 budget, clusters).
@@ -1859,26 +1927,13 @@ odpo_status odpo_online_dpo_loss_fwd_bwd_ex(const void* policy_logits, odpo_dtyp
   int dev = 0;
   cudaGetDevice(&dev);
   const DevInfo& di = dev_info(dev);
-  // AUTO = RESIDENT where the rows fit on chip (1R+1W), else FUSED.  The wave keeps every pair
-  // in L2 too but its per-pair waits cost more than the re-read saves on B200 (DESIGN.md
-  // section 4)
+  // AUTO = FUSED: the one schedule with no co-residency assumption (a CTA never waits on a
+  // row another CTA has not been guaranteed to run), so a call is safe next to any other work
+  // on the GPU.  WAVE (peer waits; launched cooperatively) and RESIDENT are explicit options
+  // (DESIGN.md section 4 records their measurements).
   const ResGeo rg = res_geo(V, T, (int)es, di.sms, opts ? opts->lookahead : -1);
   const bool res_ok = rg.nsl > 0 && (!opts || (opts->ctas_per_sm <= 0 && opts->engine < 0));
-  if (sched == ODPO_SCHED_AUTO) {
-    if (res_ok && kResAuto) {
-      sched = ODPO_SCHED_RESIDENT;
-    } else {
-      // a batch whose rows all fit the resident grid at once runs the wave schedule (pairs
-      // pinned to CTA groups): the measured tiny config is 15% faster
-      // (profiles/r01/tiny.log); larger batches run FUSED.  Same bits either way.
-      const int dti0 = dt == ODPO_F32 ? 0 : 1;
-      const int64_t grid = (int64_t)di.sms * (di.occ[0][dti0][M_FUSED] > 0 ? di.occ[0][dti0][M_FUSED] : 1);
-      const bool one_wave = kFS == 1 && pv == 0 && !(opts && (opts->engine > 0 || opts->ctas_per_sm > 0)) &&
-                            P * 2 * T <= grid;
-      const int ng = one_wave ? wave_groups(T, P, V * es, 0, -1, dti0, false, wave_gap) : 0;
-      sched = ng > 0 ? ODPO_SCHED_WAVE : ODPO_SCHED_FUSED;
-    }
-  }
+  if (sched == ODPO_SCHED_AUTO) sched = ODPO_SCHED_FUSED;
   if (sched == ODPO_SCHED_RESIDENT && !res_ok) return ODPO_ERR_UNSUPPORTED;
   if (sched == ODPO_SCHED_WAVE) {
     wave_ng = wave_groups(T, P, V * es, opts ? opts->ctas_per_sm : 0, opts ? opts->engine : -1,

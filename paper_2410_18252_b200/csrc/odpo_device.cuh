@@ -67,6 +67,11 @@ __device__ __forceinline__ f32x2 fadd2(f32x2 a, f32x2 b) {
   asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
   return r;
 }
+__device__ __forceinline__ f32x2 fmul2(f32x2 a, f32x2 b) {
+  f32x2 r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
 __device__ __forceinline__ float fmax_nan(float a, float b) {
   float d;
   asm("max.NaN.f32 %0, %1, %2;" : "=f"(d) : "f"(a), "f"(b));
@@ -253,6 +258,29 @@ __device__ __forceinline__ MR mr_merge(MR a, MR b, float k2) {
   return big;
 }
 
+// exp2 argument of the forward, invT (x - m) log2e.  fp32 inputs form it as (x - m) k2: the
+// single-FFMA form x k2 - fl(m k2) carries the rounding of m k2 (ulp(m k2)/2, i.e. 4e-5
+// relative on every term at |m| ~ 1000), above the fp32 contract of 1e-5.
+// bf16 inputs keep the FFMA form (its error is far inside the 2e-3 bf16 contract).
+template <int DT>
+__device__ __forceinline__ float fwd_arg(float x, float k2, float m) {
+  if constexpr (DT == 0) return (x - m) * k2;
+  else return fmaf(x, k2, -(m * k2));
+}
+
+// Backward exponent: |g_v| = 2^(e_v) with e_v = (x_v - m) k2 - c (fp32 inputs) or
+// e_v = x_v k2 - c (bf16 inputs, c then also holds m k2), c = log1p(r) log2e - log2|coef|.
+template <int DT>
+__device__ __forceinline__ float bwd_const(float m, float l1p, float k2, float coef) {
+  if constexpr (DT == 0) return fmaf(l1p, kLog2e, -log2f(fabsf(coef)));
+  else return fmaf(l1p, kLog2e, m * k2) - log2f(fabsf(coef));
+}
+template <int DT>
+__device__ __forceinline__ float bwd_arg(float x, float k2, float c, float m) {
+  if constexpr (DT == 0) return fmaf(x - m, k2, -c);
+  else return fmaf(x, k2, -c);
+}
+
 // Per-thread online pass over this thread's vectors of one row.
 // Vectors i = tid, tid + NT, ... (coalesced across the CTA), kU of them per batch.
 template <int DT, int LK>
@@ -269,13 +297,13 @@ __device__ __forceinline__ MR row_fwd_thread(const uint4* __restrict__ vrow, int
       v[u] = (i < nvec) ? ld16<LK>(vrow + i, pol) : make_uint4(NI, NI, NI, NI);
     }
     const float mc = batch_max<DT>(v);
+    if (mc == -INFINITY && m == -INFINITY) continue;  // all -inf so far: no contribution
     if (!(mc <= m)) {
       // new running max (or NaN): demote the old max into r, then add this batch
       // excluding exactly ONE element equal to the new max (it is the "1" of 1 + r).
       const float sc = (m == -INFINITY) ? 0.f : ex2((m - mc) * k2);
       r = (1.f + r) * sc;
       m = mc;
-      const float mk = m * k2;
       float s = 0.f;
       int neq = 0;
 #pragma unroll
@@ -285,12 +313,11 @@ __device__ __forceinline__ MR row_fwd_thread(const uint4* __restrict__ vrow, int
 #pragma unroll
         for (int j = 0; j < N; ++j) {
           if (f[j] == m) ++neq;
-          else s += ex2(fmaf(f[j], k2, -mk));
+          else s += ex2(fwd_arg<DT>(f[j], k2, m));
         }
       }
       r += s + (float)(neq - 1);
     } else {
-      const float mk = m * k2;
       float s0 = 0.f, s1 = 0.f;
 #pragma unroll
       for (int u = 0; u < kU; ++u) {
@@ -298,8 +325,8 @@ __device__ __forceinline__ MR row_fwd_thread(const uint4* __restrict__ vrow, int
         Traits<DT>::unpack(v[u], f);
 #pragma unroll
         for (int j = 0; j < N; j += 2) {
-          s0 += ex2(fmaf(f[j], k2, -mk));
-          s1 += ex2(fmaf(f[j + 1], k2, -mk));
+          s0 += ex2(fwd_arg<DT>(f[j], k2, m));
+          s1 += ex2(fwd_arg<DT>(f[j + 1], k2, m));
         }
       }
       r += s0 + s1;
@@ -310,12 +337,13 @@ __device__ __forceinline__ MR row_fwd_thread(const uint4* __restrict__ vrow, int
 
 // scalar tail element (V not a multiple of the vector width): same update rules
 __device__ __forceinline__ MR mr_push1(MR s, float y, float k2) {
+  if (y == -INFINITY) return s;  // a zero-probability entry (R14)
   if (!(y <= s.m)) {
     const float sc = (s.m == -INFINITY) ? 0.f : ex2((s.m - y) * k2);
     s.r = (1.f + s.r) * sc;
     s.m = y;
   } else {
-    s.r += ex2(fmaf(y, k2, -(s.m * k2)));
+    s.r += ex2((y - s.m) * k2);
   }
   return s;
 }
@@ -385,19 +413,20 @@ __device__ __forceinline__ RowOut row_forward(const void* row, int V, int tok, f
   return o;
 }
 
-// One 16-byte vector of the backward: |g_v| = 2^(x_v invT log2e - c') with
-// c' = m invT log2e + log1p(r) log2e - log2|coef|, so coef rides in the exponent and its sign is
-// applied to the packed result.  NPB of each 8 use the FMA-pipe exp2.
+// One 16-byte vector of the backward: |g_v| = 2^(bwd_arg) (see bwd_const), so coef rides in
+// the exponent and its sign is applied to the packed result.  NPB of
+// each 8 use the FMA-pipe exp2.
 template <int DT, int NPB, bool NEG>
-__device__ __forceinline__ uint4 bwd_vec(const uint4& v, float k2, float c) {
+__device__ __forceinline__ uint4 bwd_vec(const uint4& v, float k2, float c, float m) {
   constexpr int N = Traits<DT>::N;
   float f[N];
   Traits<DT>::unpack(v, f);
-  const f32x2 K2 = pk2(k2, k2), NC = pk2(-c, -c);
+  const f32x2 K2 = pk2(k2, k2), NC = pk2(-c, -c), NM = pk2(-m, -m);
 #pragma unroll
   for (int j = 0; j < N; j += 2) {
-    float e0, e1;   // two exp2 arguments per FFMA2
-    upk2(ffma2(pk2(f[j], f[j + 1]), K2, NC), e0, e1);
+    float e0, e1;   // two exp2 arguments per FFMA2 (fp32: x - m first, see bwd_const)
+    if constexpr (DT == 0) upk2(ffma2(fadd2(pk2(f[j], f[j + 1]), NM), K2, NC), e0, e1);
+    else upk2(ffma2(pk2(f[j], f[j + 1]), K2, NC), e0, e1);
     f[j] = j < NPB ? ex2_poly3(e0) : ex2(e0);
     f[j + 1] = j + 1 < NPB ? ex2_poly3(e1) : ex2(e1);
   }
@@ -417,7 +446,7 @@ __device__ __forceinline__ void row_backward(const void* row, void* drow, int V,
                                              float coef, uint64_t pol) {
   constexpr int N = Traits<DT>::N;
   const float k2 = invT * kLog2e;
-  const float c = fmaf(l1p, kLog2e, m * k2) - log2f(fabsf(coef));
+  const float c = bwd_const<DT>(m, l1p, k2, coef);
   const bool neg = coef < 0.f;
   const int nvec = V / N;
   const uint4* vrow = reinterpret_cast<const uint4*>(row);
@@ -433,7 +462,7 @@ __device__ __forceinline__ void row_backward(const void* row, void* drow, int V,
     for (int u = 0; u < kU; ++u) {
       const int i = base + u * kRowThreads;
       if (i < nvec)
-        st16_stream(vout + i, neg ? bwd_vec<DT, NPB, true>(v[u], k2, c) : bwd_vec<DT, NPB, false>(v[u], k2, c));
+        st16_stream(vout + i, neg ? bwd_vec<DT, NPB, true>(v[u], k2, c, m) : bwd_vec<DT, NPB, false>(v[u], k2, c, m));
     }
   }
   const float gtok = coef * expm1f(logp);
@@ -441,7 +470,7 @@ __device__ __forceinline__ void row_backward(const void* row, void* drow, int V,
   if ((int)threadIdx.x < tail) {
     const int64_t v = (int64_t)nvec * N + threadIdx.x;
     const float x = Traits<DT>::load1(row, v);
-    Traits<DT>::store1(drow, v, (v == tok) ? gtok : copysignf(ex2(fmaf(x, k2, -c)), coef));
+    Traits<DT>::store1(drow, v, (v == tok) ? gtok : copysignf(ex2(bwd_arg<DT>(x, k2, c, m)), coef));
   }
   // onehot entry: written by the thread that stored tok's vector (program order)
   if (tok >= 0 && tok < nvec * N && (tok / N) % kRowThreads == (int)threadIdx.x)

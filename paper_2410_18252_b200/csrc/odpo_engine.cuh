@@ -179,6 +179,7 @@ struct RowSlot {
   const char* row;
   char* drow;
   float c, coef, gtok, xtok;
+  float xm;              // backward rows: the row max m (fp32 inputs form (x - m) k2, bwd_const)
   float pm[32], pr[32];  // per-warp (m, r) partials: [cluster rank * kNCW + warp]
 };
 // the header (kind .. drow) is what the cluster leader broadcasts to its peers
@@ -191,7 +192,9 @@ static_assert(offsetof(RowSlot, c) == kSlotHeaderBytes, "slot header layout");
 // max element's own term (value exactly as added: p(0) = 1 for the polynomial and
 // ex2(delta) for MUFU agree to ~1e-13), keeping r free of the "1" (error ~1e-6 relative,
 // far inside the 2e-3 bf16 contract).  NPF of every 8 elements use the FMA-pipe exp2.
-template <int DT, int NB, int NPF>
+// XM: form the exp2 arguments as (x - m) k2 (fwd_arg; default for fp32 logits).  The LM-head
+// epilogue (fp32 accumulators of O(1) magnitude) keeps the single-FFMA form.
+template <int DT, int NB, int NPF, bool XM = (DT == 0)>
 __device__ __forceinline__ void mr_batch(const uint4 (&v)[NB], float k2, float& m, float& r) {
   constexpr int N = Traits<DT>::N;
   float mc;
@@ -206,6 +209,9 @@ __device__ __forceinline__ void mr_batch(const uint4 (&v)[NB], float k2, float& 
     for (int u = 1; u < NB; ++u) mc = fmax_nan(mc, Traits<0>::vmax(v[u]));
   }
   const bool rec = !(mc <= m);
+  // nothing finite yet and an all -inf batch (legal zero-probability entries, R14): no
+  // contribution (the exponent x k2 - m k2 would be -inf + inf = NaN)
+  if (!rec && m == -INFINITY) return;
   if (rec) {
     const float sc = (m == -INFINITY) ? 0.f : ex2((m - mc) * k2);
     r = (1.f + r) * sc;
@@ -222,14 +228,15 @@ __device__ __forceinline__ void mr_batch(const uint4 (&v)[NB], float k2, float& 
 #pragma unroll
       for (int j = 0; j < N; ++j) {
         if (f[j] == m) ++neq;
-        else s += ex2(fmaf(f[j], k2, -mk));
+        else s += ex2(XM ? (f[j] - m) * k2 : fmaf(f[j], k2, -mk));
       }
     }
     r += s + (float)(neq - 1);
     return;
   }
-  // fast path: exp2 arguments two at a time (FFMA2) and two running sums (FADD2)
-  const f32x2 K2 = pk2(k2, k2), NMK = pk2(-mk, -mk);
+  // fast path: exp2 arguments two at a time (bf16: x k2 - m k2 in one FFMA2; fp32: (x - m) k2,
+  // FADD2 + FMUL2, see fwd_arg) and two running sums (FADD2)
+  const f32x2 K2 = pk2(k2, k2), NMK = pk2(-mk, -mk), NM = pk2(-m, -m);
   f32x2 acc = pk2(0.f, 0.f);
 #pragma unroll
   for (int u = 0; u < NB; ++u) {
@@ -238,7 +245,8 @@ __device__ __forceinline__ void mr_batch(const uint4 (&v)[NB], float k2, float& 
 #pragma unroll
     for (int j = 0; j < N; j += 2) {
       float e0, e1;
-      upk2(ffma2(pk2(f[j], f[j + 1]), K2, NMK), e0, e1);
+      if constexpr (XM) upk2(fmul2(fadd2(pk2(f[j], f[j + 1]), NM), K2), e0, e1);
+      else upk2(ffma2(pk2(f[j], f[j + 1]), K2, NMK), e0, e1);
       acc = fadd2(acc, pk2((j < NPF) ? ex2_poly4(e0) : ex2(e0), (j + 1 < NPF) ? ex2_poly4(e1) : ex2(e1)));
     }
   }

@@ -248,7 +248,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         uint4 v[8];
 #pragma unroll
         for (int j = 0; j < 8; ++j) v[j] = make_uint4(r[4 * j], r[4 * j + 1], r[4 * j + 2], r[4 * j + 3]);
-        mr_batch<0, 8, 0>(v, k2, s.m, s.r);
+        mr_batch<0, 8, 0, false>(v, k2, s.m, s.r);
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
@@ -448,6 +448,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             float g1 = g_rs * ex2(fmaf(__uint_as_float(r[j + 1]), k2, -g_c));
             if (tok == cb + j) g0 = g_rs * expm1f(fmaf(__uint_as_float(r[j]), a.invT, -a.row_lse[row]));
             if (tok == cb + j + 1) g1 = g_rs * expm1f(fmaf(__uint_as_float(r[j + 1]), a.invT, -a.row_lse[row]));
+            if (g_rs == 0.f) g0 = g1 = 0.f;  // 0 * inf: a masked row's lse is not its own
             w[j / 2] = pack_bf16x2(g0, g1);
           }
           if (cb + 32 <= a.V) {
@@ -490,7 +491,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         uint4 v[8];
 #pragma unroll
         for (int j = 0; j < 8; ++j) v[j] = make_uint4(r[4 * j], r[4 * j + 1], r[4 * j + 2], r[4 * j + 3]);
-        mr_batch<0, 8, 0>(v, k2, s.m, s.r);
+        mr_batch<0, 8, 0, false>(v, k2, s.m, s.r);
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
@@ -592,7 +593,16 @@ static int sm_count() {
   return n;
 }
 
-constexpr int kRasterG = 64;  // row blocks per raster group (tuned: 8/16/32/64 -> 1636/1723/1751/1802 TF/s)
+// Build-time tuning knobs (no environment lookups in the library): ODPO_LMH_1CTA=1 builds the
+// single-CTA forward as the default (comparison), ODPO_LMH_G the raster group size.
+#ifndef ODPO_LMH_1CTA
+#define ODPO_LMH_1CTA 0
+#endif
+constexpr bool kLmhPair = ODPO_LMH_1CTA == 0;
+#ifndef ODPO_LMH_G
+#define ODPO_LMH_G 64
+#endif
+constexpr int kRasterG = ODPO_LMH_G;  // row blocks per raster group (tuned: 8/16/32/64 -> 1636/1723/1751/1802 TF/s)
 
 // ---------------------------------------------------------------- cuBLAS (plain GEMMs), loaded at
 // run time so that libodpo.so has no load-time dependency on it (the process -- e.g. torch --
@@ -606,7 +616,8 @@ struct Blas {
   SetStream set_stream = nullptr;
   GemmEx gemm = nullptr;
   void* handle[128] = {};
-  std::mutex mu;
+  std::mutex mu;       // guards load / handle creation
+  std::mutex call_mu;  // held by a call across cublasSetStream and its GEMMs
   bool load() {
     if (gemm) return true;
     void* h = dlopen("libcublas.so.12", RTLD_NOW | RTLD_GLOBAL);
@@ -657,8 +668,7 @@ odpo_status odpo_lmhead_seq_logprobs(const void* hidden, const void* weight, int
   const int64_t R = B * T;
   if (R > (int64_t)INT32_MAX || V > (int64_t)INT32_MAX || d > (1 << 20)) return ODPO_ERR_UNSUPPORTED;
   if (!workspace || workspace_bytes < odpo_lmhead_workspace_bytes(B, T, V)) return ODPO_ERR_WORKSPACE;
-  const char* one = getenv("ODPO_LMH_1CTA");  // tuning / comparison: the single-CTA kernel
-  const bool pair = !(one && atoi(one) != 0);
+  const bool pair = kLmhPair;
   CUtensorMap mA, mB;
   if (!make_map(&mA, hidden, R, d, d, BM) || !make_map(&mB, weight, V, d, d, pair ? BN / 2 : BN))
     return ODPO_ERR_CUDA;
@@ -679,7 +689,6 @@ odpo_status odpo_lmhead_seq_logprobs(const void* hidden, const void* weight, int
   a.NT = (V + BN - 1) / BN;
   a.Ttot = a.nrb * a.NT;
   a.G = kRasterG;
-  if (const char* g = getenv("ODPO_LMH_G")) a.G = atoi(g) > 0 ? atoi(g) : kRasterG;  // tuning
   a.invT = inv_temperature;
   a.tokens = tokens; a.mask = mask;
   a.parts = reinterpret_cast<float2*>(workspace);
@@ -689,7 +698,6 @@ odpo_status odpo_lmhead_seq_logprobs(const void* hidden, const void* weight, int
   if (pair) {
     a.nrb2 = (R + 255) / 256;
     a.G = kRasterG / 2;
-    if (const char* g = getenv("ODPO_LMH_G")) a.G = atoi(g) > 0 ? atoi(g) : a.G;  // tuning
     const int64_t t2 = a.nrb2 * a.NT;
     int clusters = sms / 2;
     if (clusters > t2) clusters = (int)t2;
@@ -750,6 +758,9 @@ odpo_status odpo_lmhead_grad(const void* hidden, const void* weight, int64_t R, 
     cudaFuncSetAttribute(k_lmhead_fwd2<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2);
   });
   cudaStream_t s = (cudaStream_t)stream;
+  // one handle per device: hold its lock from set_stream to the last GEMM enqueued, so calls
+  // from other host threads / streams cannot retarget it in between
+  std::lock_guard<std::mutex> blas_lock(g_blas.call_mu);
   if (g_blas.set_stream(blas, s) != 0) return ODPO_ERR_CUDA;
   CUtensorMap mB;
   if (!make_map(&mB, weight, V, d, d, BN / 2)) return ODPO_ERR_CUDA;

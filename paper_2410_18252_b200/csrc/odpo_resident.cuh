@@ -87,11 +87,6 @@ static_assert(kResFW == 4 || kResFW == 8, "4 or 8 forward warps");
 static_assert(kResFGr == 1 || kResFW == 4, "forward groups of 4 warps");
 static_assert(kResUB * 4 * kResFG == kResCols, "a chunk fills 32 columns of every lane");
 
-// AUTO picks RESIDENT only when this is set (measured slower than FUSED so far: DESIGN.md)
-#ifndef ODPO_RES_AUTO
-#define ODPO_RES_AUTO 0
-#endif
-constexpr bool kResAuto = ODPO_RES_AUTO != 0;
 
 enum { R_END = 0, R_LIVE = 1, R_MASK = 2, R_NONE = 3, R_ZERO = 4 };
 
@@ -492,7 +487,7 @@ __global__ void __launch_bounds__(kResThreads, 1) k_resident(LossArgs a, ResGeo 
           for (int c = 0; c < ahead; ++c) issue(c);
         mbar_wait(mready_s + 8 * it, ph);
         if (btid == 0) RES_DBG(I.tk, 5);
-        const float bc = I.c, coef = I.coef, gtok = I.gtok;
+        const float bc = I.c, coef = I.coef, gtok = I.gtok, bm = I.m;
         const bool neg = coef < 0.f;
         const int tvec = (tok >= 0 && tok < nvec * N) ? tok / N : -1;
         const uint32_t tcol = tm_base + lane_base + (uint32_t)(ts * scols + half * (kResCols / 2));
@@ -530,8 +525,8 @@ __global__ void __launch_bounds__(kResThreads, 1) k_resident(LossArgs a, ResGeo 
             for (int u = 0; u < 4; ++u) {
               const int i = ftid + (u0 + u) * kResFT;
               if (i < cnv)
-                st16_stream(vout + c0 + i, neg ? bwd_vec<DT, NPB, true>(v[q][u], k2, bc)
-                                               : bwd_vec<DT, NPB, false>(v[q][u], k2, bc));
+                st16_stream(vout + c0 + i, neg ? bwd_vec<DT, NPB, true>(v[q][u], k2, bc, bm)
+                                               : bwd_vec<DT, NPB, false>(v[q][u], k2, bc, bm));
             }
             // onehot entry: the thread that stored tok's vector overwrites it (program order)
             if (tvec >= c0 && tvec < c0 + cnv && ((tvec - c0) % kResFT) == ftid &&
@@ -542,7 +537,7 @@ __global__ void __launch_bounds__(kResThreads, 1) k_resident(LossArgs a, ResGeo 
         if (btid < tail) {
           const int64_t vv = (int64_t)nvec * N + btid;
           const float x = Traits<DT>::load1(I.row, vv);
-          Traits<DT>::store1(I.drow, vv, vv == tok ? gtok : copysignf(ex2(fmaf(x, k2, -bc)), coef));
+          Traits<DT>::store1(I.drow, vv, vv == tok ? gtok : copysignf(ex2(bwd_arg<DT>(x, k2, bc, bm)), coef));
         }
         if (ts >= 0) tm_fence_before();
         // all eight backward warps are past the row: release its TMEM slot / L2 allowance
@@ -583,7 +578,7 @@ __global__ void __launch_bounds__(kResThreads, 1) k_resident(LossArgs a, ResGeo 
             coef = __uint_as_float((uint32_t)w);
           }
           const float m = I.m, l1p = I.l1p, logp = I.logp;
-          I.c = coef != 0.f ? fmaf(l1p, kLog2e, m * k2) - log2f(fabsf(coef)) : INFINITY;
+          I.c = coef != 0.f ? bwd_const<DT>(m, l1p, k2, coef) : INFINITY;
           I.coef = coef;
           I.gtok = coef * expm1f(logp);
           RES_DBG(I.tk, 4);

@@ -110,3 +110,75 @@ def coef_from_oracle(o, P, Pg, beta, invT, pair_rows, B):
         sig = 1.0 / (1.0 + np.exp(o["z"][p]))
         coef[c] = coef[r] = beta * sig * float(np.float32(invT)) / Pg
     return coef
+
+
+def pair_members(P, pair_rows):
+    if pair_rows is None:
+        return np.arange(P) * 2, np.arange(P) * 2 + 1
+    pr = np.asarray(pair_rows).reshape(-1, 2)
+    return pr[:, 0].astype(np.int64), pr[:, 1].astype(np.int64)
+
+
+def check_stats(st_gpu, o, dtype, beta, ref, pair_rows=None, Pg=None, exact_ncorrect=None,
+                tol=None):
+    """All ten loss statistics (ODPO_ST_*) against the oracle.
+
+    Counts (npairs, token counts) are exact; ncorrect is exact wherever no oracle |z| lies
+    inside the per-pair error band (else within the number of pairs in the band).  Every
+    float statistic is a sum of per-pair terms; its bound is the sum of the per-pair bounds
+    propagated from the north_star sequence tolerance (|dS_b| <= tol max(|S_b|, 1 nat))
+    plus the fp32 roundings of S, S - ref and z:
+      S sums:            sum tol max(|S|, 1) + 2^-24 |S|
+      beta (S - ref):    beta x (the above + 2^-24 (|S| + |ref|))
+      z:                 beta (e_c + e_r) + 2^-23 |z|
+      loss (/P_global):  sum e_z / P_global  (|d softplus(-z) / dz| <= 1)."""
+    st = np.asarray(st_gpu, dtype=np.float64)[:10]
+    os_ = np.asarray(o["stats"], dtype=np.float64)
+    S = np.asarray(o["seq_logp"], dtype=np.float64)
+    z = np.asarray(o["z"], dtype=np.float64)
+    P = z.size
+    Pg = P if Pg is None else Pg
+    c, r = pair_members(P, pair_rows)
+    tol = TOL_SEQ[dtype] if tol is None else tol
+    ref = np.asarray(ref, dtype=np.float64)
+    b = float(np.float32(beta))
+    eS_c = tol * np.maximum(np.abs(S[c]), 1.0) + 2.0 ** -24 * np.abs(S[c])
+    eS_r = tol * np.maximum(np.abs(S[r]), 1.0) + 2.0 ** -24 * np.abs(S[r])
+    ed_c = eS_c + 2.0 ** -24 * (np.abs(S[c]) + np.abs(ref[c]))
+    ed_r = eS_r + 2.0 ** -24 * (np.abs(S[r]) + np.abs(ref[r]))
+    ez = b * (ed_c + ed_r) + 2.0 ** -23 * np.abs(z)
+    bounds = {1: ez.sum() / Pg, 3: ez.sum(), 4: b * ed_c.sum(), 5: b * ed_r.sum(),
+              6: eS_c.sum(), 7: eS_r.sum()}
+    for i in (0, 8, 9):
+        assert st[i] == os_[i], (i, st[i], os_[i])
+    band = np.count_nonzero(np.abs(z) <= ez)
+    if exact_ncorrect is None:
+        exact_ncorrect = band == 0
+    if exact_ncorrect:
+        assert st[2] == os_[2], ("ncorrect", st[2], os_[2])
+    else:
+        assert abs(st[2] - os_[2]) <= band, ("ncorrect", st[2], os_[2], band)
+    for i, bd in bounds.items():
+        assert abs(st[i] - os_[i]) <= bd + 1e-12, (i, st[i], os_[i], bd)
+
+
+def controlled_ref(S_orc, P, pair_rows, seed):
+    """Controlled-ref mode: ref = fl32(S - delta) with delta_r = 0 and
+    delta_c = +-(1 + h % 128)/16, so z ~ beta delta_c is never inside the fp error band.
+    S_orc is the ORACLE's sequence log-prob (an input to both sides)."""
+    c, _ = pair_members(P, pair_rows)
+    h = synth.uniform_u32(seed, synth.S_DELTA, np.arange(P))
+    delta = np.zeros(S_orc.size)
+    delta[c] = np.where(h & 1, 1.0, -1.0) * (1 + (h >> 1) % 128) / 16.0
+    return (S_orc - delta).astype(np.float32)
+
+
+def to_device_logits(h, dtype):
+    """Host logits in the oracle's encoding (float32 or bf16 bits) -> a padded device view."""
+    B, T, V = h.shape
+    d = alloc_rows(B, T, V, dtype)
+    if dtype == "f32":
+        d.copy_(torch.from_numpy(np.ascontiguousarray(h)))
+    else:
+        d.copy_(torch.from_numpy(np.ascontiguousarray(h).view(np.int16)).view(torch.bfloat16))
+    return d

@@ -208,3 +208,26 @@ def test_lmhead_grad_argument_errors(lib):
     assert grad(h=None) == 1 and grad(rs=None) == 1 and grad(R=0) == 1 and grad(chunk=0) == 1
     assert grad(invT=float("nan")) == 1 and grad(d=96) == 4 and grad(w=FAKE_MIS) == 2
     assert grad(scb=16) == 3 and grad(sc=None) == 3
+
+
+def test_seq_ppl_argument_errors(lib):
+    """odpo_seq_ppl (KL proxy): outputs required, then seq_logprobs' checks."""
+    def call(ppl=FAKE, ps=FAKE, invT=1.0, wsb=1 << 20, logits=FAKE):
+        return lib.odpo_seq_ppl(logits, 1, 4, 3, 64, 192, 64, FAKE, FAKE, invT, FAKE, ppl, ps,
+                                None, FAKE, wsb, None)
+    assert call(ppl=None) == 1
+    assert call(ps=None) == 1
+    assert call(invT=0.0) == 1
+    assert call(logits=FAKE_MIS) == 2
+    assert call(wsb=8) == 3
+
+
+def test_library_has_no_environment_lookups():
+    """Tuning knobs are build-time defines: the product sources never read the environment
+    (the statically linked CUDA runtime does, for its own CUDA_* variables)."""
+    csrc = os.path.join(ROOT, "paper_2410_18252_b200", "csrc")
+    for f in os.listdir(csrc):
+        src = open(os.path.join(csrc, f)).read()
+        assert "getenv" not in src, f
+    binding = open(os.path.join(ROOT, "paper_2410_18252_b200", "__init__.py")).read()
+    assert "os.environ" not in binding

@@ -12,8 +12,8 @@ import torch
 
 import oracle
 import synth
-from gpu_helpers import (NCPU, Batch, alloc_rows, check_dlogits, check_seq, coef_from_oracle,
-                         to_f64)
+from gpu_helpers import (NCPU, Batch, alloc_rows, check_dlogits, check_seq, check_stats,
+                         coef_from_oracle, to_f64)
 
 pytestmark = [pytest.mark.gpu,
               pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a CUDA device")]
@@ -142,6 +142,11 @@ def test_identity_rows_bit_exact(odpo, dtype, permute, sched, shape):
     assert np.array_equal(seq_gpu[ref_idx].astype(np.float64), o["seq_logp"][ref_idx])
     assert np.array_equal(seq_gpu[ref_idx].astype(np.float64), S_exp[ref_idx])
     assert np.array_equal(out.z.cpu().numpy().astype(np.float64), o["z"])
+    # statistics: S, ref, beta = 1/8 and z are exact, so every margin statistic is too
+    st = out.stats.cpu().numpy()
+    for i in (0, 2, 3, 4, 5, 6, 7, 8, 9):
+        assert st[i] == o["stats"][i], (i, st[i], o["stats"][i])
+    assert abs(st[1] - o["stats"][1]) <= 1e-6 * abs(o["stats"][1])
     # dlogits pattern: exactly two nonzeros per live row, +coef at the anchor, -coef at tok
     g = out.dlogits.float().cpu().numpy()
     seq_role = {}
@@ -188,10 +193,7 @@ def test_loss_parity_small(odpo, case, sched):
     o = oracle_loss(b, ref, beta, Pg=P + 3)
     live = np.arange(b.B) if b.pair_rows is None else b.pair_rows.reshape(-1)
     check_seq(out.seq_logp.cpu().numpy()[live], o["seq_logp"][live], dt)
-    st = out.stats.cpu().numpy()
-    for i in (0, 8, 9):
-        assert st[i] == o["stats"][i]
-    check_seq(st[1:2], o["stats"][1:2], dt, "loss")
+    check_stats(out.stats.cpu().numpy(), o, dt, beta, ref, b.pair_rows, Pg=P + 3)
     coef = coef_from_oracle(o, P, P + 3, beta, invT, b.pair_rows, b.B)
     check_dlogits(to_f64(out.dlogits), o["dlogits"], coef[:, None, None], dt)
 
@@ -236,7 +238,7 @@ def test_tiny_config_full_parity(odpo, sched):
     out = run_loss(odpo, b, torch.from_numpy(ref).cuda(), w.beta, sched)
     o = oracle_loss(b, ref, w.beta)
     check_seq(out.seq_logp.cpu().numpy(), o["seq_logp"], "f32")
-    check_seq(out.stats.cpu().numpy()[1:2], o["stats"][1:2], "f32", "loss")
+    check_stats(out.stats.cpu().numpy(), o, "f32", w.beta, ref, b.pair_rows)
     coef = coef_from_oracle(o, w.P, w.P, w.beta, 1.0, b.pair_rows, b.B)
     check_dlogits(to_f64(out.dlogits), o["dlogits"], coef[:, None, None], "f32")
     # ref pass through the GPU seq_logprobs on the device-generated ref logits
@@ -263,7 +265,7 @@ def test_controlled_ref_accuracy_exact(odpo):
     st = out.stats.cpu().numpy()
     assert st[2] == o["stats"][2]
     assert 0 < st[2] < P
-    check_seq(st[1:2], o["stats"][1:2], "bf16", "loss")
+    check_stats(st, o, "bf16", beta, ref, None, exact_ncorrect=True)
     zg = out.z.cpu().numpy().astype(np.float64)
     assert np.all(np.sign(zg) == np.sign(o["z"]))
 
@@ -336,6 +338,21 @@ def test_full_size_sampled_parity(odpo, name, mask_kind, nsample):
     assert abs(st[1] - loss) <= 1e-9 * max(abs(loss), 1e-6)
     assert st[0] == w.P and st[2] == np.count_nonzero(z_all > 0)
     assert st[8] + st[9] == b.mask.sum()
+    # margin statistics: z_sum is the sum of the published z; the implicit rewards and the
+    # sequence sums are those of the published seq_logp (any summation order: 1e-9 relative)
+    S_all = out.seq_logp.cpu().double().numpy()
+    rf = ref.cpu().double().numpy()
+    sz = np.abs(z_all).sum()
+    assert abs(st[3] - z_all.sum()) <= 1e-9 * max(sz, 1e-9)
+    Sc, Sr = S_all[0::2], S_all[1::2]
+    bt = float(np.float32(w.beta))
+    assert abs(st[6] - Sc.sum()) <= 1e-9 * np.abs(Sc).sum()
+    assert abs(st[7] - Sr.sum()) <= 1e-9 * np.abs(Sr).sum()
+    dc = (Sc.astype(np.float32) - rf[0::2].astype(np.float32)).astype(np.float64)
+    dr = (Sr.astype(np.float32) - rf[1::2].astype(np.float32)).astype(np.float64)
+    assert abs(st[4] - bt * dc.sum()) <= 1e-9 * bt * np.abs(dc).sum() + 1e-12
+    assert abs(st[5] - bt * dr.sum()) <= 1e-9 * bt * np.abs(dr).sum() + 1e-12
+    assert abs(st[3] - (st[4] - st[5])) <= 2.0 ** -23 * sz + 1e-9 * bt * (np.abs(dc).sum() + np.abs(dr).sum())
     assert int(out.status.item()) == 0
     del b, out
     torch.cuda.empty_cache()

@@ -7,7 +7,7 @@ import torch
 
 import oracle
 import synth
-from gpu_helpers import DL_RTOL, NCPU, Batch, alloc_rows, check_dlogits, check_seq, to_f64
+from gpu_helpers import DL_RTOL, NCPU, Batch, alloc_rows, check_dlogits, check_seq, check_stats, to_f64
 
 pytestmark = [pytest.mark.gpu,
               pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a CUDA device")]
@@ -66,6 +66,7 @@ def test_unscaled_parity_small(odpo, case, engine, row_gap, sched):
     check_seq(out.seq_logp.cpu().numpy()[live], o["seq_logp"][live], dt)
     check_dlogits(to_f64(out.dlogits), o["dlogits"], 1.0, dt)
     check_row_scale(out.row_scale.cpu().numpy(), o["row_scale"], dt)
+    check_stats(out.stats.cpu().numpy(), o, dt, beta, ref, b.pair_rows, Pg=Pg)
     assert int(out.status.item()) == 0
     # the loss outputs are the scaled call's, bit for bit (same rows, same reduction trees)
     sc = odpo.online_dpo_loss_fwd_bwd(b.d_logits, d_ref, b.d_tokens, b.d_mask, beta,

@@ -7,7 +7,7 @@ import torch
 
 import oracle
 import synth
-from gpu_helpers import NCPU, Batch, check_dlogits, check_seq, coef_from_oracle, to_f64
+from gpu_helpers import NCPU, Batch, check_dlogits, check_seq, check_stats, coef_from_oracle, to_f64
 
 pytestmark = [pytest.mark.gpu,
               pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a CUDA device")]
@@ -54,9 +54,7 @@ def test_vp_parity(odpo, W, dt):
         assert torch.equal(out.stats[:10], outs[0].stats[:10])
         assert int(out.status.item()) == 0
     check_seq(outs[0].seq_logp.cpu().numpy()[live], o["seq_logp"][live], dt)
-    st = outs[0].stats.cpu().numpy()
-    assert st[0] == o["stats"][0] and st[8] == o["stats"][8] and st[9] == o["stats"][9]
-    check_seq(st[1:2], o["stats"][1:2], dt, "loss")
+    check_stats(outs[0].stats.cpu().numpy(), o, dt, 0.1, ref, b.pair_rows, Pg=P + 1)
     coef = coef_from_oracle(o, P, P + 1, 0.1, 1.0, b.pair_rows, b.B)
     check_dlogits(to_f64(dl), o["dlogits"], coef[:, None, None], dt)
 
