@@ -65,6 +65,9 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--lib", default=None,
+                    help="A/B experiments only: load this build of libodpo.so instead of the "
+                         "in-tree one (e.g. build_variants/*.so from build.build(out=, defines=))")
     return ap.parse_args()
 
 
@@ -112,8 +115,8 @@ def ncu_evidence(config, form):
 
 def measure_ceilings(dev):
     """Copy and read-only HBM ceilings measured in this run: b.copy_(a) over
-    1 Gi bf16 (read + write bytes, MEASURED_PEAKS.json's method) and a bf16 -> fp32 sum over
-    4 GiB (read bytes), best of 5 with CUDA events."""
+    1 Gi bf16 (read + write bytes, MEASURED_PEAKS.json's method) and a read-only 128-bit stream
+    over 4 GiB (read bytes), best of 5 with CUDA events."""
     import torch
     out = {}
     a = torch.empty(1 << 30, dtype=torch.bfloat16, device=dev)
@@ -136,10 +139,13 @@ def measure_ceilings(dev):
     del a, b
     x = torch.empty(2 << 30, dtype=torch.bfloat16, device=dev)
     x.fill_(0.5)
-    out["read_gbs"] = best(lambda: x.sum(dtype=torch.float32), x.numel() * 2)
+    import synth
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    out["read_gbs"] = max(best(lambda: synth.read_probe(x, sms * k), x.numel() * 2) for k in (8, 16))
     del x
     torch.cuda.empty_cache()
-    out["how"] = "copy: b.copy_(a) 1 Gi bf16, read+write bytes; read: x.sum over 4 GiB bf16; best of 5"
+    out["how"] = ("copy: b.copy_(a) 1 Gi bf16, read+write bytes; read: a 128-bit read-only stream "
+                  "over 4 GiB (synth_read_probe, 8 loads in flight per thread); best of 5")
     return out
 
 
@@ -191,12 +197,13 @@ def aux_lmhead(config, B, T, reps=5):
     seqp = t(lambda: odpo.seq_logprobs(lg, tok, msk))
     del lg
     # the full head learner step: fused (logits never stored; backward recomputes them in
-    # 8192-row chunks) vs unfused (cuBLAS logits, the loss call in place, two cuBLAS GEMMs)
+    # wave-sized row chunks, tcgen05 GEMMs for dhidden / dweight) vs unfused (cuBLAS logits, the
+    # loss call in place, two cuBLAS GEMMs)
     ref_h = torch.full((B,), -4.0 * T, device="cuda")
 
     def fused_step():
         o = odpo.lmhead_online_dpo_loss_fwd(hid, Wh, ref_h, tok, msk, 0.1)
-        return odpo.lmhead_grad(hid, Wh, tok, o.row_lse, o.row_scale, chunk_rows=8192)
+        return odpo.lmhead_grad(hid, Wh, tok, o.row_lse, o.row_scale)
 
     def unfused_step():
         lg2 = torch.matmul(hid.view(B * T, d), Wh.t()).view(B, T, V)
@@ -204,6 +211,8 @@ def aux_lmhead(config, B, T, reps=5):
         dl = o.dlogits.view(B * T, V)
         return torch.matmul(dl, Wh), torch.matmul(dl.t(), hid.view(B * T, d))
 
+    o_h = odpo.lmhead_online_dpo_loss_fwd(hid, Wh, ref_h, tok, msk, 0.1)
+    grad_ms = t(lambda: odpo.lmhead_grad(hid, Wh, tok, o_h.row_lse, o_h.row_scale))
     step_f = t(fused_step)
     step_u = t(unfused_step)
     del hid, Wh
@@ -216,8 +225,12 @@ def aux_lmhead(config, B, T, reps=5):
             "cublas_gemm_ms": gemm, "cublas_tflops": flops / gemm / 1e9,
             "unfused_ms": gemm + seqp, "speedup_vs_unfused": (gemm + seqp) / fused,
             "step_fused_ms": step_f, "step_unfused_ms": step_u,
+            "grad_ms": grad_ms, "grad_tflops": 3 * flops / grad_ms / 1e9,
+            "grad_note": "odpo_lmhead_grad alone: logits recompute + G epilogue, dhidden and "
+                         "dweight GEMMs (3 x 2 R d V flops) on the library's tcgen05 kernels",
             "step_note": "fwd + DPO loss + dhidden/dweight; fused keeps no logits (backward "
-                         "recomputes them in 8192-row chunks), unfused materialises them"}
+                         "recomputes them in wave-sized row chunks and runs its own tcgen05 "
+                         "GEMMs), unfused materialises them (cuBLAS GEMMs)"}
 
 
 class ClockSampler:
@@ -368,6 +381,8 @@ def run_ours(args, rank, world, local_rank):
 
     import synth
     import paper_2410_18252_b200 as odpo
+    if args.lib:
+        odpo.LIB_PATH = os.path.abspath(args.lib)
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)

@@ -332,8 +332,9 @@ odpo_status odpo_pg_loss_fwd_bwd(const void* policy_logits, odpo_dtype dt, int64
 /*
  * Vocabulary-parallel loss: the LM head's vocabulary is
  * sharded over W ranks, rank w holding logits[:, :, v0_w : v0_w + V_shard_w] (v0 increasing
- * with w).  Two calls per rank with an all-gather of 16-byte row partials between them (the
- * caller's collective, e.g. NCCL all_gather over NVLink):
+ * with w).  Two calls per rank; the 16-byte row partials move between them either through the
+ * caller's collective (odpo_vp_row_partials + e.g. an NCCL all_gather, flags = NULL) or INSIDE
+ * the kernels over peer memory (odpo_vp_row_partials_put + flags): no host collective.
  *
  * odpo_vp_row_partials -- one read of this rank's shard: for every row with mask = 1,
  *   parts[row] = (m, log1p r, x_tok, owns) with 1 + r = sum over the shard of
@@ -347,7 +348,22 @@ odpo_status odpo_pg_loss_fwd_bwd(const void* policy_logits, odpo_dtype dt, int64
  *   odpo_online_dpo_loss_fwd_bwd (identical on every rank: the stats are already global over
  *   the vocabulary group, do not sum them over it), and writes this rank's dlogits shard
  *   coef_b (softmax - onehot) with the global normaliser.  One read of the shard again (2R+1W
- *   per shard).  Other arguments and errors as odpo_online_dpo_loss_fwd_bwd.
+ *   per shard).  flags / epoch: NULL for a caller-gathered parts_all; otherwise this rank's
+ *   [W] u32 flag words of the in-kernel exchange: the merge kernel first waits (system-scope
+ *   acquire, spinning on the device) until flags[q] has reached epoch for every rank q, and
+ *   parts_all is this rank's exchange buffer of that epoch (W <= 8).  Other arguments and
+ *   errors as odpo_online_dpo_loss_fwd_bwd.
+ *
+ * odpo_vp_row_partials_put -- odpo_vp_row_partials with the exchange in the kernel: every
+ *   row's partial is stored into slot [rank][row] of EVERY rank's buffer
+ *   (peer_parts[q] = rank q's [W][B*T][4] f32 buffer for this epoch, mapped into this process:
+ *   NVLink P2P on a multi-GPU node, CUDA IPC between processes sharing a GPU), and the last CTA
+ *   publishes `epoch` into peer_flags[q][rank] for every q (system-scope release) after a
+ *   system fence.  peer_parts / peer_flags are HOST arrays of W device pointers; `done` is this
+ *   rank's device u32 CTA counter (0 on entry; the kernel leaves it 0).  Epochs must increase
+ *   by one per step; a double-buffered parts region (by epoch parity) is safe because a rank
+ *   cannot start step k+2's put before every rank finished step k's merge.  W <= 8.
+ *   Errors: INVALID_ARG (null pointers, rank/W), ALIGNMENT, CUDA.
  */
 odpo_status odpo_vp_row_partials(const void* logits_shard, odpo_dtype dt, int64_t B, int64_t T,
                                  int64_t V_shard, int64_t stride_b, int64_t stride_t,
@@ -363,8 +379,15 @@ odpo_status odpo_vp_loss_fwd_bwd(const float* parts_all, int32_t W, const void* 
                                  int64_t P_global, float beta, float inv_temperature,
                                  void* dlogits_shard, int64_t dstride_b, int64_t dstride_t,
                                  float* seq_logp, float* pair_logit, double* stats,
-                                 uint32_t* status, void* workspace, size_t workspace_bytes,
-                                 void* stream);
+                                 const uint32_t* flags, uint32_t epoch, uint32_t* status,
+                                 void* workspace, size_t workspace_bytes, void* stream);
+odpo_status odpo_vp_row_partials_put(const void* logits_shard, odpo_dtype dt, int64_t B,
+                                     int64_t T, int64_t V_shard, int64_t stride_b,
+                                     int64_t stride_t, int64_t v0, int64_t V_total,
+                                     const int32_t* tokens, const uint8_t* mask,
+                                     float inv_temperature, float* const* peer_parts,
+                                     uint32_t* const* peer_flags, uint32_t* done, int32_t rank,
+                                     int32_t W, uint32_t epoch, uint32_t* status, void* stream);
 
 /* Host-only: device scratch bytes needed by the calls above for B sequences of T tokens
    and P pairs (about 13 bytes per row + 80 bytes per pair + small). */
@@ -413,15 +436,20 @@ size_t odpo_lmhead_workspace_bytes(int64_t B, int64_t T, int64_t V);
  *   dweight     = G^T hidden        fp32 [V, d] (overwritten)
  *
  * The logits are recomputed chunk by chunk (chunk_rows rows at a time, rounded up to 256) by
- * the NEXT-2 tcgen05 kernel, whose epilogue writes G (bf16) into `scratch` instead of
- * reducing it; the two GEMMs with G are plain cuBLAS GEMMs (bf16 in, fp32 accumulate), loaded
- * at run time.  row_lse is odpo_lmhead_seq_logprobs' row_lse (natural log, invT applied).
+ * the NEXT-2 tcgen05 kernel, whose epilogue writes G and its transpose G^T (bf16) into
+ * `scratch` instead of reducing them; the two GEMMs with G run on the library's own tcgen05
+ * CTA-pair GEMM (bf16 operands staged by TMA, fp32 accumulators in tensor memory; no cuBLAS):
+ * dhidden = G (W^T)^T with a once-per-call W^T copy, dweight += (G^T) (H^T)^T with a per-chunk
+ * H^T copy.  Deterministic: every output element is accumulated in a fixed order (chunks in
+ * row order, K in order), no atomics.  row_lse is odpo_lmhead_seq_logprobs' row_lse (natural
+ * log, invT applied).
  *   hidden bf16 [R, d], weight bf16 [V, d] contiguous, 16-byte aligned, d % 64 == 0.
- *   scratch >= odpo_lmhead_grad_scratch_bytes(chunk_rows, V) bytes, 16-byte aligned.
- * Errors: INVALID_ARG, UNSUPPORTED (d % 64, sizes, cuBLAS not loadable), ALIGNMENT,
- * WORKSPACE, CUDA.
+ *   dhidden, dweight fp32, 16-byte aligned.
+ *   scratch >= odpo_lmhead_grad_scratch_bytes(chunk_rows, d, V) bytes, 256-byte aligned
+ *   (W^T, G, G^T and H^T of one chunk: about 2 d V + 4 chunk_rows V bytes).
+ * Errors: INVALID_ARG, UNSUPPORTED (d % 64, sizes), ALIGNMENT, WORKSPACE, CUDA.
  */
-size_t odpo_lmhead_grad_scratch_bytes(int64_t chunk_rows, int64_t V);
+size_t odpo_lmhead_grad_scratch_bytes(int64_t chunk_rows, int64_t d, int64_t V);
 odpo_status odpo_lmhead_grad(const void* hidden, const void* weight, int64_t R, int64_t d,
                              int64_t V, const int32_t* tokens, const float* row_lse,
                              const float* row_scale, float inv_temperature, float* dhidden,

@@ -268,7 +268,7 @@ def lmhead_dpo_grad(hidden, weight, ref_logp, tokens, mask, beta, pair_rows=None
     p[np.arange(B * T), tok] -= 1.0
     G = o["row_scale"].reshape(B * T, 1) * p
     return dict(dhidden=(G @ w).reshape(B, T, d), dweight=G.T @ h.reshape(B * T, d),
-                row_scale=o["row_scale"], loss=o["stats"][1])
+                row_scale=o["row_scale"], loss=o["stats"][1], G=G)
 
 
 def to_bf16_bits(x) -> np.ndarray:

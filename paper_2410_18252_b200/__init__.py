@@ -21,7 +21,7 @@ from dataclasses import dataclass
 
 import torch
 
-__all__ = ["pair_select", "seq_logprobs", "seq_ppl", "online_dpo_loss_fwd_bwd", "allreduce_stats",
+__all__ = ["pair_select", "seq_logprobs", "seq_ppl", "VPExchange", "vp_loss_step", "online_dpo_loss_fwd_bwd", "allreduce_stats",
            "workspace_bytes", "LossOutput", "SelectOutput", "OdpoError", "lib_path",
            "STAT_NAMES", "SEL_NAMES", "FLAGS"]
 
@@ -80,7 +80,11 @@ def _L():
                                            f32, P, P, P, sz, P]
         L.odpo_vp_loss_fwd_bwd.argtypes = [P, i32, P, C.c_int, i64, i64, i64, i64, i64, i64, i64,
                                            P, P, P, P, i64, i64, f32, f32, P, i64, i64, P, P, P,
-                                           P, P, sz, P]
+                                           P, C.c_uint32, P, P, sz, P]
+        L.odpo_vp_row_partials_put.argtypes = [P, C.c_int, i64, i64, i64, i64, i64, i64, i64, P,
+                                               P, f32, C.POINTER(P), C.POINTER(P), P, i32, i32,
+                                               C.c_uint32, P, P]
+        L.odpo_vp_row_partials_put.restype = C.c_int
         L.odpo_vp_row_partials.restype = C.c_int
         L.odpo_vp_loss_fwd_bwd.restype = C.c_int
         L.odpo_gather_pairs.argtypes = [P, i64, i64, i64, P, P, P, P, P, P, P, P]
@@ -100,7 +104,7 @@ def _L():
         L.odpo_online_dpo_loss_from_token_logp.argtypes = [P, i64, i64, P, P, P, i64, i64, f32,
                                                            f32, P, P, P, P, P, P, sz, P]
         L.odpo_online_dpo_loss_from_token_logp.restype = C.c_int
-        L.odpo_lmhead_grad_scratch_bytes.argtypes = [i64, i64]
+        L.odpo_lmhead_grad_scratch_bytes.argtypes = [i64, i64, i64]
         L.odpo_lmhead_grad_scratch_bytes.restype = sz
         L.odpo_lmhead_grad.argtypes = [P, P, i64, i64, i64, P, P, P, f32, P, P, P, sz, i64, P]
         L.odpo_lmhead_grad.restype = C.c_int
@@ -383,10 +387,11 @@ def lmhead_online_dpo_loss_fwd(hidden: torch.Tensor, weight: torch.Tensor,
 
 def lmhead_grad(hidden: torch.Tensor, weight: torch.Tensor, tokens: torch.Tensor,
                 row_lse: torch.Tensor, row_scale: torch.Tensor, inv_temperature: float = 1.0,
-                chunk_rows: int = 16384):
+                chunk_rows: int | None = None):
     """NEXT-2 backward: (dhidden fp32 [B, T, d], dweight fp32 [V, d]) of the loss whose logit
     gradient is row_scale * (softmax - onehot); logits recomputed chunk by chunk on tcgen05,
-    G written to a bf16 scratch of chunk_rows rows, two cuBLAS GEMMs per chunk."""
+    G and G^T written to a bf16 scratch of chunk_rows rows, then the library's own tcgen05
+    GEMMs dhidden = G W and dweight += G^T H (no cuBLAS)."""
     hidden = _dev(hidden, "hidden", torch.bfloat16)
     weight = _dev(weight, "weight", torch.bfloat16)
     if not (hidden.is_contiguous() and weight.is_contiguous()):
@@ -402,9 +407,16 @@ def lmhead_grad(hidden: torch.Tensor, weight: torch.Tensor, tokens: torch.Tensor
     dev = hidden.device
     dh = torch.empty(hidden.shape, dtype=torch.float32, device=dev)
     dw = torch.empty((V, d), dtype=torch.float32, device=dev)
+    if chunk_rows is None:
+        # whole waves of the dhidden GEMM: (chunk/256 row blocks) x (d/256 column blocks) tiles
+        # a multiple of the CTA-pair count
+        import math
+        pairs = torch.cuda.get_device_properties(dev).multi_processor_count // 2
+        nnb = -(-d // 256)
+        chunk_rows = 256 * (pairs // math.gcd(pairs, nnb))
     cr = min(int(chunk_rows), R)
     cr = -(-cr // 256) * 256
-    nb = _L().odpo_lmhead_grad_scratch_bytes(cr, V)
+    nb = _L().odpo_lmhead_grad_scratch_bytes(cr, d, V)
     scratch = torch.empty(max(nb, 256), dtype=torch.uint8, device=dev)
     _check(_L().odpo_lmhead_grad(_p(hidden), _p(weight), R, d, V, _p(tokens), _p(row_lse),
                                  _p(row_scale), float(inv_temperature), _p(dh), _p(dw),
@@ -582,8 +594,8 @@ def vp_loss_fwd_bwd(parts_all: torch.Tensor, logits_shard: torch.Tensor, v0: int
                     ref_logp: torch.Tensor, tokens: torch.Tensor, mask: torch.Tensor, beta: float,
                     pair_rows: torch.Tensor | None = None, p_global: int | None = None,
                     inv_temperature: float = 1.0, dlogits: torch.Tensor | None = None,
-                    stats: torch.Tensor | None = None,
-                    status: torch.Tensor | None = None) -> LossOutput:
+                    stats: torch.Tensor | None = None, status: torch.Tensor | None = None,
+                    flags: torch.Tensor | None = None, epoch: int = 0) -> LossOutput:
     """Vocabulary-parallel loss of one shard from the all-gathered partials [W, B*T, 4]:
     global log-probs, loss and stats (identical on every rank of the vocabulary group) and
     this shard's dlogits."""
@@ -607,15 +619,110 @@ def vp_loss_fwd_bwd(parts_all: torch.Tensor, logits_shard: torch.Tensor, v0: int
         _p(parts_all), W, _p(logits_shard), dt, B, T, V, sb, st, int(v0), int(V_total),
         _p(ref_logp), _p(tokens), _p(mask), _p(pair_rows), P, Pg, float(beta),
         float(inv_temperature), _p(dl), dl.stride(0), dl.stride(1), _p(seq), _p(z), _p(stats),
-        _p(status), _p(ws), ws.numel(), _stream()), "odpo_vp_loss_fwd_bwd")
+        _p(flags), int(epoch) & 0xFFFFFFFF, _p(status), _p(ws), ws.numel(), _stream()),
+        "odpo_vp_loss_fwd_bwd")
     return LossOutput(stats, dl, seq, z[:P], status, 4)
+
+
+class VPExchange:
+    """Peer-memory exchange buffers of the vocabulary-parallel step.
+
+    Every rank owns one device buffer: the row partials of two epochs, [2][W][rows][4] f32
+    (slot [e % 2][q] written by rank q), W u32 flag words and a u32 CTA counter.  The buffers
+    are mapped into every rank's address space: over the process group the ranks exchange
+    CUDA IPC handles of their buffers (torch's CUDA tensor sharing) and open each other's, so
+    odpo_vp_row_partials_put stores straight into the peers' memory (NVLink P2P on one node;
+    IPC between processes sharing a GPU) and odpo_vp_loss_fwd_bwd waits on its own flags.
+    `VPExchange.emulate(W, rows, device)` builds W ranks' buffers inside one process (tests)."""
+
+    def __init__(self, rows: int, group=None, device=None, _bufs=None, _rank=0):
+        self.rows = int(rows)
+        if _bufs is not None:
+            self.bufs, self.rank, self.W = _bufs, _rank, len(_bufs)
+        else:
+            import torch.distributed as dist
+            from torch.multiprocessing.reductions import reduce_tensor
+            self.W = dist.get_world_size(group)
+            self.rank = dist.get_rank(group)
+            if self.W > 8:
+                raise OdpoError("the in-kernel exchange supports up to 8 ranks per vocabulary group")
+            dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+            own = torch.zeros(self.nbytes(self.W, self.rows), dtype=torch.uint8, device=dev)
+            torch.cuda.synchronize(dev)
+            handles = [None] * self.W
+            dist.all_gather_object(handles, reduce_tensor(own), group=group)
+            self.bufs = []
+            for q, (fn, args) in enumerate(handles):
+                self.bufs.append(own if q == self.rank else fn(*args))
+            dist.barrier(group)
+        self.epoch = 0
+
+    @staticmethod
+    def nbytes(W: int, rows: int) -> int:
+        return 2 * W * rows * 16 + 4 * W + 256
+
+    @classmethod
+    def emulate(cls, W: int, rows: int, device=None):
+        """W ranks' exchanges in one process (every 'peer' buffer is a local allocation)."""
+        dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        bufs = [torch.zeros(cls.nbytes(W, rows), dtype=torch.uint8, device=dev) for _ in range(W)]
+        return [cls(rows, _bufs=bufs, _rank=r) for r in range(W)]
+
+    def _parts_ptr(self, q, e):
+        return self.bufs[q].data_ptr() + (e % 2) * self.W * self.rows * 16
+
+    def _flags_ptr(self, q):
+        return self.bufs[q].data_ptr() + 2 * self.W * self.rows * 16
+
+    def parts(self, e) -> torch.Tensor:
+        """This rank's [W, rows, 4] partials of epoch e (rank q's slice written by rank q)."""
+        n = self.W * self.rows * 4
+        f = self.bufs[self.rank][: 2 * n * 4].view(torch.float32)
+        return f[(e % 2) * n:(e % 2 + 1) * n].view(self.W, self.rows, 4)
+
+    def flags(self) -> torch.Tensor:
+        off = 2 * self.W * self.rows * 16
+        return self.bufs[self.rank][off:off + 4 * self.W].view(torch.int32)
+
+    def done(self) -> int:
+        return self._flags_ptr(self.rank) + 4 * self.W
+
+
+def vp_row_partials_put(logits_shard: torch.Tensor, v0: int, V_total: int, tokens: torch.Tensor,
+                        mask: torch.Tensor, ex: VPExchange, epoch: int,
+                        inv_temperature: float = 1.0, status: torch.Tensor | None = None):
+    """Forward of this rank's shard with the exchange in the kernel: partials stored into every
+    rank's buffer (peer memory) and `epoch` published to every rank's flags."""
+    dt, B, T, V, sb, st = _logits_meta(logits_shard, "logits_shard")
+    tokens, mask = _tokmask(tokens, mask, B, T)
+    if B * T != ex.rows:
+        raise OdpoError(f"exchange built for {ex.rows} rows, shard has {B * T}")
+    status = _status(status, logits_shard.device)
+    W = ex.W
+    parts = (C.c_void_p * W)(*[ex._parts_ptr(q, epoch) for q in range(W)])
+    flags = (C.c_void_p * W)(*[ex._flags_ptr(q) for q in range(W)])
+    _check(_L().odpo_vp_row_partials_put(
+        _p(logits_shard), dt, B, T, V, sb, st, int(v0), int(V_total), _p(tokens), _p(mask),
+        float(inv_temperature), parts, flags, C.c_void_p(ex.done()), ex.rank, W,
+        int(epoch) & 0xFFFFFFFF, _p(status), _stream()), "odpo_vp_row_partials_put")
+    return status
 
 
 def vp_loss_step(logits_shard: torch.Tensor, v0: int, V_total: int, ref_logp: torch.Tensor,
                  tokens: torch.Tensor, mask: torch.Tensor, beta: float, group=None,
-                 **kw) -> LossOutput:
-    """One vocabulary-parallel learner step on this rank: partials, all-gather over the
-    vocabulary group (NCCL over NVLink with the nccl backend), loss and dlogits shard."""
+                 exchange: VPExchange | None = None, **kw) -> LossOutput:
+    """One vocabulary-parallel learner step on this rank: partials, their exchange over the
+    vocabulary group, loss and dlogits shard.  With `exchange` (a VPExchange) the partials move
+    inside the kernels over peer memory -- two launches of ours, no host collective; without
+    it they are all-gathered by the process group (NCCL over NVLink with the nccl backend)."""
+    if exchange is not None:
+        exchange.epoch += 1
+        e = exchange.epoch
+        st = vp_row_partials_put(logits_shard, v0, V_total, tokens, mask, exchange, e,
+                                 kw.get("inv_temperature", 1.0), kw.get("status"))
+        kw["status"] = st
+        return vp_loss_fwd_bwd(exchange.parts(e), logits_shard, v0, V_total, ref_logp, tokens,
+                               mask, beta, flags=exchange.flags(), epoch=e, **kw)
     import torch.distributed as dist
     parts = vp_row_partials(logits_shard, v0, V_total, tokens, mask,
                             kw.get("inv_temperature", 1.0), kw.get("status"))

@@ -110,6 +110,14 @@ __device__ __forceinline__ unsigned long long gtimer() {
 __device__ __forceinline__ void flag(uint32_t* status, uint32_t f) {
   if (f && status) atomicOr(status, f);
 }
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 
 // ------------------------------------------------------------------ K1 pair_select
 // One CTA; thread i handles prompts i, i+NT, ...; selection stats reduced in fixed order.
@@ -243,6 +251,21 @@ __global__ void k_gather_pairs(const int32_t* __restrict__ pair_rows, int64_t n_
 }
 
 // ------------------------------------------------------------------ shared arguments
+// NEXT-4 in-kernel exchange of the vocabulary-parallel row partials over peer memory (NVLink /
+// NVSwitch P2P, or CUDA IPC between processes on one GPU): rank `rank` stores each row's
+// 16-byte partial into slot [rank][g] of EVERY rank's partial buffer (parts[q]: rank q's buffer,
+// mapped into this process), then the last CTA to finish publishes `epoch` into every rank's
+// flag word flags[q][rank] with a system-scope release.  The combine kernel on rank q waits
+// for all W flags (acquire) and merges the W partials of each row in rank order.
+constexpr int kVpMaxW = 8;
+struct VpPut {
+  float4* parts[kVpMaxW];
+  uint32_t* flags[kVpMaxW];
+  uint32_t* done;   // this rank's CTA completion counter (reset by the last CTA)
+  int32_t rank, W;
+  uint32_t epoch;
+};
+
 struct LossArgs {
   const void* logits;
   int64_t B, T, V, sb, st;  // strides in elements
@@ -284,6 +307,9 @@ struct LossArgs {
   float4* vp_parts;
   int64_t tok_off;
   int64_t V_total;
+  VpPut put;            // NEXT-4 in-kernel exchange (put.W = 0: write vp_parts locally)
+  const uint32_t* vp_flags;  // combine: wait until every vp_flags[q] reached vp_epoch (NULL: none)
+  uint32_t vp_epoch;
 };
 
 __device__ __forceinline__ const char* row_ptr(const LossArgs& a, int64_t b, int64_t t) {
@@ -467,19 +493,27 @@ __global__ void __launch_bounds__(32) k_pair_reduce(LossArgs a) { pair_reduce_wa
 // One thread per row.  The token's logit comes from the shard that owns it.
 __global__ void k_vp_combine(LossArgs a, const float4* __restrict__ parts, int W) {
   const int64_t rows = a.B * a.T;
+  if (a.vp_flags) {
+    // in-kernel exchange: wait until every rank has published this epoch's partials into this
+    // rank's buffer (acquire, system scope), then read them through L2
+    if (threadIdx.x == 0)
+      for (int q = 0; q < W; ++q)
+        while ((int32_t)(ld_acquire_sys(a.vp_flags + q) - a.vp_epoch) < 0) __nanosleep(64);
+    __syncthreads();
+  }
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= rows || !a.mask[g]) return;
   int ws = 0;
   float ms = -INFINITY;
   for (int w = 0; w < W; ++w) {
-    const float mw = __ldg(&parts[(int64_t)w * rows + g].x);
+    const float mw = __ldcg(&parts[(int64_t)w * rows + g].x);
     if (mw > ms) { ms = mw; ws = w; }
   }
   uint32_t fl = 0;
   float R = 0.f, xt = 0.f;
   int owners = 0;
   for (int w = 0; w < W; ++w) {
-    const float4 pw = parts[(int64_t)w * rows + g];
+    const float4 pw = __ldcg(&parts[(int64_t)w * rows + g]);
     if (pw.w != 0.f) { xt = pw.z; ++owners; }
     if (w == ws) {
       R += expm1f(pw.y);
@@ -615,15 +649,47 @@ __global__ void __launch_bounds__(32 * kWarpRowsPerCta) k_row_bwd_warp(LossArgs 
 // 8 16-byte vectors per batch, the online (m, r) update of the engine (mr_batch), the
 // fixed-order warp merge; writes the shard partial (m, log1p r, x_tok, owns tok) as the
 // engine's vocabulary-parallel epilogue does.
+__device__ __forceinline__ void vp_store(const LossArgs& a, int64_t g, float4 v) {
+  if (a.put.W > 0) {
+    const int64_t rows = a.B * a.T;
+    for (int q = 0; q < a.put.W; ++q) a.put.parts[q][(int64_t)a.put.rank * rows + g] = v;
+  } else {
+    a.vp_parts[g] = v;
+  }
+}
+// End of a put kernel (every thread of the CTA calls it): the CTA's partial stores are made
+// visible system-wide, and the last CTA of the grid publishes the epoch to every rank.
+__device__ __forceinline__ void vp_signal(const LossArgs& a) {
+  if (a.put.W == 0) return;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    const unsigned n = atomicAdd(a.put.done, 1u);
+    if (n == gridDim.x - 1) {
+      __threadfence_system();
+      *a.put.done = 0u;   // the next call is stream-ordered after this kernel
+      for (int q = 0; q < a.put.W; ++q) st_release_sys(a.put.flags[q] + a.put.rank, a.put.epoch);
+    }
+  }
+}
+
+template <int DT>
+__device__ __forceinline__ void vp_partials_row(const LossArgs& a);
 template <int DT>
 __global__ void __launch_bounds__(32 * kWarpRowsPerCta) k_vp_partials_warp(LossArgs a) {
+  vp_partials_row<DT>(a);
+  vp_signal(a);
+}
+
+template <int DT>
+__device__ __forceinline__ void vp_partials_row(const LossArgs& a) {
   constexpr int N = Traits<DT>::N;
   constexpr int U = 8;
   const int lane = threadIdx.x & 31;
   const int64_t g = (int64_t)blockIdx.x * kWarpRowsPerCta + (threadIdx.x >> 5);
   if (g >= a.B * a.T) return;
   if (!a.mask[g]) {
-    if (lane == 0) a.vp_parts[g] = make_float4(-INFINITY, 0.f, 0.f, 0.f);
+    if (lane == 0) vp_store(a, g, make_float4(-INFINITY, 0.f, 0.f, 0.f));
     return;
   }
   const int64_t b = g / a.T, t = g % a.T;
@@ -676,7 +742,7 @@ __global__ void __launch_bounds__(32 * kWarpRowsPerCta) k_vp_partials_warp(LossA
     if (gt < 0 || gt >= a.V_total) fl |= ODPO_FLAG_TOKEN_RANGE;
     if (isnan(v.m) || v.m == INFINITY || !isfinite(v.r)) fl |= ODPO_FLAG_NONFINITE_LOGIT;
     const bool own = tok >= 0;
-    a.vp_parts[g] = make_float4(v.m, log1pf(v.r), own ? xt : 0.f, own ? 1.f : 0.f);
+    vp_store(a, g, make_float4(v.m, log1pf(v.r), own ? xt : 0.f, own ? 1.f : 0.f));
     flag(a.status, fl);
   }
 }
@@ -702,6 +768,10 @@ __global__ void __launch_bounds__(kRowThreads, 2) k_row_bwd(LossArgs a) {
 // row's forward pass and then its unscaled backward G = softmax - onehot in the same CTA (the
 // re-read is one row behind, so it is served from L2); the pair reducer writes row_scale.
 enum { M_SEQ = 0, M_FUSED = 1, M_UNSC = 2, M_NMODES = 3 };
+#ifndef ODPO_BREV
+#define ODPO_BREV 1
+#endif
+constexpr bool kBrev = ODPO_BREV != 0;   // factored backward rows stream last chunk first
 
 // Fused dispatch (adaptive, per-pair backward counters).  Forward rows are dispensed in pair
 // order from one counter (C_TICKET).  Backward rows are dispensed pair by pair: C_BPAIR is the
@@ -987,7 +1057,8 @@ __global__ void __launch_bounds__(GE::THREADS, GE::CPS) k_engine(LossArgs a) {
   __shared__ __align__(8) uint64_t part_ready[kSlots];
   __shared__ __align__(8) uint64_t param_ready[kSlots];
   __shared__ int32_t stage_slot[kStages];
-  __shared__ int32_t stage_chunk[kStages];
+  __shared__ int32_t stage_chunk[kStages];   // position of the chunk in its row's stream
+  __shared__ int32_t stage_pchunk[kStages];  // the chunk's place in the row (vector range)
   __shared__ __align__(16) RowSlot slots[kSlots];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t crank = CS > 1 ? cluster_rank() : 0u;
@@ -1166,7 +1237,12 @@ __global__ void __launch_bounds__(GE::THREADS, GE::CPS) k_engine(LossArgs a) {
             wait(empty_s + 8 * st, sph ^ 1u);
             stage_slot[st] = kind == K_END ? -1 : psl;
             stage_chunk[st] = c;
-            const int vs = s_lo + c * kCV;
+            // factored-gradient backward rows stream their chunks last-first: the chunks the
+            // row's forward read last are the likeliest still in L2 (elementwise backward,
+            // so the order does not change any result)
+            const int pc = (kBrev && MODE == M_UNSC && kind == K_B) ? nstage - 1 - c : c;
+            stage_pchunk[st] = pc;
+            const int vs = s_lo + pc * kCV;
             const int nv = data ? min(kCV, s_hi - vs) : 0;
             if (nv > 0) {
               const uint32_t bytes = (uint32_t)nv * 16u;
@@ -1369,6 +1445,7 @@ __global__ void __launch_bounds__(GE::THREADS, GE::CPS) k_engine(LossArgs a) {
       const int sl = stage_slot[st];
       if (sl < 0) break;
       const int ch = stage_chunk[st];
+      const int pch = stage_pchunk[st];
       RowSlot& S = slots[sl];
       const uint32_t Lslot = L_slots + sl * (uint32_t)sizeof(RowSlot);
       if (ch == 0) {  // a new row: cache its fields (a row's chunks occupy consecutive stages)
@@ -1395,9 +1472,9 @@ __global__ void __launch_bounds__(GE::THREADS, GE::CPS) k_engine(LossArgs a) {
       const int kind = r_kind;
       const bool last_chunk = ch == r_nst - 1;
       const uint4* sv = reinterpret_cast<const uint4*>(ring + (size_t)st * kChunk);
-      const int c0 = r_lo + ch * kCV;  // first vector of this chunk within the row
+      const int c0 = r_lo + pch * kCV;  // first vector of this chunk within the row
       const int cnv = r_hi > r_lo ? min(kCV, r_hi - c0) : 0;
-      const bool own_tok = ch == r_tch && (r_tvl % kNCT) == tid;
+      const bool own_tok = pch == r_tch && (r_tvl % kNCT) == tid;
       if (kind == K_F) {
         if (ch == 0) s = MR{-INFINITY, 0.f};
         if (cnv == kCV) {  // full chunk: no predication
@@ -1801,6 +1878,9 @@ static void base_args(LossArgs& a, const void* logits, int64_t B, int64_t T, int
   a.vp_parts = nullptr;
   a.tok_off = 0;
   a.V_total = V;
+  a.put = VpPut{};
+  a.vp_flags = nullptr;
+  a.vp_epoch = 0;
 }
 
 odpo_status odpo_seq_logprobs(const void* logits, odpo_dtype dt, int64_t B, int64_t T, int64_t V,
@@ -2214,6 +2294,43 @@ odpo_status odpo_vp_row_partials(const void* logits_shard, odpo_dtype dt, int64_
   return launch_engine(dt == ODPO_F32 ? 0 : 1, M_SEQ, kPolyDefault, a, 0, s, -1);
 }
 
+odpo_status odpo_vp_row_partials_put(const void* logits_shard, odpo_dtype dt, int64_t B,
+                                     int64_t T, int64_t V_shard, int64_t stride_b,
+                                     int64_t stride_t, int64_t v0, int64_t V_total,
+                                     const int32_t* tokens, const uint8_t* mask,
+                                     float inv_temperature, float* const* peer_parts,
+                                     uint32_t* const* peer_flags, uint32_t* done, int32_t rank,
+                                     int32_t W, uint32_t epoch, uint32_t* status, void* stream) {
+  odpo_status e = check_logits(logits_shard, dt, B, T, V_shard, stride_b, stride_t);
+  if (e != ODPO_OK) return e;
+  if (!tokens || !mask || !peer_parts || !peer_flags || !done || !finite_pos(inv_temperature))
+    return ODPO_ERR_INVALID_ARG;
+  if (W < 1 || W > kVpMaxW || rank < 0 || rank >= W) return ODPO_ERR_INVALID_ARG;
+  if (v0 < 0 || V_total < v0 + V_shard) return ODPO_ERR_INVALID_ARG;
+  LossArgs a;
+  Workspace w{};
+  base_args(a, logits_shard, B, T, V_shard, stride_b, stride_t, tokens, mask, inv_temperature,
+            status, w, dt == ODPO_F32 ? 4 : 2);
+  for (int q = 0; q < W; ++q) {
+    if (!peer_parts[q] || !peer_flags[q]) return ODPO_ERR_INVALID_ARG;
+    if (((uintptr_t)peer_parts[q] & 15u) != 0) return ODPO_ERR_ALIGNMENT;
+    a.put.parts[q] = reinterpret_cast<float4*>(peer_parts[q]);
+    a.put.flags[q] = peer_flags[q];
+  }
+  a.put.done = done;
+  a.put.rank = rank;
+  a.put.W = W;
+  a.put.epoch = epoch;
+  a.tok_off = v0;
+  a.V_total = V_total;
+  const int64_t rows = B * T;
+  const unsigned grid = (unsigned)((rows + kWarpRowsPerCta - 1) / kWarpRowsPerCta);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dt == ODPO_F32) k_vp_partials_warp<0><<<grid, 32 * kWarpRowsPerCta, 0, s>>>(a);
+  else k_vp_partials_warp<1><<<grid, 32 * kWarpRowsPerCta, 0, s>>>(a);
+  return launched();
+}
+
 odpo_status odpo_vp_loss_fwd_bwd(const float* parts_all, int32_t W, const void* logits_shard,
                                  odpo_dtype dt, int64_t B, int64_t T, int64_t V_shard,
                                  int64_t stride_b, int64_t stride_t, int64_t v0, int64_t V_total,
@@ -2222,9 +2339,9 @@ odpo_status odpo_vp_loss_fwd_bwd(const float* parts_all, int32_t W, const void* 
                                  int64_t P_global, float beta, float inv_temperature,
                                  void* dlogits_shard, int64_t dstride_b, int64_t dstride_t,
                                  float* seq_logp, float* pair_logit, double* stats,
-                                 uint32_t* status, void* workspace, size_t workspace_bytes,
-                                 void* stream) {
-  if (!parts_all || W < 1) return ODPO_ERR_INVALID_ARG;
+                                 const uint32_t* flags, uint32_t epoch, uint32_t* status,
+                                 void* workspace, size_t workspace_bytes, void* stream) {
+  if (!parts_all || W < 1 || W > (flags ? kVpMaxW : 1 << 20)) return ODPO_ERR_INVALID_ARG;
   if (v0 < 0 || V_total < v0 + V_shard) return ODPO_ERR_INVALID_ARG;
   odpo_status e = check_loss(logits_shard, dt, B, T, V_shard, stride_b, stride_t, ref_logp, tokens,
                              mask, pair_rows, P, P_global, beta, inv_temperature, dlogits_shard,
@@ -2243,6 +2360,8 @@ odpo_status odpo_vp_loss_fwd_bwd(const float* parts_all, int32_t W, const void* 
   a.seq_logp = seq_logp; a.z_out = pair_logit; a.stats = stats;
   a.tok_off = v0;
   a.V_total = V_total;
+  a.vp_flags = flags;
+  a.vp_epoch = epoch;
   k_prep<<<1, kPrepThreads, 0, s>>>(pair_rows, B, P, w, status, B * T);
   if ((e = launched()) != ODPO_OK) return e;
   const int64_t rows = B * T;

@@ -18,7 +18,6 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
-#include <dlfcn.h>
 #include <math.h>
 #include <stdint.h>
 #include <stdlib.h>
@@ -113,6 +112,8 @@ struct Args {
   const float* row_scale; // [R] coef_b * mask (d loss / d logits = row_scale * G)
   __nv_bfloat16* gout;   // [R][ldg]
   int64_t ldg;
+  __nv_bfloat16* gout_t;  // optional G^T [V][ldgt] (the K-major A operand of dweight = G^T H)
+  int64_t ldgt;
 };
 
 __device__ __forceinline__ void tile_coords(const Args& a, int64_t t, int64_t& rb, int64_t& n) {
@@ -325,8 +326,10 @@ __global__ void __launch_bounds__(THREADS, 1)
                   Args a) {
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full[STAGES2], empty[STAGES2], tfull[2], tempty[2];
-  // GRAD epilogue: per epilogue warp a 32-row x 64-byte staging tile (rows padded to 80 B)
+  // GRAD epilogue: per epilogue warp a 32-row x 64-byte staging tile (rows padded to 80 B), and
+  // its transpose (32 columns x 32 rows, columns padded to 80 B) for G^T
   __shared__ __align__(16) uint4 gstage[4][GRAD ? 32 * 5 : 1];
+  __shared__ __align__(16) unsigned short gstageT[4][GRAD ? 32 * 40 : 1];
   __shared__ uint32_t tmem_sh;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
@@ -451,6 +454,32 @@ __global__ void __launch_bounds__(THREADS, 1)
             if (g_rs == 0.f) g0 = g1 = 0.f;  // 0 * inf: a masked row's lse is not its own
             w[j / 2] = pack_bf16x2(g0, g1);
           }
+          if (a.gout_t) {
+            // G^T[v][row]: each lane writes its row's 32 values down a column of the transposed
+            // staging tile, then lane j stores column j's 32 rows (64 contiguous bytes)
+            unsigned short* stT = gstageT[q];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              stT[(2 * j) * 40 + lane] = (unsigned short)(w[j] & 0xFFFFu);
+              stT[(2 * j + 1) * 40 + lane] = (unsigned short)(w[j] >> 16);
+            }
+            __syncwarp();
+            const int64_t row0 = rb2 * 256 + rank * 128 + 32 * q;
+            const int64_t v = cb + lane;
+            if (v < a.V && row0 < a.R) {
+              const uint4* src = reinterpret_cast<const uint4*>(stT + lane * 40);
+              __nv_bfloat16* dst = a.gout_t + v * a.ldgt + row0;
+              if (row0 + 32 <= a.ldgt) {
+                uint4* d4 = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) d4[k] = src[k];
+              } else {
+                for (int k = 0; k < 32 && row0 + k < a.R; ++k)
+                  reinterpret_cast<unsigned short*>(dst)[k] = stT[lane * 40 + k];
+              }
+            }
+            __syncwarp();
+          }
           if (cb + 32 <= a.V) {
             // stage the warp's 32 rows x 64 B, then store row-contiguous: each store
             // instruction writes 64 B to each of 8 rows instead of 16 B to each of 32
@@ -506,6 +535,216 @@ __global__ void __launch_bounds__(THREADS, 1)
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS)
                  : "memory");
+  }
+}
+
+// ---------------------------------------------------------------- K6d: TN GEMM on CTA pairs
+// The two backward GEMMs of NEXT-2 (dhidden = G W, dweight = G^T H) as one hand-written kernel:
+//   C[M, N] (fp32, row-major, ldc) = (acc ? C : 0) + A[M, K] B[N, K]^T,   A, B bf16 K-major.
+// Same machinery as k_lmhead_fwd2: thread-block clusters of 2 CTAs, tcgen05.mma.cta_group::2
+// (M = 256 across the pair, N = 256, K = 16), operands staged by 2-D TMA (128-byte swizzle) into a
+// 6-stage ring, fp32 accumulators double-buffered in TMEM; the epilogue warps drain each
+// accumulator with tcgen05.ld (one row per thread), stage 32 x 32 blocks in shared memory and
+// store (or add into) C row-contiguously.  Every output element is written by exactly one
+// thread in a fixed K order: deterministic, no atomics.  M/N/K tails: TMA zero-fills the
+// out-of-range parts of a box; stores are masked.
+struct GemmArgs {
+  int64_t M, N, K;
+  float* C;
+  int64_t ldc;
+  int64_t nmb2, nnb;  // 256-row blocks (one per CTA pair), 256-column blocks
+  int G;              // row blocks per raster group
+  int acc;            // 1: C += A B^T
+};
+
+__device__ __forceinline__ void gemm_coords(const GemmArgs& g, int64_t t, int64_t& mb, int64_t& nb) {
+  const int64_t grp = t / ((int64_t)g.G * g.nnb);
+  const int64_t r0 = grp * g.G;
+  const int64_t gg = min((int64_t)g.G, g.nmb2 - r0);
+  const int64_t idx = t - grp * (int64_t)g.G * g.nnb;
+  nb = idx / gg;
+  mb = r0 + idx % gg;
+}
+
+constexpr int kCPitch = 36;  // staging row pitch (floats): 16-byte rows, conflict-free float4 use
+
+__global__ void __launch_bounds__(THREADS, 1)
+    k_gemm_tn2(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+               GemmArgs g) {
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t full[STAGES2], empty[STAGES2], tfull[2], tempty[2];
+  __shared__ __align__(16) float cstage[4][32 * kCPitch];
+  __shared__ uint32_t tmem_sh;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES2; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], 8);
+    }
+    mbar_fence_init();
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&mapA) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&mapB) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&tmem_sh)),
+                 "n"(TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cluster_sync_all();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = tmem_sh;
+  const uint32_t full_s = smem_u32(full), empty_s = smem_u32(empty);
+  const uint32_t tfull_s = smem_u32(tfull), tempty_s = smem_u32(tempty);
+  const int nkb = (int)((g.K + BK - 1) / BK);
+  const int64_t cl = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  const int64_t Tt = g.nmb2 * g.nnb;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int st = 0;
+      uint32_t ph = 0;
+      for (int64_t t = cl; t < Tt; t += ncl) {
+        int64_t mb, nb;
+        gemm_coords(g, t, mb, nb);
+        const int arow = (int)(mb * 256 + rank * 128);
+        const int brow = (int)(nb * BN + rank * (BN / 2));
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(empty_s + 8 * st, ph ^ 1u);
+          const uint32_t sa = base + (uint32_t)(st * STAGE2_BYTES);
+          const uint32_t fb = (full_s + 8 * st) & kPeerMask;
+          if (leader) mbar_arrive_tx(full_s + 8 * st, 2 * STAGE2_BYTES);
+          tma_2d_pair(sa, &mapA, kb * BK, arow, fb);
+          tma_2d_pair(sa + A_BYTES, &mapB, kb * BK, brow, fb);
+          if (++st == STAGES2) { st = 0; ph ^= 1u; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && leader) {
+      int st = 0;
+      uint32_t ph = 0;
+      int acc = 0;
+      uint32_t aph = 0;
+      for (int64_t t = cl; t < Tt; t += ncl) {
+        mbar_wait(tempty_s + 8 * acc, aph ^ 1u);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t td = tmem + (uint32_t)(acc * BN);
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(full_s + 8 * st, ph);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t sa = base + (uint32_t)(st * STAGE2_BYTES);
+          const uint64_t da = sdesc(sa), db = sdesc(sa + A_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / UK; ++k)
+            mma_bf16_pair(td, da + (uint64_t)(2 * k), db + (uint64_t)(2 * k), (kb | k) != 0);
+          mma_commit_pair(empty_s + 8 * st);
+          if (++st == STAGES2) { st = 0; ph ^= 1u; }
+        }
+        mma_commit_pair(tfull_s + 8 * acc);
+        if (++acc == 2) { acc = 0; aph ^= 1u; }
+      }
+    }
+  } else {
+    const int q = warp & 3;
+    const uint32_t lane_base = (uint32_t)(32 * q) << 16;
+    const uint32_t tempty_leader = mapa(tempty_s, 0);
+    float* stg = cstage[q];
+    int acc = 0;
+    uint32_t aph = 0;
+    for (int64_t t = cl; t < Tt; t += ncl) {
+      int64_t mb, nb;
+      gemm_coords(g, t, mb, nb);
+      const int64_t row0 = mb * 256 + rank * 128 + 32 * q;
+      mbar_wait(tfull_s + 8 * acc, aph);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t r[32];
+        tm_ld32(tmem + lane_base + (uint32_t)(acc * BN + c * 32), r);
+        const int64_t cb = nb * BN + 32 * c;
+        if (cb >= g.N) break;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          *reinterpret_cast<float4*>(stg + lane * kCPitch + 4 * k) =
+              make_float4(__uint_as_float(r[4 * k]), __uint_as_float(r[4 * k + 1]),
+                          __uint_as_float(r[4 * k + 2]), __uint_as_float(r[4 * k + 3]));
+        __syncwarp();
+        const int sg = lane & 7;
+        const int64_t col = cb + 4 * sg;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {  // 8 lanes x 16 B per row: 4 rows per pass
+          const int rr = 4 * k + (lane >> 3);
+          const int64_t row = row0 + rr;
+          if (row < g.M && col < g.N) {
+            float4 v = *reinterpret_cast<const float4*>(stg + rr * kCPitch + 4 * sg);
+            float* dst = g.C + row * g.ldc + col;
+            if (col + 4 <= g.N) {
+              if (g.acc) {
+                const float4 o = *reinterpret_cast<const float4*>(dst);
+                v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
+              }
+              *reinterpret_cast<float4*>(dst) = v;
+            } else {
+              const float vv[4] = {v.x, v.y, v.z, v.w};
+              for (int e = 0; col + e < g.N; ++e) dst[e] = g.acc ? dst[e] + vv[e] : vv[e];
+            }
+          }
+        }
+        __syncwarp();
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cl(tempty_leader + 8 * acc);
+      if (++acc == 2) { acc = 0; aph ^= 1u; }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cluster_sync_all();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS)
+                 : "memory");
+  }
+}
+
+// bf16 transpose dst[c][r] = src[r][c] (64 x 64 tiles; the K-major copies of W and of a hidden
+// chunk that the backward GEMMs consume).  Columns beyond `cols` / rows beyond `rows` are not
+// touched; dst rows are ldd elements apart.
+__global__ void __launch_bounds__(256) k_transpose_bf16(const unsigned short* __restrict__ src,
+                                                         int64_t rows, int64_t cols, int64_t lds,
+                                                         unsigned short* __restrict__ dst,
+                                                         int64_t ldd) {
+  __shared__ unsigned short tile[64][66];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int64_t r0 = (int64_t)blockIdx.y * 64, c0 = (int64_t)blockIdx.x * 64;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int r = ty + 8 * i;
+    const int64_t gr = r0 + r, gc = c0 + 2 * tx;
+    unsigned short a0 = 0, a1 = 0;
+    if (gr < rows && gc < cols) a0 = src[gr * lds + gc];
+    if (gr < rows && gc + 1 < cols) a1 = src[gr * lds + gc + 1];
+    tile[r][2 * tx] = a0;
+    tile[r][2 * tx + 1] = a1;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int c = ty + 8 * i;
+    const int64_t gc = c0 + c, gr = r0 + 2 * tx;
+    if (gc >= cols) continue;
+    if (gr < rows) dst[gc * ldd + gr] = tile[2 * tx][c];
+    if (gr + 1 < rows) dst[gc * ldd + gr + 1] = tile[2 * tx + 1][c];
   }
 }
 
@@ -602,42 +841,11 @@ constexpr bool kLmhPair = ODPO_LMH_1CTA == 0;
 #ifndef ODPO_LMH_G
 #define ODPO_LMH_G 64
 #endif
-constexpr int kRasterG = ODPO_LMH_G;  // row blocks per raster group (tuned: 8/16/32/64 -> 1636/1723/1751/1802 TF/s)
-
-// ---------------------------------------------------------------- cuBLAS (plain GEMMs), loaded at
-// run time so that libodpo.so has no load-time dependency on it (the process -- e.g. torch --
-// normally has libcublas.so.12 loaded already)
-struct Blas {
-  typedef int (*Create)(void**);
-  typedef int (*SetStream)(void*, cudaStream_t);
-  typedef int (*GemmEx)(void*, int, int, int, int, int, const void*, const void*, int, int,
-                        const void*, int, int, const void*, void*, int, int, int, int);
-  Create create = nullptr;
-  SetStream set_stream = nullptr;
-  GemmEx gemm = nullptr;
-  void* handle[128] = {};
-  std::mutex mu;       // guards load / handle creation
-  std::mutex call_mu;  // held by a call across cublasSetStream and its GEMMs
-  bool load() {
-    if (gemm) return true;
-    void* h = dlopen("libcublas.so.12", RTLD_NOW | RTLD_GLOBAL);
-    if (!h) h = dlopen("/usr/local/cuda/lib64/libcublas.so.12", RTLD_NOW | RTLD_GLOBAL);
-    if (!h) return false;
-    create = (Create)dlsym(h, "cublasCreate_v2");
-    set_stream = (SetStream)dlsym(h, "cublasSetStream_v2");
-    gemm = (GemmEx)dlsym(h, "cublasGemmEx");
-    return create && set_stream && gemm;
-  }
-  void* get(int dev) {
-    std::lock_guard<std::mutex> g(mu);
-    if (!load() || dev < 0 || dev >= 128) return nullptr;
-    if (!handle[dev] && create(&handle[dev]) != 0) handle[dev] = nullptr;
-    return handle[dev];
-  }
-};
-static Blas g_blas;
-// cuBLAS enum values (cublas_api.h / library_types.h)
-constexpr int kOpN = 0, kOpT = 1, kR16BF = 14, kR32F = 0, kCompute32F = 68, kGemmDefault = -1;
+constexpr int kRasterG = ODPO_LMH_G;
+#ifndef ODPO_GEMM_G
+#define ODPO_GEMM_G 16
+#endif
+constexpr int kGemmG = ODPO_GEMM_G;   // backward GEMMs: 256-row blocks per raster group  // row blocks per raster group (tuned: 8/16/32/64 -> 1636/1723/1751/1802 TF/s)
 
 }  // namespace lmh
 }  // namespace odpo
@@ -725,10 +933,64 @@ odpo_status odpo_lmhead_seq_logprobs(const void* hidden, const void* weight, int
   return cudaGetLastError() == cudaSuccess ? ODPO_OK : ODPO_ERR_CUDA;
 }
 
-size_t odpo_lmhead_grad_scratch_bytes(int64_t chunk_rows, int64_t V) {
-  if (chunk_rows <= 0 || V <= 0) return 0;
-  const int64_t ldg = (V + 7) / 8 * 8;
-  return (size_t)chunk_rows * (size_t)ldg * 2;
+// Scratch of odpo_lmhead_grad: W^T [d][Vp], G [CR][Vp], G^T [V][CR], H^T [d][CR] (bf16), where
+// CR = chunk_rows rounded up to 256 and Vp = V rounded up to 8 (16-byte rows for TMA).
+static size_t grad_layout(int64_t chunk_rows, int64_t d, int64_t V, char* base, char** wt,
+                          char** gm, char** gt, char** ht) {
+  const int64_t CR = (chunk_rows + 255) / 256 * 256;
+  const int64_t Vp = (V + 7) / 8 * 8;
+  auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+  size_t off = 0;
+  auto take = [&](size_t n, char** p) {
+    if (p) *p = base + off;
+    off += al(n);
+  };
+  take((size_t)d * Vp * 2, wt);
+  take((size_t)CR * Vp * 2, gm);
+  take((size_t)V * CR * 2, gt);
+  take((size_t)d * CR * 2, ht);
+  return off + 256;
+}
+
+size_t odpo_lmhead_grad_scratch_bytes(int64_t chunk_rows, int64_t d, int64_t V) {
+  if (chunk_rows <= 0 || d <= 0 || V <= 0) return 0;
+  return grad_layout(chunk_rows, d, V, nullptr, nullptr, nullptr, nullptr, nullptr);
+}
+
+static void launch_pair(const void* kern, int clusters, cudaStream_t s, void** args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(2 * clusters));
+  cfg.blockDim = dim3(THREADS);
+  cfg.dynamicSmemBytes = SMEM2;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelExC(&cfg, kern, args);
+}
+
+// C (+)= A B^T on the CTA-pair tcgen05 kernel (A [M, K], B [N, K], bf16 K-major with row pitches
+// lda / ldb elements).
+static odpo_status gemm_tn(const void* A, int64_t lda, const void* B, int64_t ldb, int64_t M,
+                           int64_t N, int64_t K, float* C, int64_t ldc, bool acc, int sms,
+                           cudaStream_t s) {
+  CUtensorMap mA, mB;
+  if (!make_map(&mA, A, M, K, lda, BM) || !make_map(&mB, B, N, K, ldb, BN / 2)) return ODPO_ERR_CUDA;
+  GemmArgs g{};
+  g.M = M; g.N = N; g.K = K; g.C = C; g.ldc = ldc;
+  g.nmb2 = (M + 255) / 256;
+  g.nnb = (N + BN - 1) / BN;
+  g.G = kGemmG;
+  g.acc = acc ? 1 : 0;
+  int clusters = sms / 2;
+  if (clusters > g.nmb2 * g.nnb) clusters = (int)(g.nmb2 * g.nnb);
+  void* args[] = {&mA, &mB, &g};
+  launch_pair((const void*)k_gemm_tn2, clusters, s, args);
+  return cudaGetLastError() == cudaSuccess ? ODPO_OK : ODPO_ERR_CUDA;
 }
 
 odpo_status odpo_lmhead_grad(const void* hidden, const void* weight, int64_t R, int64_t d,
@@ -742,35 +1004,39 @@ odpo_status odpo_lmhead_grad(const void* hidden, const void* weight, int64_t R, 
   if (!(isfinite(inv_temperature) && inv_temperature > 0.f)) return ODPO_ERR_INVALID_ARG;
   if (d % BK) return ODPO_ERR_UNSUPPORTED;
   if (R > (int64_t)INT32_MAX || V > (int64_t)INT32_MAX || d > (1 << 20)) return ODPO_ERR_UNSUPPORTED;
-  if (((uintptr_t)hidden & 15u) || ((uintptr_t)weight & 15u) || ((uintptr_t)scratch & 15u))
+  if (((uintptr_t)hidden & 15u) || ((uintptr_t)weight & 15u) || ((uintptr_t)scratch & 255u) ||
+      ((uintptr_t)dhidden & 15u) || ((uintptr_t)dweight & 15u))
     return ODPO_ERR_ALIGNMENT;
   if (chunk_rows > R) chunk_rows = R;
-  chunk_rows = (chunk_rows + 255) / 256 * 256;  // whole CTA-pair row blocks
-  if (!scratch || scratch_bytes < odpo_lmhead_grad_scratch_bytes(chunk_rows, V))
+  const int64_t CR = (chunk_rows + 255) / 256 * 256;  // whole CTA-pair row blocks
+  if (!scratch || scratch_bytes < odpo_lmhead_grad_scratch_bytes(CR, d, V))
     return ODPO_ERR_WORKSPACE;
   int dev = 0;
   cudaGetDevice(&dev);
-  void* blas = g_blas.get(dev);
-  if (!blas) return ODPO_ERR_UNSUPPORTED;  // cuBLAS not loadable
   static std::once_flag attr_once[128];
   if (dev < 0 || dev >= 128) return ODPO_ERR_UNSUPPORTED;
   std::call_once(attr_once[dev], []() {
     cudaFuncSetAttribute(k_lmhead_fwd2<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2);
+    cudaFuncSetAttribute(k_gemm_tn2, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2);
   });
   cudaStream_t s = (cudaStream_t)stream;
-  // one handle per device: hold its lock from set_stream to the last GEMM enqueued, so calls
-  // from other host threads / streams cannot retarget it in between
-  std::lock_guard<std::mutex> blas_lock(g_blas.call_mu);
-  if (g_blas.set_stream(blas, s) != 0) return ODPO_ERR_CUDA;
+  char *wt, *gm, *gt, *ht;
+  grad_layout(CR, d, V, (char*)scratch, &wt, &gm, &gt, &ht);
+  const int64_t Vp = (V + 7) / 8 * 8;
+  const int sms = sm_count();
+  // W^T [d][Vp]: the K-major (K = V) B operand of dhidden = G W
+  k_transpose_bf16<<<dim3((unsigned)((d + 63) / 64), (unsigned)((V + 63) / 64)), 256, 0, s>>>(
+      reinterpret_cast<const unsigned short*>(weight), V, d, d,
+      reinterpret_cast<unsigned short*>(wt), Vp);
   CUtensorMap mB;
   if (!make_map(&mB, weight, V, d, d, BN / 2)) return ODPO_ERR_CUDA;
-  const int sms = sm_count();
-  const int64_t ldg = (V + 7) / 8 * 8;
-  __nv_bfloat16* G = reinterpret_cast<__nv_bfloat16*>(scratch);
-  const float one = 1.f, zero = 0.f;
-  for (int64_t r0 = 0; r0 < R; r0 += chunk_rows) {
-    const int64_t Rc = min(chunk_rows, R - r0);
+  for (int64_t r0 = 0; r0 < R; r0 += CR) {
+    const int64_t Rc = min(CR, R - r0);
     const char* hc = reinterpret_cast<const char*>(hidden) + r0 * d * 2;
+    // H^T chunk [d][CR]: the K-major (K = rows) B operand of dweight = G^T H
+    k_transpose_bf16<<<dim3((unsigned)((d + 63) / 64), (unsigned)((Rc + 63) / 64)), 256, 0, s>>>(
+        reinterpret_cast<const unsigned short*>(hc), Rc, d, d,
+        reinterpret_cast<unsigned short*>(ht), CR);
     CUtensorMap mA;
     if (!make_map(&mA, hc, Rc, d, d, BM)) return ODPO_ERR_CUDA;
     Args a{};
@@ -784,34 +1050,21 @@ odpo_status odpo_lmhead_grad(const void* hidden, const void* weight, int64_t R, 
     a.tokens = tokens + r0;
     a.row_lse = row_lse + r0;
     a.row_scale = row_scale + r0;
-    a.gout = G;
-    a.ldg = ldg;
+    a.gout = reinterpret_cast<__nv_bfloat16*>(gm);
+    a.ldg = Vp;
+    a.gout_t = reinterpret_cast<__nv_bfloat16*>(gt);
+    a.ldgt = CR;
     int clusters = sms / 2;
     if (clusters > a.nrb2 * a.NT) clusters = (int)(a.nrb2 * a.NT);
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)(2 * clusters));
-    cfg.blockDim = dim3(THREADS);
-    cfg.dynamicSmemBytes = SMEM2;
-    cfg.stream = s;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = 2;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, k_lmhead_fwd2<true>, mA, mB, a);
+    void* args[] = {&mA, &mB, &a};
+    launch_pair((const void*)k_lmhead_fwd2<true>, clusters, s, args);
     if (cudaGetLastError() != cudaSuccess) return ODPO_ERR_CUDA;
-    // dH[r0:r0+Rc] = G W   (column-major: dH^T[d, Rc] = W^T[d, V] G^T[V, Rc])
-    if (g_blas.gemm(blas, kOpN, kOpN, (int)d, (int)Rc, (int)V, &one, weight, kR16BF, (int)d, G,
-                    kR16BF, (int)ldg, &zero, dhidden + r0 * d, kR32F, (int)d, kCompute32F,
-                    kGemmDefault) != 0)
-      return ODPO_ERR_CUDA;
-    // dW (+)= G^T H         (column-major: dW^T[d, V] (+)= H^T[d, Rc] G[Rc, V])
-    if (g_blas.gemm(blas, kOpN, kOpT, (int)d, (int)V, (int)Rc, &one, hc, kR16BF, (int)d, G,
-                    kR16BF, (int)ldg, r0 == 0 ? &zero : &one, dweight, kR32F, (int)d, kCompute32F,
-                    kGemmDefault) != 0)
-      return ODPO_ERR_CUDA;
+    // dhidden[r0 : r0 + Rc] = G W = G (W^T)^T          (M = Rc, N = d, K = V)
+    odpo_status e = gemm_tn(gm, Vp, wt, Vp, Rc, d, V, dhidden + r0 * d, d, false, sms, s);
+    if (e != ODPO_OK) return e;
+    // dweight (+)= G^T H = (G^T) (H^T)^T                 (M = V, N = d, K = Rc)
+    e = gemm_tn(gt, CR, ht, CR, V, d, Rc, dweight, d, r0 > 0, sms, s);
+    if (e != ODPO_OK) return e;
   }
   return ODPO_OK;
 }

@@ -2,7 +2,12 @@
 """Summarise an ncu launch list (--metrics gpu__time_duration.sum CSV) and a --set full
 report into a committed markdown file + a traffic JSON the bench reads.
 
-usage: python profiles/summarize_ncu.py TAG CONFIG [launches.csv] [prof.ncu-rep]
+usage: python profiles/summarize_ncu.py TAG CONFIG FORM [launches.csv] [prof.ncu-rep]
+
+Writes profiles/r02/ncu/TAG_ncu_summary.md and, from the --set full report, the evidence file
+profiles/r02/ncu/traffic_CONFIG_FORM.json (DRAM bytes, MUFU / issue / SM-clock figures of the
+dominant kernel) stamped with bench.src_sha() of the sources it was captured on: bench.py uses
+it as `roofline.traffic` only while the kernel sources are unchanged.
 """
 import csv
 import io
@@ -70,9 +75,11 @@ def full(path):
 
 
 def main():
-    tag, cfg = sys.argv[1], sys.argv[2]
-    lpath = sys.argv[3] if len(sys.argv) > 3 else None
-    ppath = sys.argv[4] if len(sys.argv) > 4 else None
+    tag, cfg, form = sys.argv[1], sys.argv[2], sys.argv[3]
+    lpath = sys.argv[4] if len(sys.argv) > 4 else None
+    ppath = sys.argv[5] if len(sys.argv) > 5 else None
+    outdir = os.path.join(HERE, "r02", "ncu")
+    os.makedirs(outdir, exist_ok=True)
     md = [f"# ncu summary {tag} ({cfg})", ""]
     if lpath and os.path.exists(lpath):
         agg = launches(lpath)
@@ -94,14 +101,33 @@ def main():
                 rb = to_bytes(*d["dram__bytes_read.sum"])
                 wb = to_bytes(*d["dram__bytes_write.sum"])
                 md.append(f"- DRAM traffic per launch: {(rb + wb) / 1e9:.3f} GB")
-                traffic.setdefault(d["kernel"].split("(")[0], []).append(rb + wb)
+                traffic.setdefault(d["kernel"].split("(")[0], []).append((rb + wb, d))
             md.append("")
-    open(os.path.join(HERE, f"{tag}_ncu_summary.md"), "w").write("\n".join(md) + "\n")
+    open(os.path.join(outdir, f"{tag}_ncu_summary.md"), "w").write("\n".join(md) + "\n")
     if traffic:
-        main_k = max(traffic, key=lambda k: sum(traffic[k]) / len(traffic[k]))
+        sys.path.insert(0, os.path.dirname(HERE))
+        import bench
+        main_k = max(traffic, key=lambda k: sum(t for t, _ in traffic[k]) / len(traffic[k]))
         v = traffic[main_k]
-        json.dump({"kernel": main_k, "dram_bytes_per_launch": sum(v) / len(v), "tag": tag},
-                  open(os.path.join(HERE, f"ncu_traffic_{cfg}.json"), "w"), indent=1)
+        d = v[0][1]
+
+        def num(key, scale=1.0):
+            return float(d[key][0].replace(",", "")) * scale if key in d else None
+        ev = {"kernel": main_k, "dram_bytes_per_launch": sum(t for t, _ in v) / len(v),
+              "dram_read_bytes": to_bytes(*d["dram__bytes_read.sum"]),
+              "dram_write_bytes": to_bytes(*d["dram__bytes_write.sum"]),
+              "duration_ms": num("gpu__time_duration.sum") / 1e6
+              if d.get("gpu__time_duration.sum", ("", ""))[1] == "nsecond"
+              else num("gpu__time_duration.sum") if d.get("gpu__time_duration.sum", ("", ""))[1] == "msecond"
+              else None,
+              "mufu_pipe_pct": num("sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active"),
+              "issue_active_pct": num("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+              "dram_pct_of_peak": num("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
+              "l2_hit_pct": num("lts__t_sector_hit_rate.pct"),
+              "sm_clock": " ".join(d.get("sm__cycles_elapsed.avg.per_second", ("", ""))),
+              "tag": tag, "src_sha": bench.src_sha(),
+              "how": "ncu --set full --clock-control none (one launch, cold cache)"}
+        json.dump(ev, open(os.path.join(outdir, f"traffic_{cfg}_{form}.json"), "w"), indent=1)
     print("\n".join(md))
 
 

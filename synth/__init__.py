@@ -165,6 +165,8 @@ def _dev_lib():
                                         _C.c_int64, _C.c_int64, _C.c_uint64, _C.c_int, _C.c_int64,
                                         _C.c_void_p, _C.c_float, _C.c_int, _C.c_void_p]
         L.synth_fill_logits.restype = _C.c_int
+        L.synth_read_probe.argtypes = [_C.c_void_p, _C.c_int64, _C.c_void_p, _C.c_int, _C.c_void_p]
+        L.synth_read_probe.restype = _C.c_int
         L.synth_stream_key.argtypes = [_C.c_uint64, _C.c_int]
         L.synth_stream_key.restype = _C.c_uint64
         _slib = L
@@ -189,6 +191,16 @@ def fill_logits_device(x, seed: int, row0: int = 0, tokens=None, peak: float | N
         1 if tk is not None else 0, torch.cuda.current_stream().cuda_stream)
     if rc:
         raise RuntimeError(f"synth_fill_logits failed ({rc})")
+
+
+def read_probe(x, blocks: int) -> None:
+    """bench.py ceiling probe: stream x's bytes once (read only) on the current stream."""
+    import torch
+    out = torch.zeros(1, dtype=torch.int32, device=x.device)
+    rc = _dev_lib().synth_read_probe(x.data_ptr(), x.numel() * x.element_size(), out.data_ptr(),
+                                     int(blocks), torch.cuda.current_stream().cuda_stream)
+    if rc:
+        raise RuntimeError(f"synth_read_probe failed ({rc})")
 
 
 def lmhead_inputs(seed: int, rows_global, d: int, V: int, v_rows=None):

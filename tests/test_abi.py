@@ -195,8 +195,11 @@ def test_lmhead_and_token_logp_argument_errors(lib):
 def test_lmhead_grad_argument_errors(lib):
     import paper_2410_18252_b200 as odpo
     L = odpo._L()
-    sb = L.odpo_lmhead_grad_scratch_bytes(256, 1000)
-    assert sb == 256 * 1000 * 2 and L.odpo_lmhead_grad_scratch_bytes(0, 10) == 0
+    sb = L.odpo_lmhead_grad_scratch_bytes(256, 128, 1000)
+    # W^T [d][Vp] + G [256][Vp] + G^T [V][256] + H^T [d][256], bf16, 256-byte aligned pieces
+    assert sb >= 2 * (128 * 1000 + 256 * 1000 + 1000 * 256 + 128 * 256)
+    assert sb <= 2 * (128 * 1000 + 256 * 1000 + 1000 * 256 + 128 * 256) + 5 * 256
+    assert L.odpo_lmhead_grad_scratch_bytes(0, 128, 10) == 0
 
     def grad(**kw):
         a = dict(h=FAKE, w=FAKE, R=100, d=128, V=1000, tok=FAKE, lse=FAKE, rs=FAKE, invT=1.0,
@@ -231,3 +234,37 @@ def test_library_has_no_environment_lookups():
         assert "getenv" not in src, f
     binding = open(os.path.join(ROOT, "paper_2410_18252_b200", "__init__.py")).read()
     assert "os.environ" not in binding
+
+
+def test_vp_put_argument_errors(lib):
+    """odpo_vp_row_partials_put: peer arrays required, 1 <= W <= 8, 0 <= rank < W."""
+    P = C.c_void_p
+
+    def call(W=2, rank=0, parts=True, flags=True, done=FAKE, mis=False):
+        pp = (P * 8)(*([FAKE_MIS if mis else FAKE] * 8)) if parts else None
+        ff = (P * 8)(*([FAKE] * 8)) if flags else None
+        return lib.odpo_vp_row_partials_put(FAKE, 1, 4, 3, 64, 192, 64, 0, 64, FAKE, FAKE, 1.0,
+                                            pp, ff, done, rank, W, 1, None, None)
+    import paper_2410_18252_b200  # noqa: F401  (argtypes registered by _L)
+    assert call(parts=False) == 1 and call(flags=False) == 1 and call(done=None) == 1
+    assert call(W=0) == 1 and call(W=9) == 1 and call(rank=2) == 1 and call(rank=-1) == 1
+    assert call(mis=True) == 2
+
+
+def test_vp_exchange_layout():
+    """VPExchange buffer layout (host arithmetic, no GPU): two epochs of [W][rows][4] f32
+    partials, then W flag words, then the CTA counter, all inside the buffer and disjoint."""
+    import torch
+    import paper_2410_18252_b200 as odpo
+    W, rows = 3, 10
+    bufs = [torch.zeros(odpo.VPExchange.nbytes(W, rows), dtype=torch.uint8) for _ in range(W)]
+    ex = odpo.VPExchange(rows, _bufs=bufs, _rank=1)
+    base = bufs[1].data_ptr()
+    assert ex._parts_ptr(1, 0) == base and ex._parts_ptr(1, 1) == base + W * rows * 16
+    assert ex._parts_ptr(1, 2) == ex._parts_ptr(1, 0)
+    assert ex._flags_ptr(1) == base + 2 * W * rows * 16
+    assert ex.done() == ex._flags_ptr(1) + 4 * W
+    assert ex.done() + 4 <= base + bufs[1].numel()
+    assert ex.parts(1).shape == (W, rows, 4) and ex.parts(1).data_ptr() == ex._parts_ptr(1, 1)
+    assert ex.flags().numel() == W and ex.flags().data_ptr() == ex._flags_ptr(1)
+    assert ex._parts_ptr(2, 1) == bufs[2].data_ptr() + W * rows * 16

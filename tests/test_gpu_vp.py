@@ -72,3 +72,112 @@ def test_vp_token_ownership_flags(odpo):
     odpo.vp_row_partials(b.d_logits[:, :, 0:2048], 0, 4096, tok, b.d_mask, status=st)
     torch.cuda.synchronize()
     assert int(st.item()) & odpo.FLAGS["TOKEN_RANGE"]
+
+
+# ------------------------------------------------------------------ in-kernel exchange
+def _vp_case(W, dt, seed=9):
+    P, T, V = 3, 9, 32000 if dt == "bf16" else 12345
+    b = Batch(P, T, V, dt, seed=seed, mask_kind="prefix", lbar=5, extra_seqs=1)
+    ref = (synth.rewards_for(seed, b.B, 1).reshape(-1) - 20.0).astype(np.float32)
+    align = 8 if dt == "bf16" else 4
+    return b, torch.from_numpy(ref).cuda(), shard_bounds(V, W, align)
+
+
+@pytest.mark.parametrize("W", [2, 3, 8])
+@pytest.mark.parametrize("dt", ["bf16", "f32"])
+def test_vp_in_kernel_exchange_matches_gather(odpo, W, dt):
+    """The partials exchanged INSIDE the kernels (odpo_vp_row_partials_put stores into every
+    rank's buffer and publishes the epoch; the merge waits on its flags) give the same bits as
+    the gathered path, for two consecutive epochs (both halves of the double buffer)."""
+    b, d_ref, bounds = _vp_case(W, dt)
+    P, rows = b.P, b.B * b.T
+    ex = odpo.VPExchange.emulate(W, rows)
+    for epoch in (1, 2, 3):
+        parts = torch.stack([odpo.vp_row_partials(b.d_logits[:, :, a:e], a, b.V, b.d_tokens, b.d_mask)
+                             for a, e in bounds])
+        for r, (a, e) in enumerate(bounds):   # every rank's put (one stream: all land first)
+            st = odpo.vp_row_partials_put(b.d_logits[:, :, a:e], a, b.V, b.d_tokens, b.d_mask,
+                                          ex[r], epoch)
+            assert int(st.item()) == 0
+        for r, (a, e) in enumerate(bounds):
+            assert torch.equal(ex[r].parts(epoch), parts)
+            assert ex[r].flags().tolist() == [epoch] * W
+            dl_g, dl_x = b.new_out(), b.new_out()
+            g = odpo.vp_loss_fwd_bwd(parts, b.d_logits[:, :, a:e], a, b.V, d_ref, b.d_tokens,
+                                     b.d_mask, 0.1, pair_rows=b.d_pair_rows, p_global=P + 1,
+                                     dlogits=dl_g[:, :, a:e])
+            x = odpo.vp_loss_fwd_bwd(ex[r].parts(epoch), b.d_logits[:, :, a:e], a, b.V, d_ref,
+                                     b.d_tokens, b.d_mask, 0.1, pair_rows=b.d_pair_rows,
+                                     p_global=P + 1, dlogits=dl_x[:, :, a:e],
+                                     flags=ex[r].flags(), epoch=epoch)
+            torch.cuda.synchronize()
+            assert torch.equal(g.stats[:10], x.stats[:10]) and torch.equal(g.z, x.z)
+            assert torch.equal(dl_g[:, :, a:e], dl_x[:, :, a:e])
+        for r in range(W):   # every rank's CTA counter is back at 0 after its put kernel
+            off = 2 * W * rows * 16 + 4 * W
+            assert int(ex[r].bufs[r][off:off + 4].view(torch.int32).item()) == 0
+
+
+def _vp_proc(rank, world, port, q):
+    import os
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import torch.distributed as dist
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2410_18252_b200 as odpo
+        torch.cuda.set_device(0)
+        b, d_ref, bounds = _vp_case(world, "bf16", seed=12)
+        a, e = bounds[rank]
+        ex = odpo.VPExchange(b.B * b.T)
+        res = []
+        for _ in range(3):
+            out = odpo.vp_loss_step(b.d_logits[:, :, a:e].contiguous(), a, b.V, d_ref, b.d_tokens,
+                                    b.d_mask, 0.1, exchange=ex, pair_rows=b.d_pair_rows,
+                                    p_global=b.P + 1)
+            torch.cuda.synchronize()
+            res.append((out.stats[:10].cpu(), out.dlogits.float().cpu(), int(out.status.item())))
+        # the unsharded loss on the full logits (the same process computes it for comparison)
+        full = odpo.online_dpo_loss_fwd_bwd(b.d_logits, d_ref, b.d_tokens, b.d_mask, 0.1,
+                                            pair_rows=b.d_pair_rows, p_global=b.P + 1)
+        torch.cuda.synchronize()
+        q.put((rank, res, full.stats[:10].cpu(), full.dlogits[:, :, a:e].float().cpu()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_vp_exchange_two_processes(odpo):
+    """World size 2 with real process boundaries: two ranks (processes) on this GPU exchange the
+    partials through each other's memory (CUDA IPC handles swapped over a gloo group), three
+    steps in a row; every step equals the unsharded loss (stats within fp32 rounding of the
+    merge, dlogits within one bf16 ulp) and the two ranks agree exactly on the global stats."""
+    import socket
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_vp_proc, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = {}
+    for _ in range(2):
+        r, res, fs, fdl = q.get(timeout=300)
+        got[r] = (res, fs, fdl)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for r in (0, 1):
+        res, fs, fdl = got[r]
+        for st, dl, status in res:
+            assert status == 0
+            assert torch.equal(st, res[0][0]) and torch.equal(dl, res[0][1])  # step-to-step
+            assert st[0] == fs[0] and st[8] == fs[8] and st[9] == fs[9]
+            assert torch.allclose(st, fs, rtol=1e-5, atol=1e-9)
+            assert torch.all((dl - fdl).abs() <= 2.0 ** -7 * fdl.abs() + 1e-12)
+    assert torch.equal(got[0][0][0][0], got[1][0][0][0])
