@@ -436,17 +436,18 @@ size_t odpo_lmhead_workspace_bytes(int64_t B, int64_t T, int64_t V);
  *   dweight     = G^T hidden        fp32 [V, d] (overwritten)
  *
  * The logits are recomputed chunk by chunk (chunk_rows rows at a time, rounded up to 256) by
- * the NEXT-2 tcgen05 kernel, whose epilogue writes G and its transpose G^T (bf16) into
- * `scratch` instead of reducing them; the two GEMMs with G run on the library's own tcgen05
- * CTA-pair GEMM (bf16 operands staged by TMA, fp32 accumulators in tensor memory; no cuBLAS):
- * dhidden = G (W^T)^T with a once-per-call W^T copy, dweight += (G^T) (H^T)^T with a per-chunk
- * H^T copy.  Deterministic: every output element is accumulated in a fixed order (chunks in
- * row order, K in order), no atomics.  row_lse is odpo_lmhead_seq_logprobs' row_lse (natural
- * log, invT applied).
+ * the NEXT-2 tcgen05 kernel, whose epilogue writes G (bf16) into `scratch` instead of reducing
+ * it; the two GEMMs with G run on the library's own tcgen05 CTA-pair GEMM (bf16 operands
+ * staged by TMA, fp32 accumulators in tensor memory; no cuBLAS): dhidden = G W reads W
+ * N-major and dweight += G^T H reads G M-major and H N-major straight from their stored
+ * layouts (MN-major shared-memory descriptors), so nothing is transposed or copied.
+ * Deterministic: every output element is accumulated in a fixed order (chunks in row order,
+ * K in order), no atomics.  row_lse is odpo_lmhead_seq_logprobs' row_lse (natural log, invT
+ * applied).
  *   hidden bf16 [R, d], weight bf16 [V, d] contiguous, 16-byte aligned, d % 64 == 0.
  *   dhidden, dweight fp32, 16-byte aligned.
- *   scratch >= odpo_lmhead_grad_scratch_bytes(chunk_rows, d, V) bytes, 256-byte aligned
- *   (W^T, G, G^T and H^T of one chunk: about 2 d V + 4 chunk_rows V bytes).
+ *   scratch >= odpo_lmhead_grad_scratch_bytes(chunk_rows, d, V) bytes (one chunk of G:
+ *   about 2 chunk_rows V bytes), 16-byte aligned.
  * Errors: INVALID_ARG, UNSUPPORTED (d % 64, sizes), ALIGNMENT, WORKSPACE, CUDA.
  */
 size_t odpo_lmhead_grad_scratch_bytes(int64_t chunk_rows, int64_t d, int64_t V);

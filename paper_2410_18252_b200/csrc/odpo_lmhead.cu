@@ -112,8 +112,6 @@ struct Args {
   const float* row_scale; // [R] coef_b * mask (d loss / d logits = row_scale * G)
   __nv_bfloat16* gout;   // [R][ldg]
   int64_t ldg;
-  __nv_bfloat16* gout_t;  // optional G^T [V][ldgt] (the K-major A operand of dweight = G^T H)
-  int64_t ldgt;
 };
 
 __device__ __forceinline__ void tile_coords(const Args& a, int64_t t, int64_t& rb, int64_t& n) {
@@ -326,10 +324,8 @@ __global__ void __launch_bounds__(THREADS, 1)
                   Args a) {
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full[STAGES2], empty[STAGES2], tfull[2], tempty[2];
-  // GRAD epilogue: per epilogue warp a 32-row x 64-byte staging tile (rows padded to 80 B), and
-  // its transpose (32 columns x 32 rows, columns padded to 80 B) for G^T
+  // GRAD epilogue: per epilogue warp a 32-row x 64-byte staging tile (rows padded to 80 B)
   __shared__ __align__(16) uint4 gstage[4][GRAD ? 32 * 5 : 1];
-  __shared__ __align__(16) unsigned short gstageT[4][GRAD ? 32 * 40 : 1];
   __shared__ uint32_t tmem_sh;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
@@ -430,8 +426,9 @@ __global__ void __launch_bounds__(THREADS, 1)
       float g_rs = 0.f, g_c = 0.f;
       if (GRAD && live) {
         g_rs = a.row_scale[row];
-        g_c = a.row_lse[row] * kLog2e;  // p = 2^(acc * invT * log2e - lse * log2e)
+        g_c = g_rs != 0.f ? a.row_lse[row] * kLog2e : INFINITY;  // p = 2^(acc invT log2e - lse log2e)
       }
+      if (GRAD && !live) g_c = INFINITY;
       mbar_wait(tfull_s + 8 * acc, aph);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const int64_t c0 = n * BN;
@@ -444,41 +441,28 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (GRAD) {
           // g_j = row_scale * p_j; at the sampled token row_scale * expm1(log p) (no p - 1
           // cancellation); rows with row_scale 0 (masked, unreferenced) get exact zeros
+          // two logits per FFMA2 / FMUL2; rows with row_scale 0 carry g_c = +inf (exact zeros,
+          // never 0 * inf: a masked row's lse is not its own)
           uint32_t w[16];
+          const f32x2 K2 = pk2(k2, k2), NC = pk2(-g_c, -g_c), RS = pk2(g_rs, g_rs);
 #pragma unroll
           for (int j = 0; j < 32; j += 2) {
-            float g0 = g_rs * ex2(fmaf(__uint_as_float(r[j]), k2, -g_c));
-            float g1 = g_rs * ex2(fmaf(__uint_as_float(r[j + 1]), k2, -g_c));
-            if (tok == cb + j) g0 = g_rs * expm1f(fmaf(__uint_as_float(r[j]), a.invT, -a.row_lse[row]));
-            if (tok == cb + j + 1) g1 = g_rs * expm1f(fmaf(__uint_as_float(r[j + 1]), a.invT, -a.row_lse[row]));
-            if (g_rs == 0.f) g0 = g1 = 0.f;  // 0 * inf: a masked row's lse is not its own
+            float e0, e1, g0, g1;
+            upk2(ffma2(pk2(__uint_as_float(r[j]), __uint_as_float(r[j + 1])), K2, NC), e0, e1);
+            upk2(fmul2(pk2(ex2(e0), ex2(e1)), RS), g0, g1);
             w[j / 2] = pack_bf16x2(g0, g1);
           }
-          if (a.gout_t) {
-            // G^T[v][row]: each lane writes its row's 32 values down a column of the transposed
-            // staging tile, then lane j stores column j's 32 rows (64 contiguous bytes)
-            unsigned short* stT = gstageT[q];
+          if (tok >= cb && tok < cb + 32 && g_rs != 0.f) {
+            // the sampled token: row_scale * expm1(log p) (no p - 1 cancellation)
+            const int jt = tok - (int)cb;
+            float xt = 0.f;
 #pragma unroll
-            for (int j = 0; j < 16; ++j) {
-              stT[(2 * j) * 40 + lane] = (unsigned short)(w[j] & 0xFFFFu);
-              stT[(2 * j + 1) * 40 + lane] = (unsigned short)(w[j] >> 16);
-            }
-            __syncwarp();
-            const int64_t row0 = rb2 * 256 + rank * 128 + 32 * q;
-            const int64_t v = cb + lane;
-            if (v < a.V && row0 < a.R) {
-              const uint4* src = reinterpret_cast<const uint4*>(stT + lane * 40);
-              __nv_bfloat16* dst = a.gout_t + v * a.ldgt + row0;
-              if (row0 + 32 <= a.ldgt) {
-                uint4* d4 = reinterpret_cast<uint4*>(dst);
+            for (int j = 0; j < 32; ++j) xt = j == jt ? __uint_as_float(r[j]) : xt;
+            const float gt = g_rs * expm1f(fmaf(xt, a.invT, -a.row_lse[row]));
+            const uint32_t hb = pack_bf16x2(gt, 0.f) & 0xFFFFu;
 #pragma unroll
-                for (int k = 0; k < 4; ++k) d4[k] = src[k];
-              } else {
-                for (int k = 0; k < 32 && row0 + k < a.R; ++k)
-                  reinterpret_cast<unsigned short*>(dst)[k] = stT[lane * 40 + k];
-              }
-            }
-            __syncwarp();
+            for (int j = 0; j < 16; ++j)
+              if (j == jt / 2) w[j] = (jt & 1) ? ((w[j] & 0xFFFFu) | (hb << 16)) : ((w[j] & 0xFFFF0000u) | hb);
           }
           if (cb + 32 <= a.V) {
             // stage the warp's 32 rows x 64 B, then store row-contiguous: each store
@@ -493,8 +477,10 @@ __global__ void __launch_bounds__(THREADS, 1)
             for (int k = 0; k < 4; ++k) {
               const int rr = 8 * k + (lane >> 2), sg = lane & 3;
               if (row0 + rr < a.R) {
-                uint4* d4 = reinterpret_cast<uint4*>(a.gout + (row0 + rr) * a.ldg + cb) + sg;
-                *d4 = st_w[rr * 5 + sg];
+                // streaming store: G is consumed by the next GEMM, not by this kernel's tiles,
+                // so it must not evict the hidden / weight tiles the CTAs share through L2
+                st16_stream(reinterpret_cast<uint4*>(a.gout + (row0 + rr) * a.ldg + cb) + sg,
+                            st_w[rr * 5 + sg]);
               }
             }
             __syncwarp();
@@ -568,6 +554,28 @@ __device__ __forceinline__ void gemm_coords(const GemmArgs& g, int64_t t, int64_
 
 constexpr int kCPitch = 36;  // staging row pitch (floats): 16-byte rows, conflict-free float4 use
 
+// MN-major operands (A_MN / B_MN): the operand's M (or N) index is the contiguous one in memory
+// -- G read as G^T for dweight, W and H read as they are stored -- so no transposed copy is made.
+// TMA boxes of 64 (MN, 128 B) x 64 (K) with 128-byte swizzle land as 8 K-row groups of 1024 B;
+// a CTA's 128 MN rows are two such boxes 8 KB apart.  UMMA canonical MN-major SW128 layout:
+// LBO = 8192 B between 64-element MN blocks, SBO = 1024 B between 8-row K groups, +2048 B per
+// K = 16 step; instruction-descriptor bit 15 (A) / 16 (B) = MN-major.
+__device__ __forceinline__ uint64_t sdesc_mn(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)(8192 >> 4) << 16) |
+         ((uint64_t)(1024 >> 4) << 32) | (1ull << 46) | (2ull << 61);
+}
+template <bool A_MN, bool B_MN>
+__device__ __forceinline__ void mma_gemm_pair(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t acc) {
+  constexpr uint32_t idesc = kIdesc2 | (A_MN ? (1u << 15) : 0u) | (B_MN ? (1u << 16) : 0u);
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(acc)
+      : "memory");
+}
+
+template <bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(THREADS, 1)
     k_gemm_tn2(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                GemmArgs g) {
@@ -623,8 +631,18 @@ __global__ void __launch_bounds__(THREADS, 1)
           const uint32_t sa = base + (uint32_t)(st * STAGE2_BYTES);
           const uint32_t fb = (full_s + 8 * st) & kPeerMask;
           if (leader) mbar_arrive_tx(full_s + 8 * st, 2 * STAGE2_BYTES);
-          tma_2d_pair(sa, &mapA, kb * BK, arow, fb);
-          tma_2d_pair(sa + A_BYTES, &mapB, kb * BK, brow, fb);
+          if (A_MN) {
+            tma_2d_pair(sa, &mapA, arow, kb * BK, fb);
+            tma_2d_pair(sa + 8192, &mapA, arow + 64, kb * BK, fb);
+          } else {
+            tma_2d_pair(sa, &mapA, kb * BK, arow, fb);
+          }
+          if (B_MN) {
+            tma_2d_pair(sa + A_BYTES, &mapB, brow, kb * BK, fb);
+            tma_2d_pair(sa + A_BYTES + 8192, &mapB, brow + 64, kb * BK, fb);
+          } else {
+            tma_2d_pair(sa + A_BYTES, &mapB, kb * BK, brow, fb);
+          }
           if (++st == STAGES2) { st = 0; ph ^= 1u; }
         }
       }
@@ -635,6 +653,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       uint32_t ph = 0;
       int acc = 0;
       uint32_t aph = 0;
+      // per K = 16 step: +32 B inside a K-major swizzle atom, +2048 B (16 K rows) MN-major
+      constexpr uint64_t stepA = A_MN ? 2048 >> 4 : 2, stepB = B_MN ? 2048 >> 4 : 2;
       for (int64_t t = cl; t < Tt; t += ncl) {
         mbar_wait(tempty_s + 8 * acc, aph ^ 1u);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -643,10 +663,11 @@ __global__ void __launch_bounds__(THREADS, 1)
           mbar_wait(full_s + 8 * st, ph);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint32_t sa = base + (uint32_t)(st * STAGE2_BYTES);
-          const uint64_t da = sdesc(sa), db = sdesc(sa + A_BYTES);
+          const uint64_t da = A_MN ? sdesc_mn(sa) : sdesc(sa);
+          const uint64_t db = B_MN ? sdesc_mn(sa + A_BYTES) : sdesc(sa + A_BYTES);
 #pragma unroll
           for (int k = 0; k < BK / UK; ++k)
-            mma_bf16_pair(td, da + (uint64_t)(2 * k), db + (uint64_t)(2 * k), (kb | k) != 0);
+            mma_gemm_pair<A_MN, B_MN>(td, da + stepA * k, db + stepB * k, (kb | k) != 0);
           mma_commit_pair(empty_s + 8 * st);
           if (++st == STAGES2) { st = 0; ph ^= 1u; }
         }
@@ -717,9 +738,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
 }
 
-// bf16 transpose dst[c][r] = src[r][c] (64 x 64 tiles; the K-major copies of W and of a hidden
-// chunk that the backward GEMMs consume).  Columns beyond `cols` / rows beyond `rows` are not
-// touched; dst rows are ldd elements apart.
+// bf16 transpose dst[c][r] = src[r][c] in 64 x 64 tiles (ODPO_GEMM_KB: the K-major copies of
+// W and of a hidden chunk, for comparing the MN-major operand path against K-major B operands).
 __global__ void __launch_bounds__(256) k_transpose_bf16(const unsigned short* __restrict__ src,
                                                          int64_t rows, int64_t cols, int64_t lds,
                                                          unsigned short* __restrict__ dst,
@@ -731,11 +751,8 @@ __global__ void __launch_bounds__(256) k_transpose_bf16(const unsigned short* __
   for (int i = 0; i < 8; ++i) {
     const int r = ty + 8 * i;
     const int64_t gr = r0 + r, gc = c0 + 2 * tx;
-    unsigned short a0 = 0, a1 = 0;
-    if (gr < rows && gc < cols) a0 = src[gr * lds + gc];
-    if (gr < rows && gc + 1 < cols) a1 = src[gr * lds + gc + 1];
-    tile[r][2 * tx] = a0;
-    tile[r][2 * tx + 1] = a1;
+    tile[r][2 * tx] = (gr < rows && gc < cols) ? src[gr * lds + gc] : (unsigned short)0;
+    tile[r][2 * tx + 1] = (gr < rows && gc + 1 < cols) ? src[gr * lds + gc + 1] : (unsigned short)0;
   }
   __syncthreads();
 #pragma unroll
@@ -825,6 +842,20 @@ static bool make_map(CUtensorMap* m, const void* base, int64_t rows, int64_t col
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// MN-major operand map: memory [kdim rows][mndim cols] (row pitch ld elements), 64 x 64 boxes
+// (64 MN elements = 128 B inner, 64 K rows), 128-byte swizzle.
+static bool make_map_mn(CUtensorMap* m, const void* base, int64_t kdim, int64_t mndim, int64_t ld) {
+  EncodeTiled enc = encode_fn();
+  if (!enc) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)mndim, (cuuint64_t)kdim};
+  const cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
+  const cuuint32_t box[2] = {64, (cuuint32_t)BK};
+  const cuuint32_t es[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 static int sm_count() {
   int dev = 0, n = 0;
   cudaGetDevice(&dev);
@@ -852,6 +883,65 @@ constexpr int kGemmG = ODPO_GEMM_G;   // backward GEMMs: 256-row blocks per rast
 
 using namespace odpo;
 using namespace odpo::lmh;
+
+// Scratch of odpo_lmhead_grad: G [CR][Vp] bf16, CR = chunk_rows rounded up to 256, Vp = V rounded
+// up to 8 (16-byte rows for TMA).
+#ifndef ODPO_GEMM_KB
+#define ODPO_GEMM_KB 0
+#endif
+constexpr bool kGemmKB = ODPO_GEMM_KB != 0;   // B operands as K-major copies (W^T, H^T)
+static size_t grad_layout(int64_t chunk_rows, int64_t d, int64_t V) {
+  const int64_t CR = (chunk_rows + 255) / 256 * 256;
+  const int64_t Vp = (V + 7) / 8 * 8;
+  size_t n = ((size_t)CR * Vp * 2 + 255) & ~(size_t)255;
+  if (kGemmKB) n += (((size_t)d * Vp * 2 + 255) & ~(size_t)255) + (size_t)d * CR * 2;
+  return n + 256;
+}
+
+static void launch_pair(const void* kern, int clusters, cudaStream_t s, void** args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(2 * clusters));
+  cfg.blockDim = dim3(THREADS);
+  cfg.dynamicSmemBytes = SMEM2;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelExC(&cfg, kern, args);
+}
+
+// One GEMM operand as stored in memory: `mn_major` = its M (or N) index is the contiguous one
+// (memory [K][MN] with row pitch ld), else K is (memory [MN][K]).
+struct Operand {
+  const void* p;
+  int64_t ld;
+  bool mn_major;
+};
+
+// C[M, N] (+)= A B^T on the CTA-pair tcgen05 kernel.
+template <bool A_MN, bool B_MN>
+static odpo_status gemm2(Operand A, Operand B, int64_t M, int64_t N, int64_t K, float* C,
+                         int64_t ldc, bool acc, int sms, cudaStream_t s) {
+  CUtensorMap mA, mB;
+  const bool okA = A_MN ? make_map_mn(&mA, A.p, K, M, A.ld) : make_map(&mA, A.p, M, K, A.ld, BM);
+  const bool okB = B_MN ? make_map_mn(&mB, B.p, K, N, B.ld) : make_map(&mB, B.p, N, K, B.ld, BN / 2);
+  if (!okA || !okB) return ODPO_ERR_CUDA;
+  GemmArgs g{};
+  g.M = M; g.N = N; g.K = K; g.C = C; g.ldc = ldc;
+  g.nmb2 = (M + 255) / 256;
+  g.nnb = (N + BN - 1) / BN;
+  g.G = kGemmG;
+  g.acc = acc ? 1 : 0;
+  int clusters = sms / 2;
+  if (clusters > g.nmb2 * g.nnb) clusters = (int)(g.nmb2 * g.nnb);
+  void* args[] = {&mA, &mB, &g};
+  launch_pair((const void*)k_gemm_tn2<A_MN, B_MN>, clusters, s, args);
+  return cudaGetLastError() == cudaSuccess ? ODPO_OK : ODPO_ERR_CUDA;
+}
 
 extern "C" {
 
@@ -933,64 +1023,9 @@ odpo_status odpo_lmhead_seq_logprobs(const void* hidden, const void* weight, int
   return cudaGetLastError() == cudaSuccess ? ODPO_OK : ODPO_ERR_CUDA;
 }
 
-// Scratch of odpo_lmhead_grad: W^T [d][Vp], G [CR][Vp], G^T [V][CR], H^T [d][CR] (bf16), where
-// CR = chunk_rows rounded up to 256 and Vp = V rounded up to 8 (16-byte rows for TMA).
-static size_t grad_layout(int64_t chunk_rows, int64_t d, int64_t V, char* base, char** wt,
-                          char** gm, char** gt, char** ht) {
-  const int64_t CR = (chunk_rows + 255) / 256 * 256;
-  const int64_t Vp = (V + 7) / 8 * 8;
-  auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
-  size_t off = 0;
-  auto take = [&](size_t n, char** p) {
-    if (p) *p = base + off;
-    off += al(n);
-  };
-  take((size_t)d * Vp * 2, wt);
-  take((size_t)CR * Vp * 2, gm);
-  take((size_t)V * CR * 2, gt);
-  take((size_t)d * CR * 2, ht);
-  return off + 256;
-}
-
 size_t odpo_lmhead_grad_scratch_bytes(int64_t chunk_rows, int64_t d, int64_t V) {
   if (chunk_rows <= 0 || d <= 0 || V <= 0) return 0;
-  return grad_layout(chunk_rows, d, V, nullptr, nullptr, nullptr, nullptr, nullptr);
-}
-
-static void launch_pair(const void* kern, int clusters, cudaStream_t s, void** args) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)(2 * clusters));
-  cfg.blockDim = dim3(THREADS);
-  cfg.dynamicSmemBytes = SMEM2;
-  cfg.stream = s;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = 2;
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  cudaLaunchKernelExC(&cfg, kern, args);
-}
-
-// C (+)= A B^T on the CTA-pair tcgen05 kernel (A [M, K], B [N, K], bf16 K-major with row pitches
-// lda / ldb elements).
-static odpo_status gemm_tn(const void* A, int64_t lda, const void* B, int64_t ldb, int64_t M,
-                           int64_t N, int64_t K, float* C, int64_t ldc, bool acc, int sms,
-                           cudaStream_t s) {
-  CUtensorMap mA, mB;
-  if (!make_map(&mA, A, M, K, lda, BM) || !make_map(&mB, B, N, K, ldb, BN / 2)) return ODPO_ERR_CUDA;
-  GemmArgs g{};
-  g.M = M; g.N = N; g.K = K; g.C = C; g.ldc = ldc;
-  g.nmb2 = (M + 255) / 256;
-  g.nnb = (N + BN - 1) / BN;
-  g.G = kGemmG;
-  g.acc = acc ? 1 : 0;
-  int clusters = sms / 2;
-  if (clusters > g.nmb2 * g.nnb) clusters = (int)(g.nmb2 * g.nnb);
-  void* args[] = {&mA, &mB, &g};
-  launch_pair((const void*)k_gemm_tn2, clusters, s, args);
-  return cudaGetLastError() == cudaSuccess ? ODPO_OK : ODPO_ERR_CUDA;
+  return grad_layout(chunk_rows, d, V);
 }
 
 odpo_status odpo_lmhead_grad(const void* hidden, const void* weight, int64_t R, int64_t d,
@@ -1004,7 +1039,7 @@ odpo_status odpo_lmhead_grad(const void* hidden, const void* weight, int64_t R, 
   if (!(isfinite(inv_temperature) && inv_temperature > 0.f)) return ODPO_ERR_INVALID_ARG;
   if (d % BK) return ODPO_ERR_UNSUPPORTED;
   if (R > (int64_t)INT32_MAX || V > (int64_t)INT32_MAX || d > (1 << 20)) return ODPO_ERR_UNSUPPORTED;
-  if (((uintptr_t)hidden & 15u) || ((uintptr_t)weight & 15u) || ((uintptr_t)scratch & 255u) ||
+  if (((uintptr_t)hidden & 15u) || ((uintptr_t)weight & 15u) || ((uintptr_t)scratch & 15u) ||
       ((uintptr_t)dhidden & 15u) || ((uintptr_t)dweight & 15u))
     return ODPO_ERR_ALIGNMENT;
   if (chunk_rows > R) chunk_rows = R;
@@ -1017,26 +1052,26 @@ odpo_status odpo_lmhead_grad(const void* hidden, const void* weight, int64_t R, 
   if (dev < 0 || dev >= 128) return ODPO_ERR_UNSUPPORTED;
   std::call_once(attr_once[dev], []() {
     cudaFuncSetAttribute(k_lmhead_fwd2<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2);
-    cudaFuncSetAttribute(k_gemm_tn2, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2);
+    cudaFuncSetAttribute(k_gemm_tn2<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2);
+    cudaFuncSetAttribute(k_gemm_tn2<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2);
+    cudaFuncSetAttribute(k_gemm_tn2<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2);
+    cudaFuncSetAttribute(k_gemm_tn2<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2);
   });
   cudaStream_t s = (cudaStream_t)stream;
-  char *wt, *gm, *gt, *ht;
-  grad_layout(CR, d, V, (char*)scratch, &wt, &gm, &gt, &ht);
   const int64_t Vp = (V + 7) / 8 * 8;
   const int sms = sm_count();
-  // W^T [d][Vp]: the K-major (K = V) B operand of dhidden = G W
-  k_transpose_bf16<<<dim3((unsigned)((d + 63) / 64), (unsigned)((V + 63) / 64)), 256, 0, s>>>(
-      reinterpret_cast<const unsigned short*>(weight), V, d, d,
-      reinterpret_cast<unsigned short*>(wt), Vp);
+  __nv_bfloat16* G = reinterpret_cast<__nv_bfloat16*>(scratch);
+  char* Wt = reinterpret_cast<char*>(scratch) + (((size_t)CR * Vp * 2 + 255) & ~(size_t)255);
+  char* Ht = Wt + (((size_t)d * Vp * 2 + 255) & ~(size_t)255);
+  if (kGemmKB)
+    k_transpose_bf16<<<dim3((unsigned)((d + 63) / 64), (unsigned)((V + 63) / 64)), 256, 0, s>>>(
+        reinterpret_cast<const unsigned short*>(weight), V, d, d,
+        reinterpret_cast<unsigned short*>(Wt), Vp);
   CUtensorMap mB;
   if (!make_map(&mB, weight, V, d, d, BN / 2)) return ODPO_ERR_CUDA;
   for (int64_t r0 = 0; r0 < R; r0 += CR) {
     const int64_t Rc = min(CR, R - r0);
     const char* hc = reinterpret_cast<const char*>(hidden) + r0 * d * 2;
-    // H^T chunk [d][CR]: the K-major (K = rows) B operand of dweight = G^T H
-    k_transpose_bf16<<<dim3((unsigned)((d + 63) / 64), (unsigned)((Rc + 63) / 64)), 256, 0, s>>>(
-        reinterpret_cast<const unsigned short*>(hc), Rc, d, d,
-        reinterpret_cast<unsigned short*>(ht), CR);
     CUtensorMap mA;
     if (!make_map(&mA, hc, Rc, d, d, BM)) return ODPO_ERR_CUDA;
     Args a{};
@@ -1050,20 +1085,33 @@ odpo_status odpo_lmhead_grad(const void* hidden, const void* weight, int64_t R, 
     a.tokens = tokens + r0;
     a.row_lse = row_lse + r0;
     a.row_scale = row_scale + r0;
-    a.gout = reinterpret_cast<__nv_bfloat16*>(gm);
+    a.gout = G;
     a.ldg = Vp;
-    a.gout_t = reinterpret_cast<__nv_bfloat16*>(gt);
-    a.ldgt = CR;
     int clusters = sms / 2;
     if (clusters > a.nrb2 * a.NT) clusters = (int)(a.nrb2 * a.NT);
     void* args[] = {&mA, &mB, &a};
     launch_pair((const void*)k_lmhead_fwd2<true>, clusters, s, args);
     if (cudaGetLastError() != cudaSuccess) return ODPO_ERR_CUDA;
-    // dhidden[r0 : r0 + Rc] = G W = G (W^T)^T          (M = Rc, N = d, K = V)
-    odpo_status e = gemm_tn(gm, Vp, wt, Vp, Rc, d, V, dhidden + r0 * d, d, false, sms, s);
+    odpo_status e;
+    if (kGemmKB) {
+      k_transpose_bf16<<<dim3((unsigned)((d + 63) / 64), (unsigned)((Rc + 63) / 64)), 256, 0, s>>>(
+          reinterpret_cast<const unsigned short*>(hc), Rc, d, d,
+          reinterpret_cast<unsigned short*>(Ht), CR);
+      e = gemm2<false, false>(Operand{G, Vp, false}, Operand{Wt, Vp, false}, Rc, d, V,
+                              dhidden + r0 * d, d, false, sms, s);
+      if (e != ODPO_OK) return e;
+      e = gemm2<true, false>(Operand{G, Vp, true}, Operand{Ht, CR, false}, V, d, Rc, dweight, d,
+                             r0 > 0, sms, s);
+      if (e != ODPO_OK) return e;
+      continue;
+    }
+    // dhidden[r0 : r0 + Rc] = G W: A = G (K = V contiguous), B = W read N-major (N = d contiguous)
+    e = gemm2<false, true>(Operand{G, Vp, false}, Operand{weight, d, true}, Rc, d, V,
+                           dhidden + r0 * d, d, false, sms, s);
     if (e != ODPO_OK) return e;
-    // dweight (+)= G^T H = (G^T) (H^T)^T                 (M = V, N = d, K = Rc)
-    e = gemm_tn(gt, CR, ht, CR, V, d, Rc, dweight, d, r0 > 0, sms, s);
+    // dweight (+)= G^T H: A = G read M-major (M = V contiguous), B = H chunk read N-major
+    e = gemm2<true, true>(Operand{G, Vp, true}, Operand{hc, d, true}, V, d, Rc, dweight, d, r0 > 0,
+                          sms, s);
     if (e != ODPO_OK) return e;
   }
   return ODPO_OK;

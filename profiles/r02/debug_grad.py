@@ -1,4 +1,4 @@
-"""Stage-by-stage check of odpo_lmhead_grad's scratch (W^T, G, G^T, H^T) and both GEMMs against
+"""Check of odpo_lmhead_grad's G scratch and both GEMMs (MN-major operands) against
 torch on the GPU's own intermediates (debugging aid; tests/test_lmhead.py is the parity test)."""
 import ctypes as C
 import os
@@ -37,18 +37,8 @@ for (B, T), d, V, chunk in [((11, 9), 128, 1000, 256), ((40, 53), 256, 4133, 102
     torch.cuda.synchronize()
     print("case", B, T, d, V, "chunk", CR, "rc", rc)
     Vp = -(-V // 8) * 8
-    al = lambda x: (x + 255) // 256 * 256
-    o_wt, o_g = 0, al(d * Vp * 2)
-    o_gt = o_g + al(CR * Vp * 2)
-    o_ht = o_gt + al(V * CR * 2)
-    bf = lambda off, n: sc[off:off + 2 * n].view(torch.bfloat16).float()
-    Wt = bf(o_wt, d * Vp).view(d, Vp)[:, :V]
-    print(" Wt ok", torch.equal(Wt, wd.float().t()))
     if R <= CR:
-        G = bf(o_g, CR * Vp).view(CR, Vp)[:R, :V]
-        Gt = bf(o_gt, V * CR).view(V, CR)[:, :R]
-        Ht = bf(o_ht, d * CR).view(d, CR)[:, :R]
-        print(" Gt == G^T", torch.equal(Gt, G.t()), "Ht == H^T", torch.equal(Ht, hd.view(R, d).float().t()))
+        G = sc[: 2 * CR * Vp].view(torch.bfloat16).float().view(CR, Vp)[:R, :V]
         print(" masked rows of G zero", bool((G[md.view(-1) == 0] == 0).all()),
               "rows with nonzero G", int((G.abs().sum(1) > 0).sum()), "/", R)
         dh_ref = G @ wd.float()
