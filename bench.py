@@ -46,7 +46,7 @@ def parse():
                     choices=["tiny", "pythia", "rho", "llama", "strong", "rho_k4"])
     ap.add_argument("--chunk-pairs", type=int, default=64)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--schedule", default="auto", choices=["auto", "fused", "two_pass", "wave", "resident"])
+    ap.add_argument("--schedule", default="auto", choices=["auto", "fused", "two_pass", "wave", "resident", "psync"])
     ap.add_argument("--lag", type=int, default=0)
     ap.add_argument("--ctas-per-sm", type=int, default=0)
     ap.add_argument("--exp2-split", type=int, default=-1)

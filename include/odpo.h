@@ -95,8 +95,8 @@ enum {
 
 /* Work schedules of odpo_online_dpo_loss_fwd_bwd_ex. */
 enum {
-  ODPO_SCHED_AUTO = 0,     /* = WAVE when all P * 2T rows fit the resident grid at once
-                              (small batches), else FUSED; the same results either way */
+  ODPO_SCHED_AUTO = 0,     /* = FUSED, the schedule with no co-residency assumption (safe
+                              beside any other work on the GPU)                        */
   ODPO_SCHED_FUSED = 1,    /* one persistent kernel: forward and backward rows dispatched
                               adaptively (a backward row is taken as soon as its pair's
                               forward pass has completed), per-pair completion counters  */
@@ -107,7 +107,7 @@ enum {
                               stays in L2 (1R+1W at HBM); needs 2T <= resident CTAs and
                               all CTAs co-resident (UNSUPPORTED otherwise).  Measured
                               slower than FUSED on B200          */
-  ODPO_SCHED_RESIDENT = 4  /* one persistent CTA per SM; a row's forward pass writes it into a
+  ODPO_SCHED_RESIDENT = 4, /* one persistent CTA per SM; a row's forward pass writes it into a
                               tensor-memory row slot (tcgen05.st) and its backward reads it
                               back (tcgen05.ld), so TMEM-held rows are read from HBM once;
                               rows beyond the TMEM slots are L2-backed (re-streamed for the
@@ -117,12 +117,22 @@ enum {
                               >= 4T; UNSUPPORTED otherwise.  Needs all CTAs co-resident (the
                               GPU not shared with other work).  Measured slower than FUSED
                               on B200                           */
+  ODPO_SCHED_PSYNC = 5     /* pair-synchronous split-V: every CTA takes the same fixed piece of
+                              every pair (the pair's 2T rows flattened and cut into one piece
+                              per CTA), forward pieces of pair p + lag run before the backward
+                              pieces of pair p, so lag + 1 pairs are live and the backward
+                              re-read is served by L2 where they fit (1R+1W at HBM for
+                              TLDR-like shapes).  lag = opts->lag_pairs (0 = 4, < 16).
+                              Launched cooperatively (all CTAs co-resident or the launch fails:
+                              ODPO_ERR_CUDA).  Needs V a multiple of the vector width and a
+                              piece of at most one row; UNSUPPORTED otherwise.  Deterministic;
+                              row statistics merged in piece order (not FUSED's bits).  */
 };
 
 typedef struct {
   int32_t schedule;     /* ODPO_SCHED_*                                            */
   int32_t lag_pairs;    /* FUSED: cap, in pairs, on how far the forward pass may run ahead of
-                           the backward pass (0 = no cap)                             */
+                           the backward pass (0 = no cap); PSYNC: the lag (0 = 4)     */
   int32_t ctas_per_sm;  /* FUSED: persistent CTAs per SM (0 = auto)               */
   int32_t launches;     /* OUT: number of kernels this call launched               */
   int32_t exp2_split;   /* bf16 only: index of the MUFU/FMA-polynomial exp2 split

@@ -42,6 +42,7 @@ struct Workspace {
   double* pair_vals;   // [P][ODPO_NSTATS]
   unsigned long long* seq_cf;  // [B] ready bit (bit 32) | fp32 bits of the sequence's coef
   float4* fparts;      // [B*T][kFS] forward-part partials (m, r, x_tok, owns tok) (kFS > 1)
+  float4* psparts;     // PSYNC: piece partials of a window of pairs [kPsWinPairs][G][2]
   unsigned* fpart_cnt; // [B*T] forward parts done (kFS > 1)
   unsigned long long* dbg_t;  // debug builds: [P][4] timestamps
   unsigned* counters;  // [0] ticket, [1] pairs done, [2] n_unref
@@ -51,6 +52,12 @@ enum { C_TICKET = 0, C_PAIRS_DONE = 1, C_NUNREF = 2, C_BPAIR = 3, C_ZTICKET = 4,
        C_DBG_N = 6, C_DBG_MAX = 7, C_DBG_DONE = 8, C_COUNT = 16 };
 
 static inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+#ifndef ODPO_EXPERIMENTAL
+#define ODPO_EXPERIMENTAL 0
+#endif
+#define ODPO_EXPERIMENTAL_WS ODPO_EXPERIMENTAL
+constexpr int kPsWinPairs = 16;    // PSYNC partial window (pairs); the lag must stay below it
+constexpr int kPsMaxGrid = 1024;   // PSYNC max CTAs
 constexpr unsigned long long kCfReady = 1ull << 32;
 
 static size_t ws_layout(int64_t B, int64_t T, int64_t P, char* base, Workspace* w) {
@@ -75,6 +82,7 @@ static size_t ws_layout(int64_t B, int64_t T, int64_t P, char* base, Workspace* 
   char* p_cf = take((size_t)B * 8);
   char* p_fp = kFS > 1 ? take(rows * kFS * 16) : nullptr;
   char* p_fc = kFS > 1 ? take(rows * 4) : nullptr;
+  char* p_ps = ODPO_EXPERIMENTAL_WS ? take((size_t)kPsWinPairs * kPsMaxGrid * 2 * 16) : nullptr;
   char* p_ct = take(C_COUNT * 4);
 #ifdef ODPO_DEBUG_LEAD
   char* p_dt = take((size_t)P * 4 * 8);
@@ -97,6 +105,7 @@ static size_t ws_layout(int64_t B, int64_t T, int64_t P, char* base, Workspace* 
     w->seq_cf = (unsigned long long*)p_cf;
     w->fparts = (float4*)p_fp;
     w->fpart_cnt = (unsigned*)p_fc;
+    w->psparts = (float4*)p_ps;
     w->counters = (unsigned*)p_ct;
   }
   return off;
@@ -1591,13 +1600,24 @@ __global__ void __launch_bounds__(GE::THREADS, GE::CPS) k_engine(LossArgs a) {
 
 }  // namespace odpo
 #include "odpo_resident.cuh"
+// Experimental schedules measured slower than FUSED, compiled only with
+// -DODPO_EXPERIMENTAL=1 (build.build(defines={"ODPO_EXPERIMENTAL": 1})): PSYNC.
+#ifndef ODPO_EXPERIMENTAL
+#define ODPO_EXPERIMENTAL 0
+#endif
+#if ODPO_EXPERIMENTAL
+#include "odpo_psync.cuh"
+#endif
 namespace odpo {
 
 // ------------------------------------------------------------------ host side
+constexpr int kPsLagDefault = 4;   // PSYNC: pairs between a pair's forward and backward pieces
+
 struct DevInfo {
   int sms = 0;
   int l2 = 0;
   int occ[2][2][M_NMODES] = {};  // [geometry][dtype][mode] (same for every poly variant)
+  int occ_ps[2] = {};            // PSYNC CTAs per SM [dtype]
 };
 // cluster size per mode: the unscaled mode always runs single-CTA
 template <int MODE>
@@ -1711,6 +1731,12 @@ static const DevInfo& dev_info(int dev) {
     setup_geo<Geo1>(d, 1);
     setup_pv<1>();
     setup_res<0>();
+#if ODPO_EXPERIMENTAL
+    cudaFuncSetAttribute(k_psync<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPsSmem);
+    cudaFuncSetAttribute(k_psync<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPsSmem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.occ_ps[0], k_psync<0>, kPsThreads, kPsSmem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.occ_ps[1], k_psync<1>, kPsThreads, kPsSmem);
+#endif
   });
   return g_dev[dev];
 }
@@ -1999,7 +2025,7 @@ odpo_status odpo_online_dpo_loss_fwd_bwd_ex(const void* policy_logits, odpo_dtyp
   if (e != ODPO_OK) return e;
   const int64_t es = dt == ODPO_F32 ? 4 : 2;
   int sched = opts ? opts->schedule : ODPO_SCHED_AUTO;
-  if (sched < ODPO_SCHED_AUTO || sched > ODPO_SCHED_RESIDENT) return ODPO_ERR_UNSUPPORTED;
+  if (sched < ODPO_SCHED_AUTO || sched > ODPO_SCHED_PSYNC) return ODPO_ERR_UNSUPPORTED;
   const int pv = (opts && opts->exp2_split >= 0) ? opts->exp2_split : kPolyDefault;
   if (pv >= kNumPoly) return ODPO_ERR_UNSUPPORTED;
   int wave_ng = 0;
@@ -2040,7 +2066,40 @@ odpo_status odpo_online_dpo_loss_fwd_bwd_ex(const void* policy_logits, odpo_dtyp
   const int dti = dt == ODPO_F32 ? 0 : 1;
   const int geo = opts ? opts->engine : -1;
 
-  if (sched == ODPO_SCHED_RESIDENT) {
+  if (sched == ODPO_SCHED_PSYNC) {
+#if ODPO_EXPERIMENTAL
+    // pair-synchronous split-V (odpo_psync.cuh): whole 16-byte vectors per row, a piece spans
+    // at most two rows, lag below the partial window; cooperative launch (co-residency)
+    const int Nv = dti == 0 ? 4 : 8;
+    const int64_t nvec = V / Nv;
+    int occ = di.occ_ps[dti];
+    if (occ < 1) occ = 1;
+    int grid = di.sms * occ;
+    if (grid > kPsMaxGrid) grid = kPsMaxGrid;
+    if (grid > 2 * T * nvec) grid = (int)(2 * T * nvec);   // every piece non-empty (it counts)
+    const int D = (opts && opts->lag_pairs > 0) ? opts->lag_pairs : kPsLagDefault;
+    if (V % Nv || 2 * T * nvec / grid > nvec || D >= kPsWinPairs) return ODPO_ERR_UNSUPPORTED;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(kPsThreads);
+    cfg.dynamicSmemBytes = kPsSmem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    if (dti == 0) cudaLaunchKernelEx(&cfg, k_psync<0>, a, D);
+    else cudaLaunchKernelEx(&cfg, k_psync<1>, a, D);
+    if ((e = launched()) != ODPO_OK) return e;
+    if (dti == 0) k_zero_unref<0><<<di.sms * 4, 256, 0, s>>>(a);
+    else k_zero_unref<1><<<di.sms * 4, 256, 0, s>>>(a);
+    if ((e = launched()) != ODPO_OK) return e;
+    launches += 2;
+#else
+    return ODPO_ERR_UNSUPPORTED;   // built without ODPO_EXPERIMENTAL (measured slower: DESIGN 4)
+#endif
+  } else if (sched == ODPO_SCHED_RESIDENT) {
     const int ring_bytes = (rg.rf + rg.rbs) * kChunk;
     const int smem = ring_bytes > kResSmemMin ? ring_bytes : kResSmemMin;
     if (dti == 0) k_resident<0, 0, 0><<<di.sms, kResThreads, smem, s>>>(a, rg);

@@ -18,7 +18,8 @@ from gpu_helpers import (NCPU, Batch, alloc_rows, check_dlogits, check_seq, chec
 pytestmark = [pytest.mark.gpu,
               pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a CUDA device")]
 
-SCHEDS = ["fused", "two_pass", "wave", "resident"]
+SCHEDS = ["fused", "two_pass", "wave", "resident", "psync"]
+OPTIONAL = ("resident", "psync")   # schedules that apply to some shapes only (odpo.h)
 
 
 @pytest.fixture(scope="module")
@@ -38,8 +39,8 @@ def run_loss(odpo, b: Batch, ref, beta, sched="fused", Pg=None, **kw):
     except odpo.OdpoError as e:
         # the RESIDENT schedule applies only where two rows fit in shared memory and the
         # on-chip stash holds two pairs (odpo.h); elsewhere the library refuses it
-        if sched == "resident" and "unsupported" in str(e):
-            pytest.skip(f"resident schedule does not apply: {e}")
+        if sched in OPTIONAL and "unsupported" in str(e):
+            pytest.skip(f"{sched} schedule does not apply: {e}")
         raise
     torch.cuda.synchronize()
     return out
@@ -130,8 +131,8 @@ def test_identity_rows_bit_exact(odpo, dtype, permute, sched, shape):
             pair_rows=None if pr is None else torch.from_numpy(pr).cuda(), schedule=sched,
             dlogits=alloc_rows(B, T, V, dtype))
     except odpo.OdpoError as e:
-        if sched == "resident" and "unsupported" in str(e):
-            pytest.skip(f"resident schedule does not apply: {e}")
+        if sched in OPTIONAL and "unsupported" in str(e):
+            pytest.skip(f"{sched} schedule does not apply: {e}")
         raise
     torch.cuda.synchronize()
     o = oracle.online_dpo_loss_fwd_bwd(h_x, ref, tok, mask, beta, pair_rows=pr, n_threads=NCPU)
@@ -506,3 +507,35 @@ def test_gather_pairs_bit_exact(odpo):
                                   status=status)
     assert int(status.item()) & odpo.FLAGS["PAIR_RANGE"]
     assert torch.count_nonzero(t2[11]).item() == 0 and torch.count_nonzero(m2[11]).item() == 0
+
+
+# ------------------------------------------------------------------ PSYNC at full Pythia size
+@pytest.mark.parametrize("lag", [1, 4, 12])
+def test_psync_full_pythia(odpo, lag):
+    """The pair-synchronous split-V schedule at the BASELINE Pythia shape (the shape it is for),
+    for several lags: deterministic, the same integer statistics and status as FUSED, sequence
+    log-probs / z / loss within the bf16 contract of FUSED's (different row reduction trees),
+    dlogits within one bf16 ulp of FUSED's, and sampled pairs against the oracle."""
+    from synth.configs import CONFIGS
+    w = CONFIGS["pythia"]
+    b = Batch(w.P, w.T, w.V, w.dtype, seed=0, host=False)
+    ref = torch.full((b.B,), -float(w.T) * 0.08, dtype=torch.float32, device="cuda")
+    fused = run_loss(odpo, b, ref, w.beta, "fused")
+    ps = run_loss(odpo, b, ref, w.beta, "psync", lag_pairs=lag)
+    again = run_loss(odpo, b, ref, w.beta, "psync", lag_pairs=lag)
+    assert torch.equal(ps.dlogits, again.dlogits) and torch.equal(ps.stats, again.stats)
+    assert int(ps.status.item()) == int(fused.status.item()) == 0
+    sf, sp = fused.stats.cpu().numpy(), ps.stats.cpu().numpy()
+    for i in (0, 8, 9):
+        assert sf[i] == sp[i]
+    a_ = fused.seq_logp.cpu().double().numpy()
+    b_ = ps.seq_logp.cpu().double().numpy()
+    assert np.all(np.abs(a_ - b_) <= 2e-5 * np.maximum(np.abs(a_), 1.0))
+    d = (ps.dlogits.float() - fused.dlogits.float()).abs()
+    assert bool((d <= 2.0 ** -7 * fused.dlogits.float().abs() + 1e-12).all())
+    pairs = synth.permutation(3, w.P)[:2]
+    seqs = np.stack([2 * pairs, 2 * pairs + 1], 1).reshape(-1)
+    o = oracle.online_dpo_loss_fwd_bwd(b.host_rows(seqs), np.full(len(seqs), -float(w.T) * 0.08, np.float32),
+                                       b.tokens[seqs], b.mask[seqs], w.beta, p_global=w.P,
+                                       n_threads=NCPU)
+    check_seq(ps.seq_logp.cpu().numpy()[seqs], o["seq_logp"], w.dtype)
