@@ -37,7 +37,25 @@ def main():
         rew4 = torch.from_numpy(synth.rewards_for(0, 2, 4)).to(dev)
         sel4 = odpo.pair_select(rew4)
         odpo.gather_pairs(sel4.pair_rows, tok, mask, ref)
+        odpo.seq_ppl(x, tok, mask)
+        # NEXT-4: two vocabulary shards, partials exchanged in the kernels (emulated peers)
+        h = V // 2 // 8 * 8
+        ex = odpo.VPExchange.emulate(2, B * T)
+        for r, (a, e) in enumerate(((0, h), (h, V))):
+            odpo.vp_row_partials_put(x[:, :, a:e], a, V, tok, mask, ex[r], 1)
+        for r, (a, e) in enumerate(((0, h), (h, V))):
+            odpo.vp_loss_fwd_bwd(ex[r].parts(1), x[:, :, a:e], a, V, ref, tok, mask, 0.05,
+                                 pair_rows=sel.pair_rows, flags=ex[r].flags(), epoch=1)
         torch.cuda.synchronize()
+    # NEXT-2: LM-head forward, loss, and the tcgen05 backward GEMMs on a small head
+    d, Vh = 256, 3001
+    hid, W = synth.lmhead_inputs(0, np.arange(B * T), d, Vh)
+    hd = torch.from_numpy(hid.reshape(B, T, d).astype(np.float32)).to(dev).to(torch.bfloat16)
+    wd = torch.from_numpy(W.astype(np.float32)).to(dev).to(torch.bfloat16)
+    tk = torch.from_numpy(synth.tokens_rows(0, np.arange(B * T), Vh).reshape(B, T)).to(dev)
+    o = odpo.lmhead_online_dpo_loss_fwd(hd, wd, torch.full((B,), -30.0, device=dev), tk, mask, 0.05)
+    odpo.lmhead_grad(hd, wd, tk, o.row_lse, o.row_scale, chunk_rows=256)
+    torch.cuda.synchronize()
     print("sanitize run ok")
 
 
