@@ -95,8 +95,10 @@ enum {
 
 /* Work schedules of odpo_online_dpo_loss_fwd_bwd_ex. */
 enum {
-  ODPO_SCHED_AUTO = 0,     /* = FUSED, the schedule with no co-residency assumption (safe
-                              beside any other work on the GPU)                        */
+  ODPO_SCHED_AUTO = 0,     /* = WAVE when all P * 2T rows fit the resident grid at once
+                              (small batches), launched cooperatively (co-residency
+                              guaranteed by the runtime; if it refuses, FUSED); else FUSED;
+                              the same results either way                              */
   ODPO_SCHED_FUSED = 1,    /* one persistent kernel: forward and backward rows dispatched
                               adaptively (a backward row is taken as soon as its pair's
                               forward pass has completed), per-pair completion counters  */

@@ -666,14 +666,15 @@ __device__ __forceinline__ void vp_store(const LossArgs& a, int64_t g, float4 v)
     a.vp_parts[g] = v;
   }
 }
-// End of a put kernel (every thread of the CTA calls it): the CTA's partial stores are made
-// visible system-wide, and the last CTA of the grid publishes the epoch to every rank.
+// End of a put kernel (every thread of the CTA calls it): each CTA releases its partial stores
+// at GPU scope into the grid's counter; the last CTA acquires them all, and ONE system-scope
+// fence + release per flag makes them (by causality) visible to the peer GPUs / processes before
+// the epoch they poll for.
 __device__ __forceinline__ void vp_signal(const LossArgs& a) {
   if (a.put.W == 0) return;
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence_system();
-    const unsigned n = atomicAdd(a.put.done, 1u);
+    const unsigned n = atom_add_acq_rel(a.put.done, 1u);   // release (gpu scope) + acquire
     if (n == gridDim.x - 1) {
       __threadfence_system();
       *a.put.done = 0u;   // the next call is stream-ordered after this kernel
@@ -2033,13 +2034,23 @@ odpo_status odpo_online_dpo_loss_fwd_bwd_ex(const void* policy_logits, odpo_dtyp
   int dev = 0;
   cudaGetDevice(&dev);
   const DevInfo& di = dev_info(dev);
-  // AUTO = FUSED: the one schedule with no co-residency assumption (a CTA never waits on a
-  // row another CTA has not been guaranteed to run), so a call is safe next to any other work
-  // on the GPU.  WAVE (peer waits; launched cooperatively) and RESIDENT are explicit options
-  // (DESIGN.md section 4 records their measurements).
+  // AUTO: a batch whose rows all fit the resident grid at once runs the wave schedule (pairs
+  // pinned to CTA groups; the tiny config is 15% faster, profiles/r01/tiny.log), every other
+  // batch FUSED.  WAVE's CTAs wait on peers, so it is launched COOPERATIVELY: the runtime
+  // guarantees all CTAs co-resident whatever else shares the GPU, or refuses the launch -- and
+  // AUTO then runs FUSED (no co-residency assumption) instead.  Same bits either way.
   const ResGeo rg = res_geo(V, T, (int)es, di.sms, opts ? opts->lookahead : -1);
   const bool res_ok = rg.nsl > 0 && (!opts || (opts->ctas_per_sm <= 0 && opts->engine < 0));
-  if (sched == ODPO_SCHED_AUTO) sched = ODPO_SCHED_FUSED;
+  bool auto_wave = false;
+  if (sched == ODPO_SCHED_AUTO) {
+    const int dti0 = dt == ODPO_F32 ? 0 : 1;
+    const int64_t grid = (int64_t)di.sms * (di.occ[0][dti0][M_FUSED] > 0 ? di.occ[0][dti0][M_FUSED] : 1);
+    const bool one_wave = kFS == 1 && pv == 0 && !(opts && (opts->engine > 0 || opts->ctas_per_sm > 0)) &&
+                          P * 2 * T <= grid;
+    const int ng = one_wave ? wave_groups(T, P, V * es, 0, -1, dti0, false, wave_gap) : 0;
+    auto_wave = ng > 0;
+    sched = auto_wave ? ODPO_SCHED_WAVE : ODPO_SCHED_FUSED;
+  }
   if (sched == ODPO_SCHED_RESIDENT && !res_ok) return ODPO_ERR_UNSUPPORTED;
   if (sched == ODPO_SCHED_WAVE) {
     wave_ng = wave_groups(T, P, V * es, opts ? opts->ctas_per_sm : 0, opts ? opts->engine : -1,
@@ -2129,7 +2140,14 @@ odpo_status odpo_online_dpo_loss_fwd_bwd_ex(const void* policy_logits, odpo_dtyp
     a.wave_gs = (int)(2 * T);
     a.wave_gap = wave_gap;
     const int cps = opts ? opts->ctas_per_sm : 0;
-    if ((e = launch_engine(dti, M_FUSED, pv, a, cps, s, geo)) != ODPO_OK) return e;
+    e = launch_engine(dti, M_FUSED, pv, a, cps, s, geo);
+    if (e != ODPO_OK && auto_wave) {
+      // the cooperative wave launch was refused (the GPU cannot host every CTA at once right
+      // now): FUSED instead; nothing ran, the k_prep state is intact
+      a.wave_ng = 0;
+      e = launch_engine(dti, M_FUSED, pv, a, cps, s, geo);
+    }
+    if (e != ODPO_OK) return e;
     launches += 1;
   }
   if (opts) opts->launches = launches;
