@@ -211,6 +211,10 @@ def aux_lmhead(config, B, T, reps=5):
         dl = o.dlogits.view(B * T, V)
         return torch.matmul(dl, Wh), torch.matmul(dl.t(), hid.view(B * T, d))
 
+    def chunked_step():
+        return odpo.lmhead_dpo_step(hid, Wh, ref_h, tok, msk, 0.1)
+
+    step_c = t(chunked_step)
     o_h = odpo.lmhead_online_dpo_loss_fwd(hid, Wh, ref_h, tok, msk, 0.1)
     grad_ms = t(lambda: odpo.lmhead_grad(hid, Wh, tok, o_h.row_lse, o_h.row_scale))
     step_f = t(fused_step)
@@ -224,7 +228,11 @@ def aux_lmhead(config, B, T, reps=5):
             "unit": "TFLOP/s", "peak": pk, "peak_source": src, "frac": flops / fused / 1e9 / pk,
             "cublas_gemm_ms": gemm, "cublas_tflops": flops / gemm / 1e9,
             "unfused_ms": gemm + seqp, "speedup_vs_unfused": (gemm + seqp) / fused,
-            "step_fused_ms": step_f, "step_unfused_ms": step_u,
+            "step_fused_ms": step_f, "step_unfused_ms": step_u, "step_chunked_ms": step_c,
+            "step_chunked_note": "odpo_lmhead_dpo_step: per ~1 GB chunk of whole pairs, bf16 "
+                                 "logits (own tcgen05 GEMM), the loss call in place, dhidden / "
+                                 "dweight (own tcgen05 GEMMs): three head GEMMs, one chunk of "
+                                 "logits in memory",
             "grad_ms": grad_ms, "grad_tflops": 3 * flops / grad_ms / 1e9,
             "grad_note": "odpo_lmhead_grad alone: logits recompute + G epilogue, dhidden and "
                          "dweight GEMMs (3 x 2 R d V flops) on the library's tcgen05 kernels",

@@ -470,6 +470,34 @@ odpo_status odpo_lmhead_grad(const void* hidden, const void* weight, int64_t R, 
                              int64_t chunk_rows, void* stream);
 
 /*
+ * odpo_lmhead_dpo_step -- NEXT-2 learner step of the LM head with the Online-DPO loss
+ * (Sec 2.1) in chunks of whole pairs, the [B, T, V] logits never
+ * materialised beyond one chunk.  Per chunk of chunk_pairs pairs:
+ *   logits_c = hidden_c W^T          bf16 [2 cp T, V] into scratch (the library's tcgen05 GEMM),
+ *   the Online-DPO loss call in place over the chunk (odpo_online_dpo_loss_fwd_bwd: log-softmax,
+ *   gather, masked sums, z, loss, statistics, dlogits = coef (softmax(invT logits) - onehot)),
+ *   dhidden_c = dlogits_c W,  dweight += dlogits_c^T hidden_c   (tcgen05 GEMMs, fp32 out).
+ * Three head GEMMs per row (odpo_lmhead_grad's recomputing backward needs four).
+ *   hidden bf16 [2P, T, d] with the pair's sequences at rows (2p, 2p+1) (odpo_gather_pairs
+ *   compacts a best/worst-of-K selection into this layout), weight bf16 [V, d], d % 64 == 0.
+ *   ref_logp [2P] f32, tokens [2P, T] i32, mask [2P, T] u8, P_global >= P, beta, invT > 0.
+ *   dhidden fp32 [2P, T, d], dweight fp32 [V, d] (overwritten); seq_logp [2P] f32 out;
+ *   pair_logit [P] f32 out or NULL; stats fp64 [>= ODPO_NSTATS] out (the chunks' sums: the
+ *   same statistics as the loss call over the whole batch); status as the loss call.
+ *   scratch >= odpo_lmhead_dpo_step_scratch_bytes(chunk_pairs, T, V) bytes, 256-byte aligned.
+ * The logits are rounded to bf16 (as a materialised bf16 logits tensor would be).
+ * Errors: INVALID_ARG, UNSUPPORTED (d % 64, sizes), ALIGNMENT, WORKSPACE, CUDA.
+ */
+size_t odpo_lmhead_dpo_step_scratch_bytes(int64_t chunk_pairs, int64_t T, int64_t V);
+odpo_status odpo_lmhead_dpo_step(const void* hidden, const void* weight, int64_t P, int64_t T,
+                                 int64_t d, int64_t V, const float* ref_logp,
+                                 const int32_t* tokens, const uint8_t* mask, int64_t P_global,
+                                 float beta, float inv_temperature, float* dhidden,
+                                 float* dweight, float* seq_logp, float* pair_logit,
+                                 double* stats, uint32_t* status, void* scratch,
+                                 size_t scratch_bytes, int64_t chunk_pairs, void* stream);
+
+/*
  * odpo_online_dpo_loss_from_token_logp -- the Online-DPO loss (Sec 2.1; S3/S4 of
  * SURVEY.md §8(a)) from per-token policy log-probs, e.g. those odpo_lmhead_seq_logprobs
  * produced without logits.  Same pair reduction (fixed-order sequence sums, z, -log sigma,

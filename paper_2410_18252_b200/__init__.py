@@ -108,6 +108,11 @@ def _L():
         L.odpo_lmhead_grad_scratch_bytes.restype = sz
         L.odpo_lmhead_grad.argtypes = [P, P, i64, i64, i64, P, P, P, f32, P, P, P, sz, i64, P]
         L.odpo_lmhead_grad.restype = C.c_int
+        L.odpo_lmhead_dpo_step_scratch_bytes.argtypes = [i64, i64, i64]
+        L.odpo_lmhead_dpo_step_scratch_bytes.restype = sz
+        L.odpo_lmhead_dpo_step.argtypes = [P, P, i64, i64, i64, i64, P, P, P, i64, f32, f32, P, P,
+                                           P, P, P, P, P, sz, i64, P]
+        L.odpo_lmhead_dpo_step.restype = C.c_int
         L.odpo_workspace_bytes.argtypes = [i64, i64, i64]
         L.odpo_workspace_bytes.restype = sz
         L.odpo_status_string.argtypes = [C.c_int]
@@ -422,6 +427,61 @@ def lmhead_grad(hidden: torch.Tensor, weight: torch.Tensor, tokens: torch.Tensor
                                  _p(row_scale), float(inv_temperature), _p(dh), _p(dw),
                                  _p(scratch), scratch.numel(), cr, _stream()), "odpo_lmhead_grad")
     return dh, dw
+
+
+def lmhead_dpo_step(hidden: torch.Tensor, weight: torch.Tensor, ref_logp: torch.Tensor,
+                    tokens: torch.Tensor, mask: torch.Tensor, beta: float,
+                    p_global: int | None = None, inv_temperature: float = 1.0,
+                    chunk_pairs: int | None = None, stats: torch.Tensor | None = None,
+                    status: torch.Tensor | None = None):
+    """NEXT-2 learner step in chunks of whole pairs (sequences (2p, 2p+1)): per chunk the logits
+    in bf16 (library tcgen05 GEMM), the Online-DPO loss call in place, dhidden = dlogits W and
+    dweight += dlogits^T hidden (library tcgen05 GEMMs).  Returns (LossOutput without dlogits,
+    dhidden fp32 [B, T, d], dweight fp32 [V, d])."""
+    hidden = _dev(hidden, "hidden", torch.bfloat16)
+    weight = _dev(weight, "weight", torch.bfloat16)
+    if hidden.dim() != 3 or weight.dim() != 2 or hidden.shape[2] != weight.shape[1]:
+        raise OdpoError("hidden must be [B, T, d] and weight [V, d]")
+    if not (hidden.is_contiguous() and weight.is_contiguous()):
+        raise OdpoError("hidden and weight must be contiguous")
+    B, T, d = hidden.shape
+    V = weight.shape[0]
+    if B % 2:
+        raise OdpoError("the step takes the selected pairs as sequences (2p, 2p+1)")
+    P = B // 2
+    Pg = P if p_global is None else int(p_global)
+    tokens, mask = _tokmask(tokens, mask, B, T)
+    ref_logp = _per_seq(ref_logp, "ref_logp", B)
+    dev = hidden.device
+    if chunk_pairs is None:
+        # at most ~1 GB of bf16 logits per chunk, and among those sizes the one whose dhidden
+        # GEMM tiles ((rows/256) x (d/256)) fill the CTA-pair waves best
+        cap = max(1, min(P, int((1 << 30) // max(1, 2 * T * V * 2))))
+        pairs_sm = torch.cuda.get_device_properties(dev).multi_processor_count // 2
+        nnb = -(-d // 256)
+
+        def waste(cp):
+            tiles = -(-(2 * cp * T) // 256) * nnb
+            waves = -(-tiles // pairs_sm)
+            nch = -(-P // cp)
+            return (waves * pairs_sm - tiles) / (waves * pairs_sm) + 0.02 * nch
+        chunk_pairs = min(range(max(1, cap // 2), cap + 1), key=lambda cp: (waste(cp), -cp))
+    chunk_pairs = min(int(chunk_pairs), P)
+    dh = torch.empty((B, T, d), dtype=torch.float32, device=dev)
+    dw = torch.empty((V, d), dtype=torch.float32, device=dev)
+    seq = torch.empty(B, dtype=torch.float32, device=dev)
+    z = torch.empty(P, dtype=torch.float32, device=dev)
+    stats = _stats(stats, dev)
+    status = _status(status, dev)
+    nb = _L().odpo_lmhead_dpo_step_scratch_bytes(chunk_pairs, T, V)
+    scratch = torch.empty(max(nb, 256), dtype=torch.uint8, device=dev)
+    _check(_L().odpo_lmhead_dpo_step(_p(hidden), _p(weight), P, T, d, V, _p(ref_logp), _p(tokens),
+                                     _p(mask), Pg, float(beta), float(inv_temperature), _p(dh),
+                                     _p(dw), _p(seq), _p(z), _p(stats), _p(status), _p(scratch),
+                                     scratch.numel(), chunk_pairs, _stream()),
+           "odpo_lmhead_dpo_step")
+    return LossOutput(stats=stats, dlogits=None, seq_logp=seq, z=z, status=status,
+                      launches=0), dh, dw
 
 
 @dataclass

@@ -536,7 +536,9 @@ __global__ void __launch_bounds__(THREADS, 1)
 // out-of-range parts of a box; stores are masked.
 struct GemmArgs {
   int64_t M, N, K;
-  float* C;
+  float* C;           // fp32 output (out_bf16 = 0)
+  __nv_bfloat16* Cb;  // bf16 output, round-to-nearest-even (out_bf16 = 1; acc must be 0)
+  int out_bf16;
   int64_t ldc;
   int64_t nmb2, nnb;  // 256-row blocks (one per CTA pair), 256-column blocks
   int G;              // row blocks per raster group
@@ -706,7 +708,18 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int k = 0; k < 8; ++k) {  // 8 lanes x 16 B per row: 4 rows per pass
           const int rr = 4 * k + (lane >> 3);
           const int64_t row = row0 + rr;
-          if (row < g.M && col < g.N) {
+          if (row < g.M && col < g.N && g.out_bf16) {
+            // bf16 output (the chunked learner step's logits): 4 values = 8 bytes per lane
+            const float4 v = *reinterpret_cast<const float4*>(stg + rr * kCPitch + 4 * sg);
+            __nv_bfloat16* dst = g.Cb + row * g.ldc + col;
+            if (col + 4 <= g.N) {
+              *reinterpret_cast<uint2*>(dst) = make_uint2(pack_bf16x2(v.x, v.y), pack_bf16x2(v.z, v.w));
+            } else {
+              const float vv[4] = {v.x, v.y, v.z, v.w};
+              for (int e = 0; col + e < g.N; ++e)
+                reinterpret_cast<unsigned short*>(dst)[e] = (unsigned short)(pack_bf16x2(vv[e], 0.f) & 0xFFFFu);
+            }
+          } else if (row < g.M && col < g.N) {
             float4 v = *reinterpret_cast<const float4*>(stg + rr * kCPitch + 4 * sg);
             float* dst = g.C + row * g.ldc + col;
             if (col + 4 <= g.N) {
@@ -925,13 +938,16 @@ struct Operand {
 // C[M, N] (+)= A B^T on the CTA-pair tcgen05 kernel.
 template <bool A_MN, bool B_MN>
 static odpo_status gemm2(Operand A, Operand B, int64_t M, int64_t N, int64_t K, float* C,
-                         int64_t ldc, bool acc, int sms, cudaStream_t s) {
+                         int64_t ldc, bool acc, int sms, cudaStream_t s,
+                         __nv_bfloat16* Cb = nullptr) {
   CUtensorMap mA, mB;
   const bool okA = A_MN ? make_map_mn(&mA, A.p, K, M, A.ld) : make_map(&mA, A.p, M, K, A.ld, BM);
   const bool okB = B_MN ? make_map_mn(&mB, B.p, K, N, B.ld) : make_map(&mB, B.p, N, K, B.ld, BN / 2);
   if (!okA || !okB) return ODPO_ERR_CUDA;
   GemmArgs g{};
   g.M = M; g.N = N; g.K = K; g.C = C; g.ldc = ldc;
+  g.Cb = Cb;
+  g.out_bf16 = Cb != nullptr;
   g.nmb2 = (M + 255) / 256;
   g.nnb = (N + BN - 1) / BN;
   g.G = kGemmG;
@@ -1111,6 +1127,97 @@ odpo_status odpo_lmhead_grad(const void* hidden, const void* weight, int64_t R, 
     if (e != ODPO_OK) return e;
     // dweight (+)= G^T H: A = G read M-major (M = V contiguous), B = H chunk read N-major
     e = gemm2<true, true>(Operand{G, Vp, true}, Operand{hc, d, true}, V, d, Rc, dweight, d, r0 > 0,
+                          sms, s);
+    if (e != ODPO_OK) return e;
+  }
+  return ODPO_OK;
+}
+
+
+// ---------------------------------------------------------------- the chunked LM-head learner step
+// (NEXT-2): per chunk of whole pairs, logits = H W^T in bf16 into a chunk
+// buffer (library GEMM, bf16 epilogue), the Online-DPO loss call in place over the chunk (S2-S5:
+// log-softmax, gather, masked sums, z, loss, statistics, dlogits = coef (softmax - onehot)),
+// then dhidden = dlogits W and dweight += dlogits^T H (library GEMMs, MN-major operands).
+// Three head GEMMs (the recomputing step needs four) and one chunk of logits in memory.
+__global__ void k_stats_add(double* total, const double* part, int n, int first) {
+  const int i = threadIdx.x;
+  if (i < n) total[i] = first ? part[i] : total[i] + part[i];
+}
+
+size_t odpo_lmhead_dpo_step_scratch_bytes(int64_t chunk_pairs, int64_t T, int64_t V) {
+  if (chunk_pairs <= 0 || T <= 0 || V <= 0) return 0;
+  const int64_t Vp = (V + 7) / 8 * 8;
+  const int64_t Rc = 2 * chunk_pairs * T;
+  auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+  return al((size_t)Rc * Vp * 2) + al(odpo_workspace_bytes(2 * chunk_pairs, T, chunk_pairs)) +
+         al(16 * sizeof(double)) + 256;
+}
+
+odpo_status odpo_lmhead_dpo_step(const void* hidden, const void* weight, int64_t P, int64_t T,
+                                 int64_t d, int64_t V, const float* ref_logp,
+                                 const int32_t* tokens, const uint8_t* mask, int64_t P_global,
+                                 float beta, float inv_temperature, float* dhidden,
+                                 float* dweight, float* seq_logp, float* pair_logit,
+                                 double* stats, uint32_t* status, void* scratch,
+                                 size_t scratch_bytes, int64_t chunk_pairs, void* stream) {
+  if (!hidden || !weight || !ref_logp || !tokens || !mask || !dhidden || !dweight || !seq_logp ||
+      !stats)
+    return ODPO_ERR_INVALID_ARG;
+  if (P <= 0 || T <= 0 || d <= 0 || V <= 0 || chunk_pairs <= 0 || P_global < P)
+    return ODPO_ERR_INVALID_ARG;
+  if (!(isfinite(beta) && beta > 0.f) || !(isfinite(inv_temperature) && inv_temperature > 0.f))
+    return ODPO_ERR_INVALID_ARG;
+  if (d % BK) return ODPO_ERR_UNSUPPORTED;
+  if (2 * P * T > (int64_t)INT32_MAX || V > (int64_t)INT32_MAX || d > (1 << 20))
+    return ODPO_ERR_UNSUPPORTED;
+  if (((uintptr_t)hidden & 15u) || ((uintptr_t)weight & 15u) || ((uintptr_t)scratch & 255u) ||
+      ((uintptr_t)dhidden & 15u) || ((uintptr_t)dweight & 15u))
+    return ODPO_ERR_ALIGNMENT;
+  if (chunk_pairs > P) chunk_pairs = P;
+  if (!scratch || scratch_bytes < odpo_lmhead_dpo_step_scratch_bytes(chunk_pairs, T, V))
+    return ODPO_ERR_WORKSPACE;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  static std::once_flag attr_once[128];
+  if (dev < 0 || dev >= 128) return ODPO_ERR_UNSUPPORTED;
+  std::call_once(attr_once[dev], []() {
+    cudaFuncSetAttribute(k_gemm_tn2<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2);
+    cudaFuncSetAttribute(k_gemm_tn2<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2);
+    cudaFuncSetAttribute(k_gemm_tn2<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2);
+  });
+  cudaStream_t s = (cudaStream_t)stream;
+  const int sms = sm_count();
+  const int64_t Vp = (V + 7) / 8 * 8;
+  auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+  char* base = reinterpret_cast<char*>(scratch);
+  __nv_bfloat16* L = reinterpret_cast<__nv_bfloat16*>(base);
+  const int64_t Rmax = 2 * chunk_pairs * T;
+  char* ws = base + al((size_t)Rmax * Vp * 2);
+  const size_t wsb = odpo_workspace_bytes(2 * chunk_pairs, T, chunk_pairs);
+  double* cst = reinterpret_cast<double*>(ws + al(wsb));
+  for (int64_t p0 = 0; p0 < P; p0 += chunk_pairs) {
+    const int64_t np = min(chunk_pairs, P - p0);
+    const int64_t r0 = 2 * p0 * T, Rc = 2 * np * T;
+    const char* hc = reinterpret_cast<const char*>(hidden) + r0 * d * 2;
+    // logits chunk [Rc, V] (row pitch Vp) = H_c W^T, bf16
+    odpo_status e = gemm2<false, false>(Operand{hc, d, false}, Operand{weight, d, false}, Rc, V, d,
+                                        nullptr, Vp, false, sms, s, L);
+    if (e != ODPO_OK) return e;
+    // the Online-DPO loss and dlogits, in place over the chunk
+    e = odpo_online_dpo_loss_fwd_bwd(L, ODPO_BF16, 2 * np, T, V, T * Vp, Vp, ref_logp + 2 * p0,
+                                     tokens + r0, mask + r0, nullptr, np, P_global, beta,
+                                     inv_temperature, L, T * Vp, Vp, seq_logp + 2 * p0,
+                                     pair_logit ? pair_logit + p0 : nullptr, cst, status, ws, wsb,
+                                     stream);
+    if (e != ODPO_OK) return e;
+    k_stats_add<<<1, 32, 0, s>>>(stats, cst, ODPO_NSTATS, p0 == 0);
+    if (cudaGetLastError() != cudaSuccess) return ODPO_ERR_CUDA;
+    // dhidden = dlogits W (W read N-major); dweight += dlogits^T H (both read MN-major)
+    e = gemm2<false, true>(Operand{L, Vp, false}, Operand{weight, d, true}, Rc, d, V,
+                           dhidden + r0 * d, d, false, sms, s);
+    if (e != ODPO_OK) return e;
+    e = gemm2<true, true>(Operand{L, Vp, true}, Operand{hc, d, true}, V, d, Rc, dweight, d, p0 > 0,
                           sms, s);
     if (e != ODPO_OK) return e;
   }

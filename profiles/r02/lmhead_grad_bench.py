@@ -42,6 +42,25 @@ for ch in CHUNKS:
     ms = t(lambda: odpo.lmhead_grad(hid, Wh, tok, o.row_lse, o.row_scale, chunk_rows=ch))
     res[f"grad_ms_chunk_{ch}"] = ms
     res[f"grad_tflops_chunk_{ch}"] = 3 * flops / ms / 1e9
+res["step_chunked_ms"] = t(lambda: odpo.lmhead_dpo_step(hid, Wh, ref, tok, msk, 0.1))
+
+
+def recompute_step():
+    oo = odpo.lmhead_online_dpo_loss_fwd(hid, Wh, ref, tok, msk, 0.1)
+    return odpo.lmhead_grad(hid, Wh, tok, oo.row_lse, oo.row_scale)
+
+
+res["step_recompute_ms"] = t(recompute_step)
+
+
+def unfused():
+    lg = torch.matmul(hid.view(B * T, d), Wh.t()).view(B, T, V)
+    oo = odpo.online_dpo_loss_fwd_bwd(lg, ref, tok, msk, 0.1, inplace=True)
+    dl = oo.dlogits.view(B * T, V)
+    return torch.matmul(dl, Wh), torch.matmul(dl.t(), hid.view(B * T, d))
+
+
+res["step_unfused_ms"] = t(unfused)
 gemm = t(lambda: torch.matmul(hid.view(B * T, d), Wh.t()))
 res["cublas_logits_gemm_ms"] = gemm
 print(json.dumps(res), flush=True)

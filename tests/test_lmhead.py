@@ -222,3 +222,57 @@ def test_lmhead_grad_parity(shape):
         bound = 2.0 ** -8 * mag + 1e-12
         assert np.all(err <= bound), (float(np.max(err - bound)), float(np.max(err / np.maximum(mag, 1e-30))))
         assert np.linalg.norm(gpu - orc) <= 1e-2 * np.linalg.norm(orc)
+
+
+# ------------------------------------------------------------------ NEXT-2 chunked learner step
+@pytest.mark.parametrize("shape", [(3, 9, 128, 1000, 1), (3, 9, 128, 1000, 2), (4, 53, 256, 4133, 3),
+                                   (2, 64, 640, 2500, 5)],
+                         ids=lambda s: f"P{s[0]}T{s[1]}d{s[2]}V{s[3]}cp{s[4]}")
+@pytest.mark.gpu
+@pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a CUDA device")
+def test_lmhead_dpo_step_parity(shape):
+    """odpo_lmhead_dpo_step (per chunk of pairs: bf16 logits from the library GEMM, the loss call
+    in place, dhidden / dweight from the library GEMMs) against the oracle on the same bf16
+    logits: the head's products are dyadic (synth.lmhead_inputs), so the fp32 tensor-core sum is
+    exact and both sides round the same value to bf16.  Sequence log-probs, z and all ten
+    statistics at the bf16 contract; dhidden / dweight element-wise within the propagated R17
+    bound of the dlogits: 2^-7 (|G| |W|) + 2^-20 |coef| sum|W| (resp. with |H|)."""
+    import paper_2410_18252_b200 as odpo
+    from gpu_helpers import check_seq, check_stats
+    P, T, d, V, cp = shape
+    B = 2 * P
+    rows = np.arange(B * T)
+    h, w = synth.lmhead_inputs(19, rows, d, V)
+    tok = synth.tokens_rows(19, rows, V).reshape(B, T).astype(np.int32)
+    mask = synth.mask_for(19, np.arange(B), T, "prefix", max(2, T // 2))
+    logits = (h @ w.T).reshape(B, T, V)
+    bits = oracle.to_bf16_bits(logits.astype(np.float32))
+    S0 = oracle.seq_logprobs(bits, tok, mask)["seq_logp"]
+    ref = (S0 + np.where(np.arange(B) % 2 == 0, 0.5, -0.25)).astype(np.float32)
+    beta, Pg = 0.1, P + 2
+    out, dh, dw = odpo.lmhead_dpo_step(
+        torch.from_numpy(h.reshape(B, T, d)).to(torch.bfloat16).cuda(),
+        torch.from_numpy(w).to(torch.bfloat16).cuda(), torch.from_numpy(ref).cuda(),
+        torch.from_numpy(tok).cuda(), torch.from_numpy(mask).cuda(), beta, p_global=Pg,
+        chunk_pairs=cp)
+    torch.cuda.synchronize()
+    o = oracle.online_dpo_loss_fwd_bwd(bits, ref, tok, mask, beta, p_global=Pg, want_dlogits=True)
+    assert int(out.status.item()) == 0
+    check_seq(out.seq_logp.cpu().numpy(), o["seq_logp"], "bf16")
+    check_stats(out.stats.cpu().numpy(), o, "bf16", beta, ref, None, Pg=Pg)
+    G = o["dlogits"].reshape(B * T, V)
+    aG = np.abs(G)
+    cabs = np.zeros(B * T)
+    for p in range(P):
+        sig = 1.0 / (1.0 + np.exp(o["z"][p]))
+        c = float(np.float32(beta)) * sig / Pg
+        cabs[(2 * p) * T:(2 * p + 2) * T] = c
+    dh_o = (G @ w).reshape(B, T, d)
+    dw_o = G.T @ h.reshape(B * T, d)
+    bh = 2.0 ** -7 * (aG @ np.abs(w)) + 2.0 ** -20 * cabs[:, None] * np.abs(w).sum(0)[None, :]
+    bw = 2.0 ** -7 * (aG.T @ np.abs(h.reshape(B * T, d))) + \
+        2.0 ** -20 * (cabs[:, None] * np.abs(h.reshape(B * T, d))).sum(0)[None, :]
+    eh = np.abs(dh.cpu().double().numpy().reshape(B * T, d) - dh_o.reshape(B * T, d))
+    ew = np.abs(dw.cpu().double().numpy() - dw_o)
+    assert np.all(eh <= bh + 1e-12), float(np.max(eh - bh))
+    assert np.all(ew <= bw + 1e-12), float(np.max(ew - bw))
