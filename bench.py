@@ -664,6 +664,8 @@ def run_ours(args, rank, world, local_rank):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "frac_of_copy_ceiling": achieved / ceil["copy_gbs"],
+                         "frac_of_8tbs_spec": achieved / 8000.0,
+                         "ncu_dram_gbs": (traffic / (loss_ms.mean() / 1e3) / 1e9) if traffic else None,
                          "floor_bytes_per_launch": floor_bytes if form == "scaled" else None,
                          "floor_frac": (floor_bytes / (loss_ms.mean() / 1e3) / 1e9 / peak
                                         if form == "scaled" else None),
