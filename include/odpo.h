@@ -401,6 +401,23 @@ odpo_status odpo_vp_row_partials_put(const void* logits_shard, odpo_dtype dt, in
                                      uint32_t* const* peer_flags, uint32_t* done, int32_t rank,
                                      int32_t W, uint32_t epoch, uint32_t* status, void* stream);
 
+/*
+ * odpo_stats_put / odpo_stats_sum -- the batch-sharded statistics reduction (SURVEY.md §8(e),
+ * S6: a SUM over the data-parallel ranks of the 16-double stats buffer) over peer memory instead
+ * of a collective, with the exchange buffers of odpo_vp_row_partials_put:
+ *   put: stats [16] f64 (this rank's local partials) -> slot [rank][0..16) of every rank's
+ *        stats slots (peer_slots[q] = rank q's [W][16] f64 region for this epoch, mapped into this
+ *        process), then a system fence and `epoch` into peer_flags[q][rank] (system release).
+ *   sum: waits (system acquire) until this rank's flags[q] reached `epoch` for every q, then
+ *        out[i] = sum over q = 0..W-1 IN RANK ORDER of slots[q][i]: every rank gets the same bits.
+ * peer_slots / peer_flags are HOST arrays of W device pointers; W <= 8.  Errors: INVALID_ARG, CUDA.
+ */
+odpo_status odpo_stats_put(const double* stats, double* const* peer_slots,
+                           uint32_t* const* peer_flags, int32_t rank, int32_t W, uint32_t epoch,
+                           void* stream);
+odpo_status odpo_stats_sum(const double* slots, const uint32_t* flags, int32_t W, uint32_t epoch,
+                           double* out, void* stream);
+
 /* Host-only: device scratch bytes needed by the calls above for B sequences of T tokens
    and P pairs (about 13 bytes per row + 80 bytes per pair + small). */
 size_t odpo_workspace_bytes(int64_t B, int64_t T, int64_t P);

@@ -85,6 +85,10 @@ def _L():
                                                P, f32, C.POINTER(P), C.POINTER(P), P, i32, i32,
                                                C.c_uint32, P, P]
         L.odpo_vp_row_partials_put.restype = C.c_int
+        L.odpo_stats_put.argtypes = [P, C.POINTER(P), C.POINTER(P), i32, i32, C.c_uint32, P]
+        L.odpo_stats_put.restype = C.c_int
+        L.odpo_stats_sum.argtypes = [P, P, i32, C.c_uint32, P, P]
+        L.odpo_stats_sum.restype = C.c_int
         L.odpo_vp_row_partials.restype = C.c_int
         L.odpo_vp_loss_fwd_bwd.restype = C.c_int
         L.odpo_gather_pairs.argtypes = [P, i64, i64, i64, P, P, P, P, P, P, P, P]
@@ -688,7 +692,9 @@ class VPExchange:
     """Peer-memory exchange buffers of the vocabulary-parallel step.
 
     Every rank owns one device buffer: the row partials of two epochs, [2][W][rows][4] f32
-    (slot [e % 2][q] written by rank q), W u32 flag words and a u32 CTA counter.  The buffers
+    (slot [e % 2][q] written by rank q), W u32 flag words and a u32 CTA counter, then the
+    statistics slots of two epochs, [2][W][16] f64, and their W flag words (the peer-memory
+    form of the stats all-reduce, `allreduce_stats(stats, exchange=...)`).  The buffers
     are mapped into every rank's address space: over the process group the ranks exchange
     CUDA IPC handles of their buffers (torch's CUDA tensor sharing) and open each other's, so
     odpo_vp_row_partials_put stores straight into the peers' memory (NVLink P2P on one node;
@@ -716,10 +722,15 @@ class VPExchange:
                 self.bufs.append(own if q == self.rank else fn(*args))
             dist.barrier(group)
         self.epoch = 0
+        self.stats_epoch = 0
+
+    @staticmethod
+    def _stats_off(W: int, rows: int) -> int:
+        return (2 * W * rows * 16 + 4 * W + 4 + 255) // 256 * 256
 
     @staticmethod
     def nbytes(W: int, rows: int) -> int:
-        return 2 * W * rows * 16 + 4 * W + 256
+        return VPExchange._stats_off(W, rows) + 2 * W * 128 + 4 * W + 256
 
     @classmethod
     def emulate(cls, W: int, rows: int, device=None):
@@ -746,6 +757,12 @@ class VPExchange:
 
     def done(self) -> int:
         return self._flags_ptr(self.rank) + 4 * self.W
+
+    def _sslots_ptr(self, q, e):
+        return self.bufs[q].data_ptr() + self._stats_off(self.W, self.rows) + (e % 2) * self.W * 128
+
+    def _sflags_ptr(self, q):
+        return self.bufs[q].data_ptr() + self._stats_off(self.W, self.rows) + 2 * self.W * 128
 
 
 def vp_row_partials_put(logits_shard: torch.Tensor, v0: int, V_total: int, tokens: torch.Tensor,
@@ -797,11 +814,32 @@ def vp_loss_step(logits_shard: torch.Tensor, v0: int, V_total: int, ref_logp: to
     return vp_loss_fwd_bwd(parts_all, logits_shard, v0, V_total, ref_logp, tokens, mask, beta, **kw)
 
 
-def allreduce_stats(stats: torch.Tensor, group=None) -> torch.Tensor:
+def allreduce_stats(stats: torch.Tensor, group=None, exchange: "VPExchange | None" = None
+                    ) -> torch.Tensor:
     """SUM all-reduce of the fp64 statistics buffer across data-parallel ranks (NCCL over
     NVLink/NVSwitch on GPU process groups; gloo for CPU tests).  One 128-byte message:
     the loss is already divided by the static P_global, so the summed buffer holds the
-    global loss, accuracy numerator and margins."""
+    global loss, accuracy numerator and margins.
+
+    With `exchange` (a VPExchange over the same ranks) the reduction runs over peer memory
+    instead (the SURVEY's K6 stretch): odpo_stats_put stores the buffer into every rank's slot
+    and publishes an epoch, odpo_stats_sum waits for all W flags and sums the slots in rank
+    order -- two one-warp launches of ours, no collective, the same bits on every rank."""
+    if exchange is not None:
+        _dev(stats, "stats", torch.float64)
+        if not stats.is_contiguous() or stats.numel() < STATS_BUF:
+            raise OdpoError(f"stats must be a contiguous float64 buffer of {STATS_BUF} doubles")
+        exchange.stats_epoch += 1
+        e = exchange.stats_epoch
+        W = exchange.W
+        slots = (C.c_void_p * W)(*[exchange._sslots_ptr(q, e) for q in range(W)])
+        flags = (C.c_void_p * W)(*[exchange._sflags_ptr(q) for q in range(W)])
+        _check(_L().odpo_stats_put(_p(stats), slots, flags, exchange.rank, W, e & 0xFFFFFFFF,
+                                   _stream()), "odpo_stats_put")
+        _check(_L().odpo_stats_sum(C.c_void_p(exchange._sslots_ptr(exchange.rank, e)),
+                                   C.c_void_p(exchange._sflags_ptr(exchange.rank)), W,
+                                   e & 0xFFFFFFFF, _p(stats), _stream()), "odpo_stats_sum")
+        return stats
     import torch.distributed as dist
     if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
         dist.all_reduce(stats, op=dist.ReduceOp.SUM, group=group)

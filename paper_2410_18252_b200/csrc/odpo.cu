@@ -545,6 +545,37 @@ __global__ void k_vp_combine(LossArgs a, const float4* __restrict__ parts, int W
   flag(a.status, fl);
 }
 
+// ------------------------------------------------------------------ K6 stretch: stats over peer memory
+// The batch-sharded statistics reduction without NCCL: every rank stores
+// its 16-double buffer into slot [rank] of every rank's exchange (peer memory), fences and
+// publishes the epoch; each rank then waits for the W flags and sums the slots in RANK order,
+// so every rank gets the same bits.  One warp each.
+__global__ void k_stats_put(const double* __restrict__ stats, VpPut put) {
+  const int lane = threadIdx.x;
+  const double v = lane < 16 ? stats[lane] : 0.0;
+  for (int q = 0; q < put.W; ++q)
+    if (lane < 16) reinterpret_cast<double*>(put.parts[q])[put.rank * 16 + lane] = v;
+  __syncwarp();
+  if (lane == 0) {
+    __threadfence_system();
+    for (int q = 0; q < put.W; ++q) st_release_sys(put.flags[q] + put.rank, put.epoch);
+  }
+}
+
+__global__ void k_stats_sum(const double* __restrict__ slots, const uint32_t* flags, int W,
+                            uint32_t epoch, double* out) {
+  const int lane = threadIdx.x;
+  if (lane == 0)
+    for (int q = 0; q < W; ++q)
+      while ((int32_t)(ld_acquire_sys(flags + q) - epoch) < 0) __nanosleep(64);
+  __syncwarp();
+  if (lane < 16) {
+    double s = 0.0;
+    for (int q = 0; q < W; ++q) s += __ldcg(slots + q * 16 + lane);
+    out[lane] = s;
+  }
+}
+
 // ------------------------------------------------------------------ App B known coefficients
 // KL proxy (R20): ppl_b = exp(-S_b / n_b) from the row log-probs
 // the SEQ engine left in the workspace.  One CTA of 32 warps; warp w sums sequences
@@ -2369,6 +2400,31 @@ odpo_status odpo_vp_row_partials(const void* logits_shard, odpo_dtype dt, int64_
   k_prep<<<1, kPrepThreads, 0, s>>>(nullptr, B, 0, w, nullptr, B * T);
   if ((e = launched()) != ODPO_OK) return e;
   return launch_engine(dt == ODPO_F32 ? 0 : 1, M_SEQ, kPolyDefault, a, 0, s, -1);
+}
+
+odpo_status odpo_stats_put(const double* stats, double* const* peer_slots,
+                           uint32_t* const* peer_flags, int32_t rank, int32_t W, uint32_t epoch,
+                           void* stream) {
+  if (!stats || !peer_slots || !peer_flags || W < 1 || W > kVpMaxW || rank < 0 || rank >= W)
+    return ODPO_ERR_INVALID_ARG;
+  VpPut put{};
+  for (int q = 0; q < W; ++q) {
+    if (!peer_slots[q] || !peer_flags[q]) return ODPO_ERR_INVALID_ARG;
+    put.parts[q] = reinterpret_cast<float4*>(peer_slots[q]);
+    put.flags[q] = peer_flags[q];
+  }
+  put.rank = rank;
+  put.W = W;
+  put.epoch = epoch;
+  k_stats_put<<<1, 32, 0, (cudaStream_t)stream>>>(stats, put);
+  return launched();
+}
+
+odpo_status odpo_stats_sum(const double* slots, const uint32_t* flags, int32_t W, uint32_t epoch,
+                           double* out, void* stream) {
+  if (!slots || !flags || !out || W < 1 || W > kVpMaxW) return ODPO_ERR_INVALID_ARG;
+  k_stats_sum<<<1, 32, 0, (cudaStream_t)stream>>>(slots, flags, W, epoch, out);
+  return launched();
 }
 
 odpo_status odpo_vp_row_partials_put(const void* logits_shard, odpo_dtype dt, int64_t B,

@@ -266,3 +266,17 @@ def test_vp_exchange_layout():
     assert ex.parts(1).shape == (W, rows, 4) and ex.parts(1).data_ptr() == ex._parts_ptr(1, 1)
     assert ex.flags().numel() == W and ex.flags().data_ptr() == ex._flags_ptr(1)
     assert ex._parts_ptr(2, 1) == bufs[2].data_ptr() + W * rows * 16
+
+
+def test_stats_exchange_argument_errors(lib):
+    """odpo_stats_put / odpo_stats_sum (the stats SUM over peer memory): pointers and 1 <= W <= 8."""
+    P = C.c_void_p
+    arr = (P * 8)(*([FAKE] * 8))
+    import paper_2410_18252_b200  # noqa: F401
+    assert lib.odpo_stats_put(None, arr, arr, 0, 2, 1, None) == 1
+    assert lib.odpo_stats_put(FAKE, None, arr, 0, 2, 1, None) == 1
+    assert lib.odpo_stats_put(FAKE, arr, arr, 2, 2, 1, None) == 1
+    assert lib.odpo_stats_put(FAKE, arr, arr, 0, 9, 1, None) == 1
+    assert lib.odpo_stats_sum(None, FAKE, 2, 1, FAKE, None) == 1
+    assert lib.odpo_stats_sum(FAKE, FAKE, 0, 1, FAKE, None) == 1
+    assert lib.odpo_stats_sum(FAKE, FAKE, 2, 1, None, None) == 1

@@ -139,12 +139,19 @@ def _vp_proc(rank, world, port, q):
                                     b.d_mask, 0.1, exchange=ex, pair_rows=b.d_pair_rows,
                                     p_global=b.P + 1)
             torch.cuda.synchronize()
-            res.append((out.stats[:10].cpu(), out.dlogits.float().cpu(), int(out.status.item())))
+            res.append((out.stats[:10].cpu().numpy(), out.dlogits.float().cpu().numpy(),
+                        int(out.status.item())))
         # the unsharded loss on the full logits (the same process computes it for comparison)
         full = odpo.online_dpo_loss_fwd_bwd(b.d_logits, d_ref, b.d_tokens, b.d_mask, 0.1,
                                             pair_rows=b.d_pair_rows, p_global=b.P + 1)
         torch.cuda.synchronize()
-        q.put((rank, res, full.stats[:10].cpu(), full.dlogits[:, :, a:e].float().cpu()))
+        # the statistics all-reduce over peer memory between the two processes
+        st = torch.arange(16, dtype=torch.float64, device="cuda") * (rank + 1) + 0.125
+        odpo.allreduce_stats(st, exchange=ex)
+        torch.cuda.synchronize()
+        # plain numpy (pickled): no shared-memory handles that die with this process
+        q.put((rank, res, full.stats[:10].cpu().numpy(),
+               full.dlogits[:, :, a:e].float().cpu().numpy(), st.cpu().numpy()))
     finally:
         dist.destroy_process_group()
 
@@ -167,8 +174,11 @@ def test_vp_exchange_two_processes(odpo):
         p.start()
     got = {}
     for _ in range(2):
-        r, res, fs, fdl = q.get(timeout=300)
-        got[r] = (res, fs, fdl)
+        r, res, fs, fdl, st = q.get(timeout=300)
+        got[r] = ([(torch.from_numpy(a), torch.from_numpy(b), c) for a, b, c in res],
+                  torch.from_numpy(fs), torch.from_numpy(fdl))
+        exp = (np.arange(16) * 1.0 + 0.125) + (np.arange(16) * 2.0 + 0.125)
+        assert np.array_equal(st, exp)   # peer-memory stats all-reduce: the rank-order sum
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
@@ -181,3 +191,31 @@ def test_vp_exchange_two_processes(odpo):
             assert torch.allclose(st, fs, rtol=1e-5, atol=1e-9)
             assert torch.all((dl - fdl).abs() <= 2.0 ** -7 * fdl.abs() + 1e-12)
     assert torch.equal(got[0][0][0][0], got[1][0][0][0])
+
+
+@pytest.mark.parametrize("W", [2, 3, 8])
+def test_stats_allreduce_over_peer_memory(odpo, W):
+    """The statistics SUM over peer memory (odpo_stats_put / odpo_stats_sum): every emulated
+    rank gets exactly the rank-order sum, for two epochs (both halves of the double buffer)."""
+    import ctypes as C
+    ex = odpo.VPExchange.emulate(W, 1)
+    L = odpo._L()
+    rng = np.random.default_rng(W)
+    for epoch in (1, 2, 3):
+        loc = [torch.from_numpy(rng.normal(size=16)).cuda() for _ in range(W)]
+        for r in range(W):
+            slots = (C.c_void_p * W)(*[ex[r]._sslots_ptr(q, epoch) for q in range(W)])
+            flags = (C.c_void_p * W)(*[ex[r]._sflags_ptr(q) for q in range(W)])
+            assert L.odpo_stats_put(C.c_void_p(loc[r].data_ptr()), slots, flags, r, W, epoch,
+                                    None) == 0
+        outs = [torch.empty(16, dtype=torch.float64, device="cuda") for _ in range(W)]
+        for r in range(W):
+            assert L.odpo_stats_sum(C.c_void_p(ex[r]._sslots_ptr(r, epoch)),
+                                    C.c_void_p(ex[r]._sflags_ptr(r)), W, epoch,
+                                    C.c_void_p(outs[r].data_ptr()), None) == 0
+        torch.cuda.synchronize()
+        exp = np.zeros(16)
+        for q in range(W):
+            exp = exp + loc[q].cpu().numpy()
+        for r in range(W):
+            assert np.array_equal(outs[r].cpu().numpy(), exp)
