@@ -442,10 +442,21 @@ def run_ours(args, rank, world, local_rank):
         torch.cuda.synchronize()
         ref_ms.append(e0.elapsed_time(e1))
     synth.fill_logits_device(logits, args.seed, row0=int(rows[0]), tokens=tokens, peak=14.0)
+    # per-completion offsets in [-32, 32) nats on the stored reference log-probs (hash stream
+    # 14, keyed by the global completion index): the synthetic reference model is the policy's
+    # twin, so without them z ~ 0 and the loss ~ ln 2; with them z spreads across the sigmoid
+    # (saturating for |z| >~ 1) as with a real reference model.  Inputs only: no cost change.
+    if Kc == 2:
+        off = synth.hash_u64(args.seed, 14, (np.arange(B) + 2 * p0))
+        ref_logp = ref_logp + torch.from_numpy(((off % np.uint64(256)).astype(np.float64) - 128.0)
+                                               / 4.0).to(dev).float()
     if Kc > 2:
         # per-completion reference log-probs (the selected ones from the pass above)
         ref_all = torch.full((n_src,), -0.08 * T, dtype=torch.float32, device=dev)
+        off = synth.hash_u64(args.seed, 14, seqs)
         ref_all[sel0.pair_rows.reshape(-1).long()] = ref_logp
+        ref_all = ref_all + torch.from_numpy(((off % np.uint64(256)).astype(np.float64) - 128.0)
+                                             / 4.0).to(dev).float()
     else:
         ref_all = ref_logp
     torch.cuda.synchronize()
@@ -655,7 +666,8 @@ def run_ours(args, rank, world, local_rank):
             "scaling": "weak", "vs_baseline": None, "dtype": w.dtype, "data": "synthetic",
             "config": {"workload": args.config, "pairs_per_rank": P, "global_pairs": P * world,
                        "K": Kc, "T": T, "V": V, "beta": w.beta, "mask": args.mask,
-                       "ref_logp": "seq_logprobs over independent reference logits (setup)",
+                       "ref_logp": "seq_logprobs over independent reference logits (setup) + "
+                                   "per-completion offsets in [-32, 32) nats (z spread)",
                        "schedule": args.schedule, "exp2_split": args.exp2_split,
                        "loss": args.loss, "gradient": args.gradient, "engine": args.engine,
                        "parallelism": f"dp{world}",

@@ -118,7 +118,8 @@ enum {
                               chunks (V*elt <= 131072 bytes) and SMs * (TMEM slots + cap)
                               >= 4T; UNSUPPORTED otherwise.  Needs all CTAs co-resident (the
                               GPU not shared with other work).  Measured slower than FUSED
-                              on B200                           */
+                              on B200; compiled only with
+                              -DODPO_EXPERIMENTAL=1, UNSUPPORTED in the default build  */
   ODPO_SCHED_PSYNC = 5     /* pair-synchronous split-V: every CTA takes the same fixed piece of
                               every pair (the pair's 2T rows flattened and cut into one piece
                               per CTA), forward pieces of pair p + lag run before the backward

@@ -1781,6 +1781,7 @@ static bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
 // SMs * (slots + cap), cover two pairs (one is the deadlock-freedom bound).
 static ResGeo res_geo(int64_t V, int64_t T, int es, int sms, int cap) {
   ResGeo g{0, 0, 0, 0, 0};
+  if (!ODPO_EXPERIMENTAL) return g;   // RESIDENT is compiled only with -DODPO_EXPERIMENTAL=1
   const int64_t nvec = V * es / 16;   // whole 16-byte vectors per row
   if (nvec < 1) return g;
   const int64_t nch = (nvec + kCV - 1) / kCV;
@@ -2246,6 +2247,7 @@ odpo_status odpo_online_dpo_loss_fwd_bwd_unscaled(
   if (!row_scale) return ODPO_ERR_INVALID_ARG;
   const bool resident = opts && opts->schedule == ODPO_SCHED_RESIDENT;
   if (opts && opts->schedule != ODPO_SCHED_AUTO && !resident) return ODPO_ERR_UNSUPPORTED;
+  if (resident && !ODPO_EXPERIMENTAL) return ODPO_ERR_UNSUPPORTED;
   const int pv = (opts && opts->exp2_split >= 0) ? opts->exp2_split : kPolyDefault;
   if (pv >= kNumPoly) return ODPO_ERR_UNSUPPORTED;
   Workspace w;

@@ -201,6 +201,7 @@ __device__ __forceinline__ void tm_ld16(uint32_t taddr, uint4 (&v)[4]) {
 // forward straight out of TMEM (exactly 1R+1W, no pair-completion latency).
 template <int DT, int PV, int UN>
 __global__ void __launch_bounds__(kResThreads, 1) k_resident(LossArgs a, ResGeo G) {
+#if ODPO_EXPERIMENTAL  // measured slower than FUSED: built only on request
   constexpr int N = Traits<DT>::N;
   constexpr int NPF = DT == 1 ? kPoly[PV].npf : 0;  // exp2 split
   constexpr int NPB = DT == 1 ? kPoly[PV].npb : 0;
@@ -649,6 +650,7 @@ __global__ void __launch_bounds__(kResThreads, 1) k_resident(LossArgs a, ResGeo 
                  "n"(kResTmemCols)
                  : "memory");
   }
+#endif  // ODPO_EXPERIMENTAL
 }
 
 }  // namespace odpo

