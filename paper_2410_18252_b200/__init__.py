@@ -21,7 +21,7 @@ from dataclasses import dataclass
 
 import torch
 
-__all__ = ["pair_select", "seq_logprobs", "seq_ppl", "VPExchange", "vp_loss_step", "online_dpo_loss_fwd_bwd", "allreduce_stats",
+__all__ = ["pair_select", "seq_logprobs", "seq_ppl", "VPExchange", "vp_loss_step", "set_tracing", "online_dpo_loss_fwd_bwd", "allreduce_stats",
            "workspace_bytes", "LossOutput", "SelectOutput", "OdpoError", "lib_path",
            "STAT_NAMES", "SEL_NAMES", "FLAGS"]
 
@@ -40,6 +40,33 @@ _DT = {torch.float32: 0, torch.bfloat16: 1}
 
 class OdpoError(RuntimeError):
     pass
+
+
+_TRACE = False
+
+
+def set_tracing(enabled: bool) -> None:
+    """NVTX ranges around every call of this module (SURVEY.md §5 tracing): each public call
+    pushes a range named after it (e.g. "odpo.online_dpo_loss_fwd_bwd") for nsys / ncu
+    --nvtx timelines.  Off by default (one flag test per call)."""
+    global _TRACE
+    _TRACE = bool(enabled)
+
+
+def _traced(fn):
+    import functools
+    name = "odpo." + fn.__name__
+
+    @functools.wraps(fn)
+    def wrapper(*args, **kw):
+        if not _TRACE:
+            return fn(*args, **kw)
+        torch.cuda.nvtx.range_push(name)
+        try:
+            return fn(*args, **kw)
+        finally:
+            torch.cuda.nvtx.range_pop()
+    return wrapper
 
 
 class _Opts(C.Structure):
@@ -231,6 +258,7 @@ class SelectOutput:
     status: torch.Tensor
 
 
+@_traced
 def pair_select(rewards: torch.Tensor, has_eos: torch.Tensor | None = None, eos_penalty: float = -1.0,
                 status: torch.Tensor | None = None, sel_stats: torch.Tensor | None = None) -> SelectOutput:
     """Reward-ranked pair selection (EOS penalty PAPER.md:434-435)."""
@@ -253,6 +281,7 @@ def pair_select(rewards: torch.Tensor, has_eos: torch.Tensor | None = None, eos_
     return SelectOutput(chosen, rejected, pair_rows, margin, sel_stats, status)
 
 
+@_traced
 def gather_pairs(pair_rows: torch.Tensor, tokens: torch.Tensor, mask: torch.Tensor,
                  ref_logp: torch.Tensor | None = None, status: torch.Tensor | None = None):
     """Selected completions in pair order: returns (tokens[2P, T],
@@ -293,6 +322,7 @@ def _rows_like(x: torch.Tensor) -> torch.Tensor:
     return torch.empty((B, T, vp), dtype=x.dtype, device=x.device)[:, :, :V]
 
 
+@_traced
 def seq_logprobs(logits: torch.Tensor, tokens: torch.Tensor, mask: torch.Tensor,
                  inv_temperature: float = 1.0, per_token: bool = False,
                  status: torch.Tensor | None = None):
@@ -317,6 +347,7 @@ def seq_logprobs(logits: torch.Tensor, tokens: torch.Tensor, mask: torch.Tensor,
     return seq
 
 
+@_traced
 def seq_ppl(logits: torch.Tensor, tokens: torch.Tensor, mask: torch.Tensor,
             inv_temperature: float = 1.0, status: torch.Tensor | None = None):
     """KL proxy: with the reference model's logits, the per-completion
@@ -336,6 +367,7 @@ def seq_ppl(logits: torch.Tensor, tokens: torch.Tensor, mask: torch.Tensor,
     return ppl, ps, seq, status
 
 
+@_traced
 def lmhead_seq_logprobs(hidden: torch.Tensor, weight: torch.Tensor, tokens: torch.Tensor,
                         mask: torch.Tensor, inv_temperature: float = 1.0,
                         status: torch.Tensor | None = None):
@@ -366,6 +398,7 @@ def lmhead_seq_logprobs(hidden: torch.Tensor, weight: torch.Tensor, tokens: torc
     return seq, tok, lse, status
 
 
+@_traced
 def lmhead_online_dpo_loss_fwd(hidden: torch.Tensor, weight: torch.Tensor,
                                ref_logp: torch.Tensor, tokens: torch.Tensor, mask: torch.Tensor,
                                beta: float, pair_rows: torch.Tensor | None = None,
@@ -394,6 +427,7 @@ def lmhead_online_dpo_loss_fwd(hidden: torch.Tensor, weight: torch.Tensor,
                       row_scale=row_scale, row_lse=row_lse)
 
 
+@_traced
 def lmhead_grad(hidden: torch.Tensor, weight: torch.Tensor, tokens: torch.Tensor,
                 row_lse: torch.Tensor, row_scale: torch.Tensor, inv_temperature: float = 1.0,
                 chunk_rows: int | None = None):
@@ -433,6 +467,7 @@ def lmhead_grad(hidden: torch.Tensor, weight: torch.Tensor, tokens: torch.Tensor
     return dh, dw
 
 
+@_traced
 def lmhead_dpo_step(hidden: torch.Tensor, weight: torch.Tensor, ref_logp: torch.Tensor,
                     tokens: torch.Tensor, mask: torch.Tensor, beta: float,
                     p_global: int | None = None, inv_temperature: float = 1.0,
@@ -504,6 +539,7 @@ class LossOutput:
         return {k: s[i] for i, k in enumerate(STAT_NAMES)}
 
 
+@_traced
 def online_dpo_loss_fwd_bwd(policy_logits: torch.Tensor, ref_logp: torch.Tensor,
                             tokens: torch.Tensor, mask: torch.Tensor, beta: float,
                             pair_rows: torch.Tensor | None = None, p_global: int | None = None,
@@ -547,6 +583,7 @@ def online_dpo_loss_fwd_bwd(policy_logits: torch.Tensor, ref_logp: torch.Tensor,
     return LossOutput(stats, dl, seq, z[:P], status, int(opts.launches))
 
 
+@_traced
 def online_dpo_loss_fwd_bwd_unscaled(policy_logits: torch.Tensor, ref_logp: torch.Tensor,
                                      tokens: torch.Tensor, mask: torch.Tensor, beta: float,
                                      pair_rows: torch.Tensor | None = None,
@@ -598,6 +635,7 @@ def online_dpo_loss_fwd_bwd_unscaled(policy_logits: torch.Tensor, ref_logp: torc
 PG_KINDS = {"rloo": 0, "copg": 1, "prox_rloo": 2, "sft": 3}
 
 
+@_traced
 def pg_loss_fwd_bwd(policy_logits: torch.Tensor, tokens: torch.Tensor, mask: torch.Tensor,
                     kind: str, rewards: torch.Tensor, old_logp: torch.Tensor | None = None,
                     clip_eps: float = 0.2, pair_rows: torch.Tensor | None = None,
@@ -637,6 +675,7 @@ def pg_loss_fwd_bwd(policy_logits: torch.Tensor, tokens: torch.Tensor, mask: tor
     return LossOutput(stats, dl, seq, seq[:0], status, int(opts.launches))
 
 
+@_traced
 def vp_row_partials(logits_shard: torch.Tensor, v0: int, V_total: int, tokens: torch.Tensor,
                     mask: torch.Tensor, inv_temperature: float = 1.0,
                     status: torch.Tensor | None = None) -> torch.Tensor:
@@ -654,6 +693,7 @@ def vp_row_partials(logits_shard: torch.Tensor, v0: int, V_total: int, tokens: t
     return parts
 
 
+@_traced
 def vp_loss_fwd_bwd(parts_all: torch.Tensor, logits_shard: torch.Tensor, v0: int, V_total: int,
                     ref_logp: torch.Tensor, tokens: torch.Tensor, mask: torch.Tensor, beta: float,
                     pair_rows: torch.Tensor | None = None, p_global: int | None = None,
@@ -765,6 +805,7 @@ class VPExchange:
         return self.bufs[q].data_ptr() + self._stats_off(self.W, self.rows) + 2 * self.W * 128
 
 
+@_traced
 def vp_row_partials_put(logits_shard: torch.Tensor, v0: int, V_total: int, tokens: torch.Tensor,
                         mask: torch.Tensor, ex: VPExchange, epoch: int,
                         inv_temperature: float = 1.0, status: torch.Tensor | None = None):
@@ -785,6 +826,7 @@ def vp_row_partials_put(logits_shard: torch.Tensor, v0: int, V_total: int, token
     return status
 
 
+@_traced
 def vp_loss_step(logits_shard: torch.Tensor, v0: int, V_total: int, ref_logp: torch.Tensor,
                  tokens: torch.Tensor, mask: torch.Tensor, beta: float, group=None,
                  exchange: VPExchange | None = None, **kw) -> LossOutput:
@@ -814,6 +856,7 @@ def vp_loss_step(logits_shard: torch.Tensor, v0: int, V_total: int, ref_logp: to
     return vp_loss_fwd_bwd(parts_all, logits_shard, v0, V_total, ref_logp, tokens, mask, beta, **kw)
 
 
+@_traced
 def allreduce_stats(stats: torch.Tensor, group=None, exchange: "VPExchange | None" = None
                     ) -> torch.Tensor:
     """SUM all-reduce of the fp64 statistics buffer across data-parallel ranks (NCCL over

@@ -280,3 +280,15 @@ def test_stats_exchange_argument_errors(lib):
     assert lib.odpo_stats_sum(None, FAKE, 2, 1, FAKE, None) == 1
     assert lib.odpo_stats_sum(FAKE, FAKE, 0, 1, FAKE, None) == 1
     assert lib.odpo_stats_sum(FAKE, FAKE, 2, 1, None, None) == 1
+
+
+def test_tracing_toggle_wraps_public_calls():
+    """NVTX tracing: every public call is wrapped, the flag is off by default."""
+    import paper_2410_18252_b200 as odpo
+    assert odpo._TRACE is False
+    for n in ("pair_select", "seq_logprobs", "online_dpo_loss_fwd_bwd", "lmhead_dpo_step",
+              "vp_loss_step", "allreduce_stats"):
+        assert getattr(odpo, n).__wrapped__.__name__ == n
+    odpo.set_tracing(True)
+    assert odpo._TRACE is True
+    odpo.set_tracing(False)
