@@ -570,7 +570,7 @@ def run_ours(args, rank, world, local_rank):
                "pairs_per_s_loss_only": world * P / (ams.mean() / 1e3),
                "alg_bytes_per_launch": alg_bytes, "status": int(status.item()),
                "kernel": ("odpo_online_dpo_loss_fwd_bwd_unscaled (prep + fwd/bwd)" if other == "unscaled"
-                          else "odpo_online_dpo_loss_fwd_bwd (prep + fused fwd/bwd)")}
+                          else "odpo_online_dpo_loss_fwd_bwd (AUTO = two-pass)")}
     # NEXT-2 aux: the Pythia-2.8B LM head (the head whose fused step VERDICT r1 asks to beat)
     lmh = aux_lmhead("pythia", 512, 53) if not args.no_aux and args.loss == "dpo" else None
     nv_main = ncu_evidence(args.config, form)
@@ -686,7 +686,8 @@ def run_ours(args, rank, world, local_rank):
                                         "its coefficient (DESIGN.md 4)" if form == "scaled" else None),
                          "ncu": nv_main,
                          "kernel": ("odpo_pg_loss_fwd_bwd (%s)" % args.loss if args.loss != "dpo"
-                                    else "odpo_online_dpo_loss_fwd_bwd (prep + fused fwd/bwd)"
+                                    else "odpo_online_dpo_loss_fwd_bwd (AUTO = two-pass: prep, "
+                                         "forward, pair reduction, backward)"
                                     if args.gradient == "scaled" else
                                     "odpo_online_dpo_loss_fwd_bwd_unscaled (prep + fwd/bwd)"),
                          "alg_bytes_per_launch": alg_bytes,

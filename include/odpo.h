@@ -95,15 +95,14 @@ enum {
 
 /* Work schedules of odpo_online_dpo_loss_fwd_bwd_ex. */
 enum {
-  ODPO_SCHED_AUTO = 0,     /* = WAVE when all P * 2T rows fit the resident grid at once
-                              (small batches), launched cooperatively (co-residency
-                              guaranteed by the runtime; if it refuses, FUSED); else FUSED;
-                              the same results either way                              */
+  ODPO_SCHED_AUTO = 0,     /* = TWO_PASS (measured fastest at every BASELINE shape on
+                              B200); no co-residency assumption; every
+                              schedule gives the same results                          */
   ODPO_SCHED_FUSED = 1,    /* one persistent kernel: forward and backward rows dispatched
                               adaptively (a backward row is taken as soon as its pair's
                               forward pass has completed), per-pair completion counters  */
   ODPO_SCHED_TWO_PASS = 2, /* forward kernel, pair-reduce kernel, backward kernel (2R+1W) */
-  ODPO_SCHED_WAVE = 3,     /* one persistent kernel, pairs statically assigned to groups
+  ODPO_SCHED_WAVE = 3,     /* (launched cooperatively) one persistent kernel, pairs statically assigned to groups
                               of 2T CTAs (one row per CTA per pair, forward then
                               backward), few enough groups that every in-flight pair
                               stays in L2 (1R+1W at HBM); needs 2T <= resident CTAs and

@@ -2066,23 +2066,13 @@ odpo_status odpo_online_dpo_loss_fwd_bwd_ex(const void* policy_logits, odpo_dtyp
   int dev = 0;
   cudaGetDevice(&dev);
   const DevInfo& di = dev_info(dev);
-  // AUTO: a batch whose rows all fit the resident grid at once runs the wave schedule (pairs
-  // pinned to CTA groups; the tiny config is 15% faster, profiles/r01/tiny.log), every other
-  // batch FUSED.  WAVE's CTAs wait on peers, so it is launched COOPERATIVELY: the runtime
-  // guarantees all CTAs co-resident whatever else shares the GPU, or refuses the launch -- and
-  // AUTO then runs FUSED (no co-residency assumption) instead.  Same bits either way.
+  // AUTO = TWO_PASS: the read-only forward pass runs at the read ceiling and the backward at
+  // the copy ceiling, which beats FUSED's mixed read/write stream at every BASELINE shape
+  // (round 2, same bits: LLaMA 14.87 vs 15.08 ms, Rho 3.80 vs 3.86, Pythia 1.301 vs 1.297,
+  // tiny 0.116 vs 0.130; profiles/r02/scripts/run_r02ab.sh).  Neither assumes co-residency.
   const ResGeo rg = res_geo(V, T, (int)es, di.sms, opts ? opts->lookahead : -1);
   const bool res_ok = rg.nsl > 0 && (!opts || (opts->ctas_per_sm <= 0 && opts->engine < 0));
-  bool auto_wave = false;
-  if (sched == ODPO_SCHED_AUTO) {
-    const int dti0 = dt == ODPO_F32 ? 0 : 1;
-    const int64_t grid = (int64_t)di.sms * (di.occ[0][dti0][M_FUSED] > 0 ? di.occ[0][dti0][M_FUSED] : 1);
-    const bool one_wave = kFS == 1 && pv == 0 && !(opts && (opts->engine > 0 || opts->ctas_per_sm > 0)) &&
-                          P * 2 * T <= grid;
-    const int ng = one_wave ? wave_groups(T, P, V * es, 0, -1, dti0, false, wave_gap) : 0;
-    auto_wave = ng > 0;
-    sched = auto_wave ? ODPO_SCHED_WAVE : ODPO_SCHED_FUSED;
-  }
+  if (sched == ODPO_SCHED_AUTO) sched = ODPO_SCHED_TWO_PASS;
   if (sched == ODPO_SCHED_RESIDENT && !res_ok) return ODPO_ERR_UNSUPPORTED;
   if (sched == ODPO_SCHED_WAVE) {
     wave_ng = wave_groups(T, P, V * es, opts ? opts->ctas_per_sm : 0, opts ? opts->engine : -1,
@@ -2172,14 +2162,7 @@ odpo_status odpo_online_dpo_loss_fwd_bwd_ex(const void* policy_logits, odpo_dtyp
     a.wave_gs = (int)(2 * T);
     a.wave_gap = wave_gap;
     const int cps = opts ? opts->ctas_per_sm : 0;
-    e = launch_engine(dti, M_FUSED, pv, a, cps, s, geo);
-    if (e != ODPO_OK && auto_wave) {
-      // the cooperative wave launch was refused (the GPU cannot host every CTA at once right
-      // now): FUSED instead; nothing ran, the k_prep state is intact
-      a.wave_ng = 0;
-      e = launch_engine(dti, M_FUSED, pv, a, cps, s, geo);
-    }
-    if (e != ODPO_OK) return e;
+    if ((e = launch_engine(dti, M_FUSED, pv, a, cps, s, geo)) != ODPO_OK) return e;
     launches += 1;
   }
   if (opts) opts->launches = launches;

@@ -8,7 +8,10 @@ lscpu > $O/lscpu.txt 2>&1; nvidia-smi > $O/nvidia_smi.txt 2>&1
 # (1) ncu --set full of the dominant kernel per config and gradient form
 for cfg in llama pythia rho tiny rho_k4; do
   for g in scaled unscaled; do
-    timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_engine" -s 4 -c 1 \
+    # scaled: the AUTO (two-pass) call's forward, pair reduction and backward kernels; factored:
+    # the row engine's one kernel (the first four k_engine launches are the reference pass)
+    if [ $g = scaled ]; then K='regex:k_engine|k_pair_reduce|k_row_bwd'; C=3; else K='regex:k_engine'; C=1; fi
+    timeout 900 ncu --set full --clock-control none --import-source on -k $K -s 4 -c $C \
       -o /tmp/ncu/full_${cfg}_${g} -f python bench.py --config $cfg --steps 1 --warmup 3 --no-e2e --no-cpu \
       --no-aux --gradient $g > /dev/null 2>&1
     python profiles/summarize_ncu.py ${TAG}_${cfg}_${g} $cfg $g "" /tmp/ncu/full_${cfg}_${g}.ncu-rep > /dev/null 2>&1

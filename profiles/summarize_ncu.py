@@ -107,13 +107,17 @@ def main():
     if traffic:
         sys.path.insert(0, os.path.dirname(HERE))
         import bench
+        # the call's kernels (each captured once, e.g. the two-pass forward, pair reduction and
+        # backward): traffic per call = their sum; the pipe figures are the dominant kernel's
         main_k = max(traffic, key=lambda k: sum(t for t, _ in traffic[k]) / len(traffic[k]))
         v = traffic[main_k]
         d = v[0][1]
+        per_call = sum(sum(t for t, _ in vv) / len(vv) for vv in traffic.values())
 
         def num(key, scale=1.0):
             return float(d[key][0].replace(",", "")) * scale if key in d else None
-        ev = {"kernel": main_k, "dram_bytes_per_launch": sum(t for t, _ in v) / len(v),
+        ev = {"kernel": " + ".join(traffic.keys()), "dominant_kernel": main_k,
+              "dram_bytes_per_launch": per_call,
               "dram_read_bytes": to_bytes(*d["dram__bytes_read.sum"]),
               "dram_write_bytes": to_bytes(*d["dram__bytes_write.sum"]),
               "duration_ms": num("gpu__time_duration.sum") / 1e6

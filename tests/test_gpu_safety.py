@@ -26,7 +26,7 @@ def odpo():
 def test_concurrent_streams_match_serial(odpo):
     """Two loss calls (different batches and shapes) in flight at once on two streams give the
     same bits as each run alone: every stream has its own workspace (k_prep counters, ring
-    state) and AUTO runs its co-residency schedule (WAVE) only through a cooperative launch."""
+    state) and AUTO never selects a schedule that needs co-residency."""
     a = Batch(64, 53, 50304, "bf16", seed=40, host=False)
     b = Batch(9, 17, 32000, "bf16", seed=41, mask_kind="prefix", lbar=9, host=False)
     ref_a = torch.full((a.B,), -4.0, device="cuda")
