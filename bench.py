@@ -62,6 +62,9 @@ def parse():
                     help="skip the auxiliary timing of the other gradient form")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--stats-exchange", action="store_true",
+                    help="N > 1: the statistics SUM over peer memory (odpo_stats_put/_sum through "
+                         "a VPExchange: CUDA IPC / NVLink P2P) instead of the NCCL all-reduce")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -464,6 +467,7 @@ def run_ours(args, rank, world, local_rank):
     stats = torch.zeros(16, dtype=torch.float64, device=dev)
     status = torch.zeros(1, dtype=torch.int32, device=dev)
     row_scale = torch.empty((B, T), dtype=torch.float32, device=dev)
+    sx = odpo.VPExchange(1) if (args.stats_exchange and world > 1) else None
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     launches = [0]
 
@@ -499,7 +503,7 @@ def run_ours(args, rank, world, local_rank):
             out = loss_call(gradient, None, ref_g, tok_g, msk_g)
             if timed_loss is not None:
                 timed_loss[1].record()
-            odpo.allreduce_stats(stats)
+            odpo.allreduce_stats(stats, exchange=sx)
             launches[0] = 2 + out.launches
             return out
         if timed_loss is not None:
@@ -507,7 +511,7 @@ def run_ours(args, rank, world, local_rank):
         out = loss_call(gradient, sel.pair_rows, ref_logp, tokens, mask)
         if timed_loss is not None:
             timed_loss[1].record()
-        odpo.allreduce_stats(stats)
+        odpo.allreduce_stats(stats, exchange=sx)
         launches[0] = 1 + out.launches
         return out
 
@@ -611,7 +615,7 @@ def run_ours(args, rank, world, local_rank):
                 out = loss_call(args.gradient, None, rg, tg, mg)
             else:
                 out = loss_call(args.gradient, sel.pair_rows, d_ref, d_tok, d_mask)
-            odpo.allreduce_stats(stats)
+            odpo.allreduce_stats(stats, exchange=sx)
             h_stats.copy_(stats, non_blocking=True)
             h_z.copy_(out.z, non_blocking=True)
 
@@ -671,6 +675,8 @@ def run_ours(args, rank, world, local_rank):
                        "schedule": args.schedule, "exp2_split": args.exp2_split,
                        "loss": args.loss, "gradient": args.gradient, "engine": args.engine,
                        "parallelism": f"dp{world}",
+                       "stats_reduction": ("peer memory (odpo_stats_put/_sum)" if args.stats_exchange
+                                           and world > 1 else "NCCL all_reduce" if world > 1 else "none"),
                        "l2": "inputs (%.2f GB) > L2; plus 256 MiB L2 flush between timed steps"
                              % (B * T * V * s_in / 1e9)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -736,6 +742,7 @@ def run_strong(args, rank, world, local_rank):
     stats = torch.zeros(16, dtype=torch.float64, device=dev)
     status = torch.zeros(1, dtype=torch.int32, device=dev)
     acc = torch.zeros(16, dtype=torch.float64, device=dev)
+    sx = odpo.VPExchange(1) if (args.stats_exchange and world > 1) else None
     ref_val = -0.1 * T
 
     def prep_chunk(c0, c1):
@@ -776,7 +783,7 @@ def run_strong(args, rank, world, local_rank):
             meta["launches"] = 1 + out.launches
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        odpo.allreduce_stats(acc)
+        odpo.allreduce_stats(acc, exchange=sx)
         e1.record()
         torch.cuda.synchronize()
         total_ms += e0.elapsed_time(e1)
