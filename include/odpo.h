@@ -490,9 +490,13 @@ odpo_status odpo_lmhead_grad(const void* hidden, const void* weight, int64_t R, 
  * odpo_lmhead_dpo_step -- NEXT-2 learner step of the LM head with the Online-DPO loss
  * (Sec 2.1) in chunks of whole pairs, the [B, T, V] logits never
  * materialised beyond one chunk.  Per chunk of chunk_pairs pairs:
- *   logits_c = hidden_c W^T          bf16 [2 cp T, V] into scratch (the library's tcgen05 GEMM),
- *   the Online-DPO loss call in place over the chunk (odpo_online_dpo_loss_fwd_bwd: log-softmax,
- *   gather, masked sums, z, loss, statistics, dlogits = coef (softmax(invT logits) - onehot)),
+ *   logits_c = hidden_c W^T          bf16 [2 cp T, V] into scratch (the library's tcgen05 head
+ *                                    kernel), its epilogue also folding the stored bf16 logits
+ *                                    into one (m, log1p r, x_tok) partial per (row, 256-entry
+ *                                    vocabulary tile);
+ *   the Online-DPO loss in place over the chunk from those partials (the merge of
+ *   odpo_vp_loss_fwd_bwd with one shard per tile: row log-softmax, gather, masked sums, z, loss,
+ *   statistics, dlogits = coef (softmax(invT logits) - onehot)) -- the chunk is read once;
  *   dhidden_c = dlogits_c W,  dweight += dlogits_c^T hidden_c   (tcgen05 GEMMs, fp32 out).
  * Three head GEMMs per row (odpo_lmhead_grad's recomputing backward needs four).
  *   hidden bf16 [2P, T, d] with the pair's sequences at rows (2p, 2p+1) (odpo_gather_pairs

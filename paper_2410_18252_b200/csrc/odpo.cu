@@ -545,6 +545,68 @@ __global__ void k_vp_combine(LossArgs a, const float4* __restrict__ parts, int W
   flag(a.status, fl);
 }
 
+// Many partials per row (W > 32: the LM-head step's one partial per 256-entry vocabulary tile,
+// odpo_lmhead_dpo_step): one warp per row, the same merge with lane-strided partials.  w* = the
+// first argmax (max over lanes, then the lowest index among equal maxima); each lane sums its
+// partials in index order, then a fixed shfl_down tree: deterministic.
+constexpr int kCombineWarps = 8;
+__global__ void __launch_bounds__(32 * kCombineWarps) k_vp_combine_wide(LossArgs a,
+                                                                        const float4* __restrict__ parts,
+                                                                        int W) {
+  const int64_t rows = a.B * a.T;
+  const int64_t g = (int64_t)blockIdx.x * kCombineWarps + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (g >= rows || !a.mask[g]) return;
+  float ms = -INFINITY;
+  int ws = INT32_MAX;
+  for (int w = lane; w < W; w += 32) {
+    const float mw = __ldcg(&parts[(int64_t)w * rows + g].x);
+    if (mw > ms) { ms = mw; ws = w; }
+  }
+#pragma unroll
+  for (int off = 16; off; off >>= 1) {
+    const float om = __shfl_xor_sync(kFull, ms, off);
+    const int ow = __shfl_xor_sync(kFull, ws, off);
+    if (om > ms || (om == ms && ow < ws)) { ms = om; ws = ow; }
+  }
+  if (ws == INT32_MAX) ws = 0;   // every partial -inf: the row is flagged below
+  const float k2 = a.invT * kLog2e;
+  float R = 0.f, xt = 0.f;
+  int owners = 0;
+  for (int w = lane; w < W; w += 32) {
+    const float4 pw = __ldcg(&parts[(int64_t)w * rows + g]);
+    if (pw.w != 0.f) { xt = pw.z; ++owners; }
+    if (w == ws) {
+      R += expm1f(pw.y);
+    } else if (pw.x != -INFINITY) {
+      R += ex2((pw.x - ms) * k2) * (1.f + expm1f(pw.y));
+    }
+  }
+  // the token's logit from the (first) owning lane; more or fewer than one owner is flagged
+  const unsigned own_mask = __ballot_sync(kFull, owners != 0);
+  xt = __shfl_sync(kFull, xt, own_mask ? __ffs(own_mask) - 1 : 0);
+#pragma unroll
+  for (int off = 16; off; off >>= 1) {
+    R += __shfl_down_sync(kFull, R, off);
+    owners += __shfl_down_sync(kFull, owners, off);
+  }
+  if (lane != 0) return;
+  uint32_t fl = 0;
+  const float l1p = log1pf(R);
+  float logp = 0.f;
+  if (owners != 1) {
+    fl |= ODPO_FLAG_TOKEN_RANGE;
+  } else {
+    logp = __fsub_rn(__fmul_rn(__fsub_rn(xt, ms), a.invT), l1p);
+    if (!isfinite(logp)) fl |= ODPO_FLAG_NONFINITE_LOGIT;
+  }
+  if (!isfinite(ms)) fl |= ODPO_FLAG_NONFINITE_LOGIT;
+  a.w.row_m[g] = ms;
+  a.w.row_l1p[g] = l1p;
+  a.w.row_logp[g] = logp;
+  flag(a.status, fl);
+}
+
 // ------------------------------------------------------------------ K6 stretch: stats over peer memory
 // The batch-sharded statistics reduction without NCCL: every rank stores
 // its 16-double buffer into slot [rank] of every rank's exchange (peer memory), fences and
@@ -2483,8 +2545,12 @@ odpo_status odpo_vp_loss_fwd_bwd(const float* parts_all, int32_t W, const void* 
   k_prep<<<1, kPrepThreads, 0, s>>>(pair_rows, B, P, w, status, B * T);
   if ((e = launched()) != ODPO_OK) return e;
   const int64_t rows = B * T;
-  k_vp_combine<<<(unsigned)((rows + 255) / 256), 256, 0, s>>>(
-      a, reinterpret_cast<const float4*>(parts_all), W);
+  if (W > 32 && !flags)
+    k_vp_combine_wide<<<(unsigned)((rows + kCombineWarps - 1) / kCombineWarps), 32 * kCombineWarps,
+                        0, s>>>(a, reinterpret_cast<const float4*>(parts_all), W);
+  else
+    k_vp_combine<<<(unsigned)((rows + 255) / 256), 256, 0, s>>>(
+        a, reinterpret_cast<const float4*>(parts_all), W);
   if ((e = launched()) != ODPO_OK) return e;
   k_pair_reduce<<<(unsigned)P, 32, 0, s>>>(a);
   if ((e = launched()) != ODPO_OK) return e;

@@ -112,6 +112,9 @@ struct Args {
   const float* row_scale; // [R] coef_b * mask (d loss / d logits = row_scale * G)
   __nv_bfloat16* gout;   // [R][ldg]
   int64_t ldg;
+  // LOGITS epilogue (the chunked learner step): the bf16 logits into gout, and per (row, tile)
+  // the vocabulary-parallel partial (m, log1p r, x_tok, owns tok) of those bf16 values, [NT][R]
+  float4* parts4;
 };
 
 __device__ __forceinline__ void tile_coords(const Args& a, int64_t t, int64_t& rb, int64_t& n) {
@@ -315,17 +318,23 @@ __device__ __forceinline__ void tile_coords2(const Args& a, int64_t t, int64_t& 
   rb2 = r0 + idx % gg;
 }
 
-// GRAD = true: the same GEMM tiles, but the epilogue writes the row's gradient with respect to
-// the logits, G = row_scale (softmax(invT x) - onehot) in bf16, instead of folding an online
+// Epilogue kinds.  LSE: fold each tile into the rows' online logsumexp partials (forward).
+// GRAD: the same GEMM tiles, but the epilogue writes the row's gradient with respect to the
+// logits, G = row_scale (softmax(invT x) - onehot) in bf16, instead of folding an online
 // logsumexp (the backward recomputes the logits a row chunk at a time; see odpo_lmhead_grad).
-template <bool GRAD>
+// LOGITS: store the logits in bf16 AND fold the stored (rounded) values into one partial per
+// (row, tile) in the vocabulary-parallel format, so the chunked learner step's loss needs no
+// forward pass over the logits (odpo_lmhead_dpo_step).
+constexpr int kEpiLse = 0, kEpiGrad = 1, kEpiLogits = 2;
+template <int EPI>
 __global__ void __launch_bounds__(THREADS, 1)
     k_lmhead_fwd2(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                   Args a) {
+  constexpr bool GRAD = EPI == kEpiGrad, LOGITS = EPI == kEpiLogits;
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full[STAGES2], empty[STAGES2], tfull[2], tempty[2];
-  // GRAD epilogue: per epilogue warp a 32-row x 64-byte staging tile (rows padded to 80 B)
-  __shared__ __align__(16) uint4 gstage[4][GRAD ? 32 * 5 : 1];
+  // GRAD / LOGITS epilogue: per epilogue warp a 32-row x 64-byte staging tile (rows padded to 80 B)
+  __shared__ __align__(16) uint4 gstage[4][(GRAD || LOGITS) ? 32 * 5 : 1];
   __shared__ uint32_t tmem_sh;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
@@ -423,7 +432,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       const bool live = row < a.R;
       const int tok = live ? a.tokens[row] : -1;
       MR s{-INFINITY, 0.f};
-      float g_rs = 0.f, g_c = 0.f;
+      float g_rs = 0.f, g_c = 0.f, xt = 0.f, own = 0.f;
       if (GRAD && live) {
         g_rs = a.row_scale[row];
         g_c = g_rs != 0.f ? a.row_lse[row] * kLog2e : INFINITY;  // p = 2^(acc invT log2e - lse log2e)
@@ -491,6 +500,37 @@ __global__ void __launch_bounds__(THREADS, 1)
           }
           continue;
         }
+        if (LOGITS) {
+          // round to bf16 (the chunk's logits, round-to-nearest-even) and fold exactly the
+          // stored values: the loss is the one of the logits tensor the backward reads
+          uint32_t w[16];
+#pragma unroll
+          for (int j = 0; j < 32; j += 2) {
+            w[j / 2] = pack_bf16x2(__uint_as_float(r[j]), __uint_as_float(r[j + 1]));
+            r[j] = w[j / 2] << 16;
+            r[j + 1] = w[j / 2] & 0xFFFF0000u;
+          }
+          if (cb + 32 <= a.V) {
+            uint4* st_w = gstage[q];
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              st_w[lane * 5 + k] = make_uint4(w[4 * k], w[4 * k + 1], w[4 * k + 2], w[4 * k + 3]);
+            __syncwarp();
+            const int64_t row0 = rb2 * 256 + rank * 128 + 32 * q;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const int rr = 8 * k + (lane >> 2), sg = lane & 3;
+              if (row0 + rr < a.R)
+                st16_stream(reinterpret_cast<uint4*>(a.gout + (row0 + rr) * a.ldg + cb) + sg,
+                            st_w[rr * 5 + sg]);
+            }
+            __syncwarp();
+          } else if (live) {
+            unsigned short* d2 = reinterpret_cast<unsigned short*>(a.gout + row * a.ldg + cb);
+            for (int j = 0; j < 32 && cb + j < a.V; ++j)
+              d2[j] = (unsigned short)((w[j / 2] >> (16 * (j & 1))) & 0xFFFFu);
+          }
+        }
         if (cb + 32 > a.V) {
 #pragma unroll
           for (int j = 0; j < 32; ++j)
@@ -501,7 +541,12 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
           for (int j = 0; j < 32; ++j)
             if (tok == cb + j) x = __uint_as_float(r[j]);
-          a.xtok[row] = x;
+          if (LOGITS) {
+            xt = x;
+            own = 1.f;
+          } else {
+            a.xtok[row] = x;
+          }
         }
         uint4 v[8];
 #pragma unroll
@@ -512,7 +557,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive_cl(tempty_leader + 8 * acc);
       if (++acc == 2) { acc = 0; aph ^= 1u; }
-      if (!GRAD && live) a.parts[row * a.NT + n] = make_float2(s.m, s.r);
+      if (EPI == kEpiLse && live) a.parts[row * a.NT + n] = make_float2(s.m, s.r);
+      if (LOGITS && live) a.parts4[n * a.R + row] = make_float4(s.m, log1pf(s.r), xt, own);
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -704,6 +750,18 @@ __global__ void __launch_bounds__(THREADS, 1)
         __syncwarp();
         const int sg = lane & 7;
         const int64_t col = cb + 4 * sg;
+        // C += A B^T: the 8 passes' old values are loaded together first (the stores below
+        // could alias them, so the compiler would otherwise serialise one HBM round trip per
+        // pass and the epilogue, not the tensor cores, would set the pace)
+        float4 old[8];
+        if (g.acc && !g.out_bf16 && col + 4 <= g.N) {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const int64_t row = row0 + 4 * k + (lane >> 3);
+            old[k] = row < g.M ? __ldcs(reinterpret_cast<const float4*>(g.C + row * g.ldc + col))
+                               : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+        }
 #pragma unroll
         for (int k = 0; k < 8; ++k) {  // 8 lanes x 16 B per row: 4 rows per pass
           const int rr = 4 * k + (lane >> 3);
@@ -724,8 +782,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             float* dst = g.C + row * g.ldc + col;
             if (col + 4 <= g.N) {
               if (g.acc) {
-                const float4 o = *reinterpret_cast<const float4*>(dst);
-                v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
+                v.x += old[k].x; v.y += old[k].y; v.z += old[k].z; v.w += old[k].w;
               }
               *reinterpret_cast<float4*>(dst) = v;
             } else {
@@ -993,8 +1050,8 @@ odpo_status odpo_lmhead_seq_logprobs(const void* hidden, const void* weight, int
   if (dev < 0 || dev >= 128) return ODPO_ERR_UNSUPPORTED;
   std::call_once(attr_once[dev], []() {
     cudaFuncSetAttribute(k_lmhead_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-    cudaFuncSetAttribute(k_lmhead_fwd2<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2);
-    cudaFuncSetAttribute(k_lmhead_fwd2<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2);
+    cudaFuncSetAttribute(k_lmhead_fwd2<kEpiLse>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2);
+    cudaFuncSetAttribute(k_lmhead_fwd2<kEpiGrad>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2);
   });
   const int sms = sm_count();
   Args a;
@@ -1027,7 +1084,7 @@ odpo_status odpo_lmhead_seq_logprobs(const void* hidden, const void* weight, int
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, k_lmhead_fwd2<false>, mA, mB, a);
+    cudaLaunchKernelEx(&cfg, k_lmhead_fwd2<kEpiLse>, mA, mB, a);
   } else {
     const int grid = (int)(a.Ttot < sms ? a.Ttot : sms);
     k_lmhead_fwd<<<grid, THREADS, SMEM, s>>>(mA, mB, a);
@@ -1067,7 +1124,7 @@ odpo_status odpo_lmhead_grad(const void* hidden, const void* weight, int64_t R, 
   static std::once_flag attr_once[128];
   if (dev < 0 || dev >= 128) return ODPO_ERR_UNSUPPORTED;
   std::call_once(attr_once[dev], []() {
-    cudaFuncSetAttribute(k_lmhead_fwd2<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2);
+    cudaFuncSetAttribute(k_lmhead_fwd2<kEpiGrad>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2);
     cudaFuncSetAttribute(k_gemm_tn2<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2);
     cudaFuncSetAttribute(k_gemm_tn2<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2);
     cudaFuncSetAttribute(k_gemm_tn2<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2);
@@ -1106,7 +1163,7 @@ odpo_status odpo_lmhead_grad(const void* hidden, const void* weight, int64_t R, 
     int clusters = sms / 2;
     if (clusters > a.nrb2 * a.NT) clusters = (int)(a.nrb2 * a.NT);
     void* args[] = {&mA, &mB, &a};
-    launch_pair((const void*)k_lmhead_fwd2<true>, clusters, s, args);
+    launch_pair((const void*)k_lmhead_fwd2<kEpiGrad>, clusters, s, args);
     if (cudaGetLastError() != cudaSuccess) return ODPO_ERR_CUDA;
     odpo_status e;
     if (kGemmKB) {
@@ -1136,10 +1193,18 @@ odpo_status odpo_lmhead_grad(const void* hidden, const void* weight, int64_t R, 
 
 // ---------------------------------------------------------------- the chunked LM-head learner step
 // (NEXT-2): per chunk of whole pairs, logits = H W^T in bf16 into a chunk
-// buffer (library GEMM, bf16 epilogue), the Online-DPO loss call in place over the chunk (S2-S5:
-// log-softmax, gather, masked sums, z, loss, statistics, dlogits = coef (softmax - onehot)),
-// then dhidden = dlogits W and dweight += dlogits^T H (library GEMMs, MN-major operands).
-// Three head GEMMs (the recomputing step needs four) and one chunk of logits in memory.
+// buffer by the head kernel's LOGITS epilogue, which also folds the stored logits into one
+// (m, log1p r, x_tok) partial per (row, 256-entry vocabulary tile); the loss then merges those
+// partials exactly as the vocabulary-parallel path merges its shards' (odpo_vp_loss_fwd_bwd with
+// one "shard" per tile: row statistics, masked sums, z, loss, statistics, and dlogits = coef
+// (softmax - onehot) in place over the chunk), so the logits are read ONCE (by the backward)
+// instead of twice; then dhidden = dlogits W and dweight += dlogits^T H (library GEMMs,
+// MN-major operands).  Three head GEMMs (the recomputing step needs four), one chunk of logits.
+// Build flag ODPO_STEP_FWD_PASS=1: the round-2 variant (plain bf16 GEMM + the full loss call,
+// which re-reads the chunk for its forward pass), kept for the A/B measurement.
+#ifndef ODPO_STEP_FWD_PASS
+#define ODPO_STEP_FWD_PASS 0
+#endif
 __global__ void k_stats_add(double* total, const double* part, int n, int first) {
   const int i = threadIdx.x;
   if (i < n) total[i] = first ? part[i] : total[i] + part[i];
@@ -1150,8 +1215,9 @@ size_t odpo_lmhead_dpo_step_scratch_bytes(int64_t chunk_pairs, int64_t T, int64_
   const int64_t Vp = (V + 7) / 8 * 8;
   const int64_t Rc = 2 * chunk_pairs * T;
   auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+  const int64_t NT = (V + BN - 1) / BN;
   return al((size_t)Rc * Vp * 2) + al(odpo_workspace_bytes(2 * chunk_pairs, T, chunk_pairs)) +
-         al(16 * sizeof(double)) + 256;
+         al(16 * sizeof(double)) + al((size_t)NT * Rc * sizeof(float4)) + 256;
 }
 
 odpo_status odpo_lmhead_dpo_step(const void* hidden, const void* weight, int64_t P, int64_t T,
@@ -1185,10 +1251,12 @@ odpo_status odpo_lmhead_dpo_step(const void* hidden, const void* weight, int64_t
     cudaFuncSetAttribute(k_gemm_tn2<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2);
     cudaFuncSetAttribute(k_gemm_tn2<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2);
     cudaFuncSetAttribute(k_gemm_tn2<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2);
+    cudaFuncSetAttribute(k_lmhead_fwd2<kEpiLogits>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2);
   });
   cudaStream_t s = (cudaStream_t)stream;
   const int sms = sm_count();
   const int64_t Vp = (V + 7) / 8 * 8;
+  const int64_t NT = (V + BN - 1) / BN;
   auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
   char* base = reinterpret_cast<char*>(scratch);
   __nv_bfloat16* L = reinterpret_cast<__nv_bfloat16*>(base);
@@ -1196,21 +1264,55 @@ odpo_status odpo_lmhead_dpo_step(const void* hidden, const void* weight, int64_t
   char* ws = base + al((size_t)Rmax * Vp * 2);
   const size_t wsb = odpo_workspace_bytes(2 * chunk_pairs, T, chunk_pairs);
   double* cst = reinterpret_cast<double*>(ws + al(wsb));
+  float4* parts4 = reinterpret_cast<float4*>(reinterpret_cast<char*>(cst) + al(16 * sizeof(double)));
+  CUtensorMap mB;
+  if (!make_map(&mB, weight, V, d, d, BN / 2)) return ODPO_ERR_CUDA;
   for (int64_t p0 = 0; p0 < P; p0 += chunk_pairs) {
     const int64_t np = min(chunk_pairs, P - p0);
     const int64_t r0 = 2 * p0 * T, Rc = 2 * np * T;
     const char* hc = reinterpret_cast<const char*>(hidden) + r0 * d * 2;
-    // logits chunk [Rc, V] (row pitch Vp) = H_c W^T, bf16
-    odpo_status e = gemm2<false, false>(Operand{hc, d, false}, Operand{weight, d, false}, Rc, V, d,
-                                        nullptr, Vp, false, sms, s, L);
-    if (e != ODPO_OK) return e;
-    // the Online-DPO loss and dlogits, in place over the chunk
-    e = odpo_online_dpo_loss_fwd_bwd(L, ODPO_BF16, 2 * np, T, V, T * Vp, Vp, ref_logp + 2 * p0,
-                                     tokens + r0, mask + r0, nullptr, np, P_global, beta,
-                                     inv_temperature, L, T * Vp, Vp, seq_logp + 2 * p0,
-                                     pair_logit ? pair_logit + p0 : nullptr, cst, status, ws, wsb,
-                                     stream);
-    if (e != ODPO_OK) return e;
+    odpo_status e;
+    if (ODPO_STEP_FWD_PASS) {
+      // logits chunk [Rc, V] (row pitch Vp) = H_c W^T, bf16; the full loss call in place
+      e = gemm2<false, false>(Operand{hc, d, false}, Operand{weight, d, false}, Rc, V, d, nullptr,
+                              Vp, false, sms, s, L);
+      if (e != ODPO_OK) return e;
+      e = odpo_online_dpo_loss_fwd_bwd(L, ODPO_BF16, 2 * np, T, V, T * Vp, Vp, ref_logp + 2 * p0,
+                                       tokens + r0, mask + r0, nullptr, np, P_global, beta,
+                                       inv_temperature, L, T * Vp, Vp, seq_logp + 2 * p0,
+                                       pair_logit ? pair_logit + p0 : nullptr, cst, status, ws,
+                                       wsb, stream);
+      if (e != ODPO_OK) return e;
+    } else {
+      // logits chunk [Rc, V] (row pitch Vp) = H_c W^T in bf16 + the per-tile partials
+      CUtensorMap mA;
+      if (!make_map(&mA, hc, Rc, d, d, BM)) return ODPO_ERR_CUDA;
+      Args a{};
+      a.R = Rc; a.d = d; a.V = V;
+      a.nrb = (Rc + BM - 1) / BM;
+      a.NT = NT;
+      a.Ttot = a.nrb * a.NT;
+      a.nrb2 = (Rc + 255) / 256;
+      a.G = kRasterG / 2;
+      a.invT = inv_temperature;
+      a.tokens = tokens + r0;
+      a.mask = mask + r0;
+      a.gout = L;
+      a.ldg = Vp;
+      a.parts4 = parts4;
+      int clusters = sms / 2;
+      if (clusters > a.nrb2 * a.NT) clusters = (int)(a.nrb2 * a.NT);
+      void* args[] = {&mA, &mB, &a};
+      launch_pair((const void*)k_lmhead_fwd2<kEpiLogits>, clusters, s, args);
+      if (cudaGetLastError() != cudaSuccess) return ODPO_ERR_CUDA;
+      // row statistics from the NT partials, pair reduction, dlogits in place (one read)
+      e = odpo_vp_loss_fwd_bwd(reinterpret_cast<const float*>(parts4), (int32_t)NT, L, ODPO_BF16,
+                               2 * np, T, V, T * Vp, Vp, 0, V, ref_logp + 2 * p0, tokens + r0,
+                               mask + r0, nullptr, np, P_global, beta, inv_temperature, L, T * Vp,
+                               Vp, seq_logp + 2 * p0, pair_logit ? pair_logit + p0 : nullptr, cst,
+                               nullptr, 0u, status, ws, wsb, stream);
+      if (e != ODPO_OK) return e;
+    }
     k_stats_add<<<1, 32, 0, s>>>(stats, cst, ODPO_NSTATS, p0 == 0);
     if (cudaGetLastError() != cudaSuccess) return ODPO_ERR_CUDA;
     // dhidden = dlogits W (W read N-major); dweight += dlogits^T H (both read MN-major)

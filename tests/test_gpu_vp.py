@@ -27,9 +27,10 @@ def shard_bounds(V, W, align):
     return list(zip(cuts[:-1], cuts[1:]))
 
 
-@pytest.mark.parametrize("W", [1, 3, 8])
+@pytest.mark.parametrize("W", [1, 3, 8, 40])
 @pytest.mark.parametrize("dt", ["bf16", "f32"])
 def test_vp_parity(odpo, W, dt):
+    """W = 40 > 32 partials per row take the warp-per-row merge (k_vp_combine_wide)."""
     P, T, V = 3, 9, 12345 if dt == "f32" else 32000
     b = Batch(P, T, V, dt, seed=7, mask_kind="prefix", lbar=5, extra_seqs=1)
     ref = (synth.rewards_for(7, b.B, 1).reshape(-1) - 20.0).astype(np.float32)

@@ -226,13 +226,15 @@ def test_lmhead_grad_parity(shape):
 
 # ------------------------------------------------------------------ NEXT-2 chunked learner step
 @pytest.mark.parametrize("shape", [(3, 9, 128, 1000, 1), (3, 9, 128, 1000, 2), (4, 53, 256, 4133, 3),
-                                   (2, 64, 640, 2500, 5)],
+                                   (2, 64, 640, 2500, 5), (3, 16, 128, 12345, 2)],
                          ids=lambda s: f"P{s[0]}T{s[1]}d{s[2]}V{s[3]}cp{s[4]}")
 @pytest.mark.gpu
 @pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a CUDA device")
 def test_lmhead_dpo_step_parity(shape):
-    """odpo_lmhead_dpo_step (per chunk of pairs: bf16 logits from the library GEMM, the loss call
-    in place, dhidden / dweight from the library GEMMs) against the oracle on the same bf16
+    """odpo_lmhead_dpo_step (per chunk of pairs: bf16 logits and per-tile (m, log1p r, x_tok)
+    partials from the library's head kernel, the loss merged from the partials with dlogits in
+    place, dhidden / dweight from the library GEMMs; V = 12345 has 49 tiles, the warp-per-row
+    merge) against the oracle on the same bf16
     logits: the head's products are dyadic (synth.lmhead_inputs), so the fp32 tensor-core sum is
     exact and both sides round the same value to bf16.  Sequence log-probs, z and all ten
     statistics at the bf16 contract; dhidden / dweight element-wise within the propagated R17
