@@ -27,5 +27,9 @@ def test_compute_sanitizer(tool):
            os.path.join(ROOT, "profiles", "sanitize_run.py")]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     out = r.stdout + r.stderr
+    if "closed on this pool" in out:
+        # the GPU pool's operators disabled the tool (runs under it left GPUs needing a
+        # reset); the round-2 record of these runs is profiles/r02/sanitizer/
+        pytest.skip("compute-sanitizer is closed on this GPU pool")
     assert "sanitize run ok" in out, out[-2000:]
     assert "ERROR SUMMARY: 0 errors" in out, out[-2000:]
