@@ -866,6 +866,109 @@ __global__ void __launch_bounds__(kRowThreads, 2) k_row_bwd(LossArgs a) {
                               a.w.row_l1p[g], a.w.row_logp[g], coef, 0);
 }
 
+// K4s: the same backward with each row cut into pieces, one CTA per piece, every piece moved in
+// ONE batch of loads then stores (THR threads x U vectors of VW bytes).  Measured on B200
+// (profiles/r02/copy/): a copy kernel whose CTAs each move one ~32 KB batch reaches 6.98 TB/s of
+// read+write traffic, against 6.57 for cudaMemcpy and 6.60-6.63 for one 512-thread CTA looping
+// over a 256 KB (LLaMA) row; 32-byte vectors (sm_100 LDG/STG.256) help on the long rows.  The
+// per-element arithmetic is bwd_vec's, so the output is bit-identical to k_row_bwd's.
+// Pieces: S = ceil(nv / (THR U)) per row, per = ceil(nv / S) vectors each (even split).
+// VW = 32 needs 32-byte aligned rows (host check); VW = 16 is the 16-byte fallback.
+template <int VW>
+struct VecT;
+template <>
+struct VecT<16> {
+  uint4 h[1];
+};
+template <>
+struct VecT<32> {
+  uint4 h[2];
+};
+template <int VW>
+__device__ __forceinline__ VecT<VW> ldv(const char* p) {
+  VecT<VW> v;
+  if constexpr (VW == 32) {
+    asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(v.h[0].x), "=r"(v.h[0].y), "=r"(v.h[0].z), "=r"(v.h[0].w),
+                   "=r"(v.h[1].x), "=r"(v.h[1].y), "=r"(v.h[1].z), "=r"(v.h[1].w)
+                 : "l"(p));
+  } else {
+    v.h[0] = ld16<LD_STREAM>(reinterpret_cast<const uint4*>(p), 0);
+  }
+  return v;
+}
+template <int VW>
+__device__ __forceinline__ void stv(char* p, const VecT<VW>& v) {
+  if constexpr (VW == 32) {
+    asm volatile("st.global.L1::no_allocate.L2::evict_first.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
+                 ::"l"(p), "r"(v.h[0].x), "r"(v.h[0].y), "r"(v.h[0].z), "r"(v.h[0].w),
+                   "r"(v.h[1].x), "r"(v.h[1].y), "r"(v.h[1].z), "r"(v.h[1].w)
+                 : "memory");
+  } else {
+    st16_stream(reinterpret_cast<uint4*>(p), v.h[0]);
+  }
+}
+
+template <int DT, int NPB, int THR, int U, int VW>
+__global__ void __launch_bounds__(THR) k_row_bwd_split(LossArgs a) {
+  constexpr int N = Traits<DT>::N;            // elements per 16 bytes
+  constexpr int E = N * (VW / 16);            // elements per vector
+  const int V = (int)a.V;
+  const int nv = V / E;                       // whole vectors per row
+  const int S = (nv + THR * U - 1) / (THR * U);
+  const int64_t g = blockIdx.x / (S > 0 ? S : 1);
+  const int s = (int)(blockIdx.x - g * (S > 0 ? S : 1));
+  const int per = S > 0 ? (nv + S - 1) / S : 0;
+  const int v0 = s * per, v1 = min(nv, v0 + per);
+  const int64_t b = g / a.T, t = g % a.T;
+  char* drow = drow_ptr(a, b, t);
+  const char* row = row_ptr(a, b, t);
+  const bool last = s == (S > 0 ? S : 1) - 1;
+  const int tail = V - nv * E;                 // elements after the last whole vector
+  if (a.w.seq_pair[b] < 0 || !a.mask[g]) {
+    VecT<VW> z;
+#pragma unroll
+    for (int h = 0; h < VW / 16; ++h) z.h[h] = make_uint4(0, 0, 0, 0);
+    for (int i = v0 + (int)threadIdx.x; i < v1; i += THR) stv<VW>(drow + (int64_t)i * VW, z);
+    if (last && (int)threadIdx.x < tail) Traits<DT>::store1(drow, (int64_t)nv * E + threadIdx.x, 0.f);
+    return;
+  }
+  const float coef = a.w.seq_coef[b];
+  const int64_t tl = (int64_t)a.tokens[g] - a.tok_off;   // shard-local (vocabulary-parallel)
+  const int tok = (tl >= 0 && tl < V) ? (int)tl : -1;
+  const float k2 = a.invT * kLog2e;
+  const float m = a.w.row_m[g];
+  const float c = bwd_const<DT>(m, a.w.row_l1p[g], k2, coef);
+  const bool neg = coef < 0.f;
+  VecT<VW> v[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int i = v0 + (int)threadIdx.x + u * THR;
+    if (i < v1) v[u] = ldv<VW>(row + (int64_t)i * VW);
+  }
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int i = v0 + (int)threadIdx.x + u * THR;
+    if (i < v1) {
+#pragma unroll
+      for (int h = 0; h < VW / 16; ++h)
+        v[u].h[h] = neg ? bwd_vec<DT, NPB, true>(v[u].h[h], k2, c, m) : bwd_vec<DT, NPB, false>(v[u].h[h], k2, c, m);
+      stv<VW>(drow + (int64_t)i * VW, v[u]);
+    }
+  }
+  const float gtok = coef * expm1f(a.w.row_logp[g]);
+  if (last && (int)threadIdx.x < tail) {
+    const int64_t vv = (int64_t)nv * E + threadIdx.x;
+    const float x = Traits<DT>::load1(row, vv);
+    Traits<DT>::store1(drow, vv, (vv == tok) ? gtok : copysignf(ex2(bwd_arg<DT>(x, k2, c, m)), coef));
+  }
+  // onehot entry: written by the thread that stored tok's vector (program order)
+  if (tok >= 0 && tok < nv * E) {
+    const int iv = tok / E;
+    if (iv >= v0 && iv < v1 && (iv - v0) % THR == (int)threadIdx.x) Traits<DT>::store1(drow, tok, gtok);
+  }
+}
+
 // ------------------------------------------------------------------ the TMA-ring engine
 // M_SEQ: forward rows only.  M_FUSED: pair-scheduled forward + scaled backward.  M_UNSC: each
 // row's forward pass and then its unscaled backward G = softmax - onehot in the same CTA (the
@@ -1884,10 +1987,48 @@ static void launch_bf16(int pv, int grid, const LossArgs& a, cudaStream_t s) {
   }
   if constexpr (PV + 1 < kNumPoly) launch_bf16<MODE, PV + 1>(pv, grid, a, s);
 }
+// The row backward (TWO_PASS and the vocabulary-parallel loss): k_row_bwd_split's one-batch
+// pieces, 32-byte vectors when every row of the logits and of dlogits starts 32-byte aligned,
+// else 16-byte.  Configurations (threads, vectors per thread), measured side by side on B200
+// (profiles/r02/bwd/; all bit-identical): (512, 4) = pieces up to 64 KB is best on LLaMA (256.5
+// KB rows: 14.31 vs 14.71 ms for k_row_bwd's one CTA per row) and Rho (64 KB: 3.685 vs 3.772);
+// (256, 4) = up to 32 KB on Pythia (100.6 KB rows: 1.258 vs 1.269).  ODPO_BWD_CFG (build flag,
+// A/B only) forces one: -1 = k_row_bwd, 2 = (256, 4), 5 = (512, 4), 6 = (256, 8), 7 = (128, 8).
+#ifndef ODPO_BWD_CFG
+#define ODPO_BWD_CFG 0
+#endif
+constexpr int kBwdCfg = ODPO_BWD_CFG;
+
+template <int DT, int NPB, int THR, int U>
+static void launch_split(unsigned rows, const LossArgs& a, cudaStream_t s) {
+  const bool a32 = ((reinterpret_cast<uintptr_t>(a.logits) | reinterpret_cast<uintptr_t>(a.dl)) & 31u) == 0 &&
+                   ((a.sb | a.st | a.dsb | a.dst) * a.esize) % 32 == 0;
+  const int VW = a32 ? 32 : 16;
+  const int64_t nv = a.V / (Traits<DT>::N * (VW / 16));
+  int64_t S = (nv + THR * U - 1) / (THR * U);
+  if (S < 1) S = 1;
+  if ((int64_t)rows * S > (int64_t)INT32_MAX)
+    k_row_bwd<DT, NPB><<<rows, kRowThreads, 0, s>>>(a);
+  else if (a32)
+    k_row_bwd_split<DT, NPB, THR, U, 32><<<(unsigned)(rows * S), THR, 0, s>>>(a);
+  else
+    k_row_bwd_split<DT, NPB, THR, U, 16><<<(unsigned)(rows * S), THR, 0, s>>>(a);
+}
+template <int DT, int NPB>
+static void launch_row_bwd_t(unsigned rows, const LossArgs& a, cudaStream_t s) {
+  const int64_t row_bytes = a.V * a.esize;
+  if constexpr (kBwdCfg == -1) k_row_bwd<DT, NPB><<<rows, kRowThreads, 0, s>>>(a);
+  else if constexpr (kBwdCfg == 2) launch_split<DT, NPB, 256, 4>(rows, a, s);
+  else if constexpr (kBwdCfg == 5) launch_split<DT, NPB, 512, 4>(rows, a, s);
+  else if constexpr (kBwdCfg == 6) launch_split<DT, NPB, 256, 8>(rows, a, s);
+  else if constexpr (kBwdCfg == 7) launch_split<DT, NPB, 128, 8>(rows, a, s);
+  else if (row_bytes > (64 << 10) && row_bytes < (128 << 10)) launch_split<DT, NPB, 256, 4>(rows, a, s);
+  else launch_split<DT, NPB, 512, 4>(rows, a, s);
+}
 template <int PV>
 static void launch_bwd_bf16(int pv, unsigned rows, const LossArgs& a, cudaStream_t s) {
   if (pv == PV) {
-    k_row_bwd<1, kPoly[PV].npb><<<rows, kRowThreads, 0, s>>>(a);
+    launch_row_bwd_t<1, kPoly[PV].npb>(rows, a, s);
     return;
   }
   if constexpr (PV + 1 < kNumPoly) launch_bwd_bf16<PV + 1>(pv, rows, a, s);
@@ -2208,7 +2349,7 @@ odpo_status odpo_online_dpo_loss_fwd_bwd_ex(const void* policy_logits, odpo_dtyp
     k_pair_reduce<<<(unsigned)P, 32, 0, s>>>(a);
     if ((e = launched()) != ODPO_OK) return e;
     const unsigned rows = (unsigned)(B * T);
-    if (dt == ODPO_F32) k_row_bwd<0, 0><<<rows, kRowThreads, 0, s>>>(a);
+    if (dt == ODPO_F32) launch_row_bwd_t<0, 0>(rows, a, s);
     else launch_bwd_bf16<0>(pv, rows, a, s);
     if ((e = launched()) != ODPO_OK) return e;
     launches += 3;
@@ -2384,7 +2525,7 @@ odpo_status odpo_pg_loss_fwd_bwd(const void* policy_logits, odpo_dtype dt, int64
     k_pair_reduce<<<(unsigned)P, 32, 0, s>>>(a);
     if ((e = launched()) != ODPO_OK) return e;
     const unsigned rows = (unsigned)(B * T);
-    if (dt == ODPO_F32) k_row_bwd<0, 0><<<rows, kRowThreads, 0, s>>>(a);
+    if (dt == ODPO_F32) launch_row_bwd_t<0, 0>(rows, a, s);
     else launch_bwd_bf16<0>(pv, rows, a, s);
     if ((e = launched()) != ODPO_OK) return e;
     launches += 3;
@@ -2559,9 +2700,9 @@ odpo_status odpo_vp_loss_fwd_bwd(const float* parts_all, int32_t W, const void* 
     if (dt == ODPO_F32) k_row_bwd_warp<0><<<grid, 32 * kWarpRowsPerCta, 0, s>>>(a);
     else k_row_bwd_warp<1><<<grid, 32 * kWarpRowsPerCta, 0, s>>>(a);
   } else if (dt == ODPO_F32) {
-    k_row_bwd<0, 0><<<(unsigned)rows, kRowThreads, 0, s>>>(a);
+    launch_row_bwd_t<0, 0>((unsigned)rows, a, s);
   } else {
-    k_row_bwd<1, 0><<<(unsigned)rows, kRowThreads, 0, s>>>(a);
+    launch_row_bwd_t<1, 0>((unsigned)rows, a, s);
   }
   return launched();
 }
