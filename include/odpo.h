@@ -119,7 +119,7 @@ enum {
                               GPU not shared with other work).  Measured slower than FUSED
                               on B200; compiled only with
                               -DODPO_EXPERIMENTAL=1, UNSUPPORTED in the default build  */
-  ODPO_SCHED_PSYNC = 5     /* pair-synchronous split-V: every CTA takes the same fixed piece of
+  ODPO_SCHED_PSYNC = 5,    /* pair-synchronous split-V: every CTA takes the same fixed piece of
                               every pair (the pair's 2T rows flattened and cut into one piece
                               per CTA), forward pieces of pair p + lag run before the backward
                               pieces of pair p, so lag + 1 pairs are live and the backward
@@ -129,6 +129,17 @@ enum {
                               ODPO_ERR_CUDA).  Needs V a multiple of the vector width and a
                               piece of at most one row; UNSUPPORTED otherwise.  Deterministic;
                               row statistics merged in piece order (not FUSED's bits).  */
+  ODPO_SCHED_SPLIT = 6     /* factored gradient only (odpo_online_dpo_loss_fwd_bwd_unscaled,
+                              odpo_pg_loss_fwd_bwd's single-pass kinds): each row split over a
+                              thread-block cluster of up to 8 CTAs, one vocabulary piece per
+                              CTA held in registers between its one HBM read and its one HBM
+                              write; the CTA partials merged through distributed shared
+                              memory.  Needs V * elt <= 256 KB per 8 pieces (bf16 V <=
+                              262144); UNSUPPORTED otherwise.  Deterministic; its reduction
+                              tree differs from the engine's (results agree to rounding).
+                              Measured slower than the row engine on B200 (DESIGN.md
+                              section 4); compiled only with -DODPO_EXPERIMENTAL=1,
+                              UNSUPPORTED in the default build                          */
 };
 
 typedef struct {
@@ -291,8 +302,10 @@ odpo_status odpo_online_dpo_loss_fwd_bwd_ex(const void* policy_logits, odpo_dtyp
  *   folds row_scale into its epilogue / prologue.  G does not depend on the pair outcome, so
  *   each row's backward follows its own forward in the same CTA and re-reads the row from L2:
  *   one HBM read and one HBM write of [B,T,V] for every shape.
- *   opts (may be NULL): schedule must be AUTO; ctas_per_sm, exp2_split, lookahead, row_gap apply;
- *   opts->launches returns 2.  Other arguments and errors as odpo_online_dpo_loss_fwd_bwd.
+ *   opts (may be NULL): schedule AUTO (the row engine), SPLIT (ODPO_SCHED_SPLIT: clusters
+ *   of CTAs per row, no L2 re-read) or RESIDENT (experimental build); ctas_per_sm,
+ *   exp2_split, lookahead, row_gap apply to the engine; opts->launches returns 2.  Other
+ *   arguments and errors as odpo_online_dpo_loss_fwd_bwd.
  */
 odpo_status odpo_online_dpo_loss_fwd_bwd_unscaled(
     const void* policy_logits, odpo_dtype dt, int64_t B, int64_t T, int64_t V, int64_t stride_b,

@@ -34,7 +34,8 @@ SEL_NAMES = ["margin_sum", "ndegen", "ntrunc"]
 NSTATS, NSEL, STATS_BUF = 10, 3, 16
 FLAGS = {"TOKEN_RANGE": 1, "NONFINITE_LOGIT": 2, "EMPTY_SEQ": 4, "NONFINITE_REWARD": 8,
          "DUP_ROW": 16, "DEGENERATE_PAIR": 32, "PAIR_RANGE": 64}
-SCHEDULES = {"auto": 0, "fused": 1, "two_pass": 2, "wave": 3, "resident": 4, "psync": 5}
+SCHEDULES = {"auto": 0, "fused": 1, "two_pass": 2, "wave": 3, "resident": 4, "psync": 5,
+             "split": 6}
 _DT = {torch.float32: 0, torch.bfloat16: 1}
 
 

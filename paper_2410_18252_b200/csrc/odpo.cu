@@ -10,7 +10,10 @@
 //                        finishing a pair's last forward row runs K3b; backward rows wait on
 //                        the pair's ready flag; backward re-reads hit L2 (evict_last policy)
 //   k_pair_reduce    K3b one warp per pair (TWO_PASS)
-//   k_row_bwd        K4  one CTA per row: dlogits = coef (softmax - onehot) (TWO_PASS)
+//   k_row_bwd_split  K4  dlogits = coef (softmax - onehot), each row in one-batch pieces
+//                        (TWO_PASS; k_row_bwd: one CTA per row, for grids past INT32_MAX)
+//   k_engine<UNSC>   K5' factored gradient: each row's backward right after its forward
+//   k_unsc_split/tma --  (experimental build) factored gradient over thread-block clusters
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
@@ -968,6 +971,402 @@ __global__ void __launch_bounds__(THR) k_row_bwd_split(LossArgs a) {
     if (iv >= v0 && iv < v1 && (iv - v0) % THR == (int)threadIdx.x) Traits<DT>::store1(drow, tok, gtok);
   }
 }
+
+#if ODPO_EXPERIMENTAL   // measured slower than the row engine (profiles/r02/split/)
+// K5c: the factored gradient (G = softmax - onehot; coef*G when the coefficient is known
+// before the call, App B) with each row split over a thread-block cluster of CS CTAs, one
+// vocabulary piece of <= THR*U vectors per CTA, held in registers from its load to its store:
+//   load the piece (all loads in flight) -> the piece's online (m, r) and x_tok -> fixed-order
+//   warp / CTA merge -> the CTA partial stored into every peer's shared memory (DSMEM) ->
+//   cluster barrier -> every CTA merges the CS partials in rank order (the same bits in every
+//   CTA) -> G from the registers -> rank 0 writes the row statistics and counts the row into
+//   its pair (the last row of a pair runs the pair reduction, as in the engine).
+// Exactly one HBM read and one write of every row, with no L2 re-read (the engine's factored
+// mode re-reads each row from L2 and loses 10-16% of the re-reads to misses), and each CTA
+// moves one batch: the access pattern measured fastest for read+write traffic on B200
+// (profiles/r02/copy/).  Deterministic (a fixed reduction tree per (CS, THR, U)); the tree
+// differs from the engine's, so its results agree with the engine's to rounding, not bitwise.
+// Units: the pair-ordered rows of the engine's tickets [0, 2PT); CTAs past them zero the rows of
+// unreferenced sequences (grid-stride over k_prep's list).
+template <int DT, int CS, int THR, int U, int VW>
+__global__ void __launch_bounds__(THR) k_unsc_split(const __grid_constant__ LossArgs a) {
+  constexpr int N = Traits<DT>::N;
+  constexpr int H = VW / 16;                 // 16-byte halves per vector
+  constexpr int E = N * H;                   // elements per vector
+  constexpr int NB = U * H;                  // 16-byte words per thread
+  constexpr int NW = THR / 32;
+  __shared__ float s_wm[NW], s_wr[NW], s_wx[NW];
+  __shared__ int s_wo[NW];
+  __shared__ float4 s_cp[CS];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int V = (int)a.V;
+  const int nv = V / E;
+  const int per = (nv + CS - 1) / CS;
+  const int64_t T = a.T, R = 2 * T, totalF = a.P * R;
+  const int64_t unit = blockIdx.x / CS;
+  const int rank = (int)(blockIdx.x % CS);   // == %cluster_ctarank (1-D clusters along x)
+  const int tail = V - nv * E;
+  if (unit >= totalF) {   // zero workers: rows of sequences no pair references
+    const int64_t nz = (int64_t)__ldcg(&a.w.counters[C_NUNREF]) * T;
+    const int64_t z0 = (int64_t)blockIdx.x - totalF * CS, nzw = (int64_t)gridDim.x - totalF * CS;
+    for (int64_t z = z0; z < nz; z += nzw) {
+      const int64_t s = __ldcg(a.w.unref + z / T), t = z % T;
+      char* drow = drow_ptr(a, s, t);
+      VecT<VW> zv;
+#pragma unroll
+      for (int h = 0; h < H; ++h) zv.h[h] = make_uint4(0, 0, 0, 0);
+      for (int i = tid; i < nv; i += THR) stv<VW>(drow + (int64_t)i * VW, zv);
+      if (tid < tail) Traits<DT>::store1(drow, (int64_t)nv * E + tid, 0.f);
+      if (tid == 0 && a.row_scale) a.row_scale[s * T + t] = 0.f;
+    }
+    return;
+  }
+  if (CS > 1) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");  // started
+  const int64_t p = unit / R, j = unit % R;
+  int64_t c, r;
+  pair_seqs(a, p, c, r);
+  const int64_t s = j < T ? c : r, t = j < T ? j : j - T;
+  const int64_t g = s >= 0 ? s * T + t : 0;
+  const bool live = s >= 0 && a.mask[g];
+  const int v0 = rank * per, v1 = min(nv, v0 + per);
+  const bool tail_owner = rank == CS - 1;
+  const float k2 = a.invT * kLog2e;
+  if (!live) {   // the engine's K_FSKIP (counted once) + K_ZERO
+    if (CS > 1) asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+    if (s >= 0) {
+      char* drow = drow_ptr(a, s, t);
+      VecT<VW> zv;
+#pragma unroll
+      for (int h = 0; h < H; ++h) zv.h[h] = make_uint4(0, 0, 0, 0);
+      for (int i = v0 + tid; i < v1; i += THR) stv<VW>(drow + (int64_t)i * VW, zv);
+      if (tail_owner && tid < tail) Traits<DT>::store1(drow, (int64_t)nv * E + tid, 0.f);
+      if (rank == 0 && tid == 0 && a.row_scale) a.row_scale[g] = 0.f;
+    }
+    if (rank == 0 && warp == 0) {
+      unsigned last = 0;
+      if (lane == 0) last = atom_add_acq_rel(&a.w.pair_cnt[p], 1u) == (unsigned)R - 1u;
+      last = __shfl_sync(kFull, last, 0);
+      if (last) {
+        fence_acq_rel_gpu();
+        pair_reduce_warp(a, p);
+      }
+    }
+    return;
+  }
+  const char* row = row_ptr(a, s, t);
+  char* drow = drow_ptr(a, s, t);
+  const int tok = a.tokens[g];
+  // ---- the piece, all loads in flight
+  uint4 w[NB];
+  const uint32_t NI = Traits<DT>::kNegInfWord;
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int i = v0 + tid + u * THR;
+    if (i < v1) {
+      const VecT<VW> x = ldv<VW>(row + (int64_t)i * VW);
+#pragma unroll
+      for (int h = 0; h < H; ++h) w[u * H + h] = x.h[h];
+    } else {
+#pragma unroll
+      for (int h = 0; h < H; ++h) w[u * H + h] = make_uint4(NI, NI, NI, NI);
+    }
+  }
+  MR st{-INFINITY, 0.f};
+  mr_batch<DT, NB, 0>(w, k2, st.m, st.r);
+  float xt = 0.f;
+  int own = 0;
+  const int tv = (tok >= 0 && tok < nv * E) ? tok / E : -1;
+  const bool tok_mine = tv >= v0 && tv < v1 && (tv - v0) % THR == tid;
+  if (tok_mine) {
+    const int u = (tv - v0) / THR, e = tok % E;
+    const int kk = u * H + e / N;
+    uint4 sel = w[0];
+#pragma unroll
+    for (int k = 1; k < NB; ++k) sel = (k == kk) ? w[k] : sel;   // register selects, no local copy
+    float f[N];
+    Traits<DT>::unpack(sel, f);
+    xt = f[0];
+#pragma unroll
+    for (int q = 1; q < N; ++q) xt = (e % N == q) ? f[q] : xt;
+    own = 1;
+  }
+  if (tail_owner && tid < tail) {
+    const int64_t vv = (int64_t)nv * E + tid;
+    const float x = Traits<DT>::load1(row, vv);
+    st = mr_push1(st, x, k2);
+    if (vv == tok) { xt = x; own = 1; }
+  }
+  // ---- fixed-order merges: warp, CTA, then the cluster's CS partials in rank order
+  const MR wm = warp_merge(st, k2);
+  const unsigned ob = __ballot_sync(kFull, own);
+  const float wx = __shfl_sync(kFull, xt, ob ? __ffs(ob) - 1 : 0);
+  if (lane == 0) { s_wm[warp] = wm.m; s_wr[warp] = wm.r; s_wx[warp] = wx; s_wo[warp] = ob != 0; }
+  __syncthreads();
+  if (warp == 0) {
+    MR x = lane < NW ? MR{s_wm[lane], s_wr[lane]} : MR{-INFINITY, 0.f};
+    x = warp_merge(x, k2);
+    const int o = lane < NW ? s_wo[lane] : 0;
+    const unsigned ob2 = __ballot_sync(kFull, o);
+    const float cx = __shfl_sync(kFull, lane < NW ? s_wx[lane] : 0.f, ob2 ? __ffs(ob2) - 1 : 0);
+    if (CS > 1) {
+      const float pm = __shfl_sync(kFull, x.m, 0), pr = __shfl_sync(kFull, x.r, 0);
+      asm volatile("barrier.cluster.wait.aligned;" ::: "memory");  // every peer has started
+      if (lane < CS) {   // lane q stores this CTA's partial into CTA q's slot [rank]
+        const uint32_t dst = mapa((uint32_t)__cvta_generic_to_shared(&s_cp[rank]), (uint32_t)lane);
+        st_cl_u32(dst, __float_as_uint(pm));
+        st_cl_u32(dst + 4, __float_as_uint(pr));
+        st_cl_u32(dst + 8, __float_as_uint(cx));
+        st_cl_u32(dst + 12, __float_as_uint(ob2 ? 1.f : 0.f));
+      }
+    } else if (lane == 0) {
+      s_cp[0] = make_float4(x.m, x.r, cx, ob2 ? 1.f : 0.f);
+    }
+  } else if (CS > 1) {
+    asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+  }
+  if (CS > 1) cluster_sync_all();
+  else __syncthreads();
+  MR u{-INFINITY, 0.f};
+  float xr = 0.f;
+#pragma unroll
+  for (int q = 0; q < CS; ++q) {
+    const float4 cp = s_cp[q];
+    u = mr_merge(u, MR{cp.x, cp.y}, k2);
+    if (cp.w != 0.f) xr = cp.z;
+  }
+  const float l1p = log1pf(u.r);
+  const bool tok_ok = tok >= 0 && tok < V;
+  const float logp = tok_ok ? __fsub_rn(__fmul_rn(__fsub_rn(xr, u.m), a.invT), l1p) : 0.f;
+  // ---- G (coef * G with a known coefficient) straight from the registers
+  const float cf = a.coef_known ? __ldcg(a.w.seq_coef + s) : 1.f;
+  const float cc = cf != 0.f ? bwd_const<DT>(u.m, l1p, k2, cf) : INFINITY;
+  const float gtok = cf * expm1f(logp);
+  const bool neg = cf < 0.f;
+#pragma unroll
+  for (int q = 0; q < U; ++q) {
+    const int i = v0 + tid + q * THR;
+    if (i < v1) {
+      VecT<VW> o;
+#pragma unroll
+      for (int h = 0; h < H; ++h)
+        o.h[h] = neg ? bwd_vec<DT, 0, true>(w[q * H + h], k2, cc, u.m)
+                     : bwd_vec<DT, 0, false>(w[q * H + h], k2, cc, u.m);
+      stv<VW>(drow + (int64_t)i * VW, o);
+    }
+  }
+  if (tail_owner && tid < tail) {
+    const int64_t vv = (int64_t)nv * E + tid;
+    const float x = Traits<DT>::load1(row, vv);
+    Traits<DT>::store1(drow, vv, vv == tok ? gtok : copysignf(ex2(bwd_arg<DT>(x, k2, cc, u.m)), cf));
+  }
+  if (tok_mine) Traits<DT>::store1(drow, tok, gtok);   // onehot entry (program order)
+  // ---- row statistics, then the row counts into its pair
+  if (rank == 0 && warp == 0) {
+    unsigned last = 0;
+    if (lane == 0) {
+      uint32_t fl = 0;
+      if (!tok_ok) fl |= ODPO_FLAG_TOKEN_RANGE;
+      else if (!isfinite(logp)) fl |= ODPO_FLAG_NONFINITE_LOGIT;
+      if (!isfinite(u.m) || !isfinite(u.r)) fl |= ODPO_FLAG_NONFINITE_LOGIT;
+      a.w.row_m[g] = u.m;
+      a.w.row_l1p[g] = l1p;
+      a.w.row_logp[g] = logp;
+      flag(a.status, fl);
+      last = atom_add_acq_rel(&a.w.pair_cnt[p], 1u) == (unsigned)R - 1u;
+    }
+    last = __shfl_sync(kFull, last, 0);
+    if (last) {
+      fence_acq_rel_gpu();
+      pair_reduce_warp(a, p);
+    }
+  }
+}
+
+// K5t: the same split, the piece staged in shared memory by ONE 1-D bulk TMA copy instead of
+// registers, so a CTA holds no data registers and up to 7 CTAs (32 KB pieces) share an SM:
+// more bytes in flight per SM while other CTAs of the SM sit in their merge / barrier phases.
+template <int DT, int CS, int THR>
+__global__ void __launch_bounds__(THR) k_unsc_tma(const __grid_constant__ LossArgs a) {
+  constexpr int N = Traits<DT>::N;
+  constexpr int NW = THR / 32;
+  extern __shared__ __align__(128) uint4 sm_piece[];
+  __shared__ __align__(8) uint64_t s_bar;
+  __shared__ float s_wm[NW], s_wr[NW];
+  __shared__ float4 s_cp[CS];
+  __shared__ float s_xt;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int V = (int)a.V;
+  const int nv = V / N;                      // whole 16-byte vectors per row
+  const int per = (nv + CS - 1) / CS;
+  const int64_t T = a.T, R = 2 * T, totalF = a.P * R;
+  const int64_t unit = blockIdx.x / CS;
+  const int rank = (int)(blockIdx.x % CS);
+  const int tail = V - nv * N;
+  if (unit >= totalF) {   // zero workers: rows of sequences no pair references
+    const int64_t nz = (int64_t)__ldcg(&a.w.counters[C_NUNREF]) * T;
+    const int64_t z0 = (int64_t)blockIdx.x - totalF * CS, nzw = (int64_t)gridDim.x - totalF * CS;
+    for (int64_t z = z0; z < nz; z += nzw) {
+      const int64_t s = __ldcg(a.w.unref + z / T), t = z % T;
+      uint4* drow = reinterpret_cast<uint4*>(drow_ptr(a, s, t));
+      for (int i = tid; i < nv; i += THR) st16_stream(drow + i, make_uint4(0, 0, 0, 0));
+      if (tid < tail) Traits<DT>::store1(drow, (int64_t)nv * N + tid, 0.f);
+      if (tid == 0 && a.row_scale) a.row_scale[s * T + t] = 0.f;
+    }
+    return;
+  }
+  if (CS > 1) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");  // started
+  const int64_t p = unit / R, j = unit % R;
+  int64_t c, r;
+  pair_seqs(a, p, c, r);
+  const int64_t s = j < T ? c : r, t = j < T ? j : j - T;
+  const int64_t g = s >= 0 ? s * T + t : 0;
+  const bool live = s >= 0 && a.mask[g];
+  const int v0 = rank * per, v1 = min(nv, v0 + per), n = max(v1 - v0, 0);
+  const bool tail_owner = rank == CS - 1;
+  const float k2 = a.invT * kLog2e;
+  if (!live) {   // the engine's K_FSKIP (counted once) + K_ZERO
+    if (CS > 1) asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+    if (s >= 0) {
+      uint4* drow = reinterpret_cast<uint4*>(drow_ptr(a, s, t));
+      for (int i = v0 + tid; i < v1; i += THR) st16_stream(drow + i, make_uint4(0, 0, 0, 0));
+      if (tail_owner && tid < tail) Traits<DT>::store1(drow, (int64_t)nv * N + tid, 0.f);
+      if (rank == 0 && tid == 0 && a.row_scale) a.row_scale[g] = 0.f;
+    }
+    if (rank == 0 && warp == 0) {
+      unsigned last = 0;
+      if (lane == 0) last = atom_add_acq_rel(&a.w.pair_cnt[p], 1u) == (unsigned)R - 1u;
+      last = __shfl_sync(kFull, last, 0);
+      if (last) {
+        fence_acq_rel_gpu();
+        pair_reduce_warp(a, p);
+      }
+    }
+    return;
+  }
+  const char* row = row_ptr(a, s, t);
+  char* drow = drow_ptr(a, s, t);
+  const uint32_t bar = smem_u32(&s_bar);
+  if (tid == 0) {
+    mbar_init(&s_bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (n > 0) {
+      mbar_arrive_tx(bar, (uint32_t)n * 16u);
+      tma_load_1d(smem_u32(sm_piece), row + (int64_t)v0 * 16, (uint32_t)n * 16u, bar,
+                  policy_evict_first());
+    } else {
+      mbar_arrive(bar);
+    }
+  }
+  const int tok = a.tokens[g];
+  const int tv = (tok >= 0 && tok < nv * N) ? tok / N : -1;
+  MR st{-INFINITY, 0.f};
+  float xt_tail = 0.f;
+  bool own_tail = false;
+  if (tail_owner && tid < tail) {   // the row's last V mod N elements, straight from HBM
+    const int64_t vv = (int64_t)nv * N + tid;
+    const float x = Traits<DT>::load1(row, vv);
+    st = mr_push1(st, x, k2);
+    if (vv == tok) { xt_tail = x; own_tail = true; }
+  }
+  __syncthreads();          // the barrier is initialised before anyone waits on it
+  mbar_wait(bar, 0);
+  const uint32_t NI = Traits<DT>::kNegInfWord;
+  for (int base = tid; base < n; base += 8 * THR) {
+    uint4 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = base + u * THR;
+      v[u] = i < n ? sm_piece[i] : make_uint4(NI, NI, NI, NI);
+    }
+    mr_batch<DT, 8, 0>(v, k2, st.m, st.r);
+  }
+  const MR wm = warp_merge(st, k2);
+  const unsigned otb = __ballot_sync(kFull, own_tail);
+  if (otb) {
+    const float x = __shfl_sync(kFull, xt_tail, __ffs(otb) - 1);
+    if (lane == 0) s_xt = x;
+  }
+  if (tid == 0 && tv >= v0 && tv < v1) {
+    float f[N];
+    Traits<DT>::unpack(sm_piece[tv - v0], f);
+    float x = f[0];
+#pragma unroll
+    for (int q = 1; q < N; ++q) x = (tok % N == q) ? f[q] : x;
+    s_xt = x;
+  }
+  if (lane == 0) { s_wm[warp] = wm.m; s_wr[warp] = wm.r; }
+  __syncthreads();
+  if (warp == 0) {
+    MR x = lane < NW ? MR{s_wm[lane], s_wr[lane]} : MR{-INFINITY, 0.f};
+    x = warp_merge(x, k2);
+    const bool own = (tv >= v0 && tv < v1) || (tail_owner && tok >= nv * N && tok < V);
+    const float cx = own ? s_xt : 0.f;
+    const float pm = __shfl_sync(kFull, x.m, 0), pr = __shfl_sync(kFull, x.r, 0);
+    if (CS > 1) {
+      asm volatile("barrier.cluster.wait.aligned;" ::: "memory");  // every peer has started
+      if (lane < CS) {
+        const uint32_t dst = mapa((uint32_t)__cvta_generic_to_shared(&s_cp[rank]), (uint32_t)lane);
+        st_cl_u32(dst, __float_as_uint(pm));
+        st_cl_u32(dst + 4, __float_as_uint(pr));
+        st_cl_u32(dst + 8, __float_as_uint(cx));
+        st_cl_u32(dst + 12, __float_as_uint(own ? 1.f : 0.f));
+      }
+    } else if (lane == 0) {
+      s_cp[0] = make_float4(pm, pr, cx, own ? 1.f : 0.f);
+    }
+  } else if (CS > 1) {
+    asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+  }
+  if (CS > 1) cluster_sync_all();
+  else __syncthreads();
+  MR u{-INFINITY, 0.f};
+  float xr = 0.f;
+#pragma unroll
+  for (int q = 0; q < CS; ++q) {
+    const float4 cp = s_cp[q];
+    u = mr_merge(u, MR{cp.x, cp.y}, k2);
+    if (cp.w != 0.f) xr = cp.z;
+  }
+  const float l1p = log1pf(u.r);
+  const bool tok_ok = tok >= 0 && tok < V;
+  const float logp = tok_ok ? __fsub_rn(__fmul_rn(__fsub_rn(xr, u.m), a.invT), l1p) : 0.f;
+  const float cf = a.coef_known ? __ldcg(a.w.seq_coef + s) : 1.f;
+  const float cc = cf != 0.f ? bwd_const<DT>(u.m, l1p, k2, cf) : INFINITY;
+  const float gtok = cf * expm1f(logp);
+  uint4* vout = reinterpret_cast<uint4*>(drow) + v0;
+  if (cf < 0.f) {
+    for (int i = tid; i < n; i += THR) st16_stream(vout + i, bwd_vec<DT, 0, true>(sm_piece[i], k2, cc, u.m));
+  } else {
+    for (int i = tid; i < n; i += THR) st16_stream(vout + i, bwd_vec<DT, 0, false>(sm_piece[i], k2, cc, u.m));
+  }
+  if (tail_owner && tid < tail) {
+    const int64_t vv = (int64_t)nv * N + tid;
+    const float x = Traits<DT>::load1(row, vv);
+    Traits<DT>::store1(drow, vv, vv == tok ? gtok : copysignf(ex2(bwd_arg<DT>(x, k2, cc, u.m)), cf));
+  }
+  if (tv >= v0 && tv < v1 && (tv - v0) % THR == tid) Traits<DT>::store1(drow, tok, gtok);
+  if (rank == 0 && warp == 0) {
+    unsigned last = 0;
+    if (lane == 0) {
+      uint32_t fl = 0;
+      if (!tok_ok) fl |= ODPO_FLAG_TOKEN_RANGE;
+      else if (!isfinite(logp)) fl |= ODPO_FLAG_NONFINITE_LOGIT;
+      if (!isfinite(u.m) || !isfinite(u.r)) fl |= ODPO_FLAG_NONFINITE_LOGIT;
+      a.w.row_m[g] = u.m;
+      a.w.row_l1p[g] = l1p;
+      a.w.row_logp[g] = logp;
+      flag(a.status, fl);
+      last = atom_add_acq_rel(&a.w.pair_cnt[p], 1u) == (unsigned)R - 1u;
+    }
+    last = __shfl_sync(kFull, last, 0);
+    if (last) {
+      fence_acq_rel_gpu();
+      pair_reduce_warp(a, p);
+    }
+  }
+}
+
+#endif  // ODPO_EXPERIMENTAL
 
 // ------------------------------------------------------------------ the TMA-ring engine
 // M_SEQ: forward rows only.  M_FUSED: pair-scheduled forward + scaled backward.  M_UNSC: each
@@ -2042,6 +2441,103 @@ static int pick_geo(int mode, int64_t row_bytes, int pv, int geo) {
   return (mode == M_UNSC && row_bytes > (128 << 10)) ? 1 : 0;
 }
 
+#if ODPO_EXPERIMENTAL
+// The cluster-split factored gradient (k_unsc_split): pieces of <= 1024 32-byte vectors (256
+// threads x 4) or <= 2048 (512 x 4) per CTA, CS = a power of two <= 8 CTAs per row.  Returns
+// false (nothing launched) when a row needs more than 8 pieces; the caller uses the engine.
+template <int DT, int CS, int THR, int VW>
+static void launch_split_cs(unsigned grid, const LossArgs& a, cudaStream_t s) {
+  auto kern = k_unsc_split<DT, CS, THR, 4, VW>;
+  if (CS == 1) {
+    kern<<<grid, THR, 0, s>>>(a);
+    return;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(THR);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = (unsigned)CS;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, a);
+}
+template <int DT, int THR, int VW>
+static void launch_split_thr(int cs, unsigned grid, const LossArgs& a, cudaStream_t s) {
+  if (cs == 1) launch_split_cs<DT, 1, THR, VW>(grid, a, s);
+  else if (cs == 2) launch_split_cs<DT, 2, THR, VW>(grid, a, s);
+  else if (cs == 4) launch_split_cs<DT, 4, THR, VW>(grid, a, s);
+  else launch_split_cs<DT, 8, THR, VW>(grid, a, s);
+}
+template <int DT, int CS, int THR>
+static void launch_tma_cs(unsigned grid, int smem, const LossArgs& a, cudaStream_t s) {
+  auto kern = k_unsc_tma<DT, CS, THR>;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(THR);
+  cfg.dynamicSmemBytes = (size_t)smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = (unsigned)CS;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = CS > 1 ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, kern, a);
+}
+// TMA-staged variant: pieces of <= 32 KB (<= 48 KB past 256 KB rows), CS <= 8.
+template <int DT>
+static bool launch_unsc_tma(const LossArgs& a, cudaStream_t s) {
+  const int64_t nv = a.V / Traits<DT>::N;
+  int64_t need = (nv + 2047) / 2048;
+  if (need > 8) need = 8;
+  const int cs = need <= 1 ? 1 : need <= 2 ? 2 : need <= 4 ? 4 : 8;
+  const int64_t per = (nv + cs - 1) / cs;
+  if (per * 16 > (48 << 10)) return false;
+  const int smem = (int)(per * 16);
+  const int64_t grid = (a.P * 2 * a.T + 2 * 148) * cs;
+  if (grid > (int64_t)INT32_MAX) return false;
+  if (cs == 1) launch_tma_cs<DT, 1, 128>((unsigned)grid, smem, a, s);
+  else if (cs == 2) launch_tma_cs<DT, 2, 128>((unsigned)grid, smem, a, s);
+  else if (cs == 4) launch_tma_cs<DT, 4, 128>((unsigned)grid, smem, a, s);
+  else launch_tma_cs<DT, 8, 128>((unsigned)grid, smem, a, s);
+  return true;
+}
+
+template <int DT>
+static bool launch_unsc_split(const LossArgs& a, cudaStream_t s) {
+  const bool a32 = ((reinterpret_cast<uintptr_t>(a.logits) | reinterpret_cast<uintptr_t>(a.dl)) & 31u) == 0 &&
+                   ((a.sb | a.st | a.dsb | a.dst) * a.esize) % 32 == 0;
+  const int VW = a32 ? 32 : 16;
+  const int64_t nv = a.V / (Traits<DT>::N * (VW / 16));
+  int thr = 256;
+  int64_t need = (nv + 1023) / 1024;
+  if (need > 8) {
+    thr = 512;
+    need = (nv + 2047) / 2048;
+  }
+  if (need > 8) return false;
+  const int cs = need <= 1 ? 1 : need <= 2 ? 2 : need <= 4 ? 4 : 8;
+  const int64_t zero_workers = 2 * 148;   // rows of unreferenced sequences (grid-stride)
+  const int64_t grid = (a.P * 2 * a.T + zero_workers) * cs;
+  if (grid > (int64_t)INT32_MAX) return false;
+  if (thr == 256) {
+    if (VW == 32) launch_split_thr<DT, 256, 32>(cs, (unsigned)grid, a, s);
+    else launch_split_thr<DT, 256, 16>(cs, (unsigned)grid, a, s);
+  } else {
+    if (VW == 32) launch_split_thr<DT, 512, 32>(cs, (unsigned)grid, a, s);
+    else launch_split_thr<DT, 512, 16>(cs, (unsigned)grid, a, s);
+  }
+  return true;
+}
+
+#endif  // ODPO_EXPERIMENTAL
+
 static odpo_status launch_engine(int dt, int mode, int pv, const LossArgs& a, int cps,
                                  cudaStream_t s, int geo) {
   int dev = 0;
@@ -2432,10 +2928,12 @@ odpo_status odpo_online_dpo_loss_fwd_bwd_unscaled(
   if (e != ODPO_OK) return e;
   if (!row_scale) return ODPO_ERR_INVALID_ARG;
   const bool resident = opts && opts->schedule == ODPO_SCHED_RESIDENT;
-  if (opts && opts->schedule != ODPO_SCHED_AUTO && !resident) return ODPO_ERR_UNSUPPORTED;
+  const bool split = opts && opts->schedule == ODPO_SCHED_SPLIT;
+  if (opts && opts->schedule != ODPO_SCHED_AUTO && !resident && !split) return ODPO_ERR_UNSUPPORTED;
   if (resident && !ODPO_EXPERIMENTAL) return ODPO_ERR_UNSUPPORTED;
   const int pv = (opts && opts->exp2_split >= 0) ? opts->exp2_split : kPolyDefault;
   if (pv >= kNumPoly) return ODPO_ERR_UNSUPPORTED;
+  if (split && pv != 0) return ODPO_ERR_UNSUPPORTED;
   Workspace w;
   ws_layout(B, T, P, (char*)workspace, &w);
   cudaStream_t s = (cudaStream_t)stream;
@@ -2454,6 +2952,19 @@ odpo_status odpo_online_dpo_loss_fwd_bwd_unscaled(
   a.row_gap = (opts && opts->row_gap >= 0) ? opts->row_gap : 0;
   k_prep<<<1, kPrepThreads, 0, s>>>(pair_rows, B, P, w, status, B * T);
   if ((e = launched()) != ODPO_OK) return e;
+  if (split) {
+#if ODPO_EXPERIMENTAL
+    const bool tma = opts->engine == 2;   // A/B: 2 = the TMA-staged pieces, else registers
+    if (!(tma ? (dt == ODPO_F32 ? launch_unsc_tma<0>(a, s) : launch_unsc_tma<1>(a, s))
+              : (dt == ODPO_F32 ? launch_unsc_split<0>(a, s) : launch_unsc_split<1>(a, s))))
+      return ODPO_ERR_UNSUPPORTED;
+#else
+    return ODPO_ERR_UNSUPPORTED;   // built without ODPO_EXPERIMENTAL (measured slower: DESIGN 4)
+#endif
+    if ((e = launched()) != ODPO_OK) return e;
+    opts->launches = 2;
+    return ODPO_OK;
+  }
   if (resident) {
     if (pv != 0) return ODPO_ERR_UNSUPPORTED;
     if ((e = launch_res_un(dt == ODPO_F32 ? 0 : 1, a, V, dt == ODPO_F32 ? 4 : 2, opts->lookahead,

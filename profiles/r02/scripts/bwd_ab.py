@@ -15,6 +15,11 @@ sys.path.insert(0, ROOT)
 import synth  # noqa: E402
 import paper_2410_18252_b200 as odpo  # noqa: E402
 
+PV = -1
+if "--pv" in sys.argv:   # exp2_split variant (odpo_launch_opts.exp2_split)
+    i = sys.argv.index("--pv")
+    PV = int(sys.argv[i + 1])
+    del sys.argv[i:i + 2]
 lib = sys.argv[1]
 if lib != "main":
     odpo.LIB_PATH = os.path.abspath(lib)
@@ -37,7 +42,7 @@ for name in sys.argv[2:]:
         flush.zero_()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
-        out = odpo.online_dpo_loss_fwd_bwd(x, ref, tok, mask, 0.03, dlogits=dl)
+        out = odpo.online_dpo_loss_fwd_bwd(x, ref, tok, mask, 0.03, dlogits=dl, exp2_split=PV)
         b.record()
         torch.cuda.synchronize()
         if i >= 2:
@@ -46,7 +51,7 @@ for name in sys.argv[2:]:
     w = dl.view(torch.int16).view(-1)
     h = int((w[::7].to(torch.int64) * 2654435761 % 1000003).sum().item())
     alg = 2.0 * B * T * V * 2
-    print(json.dumps({"lib": lib, "config": name, "ms": ms, "min_ms": min(times),
+    print(json.dumps({"lib": lib, "pv": PV, "config": name, "ms": ms, "min_ms": min(times),
                       "frac": alg / (ms / 1e3) / 1e9 / peak, "hash": h,
                       "loss": out.stats[1].item()}), flush=True)
     del x, dl, out
