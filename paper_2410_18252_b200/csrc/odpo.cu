@@ -2088,13 +2088,7 @@ __global__ void __launch_bounds__(GE::THREADS, GE::CPS) k_engine(LossArgs a) {
           for (int u = 0; u < kUB; ++u) v[u] = sv[tid + u * kNCT];
           mr_batch<DT, kUB, NPF>(v, k2, s.m, s.r);
         } else if (tid < cnv) {
-          uint4 v[kUB];
-#pragma unroll
-          for (int u = 0; u < kUB; ++u) {
-            const int i = tid + u * kNCT;
-            v[u] = i < cnv ? sv[i] : make_uint4(NI, NI, NI, NI);
-          }
-          mr_batch<DT, kUB, NPF>(v, k2, s.m, s.r);
+          mr_partial<DT, kUB, NPF>(sv, tid, kNCT, cnv, k2, s.m, s.r);
         }
         if (own_tok) {
           float f[N];

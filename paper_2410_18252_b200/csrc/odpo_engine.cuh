@@ -257,6 +257,39 @@ __device__ __forceinline__ void mr_batch(const uint4 (&v)[NB], float k2, float& 
   r += s;
 }
 
+#ifndef ODPO_PARTIAL_OLD
+#define ODPO_PARTIAL_OLD 0
+#endif
+// A partial chunk (cnv vectors, fewer than a full chunk): a thread with at most half a batch
+// of vectors takes them in batches of 2.  One 8-vector batch padded with -inf would spend an
+// exp2 on every padding element: for Pythia's 100.6 KB rows (six 16 KB chunks and a 2.3 KB
+// one) that was a seventh chunk's worth of MUFU work per row.
+template <int DT, int UB, int NPF>
+__device__ __forceinline__ void mr_partial(const uint4* sv, int tid, int stride, int cnv, float k2,
+                                           float& m, float& r) {
+  const uint32_t NI = Traits<DT>::kNegInfWord;
+  // this thread's vectors in the chunk; more than half a batch: the padded full batch (the
+  // extra max checks of 2-vector batches cost more than the padding's exp2s there; measured)
+  const int nr = (cnv - tid + stride - 1) / stride;
+  if (ODPO_PARTIAL_OLD || 2 * nr > UB) {
+    uint4 w[UB];
+#pragma unroll
+    for (int u = 0; u < UB; ++u) w[u] = tid + u * stride < cnv ? sv[tid + u * stride] : make_uint4(NI, NI, NI, NI);
+    mr_batch<DT, UB, NPF>(w, k2, m, r);
+    return;
+  }
+#pragma unroll
+  for (int u = 0; u < UB; u += 2) {
+    const int i0 = tid + u * stride;
+    if (i0 >= cnv) break;
+    const int i1 = i0 + stride;
+    uint4 v[2];
+    v[0] = sv[i0];
+    v[1] = (u + 1 < UB && i1 < cnv) ? sv[i1] : make_uint4(NI, NI, NI, NI);
+    mr_batch<DT, 2, NPF>(v, k2, m, r);
+  }
+}
+
 // warp-level fixed-order (m, r) merge; result valid in lane 0
 __device__ __forceinline__ MR warp_merge(MR v, float k2) {
 #pragma unroll

@@ -413,7 +413,7 @@ __global__ void __launch_bounds__(kResThreads, 1) k_resident(LossArgs a, ResGeo 
               v[u] = i < cnv ? sb[i] : make_uint4(NI, NI, NI, NI);
             }
             if (ts >= 0) tm_st<kResUB>(tcol + (uint32_t)(c * kResCols), v);
-            if (gtid < cnv) mr_batch<DT, kResUB, NPF>(v, k2, s.m, s.r);
+            if (gtid < cnv) mr_partial<DT, kResUB, NPF>(sb, gtid, kResFT, cnv, k2, s.m, s.r);
           }
           if (tvec >= c0 && tvec < c0 + cnv && ((tvec - c0) % kResFT) == gtid) {
             float f[N];

@@ -13,6 +13,8 @@ sys.path.insert(0, ROOT)
 import synth  # noqa: E402
 import paper_2410_18252_b200 as odpo  # noqa: E402
 
+if len(sys.argv) > 1 and sys.argv[1].endswith(".so"):
+    odpo.LIB_PATH = os.path.abspath(sys.argv.pop(1))
 CFG = {"pythia": (256, 53, 50304), "rho": (128, 512, 32000), "llama": (64, 1024, 128256),
        "tiny": (4, 53, 50304)}
 peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
@@ -34,12 +36,17 @@ for name in sys.argv[1:]:
                 flush.zero_()
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a.record()
-                out = odpo.online_dpo_loss_fwd_bwd_unscaled(x, ref, tok, mask, 0.03, G=G,
-                                                            schedule=sched, engine=eng)
+                try:
+                    out = odpo.online_dpo_loss_fwd_bwd_unscaled(x, ref, tok, mask, 0.03, G=G,
+                                                                schedule=sched, engine=eng)
+                except odpo.OdpoError:
+                    break   # split: experimental build only
                 b.record()
                 torch.cuda.synchronize()
                 if i >= 2:
                     times.append(a.elapsed_time(b))
+            if not times:
+                continue
             ms = float(np.median(times))
             print(json.dumps({"config": name, "schedule": sched + ("_tma" if eng == 2 else ""), "ms": ms, "min_ms": min(times),
                               "frac": 2.0 * B * T * V * 2 / (ms / 1e3) / 1e9 / peak,
