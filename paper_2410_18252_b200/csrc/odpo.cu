@@ -2391,6 +2391,15 @@ static void launch_bf16(int pv, int grid, const LossArgs& a, cudaStream_t s) {
 #define ODPO_BWD_CFG 0
 #endif
 constexpr int kBwdCfg = ODPO_BWD_CFG;
+// Short vocabulary-shard rows (<= 32 KB): the backward in one-batch pieces of 128 threads x 4
+// vectors (LLaMA W = 8: 1.28 vs 1.355 ms, Pythia W = 8: 0.139 vs 0.148, Rho W = 2: 1.27 vs 1.34;
+// profiles/r02/vp/); the forward partials stay warp-per-row (a CTA per row measured slower:
+// five fixed-order merges per row instead of one).  ODPO_VP_WARP=1 (A/B only): the warp-per-row
+// backward.
+#ifndef ODPO_VP_WARP
+#define ODPO_VP_WARP 0
+#endif
+constexpr bool kVpWarp = ODPO_VP_WARP != 0;
 
 template <int DT, int NPB, int THR, int U>
 static void launch_split(unsigned rows, const LossArgs& a, cudaStream_t s) {
@@ -3202,8 +3211,14 @@ odpo_status odpo_vp_loss_fwd_bwd(const float* parts_all, int32_t W, const void* 
   if ((e = launched()) != ODPO_OK) return e;
   if (V_shard * (dt == ODPO_F32 ? 4 : 2) <= (32 << 10)) {  // short shard rows: a warp per row
     const unsigned grid = (unsigned)((rows + kWarpRowsPerCta - 1) / kWarpRowsPerCta);
-    if (dt == ODPO_F32) k_row_bwd_warp<0><<<grid, 32 * kWarpRowsPerCta, 0, s>>>(a);
-    else k_row_bwd_warp<1><<<grid, 32 * kWarpRowsPerCta, 0, s>>>(a);
+    if (kVpWarp) {
+      if (dt == ODPO_F32) k_row_bwd_warp<0><<<grid, 32 * kWarpRowsPerCta, 0, s>>>(a);
+      else k_row_bwd_warp<1><<<grid, 32 * kWarpRowsPerCta, 0, s>>>(a);
+    } else if (dt == ODPO_F32) {
+      launch_split<0, 0, 128, 4>((unsigned)rows, a, s);
+    } else {
+      launch_split<1, 0, 128, 4>((unsigned)rows, a, s);
+    }
   } else if (dt == ODPO_F32) {
     launch_row_bwd_t<0, 0>((unsigned)rows, a, s);
   } else {

@@ -27,7 +27,10 @@ def main():
     ap.add_argument("--put", action="store_true",
                     help="the in-kernel exchange (odpo_vp_row_partials_put + the waiting merge), "
                          "the W ranks' buffers emulated on this GPU")
+    ap.add_argument("--lib", default=None, help="a variant build of libodpo.so (A/B)")
     a = ap.parse_args()
+    if a.lib:
+        odpo.LIB_PATH = os.path.abspath(a.lib)
     w = CONFIGS[a.config]
     B, T, V = 2 * w.P, w.T, w.V
     dev = torch.device("cuda:0")
