@@ -92,12 +92,15 @@ def bf16_peak():
 
 
 def src_sha() -> str:
-    """Hash of the product kernel sources (csrc + the C header): an ncu capture is used as this
-    run's traffic evidence only if it was taken on the same sources."""
+    """Hash of the sources the loss call's kernels are compiled from (odpo.cu and the headers
+    it includes, the C header; not odpo_lmhead.cu, whose NEXT-2 kernels the captured loss
+    call never launches): an ncu capture is used as this run's traffic evidence only if it was
+    taken on the same sources."""
     import glob
     import hashlib
     h = hashlib.sha256()
-    files = sorted(glob.glob(os.path.join(ROOT, "paper_2410_18252_b200", "csrc", "*.cu*")))
+    files = sorted(f for f in glob.glob(os.path.join(ROOT, "paper_2410_18252_b200", "csrc", "*.cu*"))
+                   if not f.endswith("odpo_lmhead.cu"))
     for f in files + [os.path.join(ROOT, "include", "odpo.h")]:
         h.update(open(f, "rb").read())
     return h.hexdigest()[:16]
