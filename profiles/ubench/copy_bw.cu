@@ -79,6 +79,33 @@ __global__ void __launch_bounds__(512, 2) k_row32(const u8v* __restrict__ in, u8
   }
 }
 
+template <int THR, int U, bool W32, int MINB>
+__global__ void __launch_bounds__(THR, MINB) k_chunk(const char* __restrict__ in, char* __restrict__ out, int64_t chunk) {
+  const char* r = in + (int64_t)blockIdx.x * chunk;
+  char* o = out + (int64_t)blockIdx.x * chunk;
+  if (W32) {
+    const int64_t n = chunk / 32;
+    const u8v* ri = reinterpret_cast<const u8v*>(r); u8v* oi = reinterpret_cast<u8v*>(o);
+    for (int64_t base = threadIdx.x; base < n; base += THR * U) {
+      u8v v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) if (base + THR * u < n) v[u] = ld32(ri + base + THR * u);
+#pragma unroll
+      for (int u = 0; u < U; ++u) if (base + THR * u < n) { v[u].x[0] ^= 1u; st32(oi + base + THR * u, v[u]); }
+    }
+  } else {
+    const int64_t n = chunk / 16;
+    const uint4* ri = reinterpret_cast<const uint4*>(r); uint4* oi = reinterpret_cast<uint4*>(o);
+    for (int64_t base = threadIdx.x; base < n; base += THR * U) {
+      uint4 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) if (base + THR * u < n) v[u] = ld16(ri + base + THR * u);
+#pragma unroll
+      for (int u = 0; u < U; ++u) if (base + THR * u < n) st16<0>(oi + base + THR * u, xf(v[u]));
+    }
+  }
+}
+
 __global__ void __launch_bounds__(512) k_read(const uint4* __restrict__ in, int64_t n, unsigned* sink) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   unsigned acc = 0;
@@ -177,6 +204,22 @@ int main(int argc, char** argv) {
   printf("N = %lld bytes in + out, %d SMs\n", (long long)N, sms);
   RUNK("torch-like cudaMemcpy D2D", cudaMemcpyAsync(C.out, C.in, C.nvec * 16, cudaMemcpyDeviceToDevice));
   static int G;
+
+  if (argc > 2) {   // chunk sweep only
+    static int64_t CHB;
+    for (int64_t cb : {16384LL, 32768LL, 50304LL, 65536LL, 100608LL, 131072LL, 128256LL, 256512LL}) {
+      CHB = cb;
+      G = (int)(N / cb);
+      double sb = bytes; bytes = 2.0 * (double)G * cb;
+      char nm[64];
+#define CH(T, U, W, MB) snprintf(nm, 64, "chunk %6lld T%d U%d %s mb%d", (long long)cb, T, U, W ? "v8" : "v4", MB); \
+      RUNK(nm, (k_chunk<T, U, W, MB><<<G, T>>>((const char*)C.in, (char*)C.out, CHB)));
+      CH(512, 8, false, 2) CH(512, 4, true, 2) CH(512, 2, true, 2) CH(256, 8, false, 4) CH(256, 4, true, 4)
+      CH(1024, 4, false, 1) CH(1024, 2, true, 1) CH(128, 8, false, 8) CH(128, 4, true, 8)
+      bytes = sb;
+    }
+    return 0;
+  }
   for (int mult : {2, 4, 8}) {
     G = sms * mult;
     char nm[64];
