@@ -540,3 +540,41 @@ def test_psync_full_pythia(odpo, lag):
                                        b.tokens[seqs], b.mask[seqs], w.beta, p_global=w.P,
                                        n_threads=NCPU)
     check_seq(ps.seq_logp.cpu().numpy()[seqs], o["seq_logp"], w.dtype)
+
+
+# ------------------------------------------------------------------------ split-row backward
+@pytest.mark.parametrize("V,dt,pad", [(32767, "bf16", 0), (32768, "bf16", 0), (32769, "bf16", 0),
+                                      (65552, "bf16", 0), (100000, "bf16", 0), (16384, "f32", 0),
+                                      (16391, "f32", 0), (50304, "bf16", 8), (131072, "bf16", 0)])
+def test_two_pass_piece_boundaries(odpo, V, dt, pad):
+    """k_row_bwd_split cuts each row into one-batch pieces (S = ceil(vectors / (threads x 4)),
+    32-byte vectors on 32-byte aligned rows, else 16-byte): around piece and vector boundaries,
+    with the sampled token placed in the first, a middle and the last piece and in the ragged
+    tail, the two-pass dlogits equal FUSED's (the engine's in-kernel backward, the same
+    per-element arithmetic) bit for bit, and the oracle on every row.  pad: extra row elements
+    (a row stride that is 16- but not 32-byte aligned for bf16 pad 8)."""
+    P, T = 2, 4
+    b = Batch(P, T, V, dt, seed=11, host=False)
+    if pad:
+        es = 4 if dt == "f32" else 2
+        x = torch.empty((b.B, T, V + pad), dtype=b.d_logits.dtype, device="cuda")[:, :, :V]
+        x.copy_(b.d_logits)
+        b.d_logits = x
+    tok = b.d_tokens.clone()
+    places = [0, V // 3, V // 2 + 1, V - 1, V - 2, 17, (V // 16) * 16 - 1, V // 7]
+    for i in range(b.B * T):
+        tok.view(-1)[i] = places[i % len(places)] % V
+    b.d_tokens = tok
+    b.tokens = tok.cpu().numpy()
+    ref = torch.full((b.B,), -3.0 * T, device="cuda")
+    two = run_loss(odpo, b, ref, 0.1, "two_pass")
+    fus = run_loss(odpo, b, ref, 0.1, "fused")
+    assert torch.equal(two.dlogits, fus.dlogits)
+    assert torch.equal(two.stats[:10], fus.stats[:10])
+    assert int(two.status.item()) == 0
+    h = Batch(P, T, V, dt, seed=11, host=True)
+    h.tokens = b.tokens
+    o = oracle.online_dpo_loss_fwd_bwd(h.h_logits if not pad else h.h_logits, ref.cpu().numpy(),
+                                       b.tokens, h.mask, 0.1, want_dlogits=True, n_threads=NCPU)
+    coef = coef_from_oracle(o, P, P, 0.1, 1.0, None, b.B)
+    check_dlogits(to_f64(two.dlogits), o["dlogits"], coef[:, None, None], dt)
