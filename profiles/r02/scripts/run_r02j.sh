@@ -1,16 +1,9 @@
+# Headline spread (three back-to-back default bench runs) and the multi-rank bench path (two
+# ranks sharing the GPU over gloo, with and without the peer-memory stats exchange)
 O=gpurun_out/r02j; mkdir -p $O
-timeout 900 python -m pytest tests/test_lmhead.py -q -x --timeout 600 2>&1 | tail -2
-timeout 600 python profiles/r02/lmhead_grad_bench.py --quick 2>&1 | tail -1
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k_gemm|k_lmhead_fwd2" --csv --log-file $O/grad_launches.csv python profiles/r02/lmhead_grad_bench.py --quick > /dev/null 2>&1
-python profiles/summarize_ncu.py r02j_grad pythia grad $O/grad_launches.csv 2>&1 | grep "k_"
-ab() { python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); r=d['roofline']; print('$1', d['config']['workload'], 'loss_ms %.3f frac %.3f' % (r['loss_ms_mean'], r['frac']), d['clocks']['sm_mhz'])"; }
-for cps in 0 1; do
-  timeout 300 python bench.py --config llama --gradient unscaled --steps 10 --warmup 3 --no-aux --no-e2e --no-cpu --ctas-per-sm $cps 2>/dev/null | ab llama_geo1_cps$cps
-done
-timeout 300 python bench.py --config llama --gradient unscaled --steps 10 --warmup 3 --no-aux --no-e2e --no-cpu --engine 0 2>/dev/null | ab llama_geo0
-for cps in 0 2 3; do
-  timeout 300 python bench.py --config pythia --gradient unscaled --steps 20 --warmup 5 --no-aux --no-e2e --no-cpu --ctas-per-sm $cps 2>/dev/null | ab pythia_geo0_cps$cps
-done
-timeout 300 python bench.py --config pythia --gradient unscaled --steps 20 --warmup 5 --no-aux --no-e2e --no-cpu --engine 1 2>/dev/null | ab pythia_geo1
-timeout 300 python bench.py --config rho --gradient unscaled --steps 20 --warmup 5 --no-aux --no-e2e --no-cpu 2>/dev/null | ab rho_auto
-timeout 300 python bench.py --config rho --gradient unscaled --steps 20 --warmup 5 --no-aux --no-e2e --no-cpu --engine 1 2>/dev/null | ab rho_geo1
+for i in 1 2 3; do timeout 900 python bench.py > $O/bench_llama_$i.json 2> $O/bench_llama_$i.err; done
+export ODPO_SHARE_GPU=1 ODPO_DIST_BACKEND=gloo
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29541 bench.py --gpus 2 --config pythia --steps 5 --warmup 3 --no-aux --no-e2e --stats-exchange > $O/two_ranks_exchange.json 2> $O/two_ranks_exchange.err
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29542 bench.py --gpus 2 --config pythia --steps 5 --warmup 3 --no-aux --no-e2e > $O/two_ranks_allreduce.json 2> $O/two_ranks_allreduce.err
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29543 bench.py --impl reference --gpus 2 --steps 1 --warmup 1 > $O/two_ranks_reference.json 2> $O/two_ranks_reference.err
+for f in $O/*.json; do echo $f; tail -1 $f | cut -c1-400; done
