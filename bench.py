@@ -66,6 +66,10 @@ def parse():
                     help="N > 1: the statistics SUM over peer memory (odpo_stats_put/_sum through "
                          "a VPExchange: CUDA IPC / NVLink P2P) instead of the NCCL all-reduce")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-graph", action="store_true",
+                    help="issue every timed step from Python instead of replaying CUDA graphs of "
+                         "the step's library calls (the replays keep the GPU fed: no host "
+                         "marshalling gap inside the timed region)")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--lib", default=None,
@@ -518,9 +522,64 @@ def run_ours(args, rank, world, local_rank):
         launches[0] = 1 + out.launches
         return out
 
+    def graphed(gradient):
+        """The step as two CUDA graphs sharing one memory pool -- (A) pair_select (+ gather for
+        K > 2), (B) the loss call -- replayed A then B; the statistics all-reduce stays eager
+        between replays (a collective).  Each replay launches exactly the library's kernels of
+        one eager step, on the same buffers; only the Python marshalling leaves the timed
+        region.  Returns a step(timed_loss) closure, or None when capture fails (eager)."""
+        if args.no_graph or args.stats_exchange:
+            return None
+        try:
+            pool = torch.cuda.graph_pool_handle()
+            gA, gB = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+            side = torch.cuda.Stream()
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side):     # the capture stream's workspace, allocated eagerly
+                sel_w = odpo.pair_select(rewards, eos, pen, status=status, sel_stats=stats[10:13])
+                loss_call(gradient, sel_w.pair_rows if Kc == 2 else None, ref_logp, tokens, mask)
+            torch.cuda.current_stream().wait_stream(side)
+            torch.cuda.synchronize()
+            keep = {}
+            with torch.cuda.graph(gA, pool=pool, stream=side):
+                sel = odpo.pair_select(rewards, eos, pen, status=status, sel_stats=stats[10:13])
+                keep["sel"] = sel
+                if Kc > 2:
+                    keep["g"] = odpo.gather_pairs(sel.pair_rows, tokens_all, mask_all, ref_all,
+                                                  status=status)
+            with torch.cuda.graph(gB, pool=pool, stream=side):
+                if Kc > 2:
+                    tok_g, msk_g, ref_g = keep["g"]
+                    keep["out"] = loss_call(gradient, None, ref_g, tok_g, msk_g)
+                else:
+                    keep["out"] = loss_call(gradient, sel.pair_rows, ref_logp, tokens, mask)
+            torch.cuda.synchronize()
+        except Exception as e:   # noqa: BLE001 -- report and time the eager step instead
+            print(f"bench: CUDA graph capture failed ({e}); timing eager steps", file=sys.stderr)
+            torch.cuda.synchronize()
+            return None
+
+        def gstep(timed_loss=None, gradient=gradient):
+            gA.replay()
+            if timed_loss is not None:
+                timed_loss[0].record()
+            gB.replay()
+            if timed_loss is not None:
+                timed_loss[1].record()
+            odpo.allreduce_stats(stats, exchange=sx)
+            return keep["out"]
+        gstep.keep = keep
+        return gstep
+
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    gstep_main = graphed(args.gradient)
+    if gstep_main is not None:
+        for _ in range(2):
+            gstep_main()
+        torch.cuda.synchronize()
+    timed_step = gstep_main if gstep_main is not None else step
     if world > 1:
         dist.barrier()
 
@@ -533,7 +592,7 @@ def run_ours(args, rank, world, local_rank):
             flush.zero_()                      # untimed L2 flush between steps
             torch.cuda.synchronize()
             ev[k][0].record()
-            step(lev[k])
+            timed_step(lev[k])
             ev[k][1].record()
         torch.cuda.synchronize()
     step_ms = np.array([a.elapsed_time(b) for a, b in ev])
@@ -546,6 +605,13 @@ def run_ours(args, rank, world, local_rank):
     tot_ms = float(tot.item())
     value = world * P * K / (tot_ms / 1e3)
     st = int(status.item())
+    # the replayed graphs compute what an eager step computes: same statistics, same dlogits
+    graph_check = None
+    if gstep_main is not None and world == 1:
+        g_stats, g_dl = stats[:10].clone(), dlogits.view(-1)[:: 4099].clone()
+        step()
+        torch.cuda.synchronize()
+        graph_check = bool(torch.equal(g_stats, stats[:10]) and torch.equal(g_dl, dlogits.view(-1)[:: 4099]))
 
     # algorithmic bytes per loss launch: read the live rows once, write every dlogit once
     alg_bytes = rho * B * T * V * s_in + B * T * V * s_in
@@ -560,12 +626,16 @@ def run_ours(args, rank, world, local_rank):
         other = "unscaled" if args.gradient == "scaled" else "scaled"
         for _ in range(2):
             step(gradient=other)
+        torch.cuda.synchronize()
+        gstep_aux = graphed(other)
+        aux_step = gstep_aux if gstep_aux is not None else (lambda t: step(t, gradient=other))
+        aux_step(None)
         aev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                for _ in range(K)]
         for k in range(K):
             flush.zero_()
             torch.cuda.synchronize()
-            step(aev[k], gradient=other)
+            aux_step(aev[k])
         torch.cuda.synchronize()
         ams = np.array([a.elapsed_time(b) for a, b in aev])
         aach = alg_bytes / (ams.mean() / 1e3) / 1e9
@@ -678,6 +748,10 @@ def run_ours(args, rank, world, local_rank):
                        "schedule": args.schedule, "exp2_split": args.exp2_split,
                        "loss": args.loss, "gradient": args.gradient, "engine": args.engine,
                        "parallelism": f"dp{world}",
+                       "launch": ("CUDA graph replays of the step's library calls (pair_select; "
+                                  "the loss call), statistics reduction eager"
+                                  if gstep_main is not None else "eager Python calls"),
+                       "graph_matches_eager": graph_check,
                        "stats_reduction": ("peer memory (odpo_stats_put/_sum)" if args.stats_exchange
                                            and world > 1 else "NCCL all_reduce" if world > 1 else "none"),
                        "l2": "inputs (%.2f GB) > L2; plus 256 MiB L2 flush between timed steps"
