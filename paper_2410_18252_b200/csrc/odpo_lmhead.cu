@@ -31,6 +31,9 @@
 namespace odpo {
 namespace lmh {
 
+#ifndef ODPO_LMH_NOEPI
+#define ODPO_LMH_NOEPI 0   // A/B power probe only: the forward's epilogue skips its TMEM reads
+#endif
 constexpr int BM = 128;            // rows per tile (UMMA M)
 constexpr int BN = 256;            // vocabulary per tile (UMMA N)
 constexpr int BK = 64;             // hidden elements per stage (128 B = one swizzle row)
@@ -442,7 +445,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const int64_t c0 = n * BN;
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
+      for (int c = 0; c < (ODPO_LMH_NOEPI ? 0 : BN / 32); ++c) {   // NOEPI: A/B power probe only
         uint32_t r[32];
         tm_ld32(tmem + lane_base + (uint32_t)(acc * BN + c * 32), r);
         const int64_t cb = c0 + 32 * c;
