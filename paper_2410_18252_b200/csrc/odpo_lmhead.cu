@@ -118,6 +118,7 @@ struct Args {
   // LOGITS epilogue (the chunked learner step): the bf16 logits into gout, and per (row, tile)
   // the vocabulary-parallel partial (m, log1p r, x_tok, owns tok) of those bf16 values, [NT][R]
   float4* parts4;
+  unsigned long long* tile_ctr;  // CTA-pair kernels: the dynamic tile counter (zeroed per launch)
 };
 
 __device__ __forceinline__ void tile_coords(const Args& a, int64_t t, int64_t& rb, int64_t& n) {
@@ -321,6 +322,81 @@ __device__ __forceinline__ void tile_coords2(const Args& a, int64_t t, int64_t& 
   rb2 = r0 + idx % gg;
 }
 
+// Dynamic tile order of the CTA-pair kernels.  With tiles dealt round-robin to the persistent
+// pairs, a pair that runs 1% slower falls tens of tiles behind by the end of a LLaMA-size call:
+// the pairs that should share a hidden block or a weight tile through L2 drift apart in K and
+// fetch it again from HBM (ncu: 170-400 GB of DRAM reads per LLaMA-head forward against 62 GB
+// for cuBLAS's GEMM), which at the 1000 W cap costs clock (profiles/r02/next2/power_dram.md).
+// Instead the leader's producer claims the next tile from a global counter, so the tiles in
+// flight are always a contiguous window of the raster order, and hands the index to every other
+// role of the pair through a small ring in shared memory (the peer's copy written over DSMEM):
+// qfull[q] (1 arrival: the leader's producer) in each CTA, qempty[q] in the leader (kTQCons
+// arrivals: the leader's MMA thread and 4 epilogue warps, the peer's producer and 4 epilogue
+// warps).  Index -1 ends the sequence.  ODPO_LMH_STATIC=1 (A/B only) keeps the round-robin deal.
+#ifndef ODPO_LMH_STATIC
+#define ODPO_LMH_STATIC 0
+#endif
+constexpr bool kStaticTiles = ODPO_LMH_STATIC != 0;
+constexpr int kTQ = 8;
+// Host: the counter to use for a launch of `tiles` tiles over `clusters` pairs, or nullptr for
+// the round-robin deal.  The drift that the dynamic order removes grows with the tiles each pair
+// runs; below ~512 per pair (the Pythia head: 283) the round-robin deal measured 2% faster (the
+// ring hand-off costs more than the drift), above it (the LLaMA head: 3466) the dynamic order
+// cuts DRAM reads 2x and runs 9-13% faster at the power cap (profiles/r02/next2/dyn/).
+static unsigned long long* tile_mode(unsigned long long* ctr, int64_t tiles, int clusters) {
+  if (kStaticTiles || clusters <= 0 || tiles < 512 * (int64_t)clusters) return nullptr;
+  return ctr;
+}
+// Host: pair-blocks (256 rows) per raster group of the head kernels: ~40 MB of hidden rows kept
+// for reuse across the group's pass over the weight (measured with the dynamic order: LLaMA
+// d = 4096 best at 12-24 pair-blocks, Pythia d = 2560 at 32), clamped to [8, 32].
+static int lmh_group(int64_t d) {
+  int64_t g = (40ll << 20) / (512 * d);
+  if (g < 8) g = 8;
+  if (g > 32) g = 32;
+  return (int)g;
+}
+constexpr int kTQCons = 10;
+struct TileRing {
+  uint32_t full_s, empty_leader;   // this CTA's qfull, the leader's qempty (cluster address)
+  long long* tq;
+  uint32_t tq_peer;                // the peer's tq (cluster address; leader only)
+};
+// The leader's producer: publish the i-th tile of this pair (claimed one tile ahead, so the
+// counter's round trip overlaps the previous tile's loads) to both CTAs.
+__device__ __forceinline__ int64_t tile_publish(const TileRing& R, int i, long long t,
+                                                uint32_t empty_local) {
+  const int q = i % kTQ;
+  const uint32_t ph = (uint32_t)((i / kTQ) & 1);
+  mbar_wait(empty_local + 8 * q, ph ^ 1u);
+  R.tq[q] = t;
+  st_cl_u64(R.tq_peer + 8 * q, (uint64_t)t);
+  asm volatile("fence.acq_rel.cluster;" ::: "memory");
+  mbar_arrive(R.full_s + 8 * q);
+  mbar_arrive_cl(mapa(R.full_s + 8 * q, 1));
+  return (int64_t)t;
+}
+// Every other role: read the i-th tile index (one thread), release the slot.  The release is
+// a relaxed arrive: the slot's value has been consumed (the caller's branch on it) before the
+// arrive can be performed, and a release fence here would wait for this thread's own
+// outstanding stores (the epilogue's) at every tile.
+__device__ __forceinline__ void tile_release(const TileRing& R, int i) {
+  const int q = i % kTQ;
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(R.empty_leader + 8 * q)
+               : "memory");
+}
+__device__ __forceinline__ int64_t tile_read(const TileRing& R, int i) {
+  const int q = i % kTQ;
+  const uint32_t ph = (uint32_t)((i / kTQ) & 1);
+  mbar_wait_cl(R.full_s + 8 * q, ph);
+  long long t;
+  asm volatile("ld.volatile.shared.s64 %0, [%1];" : "=l"(t) : "r"(smem_u32(R.tq + q)) : "memory");
+  // consume the value before releasing the slot (the branch orders the load before the arrive)
+  if (t < -1) __trap();
+  tile_release(R, i);
+  return (int64_t)t;
+}
+
 // Epilogue kinds.  LSE: fold each tile into the rows' online logsumexp partials (forward).
 // GRAD: the same GEMM tiles, but the epilogue writes the row's gradient with respect to the
 // logits, G = row_scale (softmax(invT x) - onehot) in bf16, instead of folding an online
@@ -336,6 +412,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   constexpr bool GRAD = EPI == kEpiGrad, LOGITS = EPI == kEpiLogits;
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full[STAGES2], empty[STAGES2], tfull[2], tempty[2];
+  __shared__ __align__(8) uint64_t qfull[kTQ], qempty[kTQ];
+  __shared__ __align__(8) long long tq[kTQ];
   // GRAD / LOGITS epilogue: per epilogue warp a 32-row x 64-byte staging tile (rows padded to 80 B)
   __shared__ __align__(16) uint4 gstage[4][(GRAD || LOGITS) ? 32 * 5 : 1];
   __shared__ uint32_t tmem_sh;
@@ -347,6 +425,10 @@ __global__ void __launch_bounds__(THREADS, 1)
     for (int s = 0; s < STAGES2; ++s) {
       mbar_init(&full[s], 1);    // the leader's producer (expect_tx of both CTAs' bytes)
       mbar_init(&empty[s], 1);   // the leader's multicast MMA commit
+    }
+    for (int q = 0; q < kTQ; ++q) {
+      mbar_init(&qfull[q], 1);         // the leader's producer (tile index published)
+      mbar_init(&qempty[q], kTQCons);  // every reader of the pair (leader's copy is the one used)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);   // multicast commit
@@ -369,16 +451,34 @@ __global__ void __launch_bounds__(THREADS, 1)
   const uint32_t tmem = tmem_sh;
   const uint32_t full_s = smem_u32(full), empty_s = smem_u32(empty);
   const uint32_t tfull_s = smem_u32(tfull), tempty_s = smem_u32(tempty);
+  TileRing R;
+  R.full_s = smem_u32(qfull);
+  R.empty_leader = mapa(smem_u32(qempty), 0);
+  R.tq = tq;
+  R.tq_peer = mapa(smem_u32(tq), 1);
+  const uint32_t qempty_s = smem_u32(qempty);
   const int nkb = (int)(a.d / BK);
   const int64_t cl = blockIdx.x >> 1, ncl = gridDim.x >> 1;
   const int64_t Tt = a.nrb2 * a.NT;
+  const bool stat = a.tile_ctr == nullptr;   // round-robin deal (short calls, see tile_mode)
 
   if (warp == 0) {
     if (lane == 0) {
       // ================= TMA producer (both CTAs): own hidden rows + own half of the weights
       int st = 0;
       uint32_t ph = 0;
-      for (int64_t t = cl; t < Tt; t += ncl) {
+      long long nxt = (!stat && leader) ? (long long)atomicAdd(a.tile_ctr, 1ull) : 0;
+      for (int i = 0;; ++i) {
+        int64_t t;
+        if (stat) {
+          t = cl + (int64_t)i * ncl < Tt ? cl + (int64_t)i * ncl : (int64_t)-1;
+        } else if (leader) {
+          t = tile_publish(R, i, nxt < Tt ? nxt : -1, qempty_s);
+          if (t >= 0) nxt = (long long)atomicAdd(a.tile_ctr, 1ull);   // used at the next tile
+        } else {
+          t = tile_read(R, i);
+        }
+        if (t < 0) break;
         int64_t rb2, nt;
         tile_coords2(a, t, rb2, nt);
         const int arow = (int)(rb2 * 256 + rank * 128);
@@ -401,7 +501,9 @@ __global__ void __launch_bounds__(THREADS, 1)
       uint32_t ph = 0;
       int acc = 0;
       uint32_t aph = 0;
-      for (int64_t t = cl; t < Tt; t += ncl) {
+      for (int i = 0;; ++i) {
+        const int64_t t = stat ? (cl + (int64_t)i * ncl < Tt ? cl + (int64_t)i * ncl : (int64_t)-1) : tile_read(R, i);
+        if (t < 0) break;
         mbar_wait(tempty_s + 8 * acc, aph ^ 1u);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t td = tmem + (uint32_t)(acc * BN);
@@ -428,7 +530,16 @@ __global__ void __launch_bounds__(THREADS, 1)
     const float k2 = a.invT * kLog2e;
     int acc = 0;
     uint32_t aph = 0;
-    for (int64_t t = cl; t < Tt; t += ncl) {
+    for (int i = 0;; ++i) {
+      int64_t t;
+      if (stat) {
+        t = cl + (int64_t)i * ncl < Tt ? cl + (int64_t)i * ncl : (int64_t)-1;
+      } else {
+        long long v = 0;
+        if (lane == 0) v = tile_read(R, i);
+        t = __shfl_sync(kFull, v, 0);
+      }
+      if (t < 0) break;
       int64_t rb2, n;
       tile_coords2(a, t, rb2, n);
       const int64_t row = rb2 * 256 + rank * 128 + 32 * q + lane;
@@ -592,6 +703,7 @@ struct GemmArgs {
   int64_t nmb2, nnb;  // 256-row blocks (one per CTA pair), 256-column blocks
   int G;              // row blocks per raster group
   int acc;            // 1: C += A B^T
+  unsigned long long* tile_ctr;  // the dynamic tile counter (zeroed per launch)
 };
 
 __device__ __forceinline__ void gemm_coords(const GemmArgs& g, int64_t t, int64_t& mb, int64_t& nb) {
@@ -632,6 +744,8 @@ __global__ void __launch_bounds__(THREADS, 1)
                GemmArgs g) {
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full[STAGES2], empty[STAGES2], tfull[2], tempty[2];
+  __shared__ __align__(8) uint64_t qfull[kTQ], qempty[kTQ];
+  __shared__ __align__(8) long long tq[kTQ];
   __shared__ __align__(16) float cstage[4][32 * kCPitch];
   __shared__ uint32_t tmem_sh;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -642,6 +756,10 @@ __global__ void __launch_bounds__(THREADS, 1)
     for (int s = 0; s < STAGES2; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
+    }
+    for (int q = 0; q < kTQ; ++q) {
+      mbar_init(&qfull[q], 1);         // the leader's producer (tile index published)
+      mbar_init(&qempty[q], kTQCons);  // every reader of the pair (leader's copy is the one used)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
@@ -664,15 +782,33 @@ __global__ void __launch_bounds__(THREADS, 1)
   const uint32_t tmem = tmem_sh;
   const uint32_t full_s = smem_u32(full), empty_s = smem_u32(empty);
   const uint32_t tfull_s = smem_u32(tfull), tempty_s = smem_u32(tempty);
+  TileRing R;
+  R.full_s = smem_u32(qfull);
+  R.empty_leader = mapa(smem_u32(qempty), 0);
+  R.tq = tq;
+  R.tq_peer = mapa(smem_u32(tq), 1);
+  const uint32_t qempty_s = smem_u32(qempty);
   const int nkb = (int)((g.K + BK - 1) / BK);
   const int64_t cl = blockIdx.x >> 1, ncl = gridDim.x >> 1;
   const int64_t Tt = g.nmb2 * g.nnb;
+  const bool stat = g.tile_ctr == nullptr;   // round-robin deal (short calls, see tile_mode)
 
   if (warp == 0) {
     if (lane == 0) {
       int st = 0;
       uint32_t ph = 0;
-      for (int64_t t = cl; t < Tt; t += ncl) {
+      long long nxt = (!stat && leader) ? (long long)atomicAdd(g.tile_ctr, 1ull) : 0;
+      for (int i = 0;; ++i) {
+        int64_t t;
+        if (stat) {
+          t = cl + (int64_t)i * ncl < Tt ? cl + (int64_t)i * ncl : (int64_t)-1;
+        } else if (leader) {
+          t = tile_publish(R, i, nxt < Tt ? nxt : -1, qempty_s);
+          if (t >= 0) nxt = (long long)atomicAdd(g.tile_ctr, 1ull);   // used at the next tile
+        } else {
+          t = tile_read(R, i);
+        }
+        if (t < 0) break;
         int64_t mb, nb;
         gemm_coords(g, t, mb, nb);
         const int arow = (int)(mb * 256 + rank * 128);
@@ -706,7 +842,9 @@ __global__ void __launch_bounds__(THREADS, 1)
       uint32_t aph = 0;
       // per K = 16 step: +32 B inside a K-major swizzle atom, +2048 B (16 K rows) MN-major
       constexpr uint64_t stepA = A_MN ? 2048 >> 4 : 2, stepB = B_MN ? 2048 >> 4 : 2;
-      for (int64_t t = cl; t < Tt; t += ncl) {
+      for (int i = 0;; ++i) {
+        const int64_t t = stat ? (cl + (int64_t)i * ncl < Tt ? cl + (int64_t)i * ncl : (int64_t)-1) : tile_read(R, i);
+        if (t < 0) break;
         mbar_wait(tempty_s + 8 * acc, aph ^ 1u);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t td = tmem + (uint32_t)(acc * BN);
@@ -733,7 +871,16 @@ __global__ void __launch_bounds__(THREADS, 1)
     float* stg = cstage[q];
     int acc = 0;
     uint32_t aph = 0;
-    for (int64_t t = cl; t < Tt; t += ncl) {
+    for (int i = 0;; ++i) {
+      int64_t t;
+      if (stat) {
+        t = cl + (int64_t)i * ncl < Tt ? cl + (int64_t)i * ncl : (int64_t)-1;
+      } else {
+        long long v = 0;
+        if (lane == 0) v = tile_read(R, i);
+        t = __shfl_sync(kFull, v, 0);
+      }
+      if (t < 0) break;
       int64_t mb, nb;
       gemm_coords(g, t, mb, nb);
       const int64_t row0 = mb * 256 + rank * 128 + 32 * q;
@@ -968,7 +1115,7 @@ static size_t grad_layout(int64_t chunk_rows, int64_t d, int64_t V) {
   const int64_t Vp = (V + 7) / 8 * 8;
   size_t n = ((size_t)CR * Vp * 2 + 255) & ~(size_t)255;
   if (kGemmKB) n += (((size_t)d * Vp * 2 + 255) & ~(size_t)255) + (size_t)d * CR * 2;
-  return n + 256;
+  return n + 512;   // the last 256 bytes: the CTA-pair kernels' tile counter
 }
 
 static void launch_pair(const void* kern, int clusters, cudaStream_t s, void** args) {
@@ -998,7 +1145,7 @@ struct Operand {
 // C[M, N] (+)= A B^T on the CTA-pair tcgen05 kernel.
 template <bool A_MN, bool B_MN>
 static odpo_status gemm2(Operand A, Operand B, int64_t M, int64_t N, int64_t K, float* C,
-                         int64_t ldc, bool acc, int sms, cudaStream_t s,
+                         int64_t ldc, bool acc, int sms, cudaStream_t s, unsigned long long* ctr,
                          __nv_bfloat16* Cb = nullptr) {
   CUtensorMap mA, mB;
   const bool okA = A_MN ? make_map_mn(&mA, A.p, K, M, A.ld) : make_map(&mA, A.p, M, K, A.ld, BM);
@@ -1014,6 +1161,9 @@ static odpo_status gemm2(Operand A, Operand B, int64_t M, int64_t N, int64_t K, 
   g.acc = acc ? 1 : 0;
   int clusters = sms / 2;
   if (clusters > g.nmb2 * g.nnb) clusters = (int)(g.nmb2 * g.nnb);
+  g.tile_ctr = tile_mode(ctr, g.nmb2 * g.nnb, clusters);
+  if (g.tile_ctr && cudaMemsetAsync(g.tile_ctr, 0, sizeof(unsigned long long), s) != cudaSuccess)
+    return ODPO_ERR_CUDA;
   void* args[] = {&mA, &mB, &g};
   launch_pair((const void*)k_gemm_tn2<A_MN, B_MN>, clusters, s, args);
   return cudaGetLastError() == cudaSuccess ? ODPO_OK : ODPO_ERR_CUDA;
@@ -1026,7 +1176,7 @@ size_t odpo_lmhead_workspace_bytes(int64_t B, int64_t T, int64_t V) {
   const int64_t R = B * T;
   const int64_t NT = (V + BN - 1) / BN;
   // per row: NT (m, r) partials, the sampled logit, and an fp32 log-prob scratch
-  return (size_t)R * (size_t)NT * sizeof(float2) + (size_t)R * 8 + 256;
+  return (size_t)R * (size_t)NT * sizeof(float2) + (size_t)R * 8 + 512;   // last 256: tile counter
 }
 
 odpo_status odpo_lmhead_seq_logprobs(const void* hidden, const void* weight, int64_t B, int64_t T,
@@ -1071,7 +1221,7 @@ odpo_status odpo_lmhead_seq_logprobs(const void* hidden, const void* weight, int
   cudaStream_t s = (cudaStream_t)stream;
   if (pair) {
     a.nrb2 = (R + 255) / 256;
-    a.G = kRasterG / 2;
+    a.G = lmh_group(d);
     const int64_t t2 = a.nrb2 * a.NT;
     int clusters = sms / 2;
     if (clusters > t2) clusters = (int)t2;
@@ -1087,6 +1237,11 @@ odpo_status odpo_lmhead_seq_logprobs(const void* hidden, const void* weight, int
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
+    a.tile_ctr = tile_mode(reinterpret_cast<unsigned long long*>(
+                               reinterpret_cast<char*>(workspace) + odpo_lmhead_workspace_bytes(B, T, V) - 256),
+                           t2, clusters);
+    if (a.tile_ctr && cudaMemsetAsync(a.tile_ctr, 0, sizeof(unsigned long long), s) != cudaSuccess)
+      return ODPO_ERR_CUDA;
     cudaLaunchKernelEx(&cfg, k_lmhead_fwd2<kEpiLse>, mA, mB, a);
   } else {
     const int grid = (int)(a.Ttot < sms ? a.Ttot : sms);
@@ -1136,6 +1291,8 @@ odpo_status odpo_lmhead_grad(const void* hidden, const void* weight, int64_t R, 
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t Vp = (V + 7) / 8 * 8;
   const int sms = sm_count();
+  unsigned long long* ctr = reinterpret_cast<unsigned long long*>(
+      reinterpret_cast<char*>(scratch) + odpo_lmhead_grad_scratch_bytes(CR, d, V) - 256);
   __nv_bfloat16* G = reinterpret_cast<__nv_bfloat16*>(scratch);
   char* Wt = reinterpret_cast<char*>(scratch) + (((size_t)CR * Vp * 2 + 255) & ~(size_t)255);
   char* Ht = Wt + (((size_t)d * Vp * 2 + 255) & ~(size_t)255);
@@ -1156,7 +1313,7 @@ odpo_status odpo_lmhead_grad(const void* hidden, const void* weight, int64_t R, 
     a.NT = (V + BN - 1) / BN;
     a.Ttot = a.nrb * a.NT;
     a.nrb2 = (Rc + 255) / 256;
-    a.G = kRasterG / 2;
+    a.G = lmh_group(d);
     a.invT = inv_temperature;
     a.tokens = tokens + r0;
     a.row_lse = row_lse + r0;
@@ -1165,6 +1322,9 @@ odpo_status odpo_lmhead_grad(const void* hidden, const void* weight, int64_t R, 
     a.ldg = Vp;
     int clusters = sms / 2;
     if (clusters > a.nrb2 * a.NT) clusters = (int)(a.nrb2 * a.NT);
+    a.tile_ctr = tile_mode(ctr, a.nrb2 * a.NT, clusters);
+    if (a.tile_ctr && cudaMemsetAsync(a.tile_ctr, 0, sizeof(unsigned long long), s) != cudaSuccess)
+      return ODPO_ERR_CUDA;
     void* args[] = {&mA, &mB, &a};
     launch_pair((const void*)k_lmhead_fwd2<kEpiGrad>, clusters, s, args);
     if (cudaGetLastError() != cudaSuccess) return ODPO_ERR_CUDA;
@@ -1174,20 +1334,20 @@ odpo_status odpo_lmhead_grad(const void* hidden, const void* weight, int64_t R, 
           reinterpret_cast<const unsigned short*>(hc), Rc, d, d,
           reinterpret_cast<unsigned short*>(Ht), CR);
       e = gemm2<false, false>(Operand{G, Vp, false}, Operand{Wt, Vp, false}, Rc, d, V,
-                              dhidden + r0 * d, d, false, sms, s);
+                              dhidden + r0 * d, d, false, sms, s, ctr);
       if (e != ODPO_OK) return e;
       e = gemm2<true, false>(Operand{G, Vp, true}, Operand{Ht, CR, false}, V, d, Rc, dweight, d,
-                             r0 > 0, sms, s);
+                             r0 > 0, sms, s, ctr);
       if (e != ODPO_OK) return e;
       continue;
     }
     // dhidden[r0 : r0 + Rc] = G W: A = G (K = V contiguous), B = W read N-major (N = d contiguous)
     e = gemm2<false, true>(Operand{G, Vp, false}, Operand{weight, d, true}, Rc, d, V,
-                           dhidden + r0 * d, d, false, sms, s);
+                           dhidden + r0 * d, d, false, sms, s, ctr);
     if (e != ODPO_OK) return e;
     // dweight (+)= G^T H: A = G read M-major (M = V contiguous), B = H chunk read N-major
     e = gemm2<true, true>(Operand{G, Vp, true}, Operand{hc, d, true}, V, d, Rc, dweight, d, r0 > 0,
-                          sms, s);
+                          sms, s, ctr);
     if (e != ODPO_OK) return e;
   }
   return ODPO_OK;
@@ -1220,7 +1380,7 @@ size_t odpo_lmhead_dpo_step_scratch_bytes(int64_t chunk_pairs, int64_t T, int64_
   auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
   const int64_t NT = (V + BN - 1) / BN;
   return al((size_t)Rc * Vp * 2) + al(odpo_workspace_bytes(2 * chunk_pairs, T, chunk_pairs)) +
-         al(16 * sizeof(double)) + al((size_t)NT * Rc * sizeof(float4)) + 256;
+         al(16 * sizeof(double)) + al((size_t)NT * Rc * sizeof(float4)) + 512;   // last 256: tile counter
 }
 
 odpo_status odpo_lmhead_dpo_step(const void* hidden, const void* weight, int64_t P, int64_t T,
@@ -1262,6 +1422,8 @@ odpo_status odpo_lmhead_dpo_step(const void* hidden, const void* weight, int64_t
   const int64_t NT = (V + BN - 1) / BN;
   auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
   char* base = reinterpret_cast<char*>(scratch);
+  unsigned long long* ctr = reinterpret_cast<unsigned long long*>(
+      base + odpo_lmhead_dpo_step_scratch_bytes(chunk_pairs, T, V) - 256);
   __nv_bfloat16* L = reinterpret_cast<__nv_bfloat16*>(base);
   const int64_t Rmax = 2 * chunk_pairs * T;
   char* ws = base + al((size_t)Rmax * Vp * 2);
@@ -1278,7 +1440,7 @@ odpo_status odpo_lmhead_dpo_step(const void* hidden, const void* weight, int64_t
     if (ODPO_STEP_FWD_PASS) {
       // logits chunk [Rc, V] (row pitch Vp) = H_c W^T, bf16; the full loss call in place
       e = gemm2<false, false>(Operand{hc, d, false}, Operand{weight, d, false}, Rc, V, d, nullptr,
-                              Vp, false, sms, s, L);
+                              Vp, false, sms, s, ctr, L);
       if (e != ODPO_OK) return e;
       e = odpo_online_dpo_loss_fwd_bwd(L, ODPO_BF16, 2 * np, T, V, T * Vp, Vp, ref_logp + 2 * p0,
                                        tokens + r0, mask + r0, nullptr, np, P_global, beta,
@@ -1296,7 +1458,7 @@ odpo_status odpo_lmhead_dpo_step(const void* hidden, const void* weight, int64_t
       a.NT = NT;
       a.Ttot = a.nrb * a.NT;
       a.nrb2 = (Rc + 255) / 256;
-      a.G = kRasterG / 2;
+      a.G = lmh_group(d);
       a.invT = inv_temperature;
       a.tokens = tokens + r0;
       a.mask = mask + r0;
@@ -1305,6 +1467,9 @@ odpo_status odpo_lmhead_dpo_step(const void* hidden, const void* weight, int64_t
       a.parts4 = parts4;
       int clusters = sms / 2;
       if (clusters > a.nrb2 * a.NT) clusters = (int)(a.nrb2 * a.NT);
+      a.tile_ctr = tile_mode(ctr, a.nrb2 * a.NT, clusters);
+      if (a.tile_ctr && cudaMemsetAsync(a.tile_ctr, 0, sizeof(unsigned long long), s) != cudaSuccess)
+        return ODPO_ERR_CUDA;
       void* args[] = {&mA, &mB, &a};
       launch_pair((const void*)k_lmhead_fwd2<kEpiLogits>, clusters, s, args);
       if (cudaGetLastError() != cudaSuccess) return ODPO_ERR_CUDA;
@@ -1320,10 +1485,10 @@ odpo_status odpo_lmhead_dpo_step(const void* hidden, const void* weight, int64_t
     if (cudaGetLastError() != cudaSuccess) return ODPO_ERR_CUDA;
     // dhidden = dlogits W (W read N-major); dweight += dlogits^T H (both read MN-major)
     e = gemm2<false, true>(Operand{L, Vp, false}, Operand{weight, d, true}, Rc, d, V,
-                           dhidden + r0 * d, d, false, sms, s);
+                           dhidden + r0 * d, d, false, sms, s, ctr);
     if (e != ODPO_OK) return e;
     e = gemm2<true, true>(Operand{L, Vp, true}, Operand{hc, d, true}, V, d, Rc, dweight, d, p0 > 0,
-                          sms, s);
+                          sms, s, ctr);
     if (e != ODPO_OK) return e;
   }
   return ODPO_OK;
