@@ -343,8 +343,11 @@ constexpr int kTQ = 8;
 // runs; below ~512 per pair (the Pythia head: 283) the round-robin deal measured 2% faster (the
 // ring hand-off costs more than the drift), above it (the LLaMA head: 3466) the dynamic order
 // cuts DRAM reads 2x and runs 9-13% faster at the power cap (profiles/r02/next2/dyn/).
+#ifndef ODPO_DYN_MIN
+#define ODPO_DYN_MIN 512   // tiles per pair from which the dynamic order is used (A/B knob)
+#endif
 static unsigned long long* tile_mode(unsigned long long* ctr, int64_t tiles, int clusters) {
-  if (kStaticTiles || clusters <= 0 || tiles < 512 * (int64_t)clusters) return nullptr;
+  if (kStaticTiles || clusters <= 0 || tiles < (int64_t)ODPO_DYN_MIN * clusters) return nullptr;
   return ctr;
 }
 // Host: pair-blocks (256 rows) per raster group of the head kernels: ~40 MB of hidden rows kept
@@ -1094,9 +1097,9 @@ constexpr bool kLmhPair = ODPO_LMH_1CTA == 0;
 #endif
 constexpr int kRasterG = ODPO_LMH_G;
 #ifndef ODPO_GEMM_G
-#define ODPO_GEMM_G 16
+#define ODPO_GEMM_G 8
 #endif
-constexpr int kGemmG = ODPO_GEMM_G;   // backward GEMMs: 256-row blocks per raster group  // row blocks per raster group (tuned: 8/16/32/64 -> 1636/1723/1751/1802 TF/s)
+constexpr int kGemmG = ODPO_GEMM_G;   // backward GEMMs: 256-row blocks per raster group (round-robin deal, burst: 8/16/32/64 -> 1636/1723/1751/1802 TF/s; dynamic order at the power cap: 8 best, profiles/r02/next2/gemm_ab/)
 
 }  // namespace lmh
 }  // namespace odpo
@@ -1161,7 +1164,9 @@ static odpo_status gemm2(Operand A, Operand B, int64_t M, int64_t N, int64_t K, 
   g.acc = acc ? 1 : 0;
   int clusters = sms / 2;
   if (clusters > g.nmb2 * g.nnb) clusters = (int)(g.nmb2 * g.nnb);
-  g.tile_ctr = tile_mode(ctr, g.nmb2 * g.nnb, clusters);
+  // the backward GEMMs take the dynamic order at every size (few, long-K tiles: measured with
+  // 8-row-block raster groups, LLaMA-head grad 310.8 -> 298.8-300.1 ms, profiles/r02/next2/gemm_ab/)
+  g.tile_ctr = kStaticTiles ? nullptr : ctr;
   if (g.tile_ctr && cudaMemsetAsync(g.tile_ctr, 0, sizeof(unsigned long long), s) != cudaSuccess)
     return ODPO_ERR_CUDA;
   void* args[] = {&mA, &mB, &g};

@@ -9,6 +9,10 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import paper_2410_18252_b200 as odpo  # noqa: E402
 
+for _a in sys.argv[1:]:
+    if _a.endswith(".so"):   # a variant build (A/B)
+        odpo.LIB_PATH = os.path.abspath(_a)
+
 
 def t(fn, reps=5):
     for _ in range(2):
