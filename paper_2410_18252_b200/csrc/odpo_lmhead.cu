@@ -95,7 +95,8 @@ __device__ __forceinline__ void tm_ld32(uint32_t taddr, uint32_t (&r)[32]) {
 
 // Work split: the nrb x NT grid of (128-row block, 256-wide vocabulary tile) tiles, ordered in
 // groups of G row blocks, vocabulary-major inside a group, and dealt round-robin to the
-// persistent CTAs (tile i*grid + c to CTA c).  The ~grid tiles in flight at any moment span G
+// persistent CTAs (tile i*grid + c to CTA c) -- in this single-CTA kernel; the CTA-pair kernels
+// below claim tiles dynamically (see "Dynamic tile order").  The ~grid tiles in flight at any moment span G
 // row blocks x grid/G vocabulary tiles, so their hidden blocks and weight tiles are shared
 // through L2.  Every tile writes its rows' partial (m, r) -- the merge order (vocabulary tile
 // order) does not depend on the CTA mapping.
