@@ -278,3 +278,35 @@ def test_lmhead_dpo_step_parity(shape):
     ew = np.abs(dw.cpu().double().numpy() - dw_o)
     assert np.all(eh <= bh + 1e-12), float(np.max(eh - bh))
     assert np.all(ew <= bw + 1e-12), float(np.max(ew - bw))
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a CUDA device")
+def test_lmhead_dynamic_tile_order_sampled():
+    """A head large enough for the CTA-pair kernel's dynamic tile order (>= 512 tiles per pair:
+    32768 rows = 128 pair-blocks x 296 vocabulary tiles = 37888 tiles over 74 pairs): every
+    tile's partial lands in its fixed slot whatever pair claims it, so sampled rows match the
+    oracle (the head's fp64 matmul, then seq_logprobs) at the usual 1e-4 bound, and two calls
+    give the same bits."""
+    import paper_2410_18252_b200 as odpo
+    B, T, d, V = 32, 1024, 64, 75776
+    rows = np.arange(B * T)
+    h, w = synth.lmhead_inputs(23, rows, d, V)
+    tok = synth.tokens_rows(23, rows, V).reshape(B, T).astype(np.int32)
+    mask = np.ones((B, T), np.uint8)
+    hd = torch.from_numpy(h.reshape(B, T, d)).to(torch.bfloat16).cuda()
+    wd = torch.from_numpy(w).to(torch.bfloat16).cuda()
+    tk, mk = torch.from_numpy(tok).cuda(), torch.from_numpy(mask).cuda()
+    seq, tlp, lse, st = odpo.lmhead_seq_logprobs(hd, wd, tk, mk)
+    seq2, tlp2, lse2, _ = odpo.lmhead_seq_logprobs(hd, wd, tk, mk)
+    torch.cuda.synchronize()
+    assert int(st.item()) == 0
+    assert torch.equal(tlp, tlp2) and torch.equal(lse, lse2) and torch.equal(seq, seq2)
+    take = np.unique(np.concatenate([np.arange(0, B * T, 997), [1, 255, 256, 4095, B * T - 1]]))
+    o = oracle.lmhead_seq_logprobs(h[take].reshape(1, len(take), d), w,
+                                   tok.reshape(-1)[take].reshape(1, -1),
+                                   np.ones((1, len(take)), np.uint8), n_threads=8)
+    g = tlp.reshape(-1).cpu().numpy().astype(np.float64)[take]
+    assert np.all(np.abs(g - o["tok_logp"].reshape(-1)) <= 1e-4 * np.maximum(1.0, np.abs(o["tok_logp"].reshape(-1))))
+    gl = lse.reshape(-1).cpu().numpy().astype(np.float64)[take]
+    assert np.all(np.abs(gl - o["row_lse"].reshape(-1)) <= 1e-4 * np.maximum(1.0, np.abs(o["row_lse"].reshape(-1))))
