@@ -658,60 +658,87 @@ def run_ours(args, rank, world, local_rank):
     # ---------------- e2e through host buffers (pinned H2D inputs, D2H stats + z each step)
     e2e = None
     if not args.no_e2e:
-        h_logits = torch.empty(logits.shape, dtype=tdt, pin_memory=True)
-        h_logits.copy_(logits)
-        h_rew = rewards.cpu().pin_memory()
-        h_eos = eos.cpu().pin_memory() if eos is not None else None
-        h_tok = tokens_all.cpu().pin_memory()
-        h_mask = mask_all.cpu().pin_memory()
-        h_ref = ref_all.cpu().pin_memory()
-        h_stats = torch.empty(16, dtype=torch.float64, pin_memory=True)
-        h_z = torch.empty(P, dtype=torch.float32, pin_memory=True)
-        d_rew, d_tok, d_mask, d_ref = (torch.empty_like(rewards), torch.empty_like(tokens_all),
-                                       torch.empty_like(mask_all), torch.empty_like(ref_all))
-        d_eos = torch.empty_like(eos) if eos is not None else None
-        h2d = (h_logits.numel() * s_in + h_rew.numel() * 4 + (h_eos.numel() if h_eos is not None else 0)
-               + h_tok.numel() * 4 + h_mask.numel() + h_ref.numel() * 4)
-        d2h = 16 * 8 + P * 4
-
-        def e2e_step():
-            logits.copy_(h_logits, non_blocking=True)
-            d_rew.copy_(h_rew, non_blocking=True)
-            if d_eos is not None:
-                d_eos.copy_(h_eos, non_blocking=True)
-            d_tok.copy_(h_tok, non_blocking=True)
-            d_mask.copy_(h_mask, non_blocking=True)
-            d_ref.copy_(h_ref, non_blocking=True)
-            sel = odpo.pair_select(d_rew, d_eos, pen, status=status, sel_stats=stats[10:13])
-            if Kc > 2:
-                tg, mg, rg = odpo.gather_pairs(sel.pair_rows, d_tok, d_mask, d_ref, status=status)
-                out = loss_call(args.gradient, None, rg, tg, mg)
-            else:
-                out = loss_call(args.gradient, sel.pair_rows, d_ref, d_tok, d_mask)
-            odpo.allreduce_stats(stats, exchange=sx)
-            h_stats.copy_(stats, non_blocking=True)
-            h_z.copy_(out.z, non_blocking=True)
-
-        e2e_step()
-        torch.cuda.synchronize()
+        # every rank pins one step's inputs (33.6 GB for LLaMA): check the host can hold all the
+        # node's ranks' buffers, and agree across ranks, before any of them starts the e2e loop
+        need = logits.numel() * s_in
+        ok, reason = 1, ""
+        try:
+            import psutil
+            nloc = int(os.environ.get("LOCAL_WORLD_SIZE", world))
+            avail = psutil.virtual_memory().available
+            if avail < 1.25 * need * nloc:
+                ok, reason = 0, (f"host memory: {avail / 1e9:.0f} GB available for {nloc} pinned "
+                                 f"buffers of {need / 1e9:.1f} GB")
+        except ImportError:
+            pass
+        h_logits = None
+        if ok:
+            try:
+                h_logits = torch.empty(logits.shape, dtype=tdt, pin_memory=True)
+            except RuntimeError as e:
+                ok, reason = 0, f"pinned host allocation failed: {e}"[:200]
         if world > 1:
-            dist.barrier()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
-        for _ in range(args.e2e_steps):
+            t_ok = torch.tensor([ok], dtype=torch.int32, device=dev)
+            dist.all_reduce(t_ok, op=dist.ReduceOp.MIN)
+            if int(t_ok.item()) == 0 and ok:
+                ok, reason = 0, "another rank could not pin its host buffer"
+        if not ok:
+            e2e = {"unavailable": reason}
+            h_logits = None
+        else:
+            h_logits.copy_(logits)
+            h_rew = rewards.cpu().pin_memory()
+            h_eos = eos.cpu().pin_memory() if eos is not None else None
+            h_tok = tokens_all.cpu().pin_memory()
+            h_mask = mask_all.cpu().pin_memory()
+            h_ref = ref_all.cpu().pin_memory()
+            h_stats = torch.empty(16, dtype=torch.float64, pin_memory=True)
+            h_z = torch.empty(P, dtype=torch.float32, pin_memory=True)
+            d_rew, d_tok, d_mask, d_ref = (torch.empty_like(rewards), torch.empty_like(tokens_all),
+                                           torch.empty_like(mask_all), torch.empty_like(ref_all))
+            d_eos = torch.empty_like(eos) if eos is not None else None
+            h2d = (h_logits.numel() * s_in + h_rew.numel() * 4 + (h_eos.numel() if h_eos is not None else 0)
+                   + h_tok.numel() * 4 + h_mask.numel() + h_ref.numel() * 4)
+            d2h = 16 * 8 + P * 4
+
+            def e2e_step():
+                logits.copy_(h_logits, non_blocking=True)
+                d_rew.copy_(h_rew, non_blocking=True)
+                if d_eos is not None:
+                    d_eos.copy_(h_eos, non_blocking=True)
+                d_tok.copy_(h_tok, non_blocking=True)
+                d_mask.copy_(h_mask, non_blocking=True)
+                d_ref.copy_(h_ref, non_blocking=True)
+                sel = odpo.pair_select(d_rew, d_eos, pen, status=status, sel_stats=stats[10:13])
+                if Kc > 2:
+                    tg, mg, rg = odpo.gather_pairs(sel.pair_rows, d_tok, d_mask, d_ref, status=status)
+                    out = loss_call(args.gradient, None, rg, tg, mg)
+                else:
+                    out = loss_call(args.gradient, sel.pair_rows, d_ref, d_tok, d_mask)
+                odpo.allreduce_stats(stats, exchange=sx)
+                h_stats.copy_(stats, non_blocking=True)
+                h_z.copy_(out.z, non_blocking=True)
+
             e2e_step()
-        b.record()
-        torch.cuda.synchronize()
-        et = torch.tensor([a.elapsed_time(b)], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(et, op=dist.ReduceOp.MAX)
-        e2e = {"value": world * P * args.e2e_steps / (float(et.item()) / 1e3), "unit": "pairs/s",
-               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-               "steps": args.e2e_steps,
-               "note": "pinned host->device copy of logits, rewards, eos, tokens, mask, ref_logp; "
-                       "device->host of the stats buffer and per-pair z; dlogits stay resident "
-                       "for the LM-head backward"}
-        del h_logits
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            for _ in range(args.e2e_steps):
+                e2e_step()
+            b.record()
+            torch.cuda.synchronize()
+            et = torch.tensor([a.elapsed_time(b)], dtype=torch.float64, device=dev)
+            if world > 1:
+                dist.all_reduce(et, op=dist.ReduceOp.MAX)
+            e2e = {"value": world * P * args.e2e_steps / (float(et.item()) / 1e3), "unit": "pairs/s",
+                   "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                   "steps": args.e2e_steps,
+                   "note": "pinned host->device copy of logits, rewards, eos, tokens, mask, ref_logp; "
+                           "device->host of the stats buffer and per-pair z; dlogits stay resident "
+                           "for the LM-head backward"}
+            del h_logits
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
